@@ -1,0 +1,144 @@
+/*
+ * tls_b200.h — C ABI of the B200-native two-level Schwarz Krylov hot path.
+ *
+ * Drop-in boundary for the reference package ``tlschwarz`` (pure Python over
+ * numpy/scipy, /root/reference/pkg/src/tlschwarz).  Each entry point names
+ * the reference interface it replaces (file:line, prefix src/ =
+ * pkg/src/tlschwarz/).  The Python mirror of the reference API
+ * (paper_2401_03915_b200/{sparsemat,precond,krylov}.py) binds these through
+ * ctypes; INTEGRATION.md shows the binding a tlschwarz maintainer would add.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; ``stream`` is a cudaStream_t passed as
+ *    void* (NULL = legacy default stream);
+ *  - vectors (r, z, x, b) are DEVICE pointers of length n (fp64) unless a
+ *    parameter says "host";
+ *  - every call returns a tls_code; on failure tls_ctx_last_error() holds a
+ *    message and tls_status (for solves) the reference exception payload;
+ *  - the handle owns the CSR, subdomain maps, local inverse tiles and the
+ *    coarse data; all are immutable after tls_precond_finalize (mirrors the
+ *    read-only SparseMat buffers, src/sparsemat.py:51-52).  Calls on one
+ *    handle must be serialised by the caller.
+ */
+#ifndef TLS_B200_H
+#define TLS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLS_ABI_VERSION 1
+#define TLS_TILE 64           /* edge of the dense tiles of local operators */
+
+typedef enum {
+  TLS_OK = 0,
+  TLS_ERR_DIM = 1,        /* ValueError "dimension mismatch"  (src/sparsemat.py:127-128) */
+  TLS_ERR_BREAKDOWN = 2,  /* BreakdownError(iteration, curvature) (src/krylov.py:22-29)   */
+  TLS_ERR_SUBDOMAIN = 3,  /* SubdomainSetupError(subdomain)       (src/subdomain.py:22-27) */
+  TLS_ERR_COARSE = 4,     /* RuntimeError coarse not SPD/singular (src/coarse.py:175-181)  */
+  TLS_ERR_CAP = 5,        /* ValueError maxit above hard cap 1000 (src/krylov.py:136-137)  */
+  TLS_ERR_ARG = 6,        /* invalid argument / unsupported option                         */
+  TLS_ERR_STATE = 7,      /* call order violated (e.g. apply before finalize)              */
+  TLS_ERR_CUDA = 8,       /* CUDA runtime failure                                          */
+  TLS_ERR_OOM = 9         /* device allocation failed                                      */
+} tls_code;
+
+typedef enum { TLS_ASM = 0, TLS_RAS = 1 } tls_one_level;                       /* src/precond.py:34 */
+typedef enum { TLS_NONE = 0, TLS_ADDITIVE = 1, TLS_DEFLATED = 2 } tls_combine; /* src/precond.py:35 */
+
+/* Solve outcome; mirrors SolveReport (src/krylov.py:32-49) + the exception payloads. */
+typedef struct tls_status {
+  int32_t code;          /* tls_code */
+  int32_t iterations;    /* SolveReport.iterations */
+  int32_t converged;     /* SolveReport.converged */
+  int32_t iteration;     /* BreakdownError.iteration (code == TLS_ERR_BREAKDOWN) */
+  double value;          /* BreakdownError curvature */
+  int32_t gpu_launches;  /* kernels enqueued by this call (bench evidence) */
+  int32_t pad_;
+} tls_status;
+
+typedef struct tls_ctx tls_ctx;
+
+/* per-iteration hook: (user, iteration, HOST copy of the current iterate, or NULL for GMRES).
+ * Non-NULL forces one host sync per iteration (src/krylov.py:92-93, 182-183). */
+typedef void (*tls_iter_cb)(void* user, int32_t iteration, const double* x_host);
+
+/* ---- lifecycle --------------------------------------------------------- */
+int32_t tls_abi_version(void);
+int32_t tls_ctx_create(int32_t device, tls_ctx** out);
+void tls_ctx_destroy(tls_ctx* ctx);
+const char* tls_ctx_last_error(const tls_ctx* ctx);
+/* device bytes owned by the handle (tiles, maps, workspaces) */
+int64_t tls_ctx_device_bytes(const tls_ctx* ctx);
+
+/* ---- SparseMat: replaces SparseMat(csr) canonical storage (src/sparsemat.py:36-52)
+ * indptr/indices/data are HOST arrays of a canonical CSR (sorted, unique columns). */
+int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_t* indptr,
+                          const int32_t* indices, const double* data, int32_t symmetric);
+/* y = A x : replaces SparseMat.matvec (src/sparsemat.py:125-129) */
+int32_t tls_spmv(tls_ctx* ctx, const double* x, double* y, void* stream);
+
+/* ---- SubdomainMap list: replaces extend_overlap output (src/partition.py:201-231, 278-301)
+ * offsets[n_sub+1], indices[offsets[n_sub]] (local order: interior ascending, then each
+ * layer ascending), n_interior[n_sub]; all HOST arrays. */
+int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub, const int64_t* offsets,
+                              const int64_t* indices, const int32_t* n_interior);
+/* largest local size (for the setup batch workspace) */
+int32_t tls_subdomain_max_size(const tls_ctx* ctx);
+
+/* ---- setup helpers on the device --------------------------------------
+ * Dense local blocks A_ii = A[idx][:, idx] (src/subdomain.py:53-69) for subdomains
+ * [first, first+count), written row-major into out (count x ld x ld, device), padded
+ * with the identity beyond n_i. */
+int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first, int32_t count, double* out,
+                           int64_t ld, void* stream);
+/* Store A_ii^{-1} (row-major, count x ld x ld, device) as 64x64 tiles: packed lower
+ * triangle if the matrix is symmetric, all tiles otherwise.  Replaces the
+ * factor_dense solve closures (src/subdomain.py:72-95) used at src/precond.py:117-118. */
+int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first, int32_t count, const double* inv,
+                                int64_t ld, void* stream);
+/* Coarse space (src/coarse.py:23-49): per subdomain a dense block Z_s of shape
+ * n_interior[s] x k[s] (row-major, device, concatenated in subdomain order), columns
+ * [col_start[s], col_start[s]+k[s]) of the global basis; a0inv = (Z^T A Z)^{-1}
+ * (row-major n_coarse^2, device).  k == NULL or n_coarse == 0 disables the coarse level. */
+int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, const double* basis,
+                          const double* a0inv, void* stream);
+/* Build the apply schedule (work units, reduction lists, prolongation pull map). */
+int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine);
+
+/* ---- apply: replaces Preconditioner.apply / apply_one_level / coarse_apply
+ * (src/precond.py:114-136) */
+int32_t tls_precond_apply(tls_ctx* ctx, const double* r, double* z, void* stream);
+int32_t tls_apply_one_level(tls_ctx* ctx, const double* r, double* z, void* stream);
+int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream);
+
+/* ---- Krylov: replaces pcg (src/krylov.py:58-107) and gmres (src/krylov.py:127-195).
+ * b, x device; history HOST buffer of maxit+1 doubles (SolveReport.residuals);
+ * coeffs (pcg, may be NULL) HOST buffer of 2*maxit doubles receiving (alpha_k, beta_k) for
+ * the tridiagonal condition estimate (src/krylov.py:110-124);
+ * use_precond = 0 reproduces precond=None (src/krylov.py:52-55).
+ * gmres: restart <= 0 is the reference's unrestarted GMRES (maxit <= 1000);
+ * restart > 0 runs GMRES(restart) cycles on the true residual (build extension). */
+int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t maxit,
+                int32_t use_precond, double* history, double* coeffs, tls_status* st,
+                tls_iter_cb cb, void* user, void* stream);
+int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t maxit,
+                  int32_t restart, int32_t use_precond, double* history, tls_status* st,
+                  tls_iter_cb cb, void* user, void* stream);
+
+/* ---- SetupReport getters (src/precond.py:39-83) */
+int32_t tls_report(const tls_ctx* ctx, int64_t* n, int32_t* n_sub, int32_t* n_coarse,
+                   int64_t* tile_bytes);
+
+/* ---- measurement: average device time (ms) of the dominant kernel (batched local
+ * solve) over the last solve, timed with CUDA events on the launching stream, and
+ * the algorithmic bytes one launch of it must move. */
+int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms,
+                                double* algorithmic_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLS_B200_H */

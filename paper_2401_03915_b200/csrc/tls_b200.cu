@@ -1,0 +1,1058 @@
+// tls_b200.cu — host side of libtls_b200.so: handle, apply schedule, CUDA-graph Krylov drivers.
+//
+// C ABI declared in include/tls_b200.h.  All per-iteration work is enqueued on the caller's
+// stream; the PCG iteration (25 iterations = one residual-replacement period,
+// src/krylov.py:88-89) and the GMRES cycle are captured once into CUDA graphs and replayed,
+// with a device-side `done` flag turning the remaining kernels into no-ops after convergence,
+// so one host sync happens per 25 PCG iterations / per GMRES cycle instead of per kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tls_b200.h"
+#include "tls_kernels.cuh"
+
+using namespace tls;
+
+namespace {
+
+constexpr int PCG_GRAPH_ITERS = 25;  // replacement period of src/krylov.py:88
+constexpr int MAX_GRID = 148 * 8;    // 148 SMs x 8 resident 256-thread CTAs
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree((void*)p);
+  p = nullptr;
+}
+
+}  // namespace
+
+struct tls_ctx {
+  int device = 0;
+  std::string err;
+  int64_t dev_bytes = 0;
+  cudaStream_t cap = nullptr;
+  // ---- matrix (CSR, int32 indices)
+  int n = 0;
+  int64_t nnz = 0;
+  int sym = 0;
+  int lpr = 8;
+  int *rowptr = nullptr, *col = nullptr;
+  double* val = nullptr;
+  // ---- subdomains
+  int nsub = 0, max_n = 0;
+  std::vector<int64_t> h_off;
+  std::vector<int> h_idx, h_n, h_nint;
+  long long* d_sub_idxoff = nullptr;
+  int *d_sub_n = nullptr, *d_idx = nullptr, *d_nint = nullptr;
+  // ---- local operators
+  std::vector<BlkDesc> h_blk;  // nsub local blocks (+1 coarse after finalize)
+  BlkDesc* d_blk = nullptr;
+  double* tiles = nullptr;
+  int64_t tile_doubles = 0;
+  std::vector<int> stored;  // which subdomains have their inverse stored
+  // ---- coarse
+  int ncoarse = 0;
+  std::vector<int> h_k, h_cstart;
+  std::vector<long long> h_zoff;
+  double *d_Z = nullptr, *ctiles = nullptr;
+  long long* d_zoff = nullptr;
+  int *d_kcnt = nullptr, *d_cstart = nullptr;
+  // ---- schedule
+  bool finalized = false;
+  int one_level = 0, combine = 0;
+  long long X = 0, Xloc = 0, coarse_xoff = 0;
+  Unit* d_units = nullptr;  // [local | coarse]
+  int nu_local = 0, nu_coarse = 0;
+  OutTile* d_outs = nullptr;  // [local | coarse]
+  int no_local = 0, no_coarse = 0;
+  int* d_red = nullptr;
+  int* d_gidx = nullptr;
+  int *d_pull_ptr = nullptr, *d_pull_pos = nullptr;
+  long long* d_zrow = nullptr;
+  int *d_zk = nullptr, *d_zc = nullptr;
+  double *xloc = nullptr, *yloc = nullptr, *slots = nullptr;
+  int64_t nslots = 0;
+  double algo_local = 0.0, algo_coarse = 0.0;
+  // ---- work vectors
+  double *t1 = nullptr, *t2 = nullptr, *t3 = nullptr, *t4 = nullptr, *t5 = nullptr, *t6 = nullptr,
+         *t7 = nullptr, *vb = nullptr, *vx = nullptr, *vr = nullptr, *vp = nullptr, *vap = nullptr,
+         *vz = nullptr, *hist = nullptr, *ab = nullptr, *h_x = nullptr;
+  int hist_cap = 0;
+  double* part = nullptr;
+  int64_t part_cap = 0;
+  int G = 1, Gs = 1;
+  PcgState* pcg = nullptr;
+  GmState* gm = nullptr;
+  int* h_flag = nullptr;  // pinned
+  // ---- gmres workspace
+  double *V = nullptr, *H = nullptr, *cs = nullptr, *sn = nullptr, *gv = nullptr, *yv = nullptr,
+         *h1 = nullptr, *h2 = nullptr;
+  int gm_cols = 0;
+  // ---- graphs
+  cudaGraphExec_t pcg_exec[2] = {nullptr, nullptr};
+  int pcg_exec_launches[2] = {0, 0};
+  cudaGraphExec_t gm_exec[2] = {nullptr, nullptr};
+  int gm_exec_cols[2] = {0, 0};
+  int gm_exec_launches[2] = {0, 0};
+  int launches = 0;  // kernels enqueued since the counter was reset
+};
+
+#define CK(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                         \
+      return e_ == cudaErrorMemoryAllocation ? TLS_ERR_OOM : TLS_ERR_CUDA;                   \
+    }                                                                                        \
+  } while (0)
+
+#define CKL()                                                                                \
+  do {                                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                                     \
+    if (e_ != cudaSuccess) {                                                                 \
+      ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e_);                    \
+      return TLS_ERR_CUDA;                                                                   \
+    }                                                                                        \
+    ctx->launches++;                                                                         \
+  } while (0)
+
+#define TRY(...)               \
+  do {                         \
+    int rc_ = (__VA_ARGS__);   \
+    if (rc_ != TLS_OK) return rc_; \
+  } while (0)
+
+static int fail(tls_ctx* ctx, int code, const std::string& msg) {
+  ctx->err = msg;
+  return code;
+}
+
+template <class T>
+static int dalloc(tls_ctx* ctx, T*& p, int64_t count) {
+  dfree(p);
+  if (count <= 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)&p, sizeof(T) * (size_t)count);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    ctx->err = "cudaMalloc(" + std::to_string(sizeof(T) * (size_t)count) + " B): " + cudaGetErrorString(e);
+    return TLS_ERR_OOM;
+  }
+  ctx->dev_bytes += (int64_t)sizeof(T) * count;
+  return TLS_OK;
+}
+
+template <class T>
+static int upload(tls_ctx* ctx, T*& d, const T* h, int64_t count) {
+  TRY(dalloc(ctx, d, count));
+  if (count > 0) CK(cudaMemcpy(d, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+  return TLS_OK;
+}
+
+static int grid_for(int64_t work, int per_block) {
+  int64_t g = (work + per_block - 1) / per_block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, MAX_GRID));
+}
+
+static void destroy_graphs(tls_ctx* ctx) {
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->pcg_exec[i]) cudaGraphExecDestroy(ctx->pcg_exec[i]);
+    if (ctx->gm_exec[i]) cudaGraphExecDestroy(ctx->gm_exec[i]);
+    ctx->pcg_exec[i] = ctx->gm_exec[i] = nullptr;
+    ctx->gm_exec_cols[i] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// enqueue helpers
+// ---------------------------------------------------------------------------------------------
+template <int MODE, int DOT>
+static int spmv_lpr(tls_ctx* ctx, cudaStream_t s, const double* x, double* y, const double* b,
+                    double* part, const int* done) {
+  const int grid = ctx->Gs;
+#define SPMV_CASE(L)                                                                              \
+  case L:                                                                                         \
+    k_spmv<L, MODE, DOT><<<grid, NTHR, 0, s>>>(ctx->n, ctx->rowptr, ctx->col, ctx->val, x, y, b, \
+                                               part, done);                                       \
+    break;
+  switch (ctx->lpr) {
+    SPMV_CASE(2)
+    SPMV_CASE(4)
+    SPMV_CASE(8)
+    SPMV_CASE(16)
+    SPMV_CASE(32)
+    default: return fail(ctx, TLS_ERR_ARG, "bad lanes-per-row");
+  }
+#undef SPMV_CASE
+  CKL();
+  return TLS_OK;
+}
+
+// which unit/out lists a solve stage uses
+enum { L_LOCAL = 0, L_COARSE = 1, L_ALL = 2 };
+
+static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done) {
+  int u0 = 0, nu = 0, o0 = 0, no = 0;
+  if (which == L_LOCAL) { nu = ctx->nu_local; no = ctx->no_local; }
+  if (which == L_COARSE) { u0 = ctx->nu_local; nu = ctx->nu_coarse; o0 = ctx->no_local; no = ctx->no_coarse; }
+  if (which == L_ALL) { nu = ctx->nu_local + ctx->nu_coarse; no = ctx->no_local + ctx->no_coarse; }
+  if (nu > 0) {
+    k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, done);
+    CKL();
+  }
+  if (no > 0) {
+    k_reduce_tiles<<<(no + 7) / 8, NTHR, 0, s>>>(ctx->d_blk, ctx->d_outs + o0, no, ctx->d_red,
+                                                 ctx->slots, ctx->yloc, done);
+    CKL();
+  }
+  return TLS_OK;
+}
+
+static int enq_gather(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
+  k_gather<<<grid_for(ctx->Xloc, NTHR), NTHR, 0, s>>>(ctx->Xloc, ctx->d_gidx, r, ctx->xloc, done);
+  CKL();
+  return TLS_OK;
+}
+
+static int enq_restrict(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
+  k_restrict<<<ctx->nsub, NTHR, 0, s>>>(ctx->d_sub_idxoff, ctx->d_idx, ctx->d_nint, ctx->d_zoff,
+                                        ctx->d_kcnt, ctx->d_cstart, ctx->d_Z, r,
+                                        ctx->xloc + ctx->coarse_xoff, done);
+  CKL();
+  return TLS_OK;
+}
+
+template <int MODE, int DOT>
+static int enq_prolong(tls_ctx* ctx, cudaStream_t s, const double* qv, const double* wv,
+                       const double* rdot, double* z, const int* done) {
+  k_prolong<MODE, DOT><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->d_pull_ptr, ctx->d_pull_pos, ctx->yloc,
+                                               ctx->d_zrow, ctx->d_zk, ctx->d_zc, ctx->d_Z,
+                                               ctx->yloc + ctx->coarse_xoff, qv, wv, rdot, z,
+                                               ctx->part, done);
+  CKL();
+  return TLS_OK;
+}
+
+static bool has_coarse(const tls_ctx* ctx) { return ctx->ncoarse > 0 && ctx->combine != TLS_NONE; }
+
+// z = M^{-1} r (src/precond.py:128-136).  dot: partial r.z into ctx->part (G partials).
+static int enq_apply(tls_ctx* ctx, cudaStream_t s, const double* r, double* z, bool dot,
+                     const int* done) {
+  if (!has_coarse(ctx)) {
+    TRY(enq_gather(ctx, s, r, done));
+    TRY(enq_solve(ctx, s, L_LOCAL, done));
+    return dot ? enq_prolong<0, 1>(ctx, s, nullptr, nullptr, r, z, done)
+               : enq_prolong<0, 0>(ctx, s, nullptr, nullptr, r, z, done);
+  }
+  if (ctx->combine == TLS_ADDITIVE) {
+    TRY(enq_gather(ctx, s, r, done));
+    TRY(enq_restrict(ctx, s, r, done));
+    TRY(enq_solve(ctx, s, L_ALL, done));
+    return dot ? enq_prolong<1, 1>(ctx, s, nullptr, nullptr, r, z, done)
+               : enq_prolong<1, 0>(ctx, s, nullptr, nullptr, r, z, done);
+  }
+  // deflated: q = Q r; w = M1 (r - A q); z = q + w - Q A w
+  TRY(enq_restrict(ctx, s, r, done));
+  TRY(enq_solve(ctx, s, L_COARSE, done));
+  TRY(enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t1, done));
+  TRY((spmv_lpr<1, 0>(ctx, s, ctx->t1, ctx->t2, r, nullptr, done)));
+  TRY(enq_gather(ctx, s, ctx->t2, done));
+  TRY(enq_solve(ctx, s, L_LOCAL, done));
+  TRY(enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t3, done));
+  TRY((spmv_lpr<0, 0>(ctx, s, ctx->t3, ctx->t4, nullptr, nullptr, done)));
+  TRY(enq_restrict(ctx, s, ctx->t4, done));
+  TRY(enq_solve(ctx, s, L_COARSE, done));
+  return dot ? enq_prolong<3, 1>(ctx, s, ctx->t1, ctx->t3, r, z, done)
+             : enq_prolong<3, 0>(ctx, s, ctx->t1, ctx->t3, r, z, done);
+}
+
+static int enq_identity(tls_ctx* ctx, cudaStream_t s, const double* r, double* z, bool dot,
+                        const int* done) {
+  if (dot)
+    k_copy_dot<1><<<ctx->G, NTHR, 0, s>>>(ctx->n, r, z, ctx->part, done);
+  else
+    k_copy_dot<0><<<ctx->G, NTHR, 0, s>>>(ctx->n, r, z, ctx->part, done);
+  CKL();
+  return TLS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------------------------
+extern "C" {
+
+int32_t tls_abi_version(void) { return TLS_ABI_VERSION; }
+
+int32_t tls_ctx_create(int32_t device, tls_ctx** out) {
+  if (!out) return TLS_ERR_ARG;
+  *out = nullptr;
+  tls_ctx* ctx = new tls_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&ctx->h_flag, sizeof(int) * 4);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return TLS_ERR_CUDA;
+  }
+  if (cudaMalloc((void**)&ctx->pcg, sizeof(PcgState)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->gm, sizeof(GmState)) != cudaSuccess) {
+    delete ctx;
+    return TLS_ERR_OOM;
+  }
+  *out = ctx;
+  return TLS_OK;
+}
+
+void tls_ctx_destroy(tls_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  destroy_graphs(ctx);
+  dfree(ctx->rowptr); dfree(ctx->col); dfree(ctx->val);
+  dfree(ctx->d_sub_idxoff); dfree(ctx->d_sub_n); dfree(ctx->d_idx); dfree(ctx->d_nint);
+  dfree(ctx->d_blk); dfree(ctx->tiles); dfree(ctx->d_Z); dfree(ctx->ctiles); dfree(ctx->d_zoff);
+  dfree(ctx->d_kcnt); dfree(ctx->d_cstart); dfree(ctx->d_units); dfree(ctx->d_outs); dfree(ctx->d_red);
+  dfree(ctx->d_gidx); dfree(ctx->d_pull_ptr); dfree(ctx->d_pull_pos); dfree(ctx->d_zrow);
+  dfree(ctx->d_zk); dfree(ctx->d_zc); dfree(ctx->xloc); dfree(ctx->yloc); dfree(ctx->slots);
+  double** vecs[] = {&ctx->t1, &ctx->t2, &ctx->t3, &ctx->t4, &ctx->t5, &ctx->t6, &ctx->t7, &ctx->vb,
+                     &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz, &ctx->hist, &ctx->part,
+                     &ctx->V, &ctx->H, &ctx->cs, &ctx->sn, &ctx->gv, &ctx->yv, &ctx->h1, &ctx->h2};
+  for (double** v : vecs) dfree(*v);
+  dfree(ctx->pcg); dfree(ctx->gm);
+  if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+  if (ctx->h_x) cudaFreeHost(ctx->h_x);
+  dfree(ctx->ab);
+  if (ctx->cap) cudaStreamDestroy(ctx->cap);
+  delete ctx;
+}
+
+const char* tls_ctx_last_error(const tls_ctx* ctx) { return ctx ? ctx->err.c_str() : "null handle"; }
+
+int64_t tls_ctx_device_bytes(const tls_ctx* ctx) { return ctx ? ctx->dev_bytes : 0; }
+
+int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_t* indptr,
+                          const int32_t* indices, const double* data, int32_t symmetric) {
+  if (!ctx || nrows <= 0 || nrows > INT32_MAX || nnz < 0 || nnz >= INT32_MAX)
+    return ctx ? fail(ctx, TLS_ERR_ARG, "matrix size out of the supported int32 range") : TLS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  ctx->n = (int)nrows;
+  ctx->nnz = nnz;
+  ctx->sym = symmetric ? 1 : 0;
+  std::vector<int> rp(nrows + 1);
+  for (int64_t i = 0; i <= nrows; ++i) rp[i] = (int)indptr[i];
+  TRY(upload(ctx, ctx->rowptr, rp.data(), nrows + 1));
+  TRY(upload(ctx, ctx->col, indices, nnz));
+  TRY(upload(ctx, ctx->val, data, nnz));
+  const double avg = nrows ? (double)nnz / (double)nrows : 1.0;
+  int l = 2;
+  while (l < 32 && l < avg) l *= 2;
+  ctx->lpr = l;
+  ctx->G = grid_for(nrows, NTHR);
+  ctx->Gs = grid_for(nrows, NTHR / l);
+  const int64_t need = std::max<int64_t>(ctx->G, ctx->Gs);
+  if (need > ctx->part_cap) {
+    TRY(dalloc(ctx, ctx->part, need));
+    ctx->part_cap = need;
+  }
+  double** vecs[] = {&ctx->t1, &ctx->t2, &ctx->t3, &ctx->t4, &ctx->t5, &ctx->t6, &ctx->t7,
+                     &ctx->vb, &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz};
+  for (double** v : vecs) TRY(dalloc(ctx, *v, nrows));
+  if (ctx->h_x) cudaFreeHost(ctx->h_x);
+  CK(cudaMallocHost((void**)&ctx->h_x, sizeof(double) * nrows));
+  destroy_graphs(ctx);
+  ctx->finalized = false;
+  return TLS_OK;
+}
+
+int32_t tls_spmv(tls_ctx* ctx, const double* x, double* y, void* stream) {
+  if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "no matrix uploaded") : TLS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  return spmv_lpr<0, 0>(ctx, (cudaStream_t)stream, x, y, nullptr, nullptr, nullptr);
+}
+
+int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub, const int64_t* offsets,
+                              const int64_t* indices, const int32_t* n_interior) {
+  if (!ctx || n_sub <= 0) return ctx ? fail(ctx, TLS_ERR_ARG, "n_sub must be positive") : TLS_ERR_ARG;
+  if (!ctx->rowptr) return fail(ctx, TLS_ERR_STATE, "upload the matrix first");
+  CK(cudaSetDevice(ctx->device));
+  ctx->nsub = n_sub;
+  ctx->h_off.assign(offsets, offsets + n_sub + 1);
+  const int64_t tot = offsets[n_sub];
+  ctx->h_idx.resize(tot);
+  for (int64_t i = 0; i < tot; ++i) {
+    if (indices[i] < 0 || indices[i] >= ctx->n) return fail(ctx, TLS_ERR_DIM, "subdomain index out of range");
+    ctx->h_idx[i] = (int)indices[i];
+  }
+  ctx->h_n.resize(n_sub);
+  ctx->h_nint.assign(n_interior, n_interior + n_sub);
+  ctx->max_n = 0;
+  std::vector<long long> idxoff(n_sub);
+  for (int s = 0; s < n_sub; ++s) {
+    ctx->h_n[s] = (int)(offsets[s + 1] - offsets[s]);
+    idxoff[s] = offsets[s];
+    ctx->max_n = std::max(ctx->max_n, ctx->h_n[s]);
+  }
+  TRY(upload(ctx, ctx->d_sub_idxoff, idxoff.data(), n_sub));
+  TRY(upload(ctx, ctx->d_idx, ctx->h_idx.data(), tot));
+  TRY(upload(ctx, ctx->d_sub_n, ctx->h_n.data(), n_sub));
+  TRY(upload(ctx, ctx->d_nint, ctx->h_nint.data(), n_sub));
+  // tile storage for the local inverses: packed lower triangle (symmetric) or full
+  ctx->h_blk.assign(n_sub + 1, BlkDesc{});
+  int64_t tiles = 0;
+  long long xo = 0;
+  std::vector<int64_t> tbase(n_sub);
+  for (int s = 0; s < n_sub; ++s) {
+    const int nt = (ctx->h_n[s] + TT - 1) / TT;
+    tbase[s] = tiles;
+    tiles += ctx->sym ? (int64_t)nt * (nt + 1) / 2 : (int64_t)nt * nt;
+    ctx->h_blk[s].n = ctx->h_n[s];
+    ctx->h_blk[s].nt = nt;
+    ctx->h_blk[s].sym = ctx->sym;
+    ctx->h_blk[s].xoff = xo;
+    xo += (long long)nt * TT;
+  }
+  ctx->Xloc = xo;
+  ctx->tile_doubles = tiles * TT * TT;
+  dfree(ctx->tiles);
+  TRY(dalloc(ctx, ctx->tiles, ctx->tile_doubles));
+  for (int s = 0; s < n_sub; ++s) ctx->h_blk[s].tiles = ctx->tiles + tbase[s] * TT * TT;
+  TRY(upload(ctx, ctx->d_blk, ctx->h_blk.data(), n_sub + 1));
+  ctx->stored.assign(n_sub, 0);
+  ctx->ncoarse = 0;
+  ctx->finalized = false;
+  destroy_graphs(ctx);
+  return TLS_OK;
+}
+
+int32_t tls_subdomain_max_size(const tls_ctx* ctx) { return ctx ? ctx->max_n : 0; }
+
+int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first, int32_t count, double* out, int64_t ld,
+                           void* stream) {
+  if (!ctx || first < 0 || count <= 0 || first + count > ctx->nsub)
+    return ctx ? fail(ctx, TLS_ERR_ARG, "bad subdomain range") : TLS_ERR_ARG;
+  for (int s = first; s < first + count; ++s)
+    if (ctx->h_n[s] > ld) return fail(ctx, TLS_ERR_ARG, "ld smaller than a local block");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int* loc = nullptr;
+  CK(cudaMallocAsync((void**)&loc, sizeof(int) * (size_t)count * ctx->n, s));
+  CK(cudaMemsetAsync(loc, 0xff, sizeof(int) * (size_t)count * ctx->n, s));
+  CK(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)count * ld * ld, s));
+  dim3 g1(grid_for(ctx->max_n, NTHR) / 4 + 1, count);
+  k_loc_map<<<g1, NTHR, 0, s>>>(count, ctx->d_sub_idxoff, ctx->d_sub_n, ctx->d_idx, first, ctx->n, loc);
+  CKL();
+  dim3 g2(std::max<int>(1, (int)std::min<int64_t>((ld + 7) / 8, 4096)), count);
+  k_extract<<<g2, NTHR, 0, s>>>(count, ctx->d_sub_idxoff, ctx->d_sub_n, ctx->d_idx, first, ctx->n,
+                                loc, ctx->rowptr, ctx->col, ctx->val, out, ld);
+  CKL();
+  CK(cudaFreeAsync(loc, s));
+  return TLS_OK;
+}
+
+int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first, int32_t count, const double* inv,
+                                int64_t ld, void* stream) {
+  if (!ctx || first < 0 || count <= 0 || first + count > ctx->nsub)
+    return ctx ? fail(ctx, TLS_ERR_ARG, "bad subdomain range") : TLS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 g(512, count);
+  k_pack_tiles<<<g, NTHR, 0, s>>>(ctx->d_blk, first, inv, ld, ld * ld);
+  CKL();
+  for (int i = first; i < first + count; ++i) ctx->stored[i] = 1;
+  ctx->finalized = false;
+  return TLS_OK;
+}
+
+int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, const double* basis,
+                          const double* a0inv, void* stream) {
+  if (!ctx || !ctx->nsub) return ctx ? fail(ctx, TLS_ERR_STATE, "upload subdomains first") : TLS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->finalized = false;
+  destroy_graphs(ctx);
+  if (n_coarse <= 0 || !k) {
+    ctx->ncoarse = 0;
+    return TLS_OK;
+  }
+  ctx->h_k.assign(k, k + ctx->nsub);
+  ctx->h_cstart.resize(ctx->nsub);
+  ctx->h_zoff.resize(ctx->nsub);
+  int c = 0;
+  long long zo = 0;
+  for (int i = 0; i < ctx->nsub; ++i) {
+    ctx->h_cstart[i] = c;
+    ctx->h_zoff[i] = zo;
+    c += ctx->h_k[i];
+    zo += (long long)ctx->h_nint[i] * ctx->h_k[i];
+  }
+  if (c != n_coarse) return fail(ctx, TLS_ERR_ARG, "sum of k differs from n_coarse");
+  ctx->ncoarse = n_coarse;
+  TRY(dalloc(ctx, ctx->d_Z, zo));
+  if (zo) CK(cudaMemcpyAsync(ctx->d_Z, basis, sizeof(double) * zo, cudaMemcpyDeviceToDevice, s));
+  TRY(upload(ctx, ctx->d_zoff, ctx->h_zoff.data(), ctx->nsub));
+  TRY(upload(ctx, ctx->d_kcnt, ctx->h_k.data(), ctx->nsub));
+  TRY(upload(ctx, ctx->d_cstart, ctx->h_cstart.data(), ctx->nsub));
+  // coarse operator tiles (block index nsub)
+  BlkDesc cb{};
+  cb.n = n_coarse;
+  cb.nt = (n_coarse + TT - 1) / TT;
+  cb.sym = ctx->sym;
+  cb.xoff = ctx->Xloc;
+  const int64_t ntiles = cb.sym ? (int64_t)cb.nt * (cb.nt + 1) / 2 : (int64_t)cb.nt * cb.nt;
+  TRY(dalloc(ctx, ctx->ctiles, ntiles * TT * TT));
+  cb.tiles = ctx->ctiles;
+  ctx->h_blk[ctx->nsub] = cb;
+  CK(cudaMemcpy(ctx->d_blk, ctx->h_blk.data(), sizeof(BlkDesc) * (ctx->nsub + 1), cudaMemcpyHostToDevice));
+  dim3 g(512, 1);
+  k_pack_tiles<<<g, NTHR, 0, s>>>(ctx->d_blk, ctx->nsub, a0inv, n_coarse, 0);
+  CKL();
+  return TLS_OK;
+}
+
+// Units and reduction lists for one block (see k_symv_tiles).
+static void plan_block(int blk, int nt, int sym, int& slot, std::vector<Unit>& units,
+                       std::vector<OutTile>& outs, std::vector<int>& red) {
+  const int np = (nt + UR - 1) / UR, nq = (nt + UW - 1) / UW;
+  std::vector<int> uid((size_t)np * nq, -1);
+  std::vector<int> uslot((size_t)np * nq, -1);
+  for (int p = 0; p < np; ++p)
+    for (int q = 0; q < (sym ? p + 1 : nq); ++q) {
+      uslot[(size_t)p * nq + q] = slot;
+      units.push_back(Unit{blk, p, q, slot});
+      slot += SLOTS_PER_UNIT;
+    }
+  for (int J = 0; J < nt; ++J) {
+    OutTile ot{blk, J, (int)red.size(), 0};
+    const int p = J / UR;
+    for (int q = 0; q < (sym ? p + 1 : nq); ++q) red.push_back(uslot[(size_t)p * nq + q] + (J - p * UR));
+    if (sym) {
+      const int q = J / UW;
+      for (int pp = q; pp < np; ++pp) {
+        const int imax = std::min((pp + 1) * UR, nt) - 1;
+        if (imax > J) red.push_back(uslot[(size_t)pp * nq + q] + UR + (J - q * UW));
+      }
+    }
+    ot.end = (int)red.size();
+    outs.push_back(ot);
+  }
+}
+
+int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
+  if (!ctx || !ctx->nsub) return ctx ? fail(ctx, TLS_ERR_STATE, "upload subdomains first") : TLS_ERR_ARG;
+  if (one_level != TLS_ASM && one_level != TLS_RAS) return fail(ctx, TLS_ERR_ARG, "unknown one-level kind");
+  if (combine < TLS_NONE || combine > TLS_DEFLATED) return fail(ctx, TLS_ERR_ARG, "unknown combination");
+  for (int s = 0; s < ctx->nsub; ++s)
+    if (!ctx->stored[s]) return fail(ctx, TLS_ERR_STATE, "local inverse of subdomain " + std::to_string(s) + " missing");
+  CK(cudaSetDevice(ctx->device));
+  ctx->one_level = one_level;
+  ctx->combine = ctx->ncoarse > 0 ? combine : TLS_NONE;
+  const int nsub = ctx->nsub, n = ctx->n;
+  // padded local layout
+  std::vector<int> gidx(ctx->Xloc, -1);
+  for (int s = 0; s < nsub; ++s)
+    for (int l = 0; l < ctx->h_n[s]; ++l) gidx[ctx->h_blk[s].xoff + l] = ctx->h_idx[ctx->h_off[s] + l];
+  TRY(upload(ctx, ctx->d_gidx, gidx.data(), ctx->Xloc));
+  ctx->coarse_xoff = ctx->Xloc;
+  ctx->X = ctx->Xloc + (ctx->ncoarse > 0 ? (long long)ctx->h_blk[nsub].nt * TT : 0);
+  TRY(dalloc(ctx, ctx->xloc, ctx->X));
+  TRY(dalloc(ctx, ctx->yloc, ctx->X));
+  CK(cudaMemset(ctx->xloc, 0, sizeof(double) * ctx->X));
+  CK(cudaMemset(ctx->yloc, 0, sizeof(double) * ctx->X));
+  // work units + reduction lists
+  std::vector<Unit> units;
+  std::vector<OutTile> outs;
+  std::vector<int> red;
+  int slot = 0;
+  ctx->algo_local = 0.0;
+  for (int s = 0; s < nsub; ++s) {
+    plan_block(s, ctx->h_blk[s].nt, ctx->sym, slot, units, outs, red);
+    const double ns = ctx->h_n[s];
+    ctx->algo_local += ctx->sym ? 8.0 * ns * (ns + 1) / 2 + 8.0 * ns : 8.0 * ns * ns + 8.0 * ns;
+  }
+  ctx->nu_local = (int)units.size();
+  ctx->no_local = (int)outs.size();
+  ctx->nu_coarse = ctx->no_coarse = 0;
+  ctx->algo_coarse = 0.0;
+  if (ctx->ncoarse > 0) {
+    plan_block(nsub, ctx->h_blk[nsub].nt, ctx->sym, slot, units, outs, red);
+    ctx->nu_coarse = (int)units.size() - ctx->nu_local;
+    ctx->no_coarse = (int)outs.size() - ctx->no_local;
+    const double nc = ctx->ncoarse;
+    ctx->algo_coarse = ctx->sym ? 8.0 * nc * (nc + 1) / 2 + 8.0 * nc : 8.0 * nc * nc + 8.0 * nc;
+  }
+  TRY(upload(ctx, ctx->d_units, units.data(), (int64_t)units.size()));
+  TRY(upload(ctx, ctx->d_outs, outs.data(), (int64_t)outs.size()));
+  TRY(upload(ctx, ctx->d_red, red.data(), (int64_t)red.size()));
+  ctx->nslots = slot;
+  TRY(dalloc(ctx, ctx->slots, (int64_t)slot * TT));
+  // prolongation pull map: contributions to node g in ascending subdomain order (np.add.at)
+  std::vector<int> cnt(n + 1, 0);
+  for (int s = 0; s < nsub; ++s) {
+    const int lim = one_level == TLS_RAS ? ctx->h_nint[s] : ctx->h_n[s];
+    for (int l = 0; l < lim; ++l) cnt[ctx->h_idx[ctx->h_off[s] + l] + 1]++;
+  }
+  for (int g = 0; g < n; ++g) cnt[g + 1] += cnt[g];
+  std::vector<int> pos(cnt[n]);
+  std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+  for (int s = 0; s < nsub; ++s) {
+    const int lim = one_level == TLS_RAS ? ctx->h_nint[s] : ctx->h_n[s];
+    for (int l = 0; l < lim; ++l) {
+      const int g = ctx->h_idx[ctx->h_off[s] + l];
+      pos[fill[g]++] = (int)(ctx->h_blk[s].xoff + l);
+    }
+  }
+  TRY(upload(ctx, ctx->d_pull_ptr, cnt.data(), n + 1));
+  TRY(upload(ctx, ctx->d_pull_pos, pos.data(), (int64_t)pos.size()));
+  // coarse prolongation rows: node g in the interior of s at position p -> Z_s[p, :]
+  std::vector<long long> zrow(n, -1);
+  std::vector<int> zk(n, 0), zc(n, 0);
+  if (ctx->ncoarse > 0) {
+    for (int s = 0; s < nsub; ++s) {
+      if (ctx->h_k[s] == 0) continue;
+      for (int p = 0; p < ctx->h_nint[s]; ++p) {
+        const int g = ctx->h_idx[ctx->h_off[s] + p];
+        zrow[g] = ctx->h_zoff[s] + (long long)p * ctx->h_k[s];
+        zk[g] = ctx->h_k[s];
+        zc[g] = ctx->h_cstart[s];
+      }
+    }
+  } else {
+    TRY(dalloc(ctx, ctx->d_Z, 1));
+  }
+  TRY(upload(ctx, ctx->d_zrow, zrow.data(), n));
+  TRY(upload(ctx, ctx->d_zk, zk.data(), n));
+  TRY(upload(ctx, ctx->d_zc, zc.data(), n));
+  if (ctx->ncoarse == 0) {
+    std::vector<int> zero(nsub, 0);
+    std::vector<long long> zero64(nsub, 0);
+    TRY(upload(ctx, ctx->d_kcnt, zero.data(), nsub));
+    TRY(upload(ctx, ctx->d_cstart, zero.data(), nsub));
+    TRY(upload(ctx, ctx->d_zoff, zero64.data(), nsub));
+  }
+  destroy_graphs(ctx);
+  CK(cudaDeviceSynchronize());
+  ctx->finalized = true;
+  return TLS_OK;
+}
+
+static int need_final(tls_ctx* ctx) {
+  if (!ctx) return TLS_ERR_ARG;
+  if (!ctx->finalized) return fail(ctx, TLS_ERR_STATE, "preconditioner not finalized");
+  return TLS_OK;
+}
+
+int32_t tls_precond_apply(tls_ctx* ctx, const double* r, double* z, void* stream) {
+  TRY(need_final(ctx));
+  CK(cudaSetDevice(ctx->device));
+  return enq_apply(ctx, (cudaStream_t)stream, r, z, false, nullptr);
+}
+
+int32_t tls_apply_one_level(tls_ctx* ctx, const double* r, double* z, void* stream) {
+  TRY(need_final(ctx));
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enq_gather(ctx, s, r, nullptr));
+  TRY(enq_solve(ctx, s, L_LOCAL, nullptr));
+  return enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, z, nullptr);
+}
+
+int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream) {
+  TRY(need_final(ctx));
+  if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "no coarse space");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(enq_restrict(ctx, s, r, nullptr));
+  TRY(enq_solve(ctx, s, L_COARSE, nullptr));
+  return enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, z, nullptr);
+}
+
+// ---------------------------------------------------------------------------------------------
+// PCG (src/krylov.py:58-107)
+// ---------------------------------------------------------------------------------------------
+static int enq_pcg_iter(tls_ctx* ctx, cudaStream_t s, bool replace, bool prec) {
+  PcgState* st = ctx->pcg;
+  const int* done = &st->done;
+  TRY((spmv_lpr<0, 1>(ctx, s, ctx->vp, ctx->vap, nullptr, ctx->part, done)));
+  k_pcg_alpha<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->ab);
+  CKL();
+  if (!replace) {
+    k_pcg_update<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, ctx->vx, ctx->vr, ctx->vp, ctx->vap, ctx->part, 1);
+    CKL();
+    k_pcg_hist<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->G, ctx->hist);
+    CKL();
+  } else {
+    k_pcg_update<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, ctx->vx, ctx->vr, ctx->vp, ctx->vap, ctx->part, 0);
+    CKL();
+    TRY((spmv_lpr<1, 2>(ctx, s, ctx->vx, ctx->vr, ctx->vb, ctx->part, done)));
+    k_pcg_hist<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->hist);
+    CKL();
+  }
+  if (prec)
+    TRY(enq_apply(ctx, s, ctx->vr, ctx->vz, true, done));
+  else
+    TRY(enq_identity(ctx, s, ctx->vr, ctx->vz, true, done));
+  k_pcg_beta<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->G, ctx->ab);
+  CKL();
+  k_pcg_pupdate<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, ctx->vp, ctx->vz);
+  CKL();
+  return TLS_OK;
+}
+
+static int ensure_hist(tls_ctx* ctx, int maxit) {
+  if (maxit + 2 > ctx->hist_cap) {
+    TRY(dalloc(ctx, ctx->hist, maxit + 2));
+    TRY(dalloc(ctx, ctx->ab, 2 * (int64_t)maxit + 4));
+    destroy_graphs(ctx);
+    ctx->hist_cap = maxit + 2;
+  }
+  return TLS_OK;
+}
+
+int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t maxit,
+                int32_t use_precond, double* history, double* coeffs, tls_status* st_out,
+                tls_iter_cb cb, void* user, void* stream) {
+  if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "no matrix uploaded") : TLS_ERR_ARG;
+  if (use_precond) TRY(need_final(ctx));
+  if (maxit < 0) return fail(ctx, TLS_ERR_ARG, "maxit must be non-negative");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool prec = use_precond != 0;
+  const int n = ctx->n;
+  TRY(ensure_hist(ctx, maxit));
+  const int launches0 = ctx->launches;
+  tls_status stt{};
+  // init: x = 0, r = b, ||b||
+  CK(cudaMemcpyAsync(ctx->vb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(ctx->vr, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemsetAsync(ctx->vx, 0, sizeof(double) * n, s));
+  PcgState h{};
+  h.tol = tol;
+  h.maxit = maxit;
+  CK(cudaMemcpyAsync(ctx->pcg, &h, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+  k_dot<<<ctx->G, NTHR, 0, s>>>(n, ctx->vb, ctx->vb, ctx->part, nullptr);
+  CKL();
+  k_pcg_init<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
+  CKL();
+  CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h.bnorm == 0.0) {  // src/krylov.py:69-70
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    CK(cudaStreamSynchronize(s));
+    history[0] = 0.0;
+    stt.iterations = 0;
+    stt.converged = 1;
+    stt.gpu_launches = ctx->launches - launches0;
+    if (st_out) *st_out = stt;
+    return TLS_OK;
+  }
+  const double one = 1.0;
+  CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+  if (prec)
+    TRY(enq_apply(ctx, s, ctx->vr, ctx->vz, true, nullptr));
+  else
+    TRY(enq_identity(ctx, s, ctx->vr, ctx->vz, true, nullptr));
+  k_pcg_rz0<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->vp, ctx->vz, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (maxit > 0) {
+    if (cb) {
+      // per-iteration host loop (callback(it, x.copy()), src/krylov.py:92-93)
+      for (int it = 1; it <= maxit; ++it) {
+        TRY(enq_pcg_iter(ctx, s, it % PCG_GRAPH_ITERS == 0, prec));
+        CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (h.status == 2) break;
+        CK(cudaMemcpy(ctx->h_x, ctx->vx, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        cb(user, h.it, ctx->h_x);
+        if (h.done) break;
+      }
+    } else {
+      const int gi = prec ? 1 : 0;
+      if (!ctx->pcg_exec[gi]) {
+        const int before = ctx->launches;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal));
+        int rc = TLS_OK;
+        for (int i = 1; i <= PCG_GRAPH_ITERS && rc == TLS_OK; ++i)
+          rc = enq_pcg_iter(ctx, ctx->cap, i == PCG_GRAPH_ITERS, prec);
+        cudaError_t ec = cudaStreamEndCapture(ctx->cap, &graph);
+        if (rc != TLS_OK) return rc;
+        if (ec != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+        CK(cudaGraphInstantiate(&ctx->pcg_exec[gi], graph, 0));
+        cudaGraphDestroy(graph);
+        ctx->pcg_exec_launches[gi] = ctx->launches - before;
+        ctx->launches = before;
+      }
+      const int max_launch = (maxit + PCG_GRAPH_ITERS - 1) / PCG_GRAPH_ITERS;
+      for (int L = 0; L < max_launch; ++L) {
+        CK(cudaGraphLaunch(ctx->pcg_exec[gi], s));
+        ctx->launches += ctx->pcg_exec_launches[gi];
+        CK(cudaMemcpyAsync(ctx->h_flag, &ctx->pcg->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (ctx->h_flag[0]) break;
+      }
+    }
+  }
+  CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  const int its = h.it;
+  CK(cudaMemcpy(history, ctx->hist, sizeof(double) * (its + 1), cudaMemcpyDeviceToHost));
+  if (coeffs && its > 0) CK(cudaMemcpy(coeffs, ctx->ab, sizeof(double) * 2 * its, cudaMemcpyDeviceToHost));
+  stt.iterations = its;
+  stt.converged = h.converged;
+  stt.gpu_launches = ctx->launches - launches0;
+  if (h.status == 2) {
+    stt.code = TLS_ERR_BREAKDOWN;
+    stt.iteration = h.bad_it;
+    stt.value = h.bad_val;
+    if (st_out) *st_out = stt;
+    char buf[128];
+    snprintf(buf, sizeof buf, "non-positive curvature %.3e at iteration %d; matrix is not SPD", h.bad_val, h.bad_it);
+    return fail(ctx, TLS_ERR_BREAKDOWN, buf);
+  }
+  if (st_out) *st_out = stt;
+  return TLS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// GMRES (src/krylov.py:127-195) + GMRES(m) restarts
+// ---------------------------------------------------------------------------------------------
+static int enq_gm_step(tls_ctx* ctx, cudaStream_t s, int j, bool prec) {
+  GmState* st = ctx->gm;
+  const int* stop = &st->cycle_stop;
+  const long long ldv = ctx->n;
+  const double* vj = ctx->V + (long long)j * ldv;
+  double* w = ctx->t6;
+  if (prec) {
+    TRY(enq_apply(ctx, s, vj, ctx->t5, false, stop));
+    TRY((spmv_lpr<0, 0>(ctx, s, ctx->t5, w, nullptr, nullptr, stop)));
+  } else {
+    TRY((spmv_lpr<0, 0>(ctx, s, vj, w, nullptr, nullptr, stop)));
+  }
+  const int nc = j + 1;
+  double* hs[2] = {ctx->h1, ctx->h2};
+  for (int pass = 0; pass < 2; ++pass) {
+    k_gm_gemvt<<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->V, ldv, nc, w, ctx->part, stop);
+    CKL();
+    k_gm_hreduce<<<nc, NTHR, 0, s>>>(ctx->part, ctx->G, hs[pass], stop);
+    CKL();
+    if (pass == 0)
+      k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->V, ldv, nc, st, hs[pass], w, ctx->part, 1, stop);
+    else
+      k_gm_gemvn<1><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->V, ldv, nc, st, hs[pass], w, ctx->part, 1, stop);
+    CKL();
+  }
+  k_gm_givens<<<1, NTHR, 0, s>>>(st, j, ctx->gm_cols + 1, ctx->H, ctx->h1, ctx->h2, ctx->part, ctx->G,
+                                 ctx->cs, ctx->sn, ctx->gv, ctx->hist);
+  CKL();
+  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, w, ctx->V + (long long)(j + 1) * ldv, 0);
+  CKL();
+  return TLS_OK;
+}
+
+static int enq_gm_cycle_end(tls_ctx* ctx, cudaStream_t s, bool prec) {
+  GmState* st = ctx->gm;
+  k_gm_trisolve<<<1, 32, 0, s>>>(st, ctx->gm_cols + 1, ctx->H, ctx->gv, ctx->yv);
+  CKL();
+  k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->V, ctx->n, -1, st, ctx->yv, ctx->t7, nullptr, 0, nullptr);
+  CKL();
+  if (prec) {
+    TRY(enq_apply(ctx, s, ctx->t7, ctx->t5, false, nullptr));
+    k_axpy1<<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->vx, ctx->t5, nullptr);
+  } else {
+    k_axpy1<<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->vx, ctx->t7, nullptr);
+  }
+  CKL();
+  k_gm_cycle_end<<<1, 32, 0, s>>>(st);
+  CKL();
+  TRY((spmv_lpr<1, 2>(ctx, s, ctx->vx, ctx->vr, ctx->vb, ctx->part, &st->done)));
+  k_gm_cycle_begin<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->gv, ctx->gm_cols);
+  CKL();
+  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, ctx->vr, ctx->V, 1);
+  CKL();
+  return TLS_OK;
+}
+
+static int ensure_gm(tls_ctx* ctx, int mcols) {
+  if (mcols == ctx->gm_cols && ctx->V) return TLS_OK;
+  const int64_t n = ctx->n;
+  TRY(dalloc(ctx, ctx->V, n * (mcols + 1)));
+  TRY(dalloc(ctx, ctx->H, (int64_t)(mcols + 1) * (mcols + 1)));
+  TRY(dalloc(ctx, ctx->cs, mcols + 1));
+  TRY(dalloc(ctx, ctx->sn, mcols + 1));
+  TRY(dalloc(ctx, ctx->gv, mcols + 2));
+  TRY(dalloc(ctx, ctx->yv, mcols + 1));
+  TRY(dalloc(ctx, ctx->h1, mcols + 1));
+  TRY(dalloc(ctx, ctx->h2, mcols + 1));
+  const int64_t need = std::max<int64_t>((int64_t)(mcols + 1) * ctx->G, ctx->Gs);
+  if (need > ctx->part_cap) {
+    TRY(dalloc(ctx, ctx->part, need));
+    ctx->part_cap = need;
+    destroy_graphs(ctx);
+  }
+  ctx->gm_cols = mcols;
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->gm_exec[i]) cudaGraphExecDestroy(ctx->gm_exec[i]);
+    ctx->gm_exec[i] = nullptr;
+  }
+  return TLS_OK;
+}
+
+int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t maxit,
+                  int32_t restart, int32_t use_precond, double* history, tls_status* st_out,
+                  tls_iter_cb cb, void* user, void* stream) {
+  if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "no matrix uploaded") : TLS_ERR_ARG;
+  if (use_precond) TRY(need_final(ctx));
+  const bool restarted = restart > 0 && restart < maxit;
+  if (!restarted && maxit > 1000) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "maxit %d exceeds the hard cap 1000", maxit);
+    return fail(ctx, TLS_ERR_CAP, buf);
+  }
+  if (restarted && restart > 1000) return fail(ctx, TLS_ERR_CAP, "restart exceeds the hard cap 1000");
+  if (maxit < 0) return fail(ctx, TLS_ERR_ARG, "maxit must be non-negative");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool prec = use_precond != 0;
+  const int n = ctx->n;
+  const int mcols = std::max(1, std::min(restarted ? restart : maxit, n));
+  TRY(ensure_gm(ctx, mcols));
+  TRY(ensure_hist(ctx, maxit));
+  const int launches0 = ctx->launches;
+  tls_status stt{};
+  GmState h{};
+  h.tol = tol;
+  h.maxit = maxit;
+  h.restart = restarted ? restart : 0;
+  h.restarted = restarted ? 1 : 0;
+  CK(cudaMemcpyAsync(ctx->gm, &h, sizeof(GmState), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->vb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(ctx->vr, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemsetAsync(ctx->vx, 0, sizeof(double) * n, s));
+  CK(cudaMemsetAsync(ctx->H, 0, sizeof(double) * (size_t)(mcols + 1) * (mcols + 1), s));
+  k_dot<<<ctx->G, NTHR, 0, s>>>(n, ctx->vb, ctx->vb, ctx->part, nullptr);
+  CKL();
+  // reuse pcg init to get ||b|| then seed the first cycle
+  k_pcg_init<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
+  CKL();
+  PcgState hp{};
+  CK(cudaMemcpyAsync(&hp, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hp.bnorm == 0.0 || maxit == 0) {  // src/krylov.py:140-141
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    CK(cudaStreamSynchronize(s));
+    history[0] = hp.bnorm == 0.0 ? 0.0 : 1.0;
+    stt.converged = hp.bnorm == 0.0;
+    stt.gpu_launches = ctx->launches - launches0;
+    if (st_out) *st_out = stt;
+    return TLS_OK;
+  }
+  h.bnorm = hp.bnorm;
+  CK(cudaMemcpyAsync(ctx->gm, &h, sizeof(GmState), cudaMemcpyHostToDevice, s));
+  k_gm_cycle_begin<<<1, NTHR, 0, s>>>(ctx->gm, ctx->part, ctx->G, ctx->gv, mcols);
+  CKL();
+  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(n, ctx->gm, ctx->vr, ctx->V, 1);
+  CKL();
+  const double one = 1.0;
+  CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+  GmState hs{};
+  if (cb) {
+    for (int guard = 0; guard <= maxit; ++guard) {
+      for (int j = 0; j < mcols; ++j) {
+        TRY(enq_gm_step(ctx, s, j, prec));
+        CK(cudaMemcpyAsync(&hs, ctx->gm, sizeof(GmState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        cb(user, hs.total + hs.k, nullptr);
+        if (hs.cycle_stop) break;
+      }
+      TRY(enq_gm_cycle_end(ctx, s, prec));
+      CK(cudaMemcpyAsync(&hs, ctx->gm, sizeof(GmState), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (hs.done) break;
+    }
+  } else {
+    const int gi = prec ? 1 : 0;
+    if (!ctx->gm_exec[gi] || ctx->gm_exec_cols[gi] != mcols) {
+      if (ctx->gm_exec[gi]) cudaGraphExecDestroy(ctx->gm_exec[gi]);
+      ctx->gm_exec[gi] = nullptr;
+      const int before = ctx->launches;
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal));
+      int rc = TLS_OK;
+      for (int j = 0; j < mcols && rc == TLS_OK; ++j) rc = enq_gm_step(ctx, ctx->cap, j, prec);
+      if (rc == TLS_OK) rc = enq_gm_cycle_end(ctx, ctx->cap, prec);
+      cudaError_t ec = cudaStreamEndCapture(ctx->cap, &graph);
+      if (rc != TLS_OK) return rc;
+      if (ec != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+      CK(cudaGraphInstantiate(&ctx->gm_exec[gi], graph, 0));
+      cudaGraphDestroy(graph);
+      ctx->gm_exec_cols[gi] = mcols;
+      ctx->gm_exec_launches[gi] = ctx->launches - before;
+      ctx->launches = before;
+    }
+    for (int guard = 0; guard <= maxit; ++guard) {
+      CK(cudaGraphLaunch(ctx->gm_exec[gi], s));
+      ctx->launches += ctx->gm_exec_launches[gi];
+      CK(cudaMemcpyAsync(ctx->h_flag, &ctx->gm->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (ctx->h_flag[0]) break;
+    }
+  }
+  CK(cudaMemcpyAsync(&hs, ctx->gm, sizeof(GmState), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemcpy(history, ctx->hist, sizeof(double) * (hs.total + 1), cudaMemcpyDeviceToHost));
+  stt.iterations = hs.total;
+  stt.converged = hs.converged;
+  stt.gpu_launches = ctx->launches - launches0;
+  if (st_out) *st_out = stt;
+  return TLS_OK;
+}
+
+int32_t tls_report(const tls_ctx* ctx, int64_t* n, int32_t* n_sub, int32_t* n_coarse, int64_t* tile_bytes) {
+  if (!ctx) return TLS_ERR_ARG;
+  if (n) *n = ctx->n;
+  if (n_sub) *n_sub = ctx->nsub;
+  if (n_coarse) *n_coarse = ctx->ncoarse;
+  if (tile_bytes) *tile_bytes = ctx->tile_doubles * 8;
+  return TLS_OK;
+}
+
+int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, double* algorithmic_bytes,
+                                void* stream) {
+  TRY(need_final(ctx));
+  if (reps <= 0) return fail(ctx, TLS_ERR_ARG, "reps must be positive");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int which = ctx->combine == TLS_ADDITIVE ? L_ALL : L_LOCAL;
+  const int u0 = 0;
+  const int nu = which == L_ALL ? ctx->nu_local + ctx->nu_coarse : ctx->nu_local;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
+  CKL();
+  CK(cudaEventRecord(e0, s));
+  for (int i = 0; i < reps; ++i) {
+    k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
+    CKL();
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (avg_ms) *avg_ms = ms / reps;
+  if (algorithmic_bytes) *algorithmic_bytes = ctx->algo_local + (which == L_ALL ? ctx->algo_coarse : 0.0);
+  return TLS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,720 @@
+// tls_kernels.cuh — sm_100a device kernels of the two-level Schwarz Krylov hot path.
+//
+// Every per-iteration operator of the reference is one of the
+// kernels below; all are HBM-bound fp64 (single right-hand side), so the design rules are
+// coalesced 128-bit loads, enough bytes in flight per SM, and fixed-shape (deterministic)
+// reductions.  File:line citations are into /root/reference/pkg/src/tlschwarz (src/...).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tls {
+
+constexpr int TT = 64;          // tile edge (64x64 fp64 = 32 KiB, column-major inside)
+constexpr int UR = 8;           // tile-rows per work unit
+constexpr int UW = 8;           // tile-cols per work unit
+constexpr int SLOTS_PER_UNIT = UR + UW;
+constexpr int NTHR = 256;
+constexpr unsigned FULL = 0xffffffffu;
+
+struct BlkDesc {                // one dense local operator (a subdomain or the coarse A0^{-1})
+  const double* tiles;          // tile (I,J) at tiles + tile_index(I,J)*TT*TT
+  long long xoff;               // offset of its local vector in xloc / yloc (multiple of TT)
+  int n, nt, sym, pad_;
+};
+struct Unit { int blk, p, q, slot; };       // tile-rows [p*UR, +UR) x tile-cols [q*UW, +UW)
+struct OutTile { int blk, J, beg, end; };   // reduce slots red[beg:end] into y tile J of blk
+
+struct PcgState {
+  double bnorm, tol, rz, alpha, beta, pap, rnorm, pad0;
+  int it, maxit, done, converged, status, bad_it, pad1, pad2;
+  double bad_val;
+};
+
+struct GmState {
+  double bnorm, tol, rn, tolc, scale, hn;
+  int m_cycle, k, total, maxit, restart, cycle_stop, done, converged, restarted, pad_;
+};
+
+__device__ __forceinline__ long long tile_index(int I, int J, int nt, int sym) {
+  return sym ? (long long)I * (I + 1) / 2 + J : (long long)I * nt + J;
+}
+
+__device__ __forceinline__ double2 ldg_stream2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// Deterministic block sum (fixed xor-butterfly then fixed warp order); result in all threads
+// of warp 0.  Must be called by all threads of the block.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nw ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  }
+  return v;
+}
+
+// Sum of np partials, fixed assignment; valid in thread 0.
+__device__ __forceinline__ double sum_partials(const double* __restrict__ p, int np, double* sh) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) v += p[i];
+  return block_sum(v, sh);
+}
+
+// ---------------------------------------------------------------------------------------
+// K1  CSR SpMV  (replaces scipy csr_matvec behind SparseMat.matvec, src/sparsemat.py:125-129)
+//   MODE 0: y = A x          MODE 1: y = b - A x       (src/krylov.py:88-89 replacement)
+//   DOT  0: none   1: partial sum x.y   2: partial sum y.y
+// LPR lanes per row, grid-stride over row groups with a fixed grid -> deterministic partials.
+// ---------------------------------------------------------------------------------------
+template <int LPR, int MODE, int DOT>
+__global__ void __launch_bounds__(NTHR) k_spmv(int n, const int* __restrict__ rowptr,
+                                               const int* __restrict__ col,
+                                               const double* __restrict__ val,
+                                               const double* __restrict__ x, double* __restrict__ y,
+                                               const double* __restrict__ b,
+                                               double* __restrict__ part, const int* done) {
+  if (done && *done) return;
+  __shared__ double sh[32];
+  const int g = threadIdx.x / LPR, gl = threadIdx.x % LPR;
+  const int rows_per_block = NTHR / LPR;
+  double dacc = 0.0;
+  for (int row0 = blockIdx.x * rows_per_block; row0 < n; row0 += gridDim.x * rows_per_block) {
+    const int row = row0 + g;
+    double s = 0.0;
+    if (row < n) {
+      const int beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+      for (int e = beg + gl; e < end; e += LPR) s += __ldg(val + e) * __ldg(x + __ldg(col + e));
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, LPR);
+    if (row < n && gl == 0) {
+      const double out = MODE == 1 ? __ldg(b + row) - s : s;
+      y[row] = out;
+      if (DOT == 1) dacc += x[row] * out;
+      if (DOT == 2) dacc += out * out;
+    }
+  }
+  if (DOT) {
+    const double t = block_sum(dacc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2  overlap restriction r_i = R_i r for every subdomain at once (src/precond.py:118,
+//     SubdomainMap.restrict src/partition.py:83-84).  gidx[p] = global row of padded local
+//     position p, -1 on padding.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHR) k_gather(long long m, const int* __restrict__ gidx,
+                                                 const double* __restrict__ r,
+                                                 double* __restrict__ xloc, const int* done) {
+  if (done && *done) return;
+  for (long long p = blockIdx.x * (long long)NTHR + threadIdx.x; p < m;
+       p += (long long)gridDim.x * NTHR) {
+    const int gi = __ldg(gidx + p);
+    xloc[p] = gi >= 0 ? __ldg(r + gi) : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K5  coarse restriction c = Z^T r (CoarseSpace.restrict, src/coarse.py:40-41).  Z is
+//     block-diagonal by subdomain with interior support (src/coarse.py:1-7): one CTA per
+//     subdomain, Z_s row-major n_int x k.  c lands in the coarse segment of xloc.
+// ---------------------------------------------------------------------------------------
+constexpr int KCH = 16;  // columns per pass
+__global__ void __launch_bounds__(NTHR) k_restrict(const long long* __restrict__ sub_idxoff,
+                                                   const int* __restrict__ idx,
+                                                   const int* __restrict__ nint,
+                                                   const long long* __restrict__ zoff,
+                                                   const int* __restrict__ kcnt,
+                                                   const int* __restrict__ cstart,
+                                                   const double* __restrict__ Z,
+                                                   const double* __restrict__ r,
+                                                   double* __restrict__ c, const int* done) {
+  if (done && *done) return;
+  __shared__ double sh[NTHR / 32][KCH];
+  const int s = blockIdx.x;
+  const int ks = kcnt[s], ni = nint[s];
+  if (ks == 0) return;
+  const int* id = idx + sub_idxoff[s];
+  const double* zs = Z + zoff[s];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k0 = 0; k0 < ks; k0 += KCH) {
+    double acc[KCH];
+#pragma unroll
+    for (int k = 0; k < KCH; ++k) acc[k] = 0.0;
+    for (int p = threadIdx.x; p < ni; p += NTHR) {
+      const double rv = __ldg(r + __ldg(id + p));
+      const double* zr = zs + (long long)p * ks + k0;
+#pragma unroll
+      for (int k = 0; k < KCH; ++k)
+        if (k0 + k < ks) acc[k] += __ldg(zr + k) * rv;
+    }
+#pragma unroll
+    for (int k = 0; k < KCH; ++k) {
+      double v = acc[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (lane == 0) sh[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < KCH && k0 + threadIdx.x < ks) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < NTHR / 32; ++w) v += sh[w][threadIdx.x];
+      c[cstart[s] + k0 + threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// 8-value transpose-reduction across a warp: returns, in every lane, the full 32-lane sum
+// of v[colsel(lane)], colsel = 4*bit4 + 2*bit3 + bit2 (9 shuffles instead of 40).
+__device__ __forceinline__ double warp_reduce8(const double (&v)[8], int lane) {
+  double w[4];
+  const bool h16 = lane & 16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double keep = h16 ? v[i + 4] : v[i], send = h16 ? v[i] : v[i + 4];
+    w[i] = keep + __shfl_xor_sync(FULL, send, 16);
+  }
+  const bool h8 = lane & 8;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double keep = h8 ? w[i + 2] : w[i], send = h8 ? w[i] : w[i + 2];
+    w[i] = keep + __shfl_xor_sync(FULL, send, 8);
+  }
+  const bool h4 = lane & 4;
+  const double keep = h4 ? w[1] : w[0], send = h4 ? w[0] : w[1];
+  double t = keep + __shfl_xor_sync(FULL, send, 4);
+  t += __shfl_xor_sync(FULL, t, 2);
+  t += __shfl_xor_sync(FULL, t, 1);
+  return t;
+}
+
+// ---------------------------------------------------------------------------------------
+// K3/K6  batched local solves y_i = A_ii^{-1} r_i and the coarse solve y = A0^{-1} c
+//   (the factor_dense solve closures src/subdomain.py:80-89 called at src/precond.py:117-118,
+//    CoarseSpace.solve_coarse src/coarse.py:46-49).
+// Each operator is stored as 64x64 fp64 tiles (column-major inside a tile); symmetric
+// operators keep only the lower triangle of tiles, so every stored byte is read ONCE per
+// apply and used twice: row partial (y_I += S_IJ x_J) and column partial (y_J += S_IJ^T x_I).
+// CTA = 8 warps; warp w owns tile columns [8w, 8w+8), lane l owns rows {2l, 2l+1}: each
+// 128-bit load instruction of a warp covers 512 contiguous bytes.  Row partials stay in
+// registers across the unit's tile-columns (one smem cross-warp sum per tile-row); column
+// partials are completed inside the warp with warp_reduce8.  Partials go to fixed slots that
+// k_reduce_tiles sums in a fixed order -> bit-reproducible.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHR, 2) k_symv_tiles(const BlkDesc* __restrict__ blks,
+                                                        const Unit* __restrict__ units,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ slots,
+                                                        const int* done) {
+  if (done && *done) return;
+  __shared__ __align__(16) double xr[UR * TT];
+  __shared__ __align__(16) double xc[UW * TT];
+  __shared__ __align__(16) double red[NTHR / 32][TT];
+  const Unit un = units[blockIdx.x];
+  const BlkDesc b = blks[un.blk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int I0 = un.p * UR, J0 = un.q * UW;
+  const int nI = min(UR, b.nt - I0), nJ = min(UW, b.nt - J0);
+  for (int t = threadIdx.x; t < UR * TT; t += NTHR) {
+    xr[t] = t < nI * TT ? x[b.xoff + (long long)I0 * TT + t] : 0.0;
+    xc[t] = t < nJ * TT ? x[b.xoff + (long long)J0 * TT + t] : 0.0;
+  }
+  __syncthreads();
+  const int c0 = warp * 8;
+  double cacc[UW];
+#pragma unroll
+  for (int j = 0; j < UW; ++j) cacc[j] = 0.0;
+  for (int i = 0; i < nI; ++i) {
+    const int I = I0 + i;
+    const double xi0 = xr[i * TT + 2 * lane], xi1 = xr[i * TT + 2 * lane + 1];
+    const int jmax = b.sym ? min(nJ, I - J0 + 1) : nJ;
+    double ra0 = 0.0, ra1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < UW; ++j) {
+      if (j < jmax) {
+        const int J = J0 + j;
+        const double* tp = b.tiles + tile_index(I, J, b.nt, b.sym) * (TT * TT) + c0 * TT + 2 * lane;
+        double2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = ldg_stream2(tp + k * TT);
+        const double2* xj2 = reinterpret_cast<const double2*>(xc + j * TT + c0);
+        double xj[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { const double2 t2 = xj2[k]; xj[2 * k] = t2.x; xj[2 * k + 1] = t2.y; }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { ra0 += v[k].x * xj[k]; ra1 += v[k].y * xj[k]; }
+        if (b.sym && J < I) {
+          double cp[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cp[k] = v[k].x * xi0 + v[k].y * xi1;
+          cacc[j] += warp_reduce8(cp, lane);
+        }
+      }
+    }
+    // cross-warp sum of the row partial of tile-row I
+    red[warp][2 * lane] = ra0;
+    red[warp][2 * lane + 1] = ra1;
+    __syncthreads();
+    if (threadIdx.x < TT) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NTHR / 32; ++w) s += red[w][threadIdx.x];
+      slots[(long long)(un.slot + i) * TT + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+  if (b.sym) {
+    const int colsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    if ((lane & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < UW; ++j)
+        if (j < nJ) slots[(long long)(un.slot + UR + j) * TT + c0 + colsel] = cacc[j];
+    }
+  }
+}
+
+// Sum the slot partials of each output tile in list order (one warp per tile).
+__global__ void __launch_bounds__(NTHR) k_reduce_tiles(const BlkDesc* __restrict__ blks,
+                                                       const OutTile* __restrict__ outs, int nout,
+                                                       const int* __restrict__ red,
+                                                       const double* __restrict__ slots,
+                                                       double* __restrict__ y, const int* done) {
+  if (done && *done) return;
+  const int o = blockIdx.x * (NTHR / 32) + (threadIdx.x >> 5);
+  if (o >= nout) return;
+  const int lane = threadIdx.x & 31;
+  const OutTile ot = outs[o];
+  double a0 = 0.0, a1 = 0.0;
+  for (int q = ot.beg; q < ot.end; ++q) {
+    const double2 v = *reinterpret_cast<const double2*>(slots + (long long)__ldg(red + q) * TT + 2 * lane);
+    a0 += v.x;
+    a1 += v.y;
+  }
+  double2* yp = reinterpret_cast<double2*>(y + blks[ot.blk].xoff + (long long)ot.J * TT + 2 * lane);
+  *yp = make_double2(a0, a1);
+}
+
+// ---------------------------------------------------------------------------------------
+// K4/K7  prolongation.  One-level part: z[g] = sum over the subdomains containing g (RAS:
+// only the owner, the Boolean PoU src/precond.py:119-120) of y_s at g, added in ascending
+// subdomain order exactly like np.add.at (src/precond.py:121) -> conflict-free pull, no
+// atomics.  Coarse part: (Z yc)[g] = Z_owner[p, :] . yc[cols] (CoarseSpace.prolong,
+// src/coarse.py:43-44).
+//   MODE 0: z = one-level          1: z = one-level + coarse  (additive, src/precond.py:132)
+//   MODE 2: z = coarse             3: z = (q + w) - coarse    (deflated, src/precond.py:134-136)
+//   DOT: partial sum rdot[g] * z[g]
+// ---------------------------------------------------------------------------------------
+template <int MODE, int DOT>
+__global__ void __launch_bounds__(NTHR) k_prolong(int n, const int* __restrict__ pull_ptr,
+                                                  const int* __restrict__ pull_pos,
+                                                  const double* __restrict__ yloc,
+                                                  const long long* __restrict__ zrow,
+                                                  const int* __restrict__ zk,
+                                                  const int* __restrict__ zc,
+                                                  const double* __restrict__ Z,
+                                                  const double* __restrict__ yc,
+                                                  const double* __restrict__ qv,
+                                                  const double* __restrict__ wv,
+                                                  const double* __restrict__ rdot,
+                                                  double* __restrict__ z, double* __restrict__ part,
+                                                  const int* done) {
+  if (done && *done) return;
+  __shared__ double sh[32];
+  double dacc = 0.0;
+  for (int g = blockIdx.x * NTHR + threadIdx.x; g < n; g += gridDim.x * NTHR) {
+    double one = 0.0, cz = 0.0;
+    if (MODE == 0 || MODE == 1) {
+      const int beg = __ldg(pull_ptr + g), end = __ldg(pull_ptr + g + 1);
+      for (int q = beg; q < end; ++q) one += __ldg(yloc + __ldg(pull_pos + q));
+    }
+    if (MODE >= 1) {
+      const long long zo = __ldg(zrow + g);
+      if (zo >= 0) {
+        const int k = __ldg(zk + g), c0 = __ldg(zc + g);
+        for (int t = 0; t < k; ++t) cz += __ldg(Z + zo + t) * __ldg(yc + c0 + t);
+      }
+    }
+    double out;
+    if (MODE == 0) out = one;
+    else if (MODE == 1) out = one + cz;
+    else if (MODE == 2) out = cz;
+    else out = (qv[g] + wv[g]) - cz;
+    z[g] = out;
+    if (DOT) dacc += rdot[g] * out;
+  }
+  if (DOT) {
+    const double t = block_sum(dacc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K8  Krylov vector kernels and scalar steps (src/krylov.py:58-107)
+// ---------------------------------------------------------------------------------------
+template <int DOT>  // z = r (precond None, src/krylov.py:52-55); DOT: partial r.z
+__global__ void __launch_bounds__(NTHR) k_copy_dot(int n, const double* __restrict__ r,
+                                                   double* __restrict__ z, double* __restrict__ part,
+                                                   const int* done) {
+  if (done && *done) return;
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) {
+    const double v = r[i];
+    z[i] = v;
+    if (DOT) acc += v * v;
+  }
+  if (DOT) {
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(NTHR) k_dot(int n, const double* __restrict__ a,
+                                              const double* __restrict__ b,
+                                              double* __restrict__ part, const int* done) {
+  if (done && *done) return;
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) acc += a[i] * b[i];
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+// PCG scalars ------------------------------------------------------------------------------
+__global__ void k_pcg_init(PcgState* st, const double* part, int np) {
+  __shared__ double sh[32];
+  const double s = sum_partials(part, np, sh);
+  if (threadIdx.x == 0) {
+    st->bnorm = sqrt(s);
+    st->it = 0;
+    st->done = st->bnorm == 0.0 ? 1 : 0;
+    st->converged = st->done;
+    st->status = 0;
+  }
+}
+__global__ void k_pcg_rz0(PcgState* st, const double* part, int np) {
+  __shared__ double sh[32];
+  const double s = sum_partials(part, np, sh);
+  if (threadIdx.x == 0) st->rz = s;
+}
+// curvature p.Ap -> alpha; BreakdownError when <= 0 (src/krylov.py:81-85)
+__global__ void k_pcg_alpha(PcgState* st, const double* part, int np, double* ab) {
+  if (st->done) return;
+  __shared__ double sh[32];
+  const double s = sum_partials(part, np, sh);
+  if (threadIdx.x == 0) {
+    st->it += 1;
+    st->pap = s;
+    if (!(s > 0.0)) {
+      st->status = 2;
+      st->bad_it = st->it;
+      st->bad_val = s;
+      st->done = 1;
+    } else {
+      st->alpha = st->rz / s;
+      ab[2 * (st->it - 1)] = st->alpha;
+    }
+  }
+}
+// x += alpha p; r -= alpha Ap; partial r.r (src/krylov.py:86-87)
+__global__ void __launch_bounds__(NTHR) k_pcg_update(int n, const PcgState* st, double* __restrict__ x,
+                                                     double* __restrict__ r,
+                                                     const double* __restrict__ p,
+                                                     const double* __restrict__ ap,
+                                                     double* __restrict__ part, int update_r) {
+  if (st->done) return;
+  __shared__ double sh[32];
+  const double alpha = st->alpha;
+  double acc = 0.0;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) {
+    x[i] += alpha * p[i];
+    if (update_r) {
+      const double rv = r[i] - alpha * ap[i];
+      r[i] = rv;
+      acc += rv * rv;
+    }
+  }
+  if (update_r) {
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+// history entry and stopping test (src/krylov.py:90-96)
+__global__ void k_pcg_hist(PcgState* st, const double* part, int np, double* hist) {
+  if (st->done) return;
+  __shared__ double sh[32];
+  const double s = sum_partials(part, np, sh);
+  if (threadIdx.x == 0) {
+    st->rnorm = sqrt(s);
+    const double h = st->rnorm / st->bnorm;
+    hist[st->it] = h;
+    if (h <= st->tol) {
+      st->converged = 1;
+      st->done = 1;
+    } else if (st->it >= st->maxit) {
+      st->done = 1;
+    }
+  }
+}
+__global__ void k_pcg_beta(PcgState* st, const double* part, int np, double* ab) {
+  if (st->done) return;
+  __shared__ double sh[32];
+  const double s = sum_partials(part, np, sh);
+  if (threadIdx.x == 0) {
+    st->beta = s / st->rz;
+    ab[2 * (st->it - 1) + 1] = st->beta;
+    st->rz = s;
+  }
+}
+// p = z + beta p (src/krylov.py:101)
+__global__ void __launch_bounds__(NTHR) k_pcg_pupdate(int n, const PcgState* st, double* __restrict__ p,
+                                                      const double* __restrict__ z) {
+  if (st->done) return;
+  const double beta = st->beta;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) p[i] = z[i] + beta * p[i];
+}
+
+// ---------------------------------------------------------------------------------------
+// GMRES (src/krylov.py:127-195): Arnoldi with classical Gram-Schmidt twice (CGS2 — the
+// reference's MGS + correction pass, src/krylov.py:157-165, to the same accuracy), Givens
+// rotations, both stopping rules, x += M^{-1} V y at the end of each cycle.
+// ---------------------------------------------------------------------------------------
+constexpr int GCH = 8;  // columns per gemv_t pass
+// part[i*G + block] = partial V[:, i] . w for i < ncols
+__global__ void __launch_bounds__(NTHR) k_gm_gemvt(int n, const double* __restrict__ V, long long ldv,
+                                                   int ncols, const double* __restrict__ w,
+                                                   double* __restrict__ part, const int* stop) {
+  if (*stop) return;
+  __shared__ double sh[NTHR / 32][GCH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < ncols; c0 += GCH) {
+    double acc[GCH];
+#pragma unroll
+    for (int k = 0; k < GCH; ++k) acc[k] = 0.0;
+    for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) {
+      const double wv = w[i];
+#pragma unroll
+      for (int k = 0; k < GCH; ++k)
+        if (c0 + k < ncols) acc[k] += V[(long long)(c0 + k) * ldv + i] * wv;
+    }
+#pragma unroll
+    for (int k = 0; k < GCH; ++k) {
+      double v = acc[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (lane == 0) sh[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < GCH && c0 + threadIdx.x < ncols) {
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < NTHR / 32; ++q) v += sh[q][threadIdx.x];
+      part[(long long)(c0 + threadIdx.x) * gridDim.x + blockIdx.x] = v;
+    }
+    __syncthreads();
+  }
+}
+// h[i] = sum_b part[i*G + b]; one block per column
+__global__ void k_gm_hreduce(const double* __restrict__ part, int G, double* __restrict__ h,
+                             const int* stop) {
+  if (*stop) return;
+  __shared__ double sh[32];
+  const double s = sum_partials(part + (long long)blockIdx.x * G, G, sh);
+  if (threadIdx.x == 0) h[blockIdx.x] = s;
+}
+// w -= V[:, :ncols] h  (ncols < 0: read the count from st->k); optional partial w.w
+template <int NORM>
+__global__ void __launch_bounds__(NTHR) k_gm_gemvn(int n, const double* __restrict__ V, long long ldv,
+                                                   int ncols, const GmState* st,
+                                                   const double* __restrict__ h,
+                                                   double* __restrict__ w, double* __restrict__ part,
+                                                   int subtract, const int* stop) {
+  if (stop && *stop) return;
+  __shared__ double sh[32];
+  const int nc = ncols >= 0 ? ncols : st->k;
+  double acc2 = 0.0;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) {
+    double s = 0.0;
+    for (int c = 0; c < nc; ++c) s += V[(long long)c * ldv + i] * __ldg(h + c);
+    const double out = subtract ? w[i] - s : s;
+    w[i] = out;
+    if (NORM) acc2 += out * out;
+  }
+  if (NORM) {
+    const double t = block_sum(acc2, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+// Hessenberg column j, rotations, residual estimate, both stopping tests (src/krylov.py:166-189)
+__global__ void k_gm_givens(GmState* st, int j, int ldh, double* __restrict__ H,
+                            const double* __restrict__ h1, const double* __restrict__ h2,
+                            const double* __restrict__ part, int np, double* __restrict__ cs,
+                            double* __restrict__ sn, double* __restrict__ g, double* __restrict__ hist) {
+  if (st->cycle_stop) return;
+  __shared__ double sh[32];
+  const double s = sum_partials(part, np, sh);
+  if (threadIdx.x != 0) return;
+  double* hc = H + (long long)j * ldh;
+  for (int i = 0; i <= j; ++i) hc[i] = h1[i] + h2[i];
+  const double hn = sqrt(s);
+  st->hn = hn;
+  hc[j + 1] = hn;
+  for (int i = 0; i < j; ++i) {
+    const double t = cs[i] * hc[i] + sn[i] * hc[i + 1];
+    hc[i + 1] = -sn[i] * hc[i] + cs[i] * hc[i + 1];
+    hc[i] = t;
+  }
+  const double den = hypot(hc[j], hc[j + 1]);
+  cs[j] = den != 0.0 ? hc[j] / den : 1.0;
+  sn[j] = den != 0.0 ? hc[j + 1] / den : 0.0;
+  hc[j] = den;
+  hc[j + 1] = 0.0;
+  g[j + 1] = -sn[j] * g[j];
+  g[j] = cs[j] * g[j];
+  st->k = j + 1;
+  const double rel = fabs(g[j + 1]) / st->rn;
+  hist[st->total + j + 1] = st->restarted ? rel * st->scale : rel;
+  if (rel <= st->tolc) {
+    st->converged = 1;
+    st->cycle_stop = 1;
+  } else if (hn <= 1e-14 * st->rn) {
+    st->converged = 1;  // happy breakdown (src/krylov.py:187-189)
+    st->cycle_stop = 1;
+  } else if (j + 1 >= st->m_cycle) {
+    st->cycle_stop = 1;
+  }
+}
+// v_{j+1} = w / hn
+__global__ void __launch_bounds__(NTHR) k_gm_scale(int n, const GmState* st, const double* __restrict__ w,
+                                                   double* __restrict__ v, int use_rn) {
+  if (!use_rn && st->cycle_stop) return;
+  const double d = use_rn ? st->rn : st->hn;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) v[i] = w[i] / d;
+}
+// y = H[:k,:k]^{-1} g[:k] (solve_triangular, src/krylov.py:191)
+__global__ void k_gm_trisolve(const GmState* st, int ldh, const double* __restrict__ H,
+                              const double* __restrict__ g, double* __restrict__ y) {
+  if (threadIdx.x != 0) return;
+  const int k = st->k;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int l = i + 1; l < k; ++l) s -= H[(long long)l * ldh + i] * y[l];
+    y[i] = s / H[(long long)i * ldh + i];
+  }
+}
+__global__ void __launch_bounds__(NTHR) k_axpy1(int n, double* __restrict__ x, const double* __restrict__ t,
+                                                const int* done) {
+  if (done && *done) return;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) x[i] += t[i];
+}
+// end of a cycle: account iterations, decide whether to restart
+__global__ void k_gm_cycle_end(GmState* st) {
+  if (threadIdx.x != 0) return;
+  st->total += st->k;
+  if (st->converged || st->total >= st->maxit || !st->restarted) st->done = 1;
+}
+// new cycle on r = b - A x: rn, tolerance rescale, V_0 = r / rn, g = rn e1
+__global__ void k_gm_cycle_begin(GmState* st, const double* part, int np, double* g, int mcols) {
+  if (st->done) return;
+  __shared__ double sh[32];
+  const double s = sum_partials(part, np, sh);
+  if (threadIdx.x != 0) return;
+  st->rn = sqrt(s);
+  if (st->rn == 0.0) {
+    st->done = 1;
+    st->converged = 1;
+    return;
+  }
+  st->tolc = st->restarted ? st->tol * st->bnorm / st->rn : st->tol;
+  st->scale = st->rn / st->bnorm;
+  int m = st->maxit - st->total;
+  if (st->restarted && st->restart < m) m = st->restart;
+  if (m > mcols) m = mcols;
+  st->m_cycle = m;
+  st->k = 0;
+  st->cycle_stop = 0;
+  for (int i = 0; i <= mcols; ++i) g[i] = 0.0;
+  g[0] = st->rn;
+}
+
+// ---------------------------------------------------------------------------------------
+// Setup kernels (src/subdomain.py:53-69 extraction; tile packing of local inverses)
+// ---------------------------------------------------------------------------------------
+__global__ void k_loc_map(int count, const long long* __restrict__ sub_idxoff,
+                          const int* __restrict__ sub_n, const int* __restrict__ idx, int first,
+                          long long n, int* __restrict__ loc) {
+  const int b = blockIdx.y;
+  const int s = first + b;
+  const int ns = sub_n[s];
+  const int* id = idx + sub_idxoff[s];
+  for (int l = blockIdx.x * NTHR + threadIdx.x; l < ns; l += gridDim.x * NTHR)
+    loc[(long long)b * n + id[l]] = l;
+}
+__global__ void k_extract(int count, const long long* __restrict__ sub_idxoff,
+                          const int* __restrict__ sub_n, const int* __restrict__ idx, int first,
+                          long long n, const int* __restrict__ loc, const int* __restrict__ rowptr,
+                          const int* __restrict__ col, const double* __restrict__ val,
+                          double* __restrict__ out, long long ld) {
+  const int b = blockIdx.y;
+  const int s = first + b;
+  const int ns = sub_n[s];
+  const int* id = idx + sub_idxoff[s];
+  const int* lb = loc + (long long)b * n;
+  double* ob = out + (long long)b * ld * ld;
+  const int warp = (blockIdx.x * NTHR + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (NTHR / 32);
+  for (int l = warp; l < (int)ld; l += nwarps) {
+    if (l >= ns) {
+      if (lane == 0) ob[(long long)l * ld + l] = 1.0;
+      continue;
+    }
+    const int g = id[l];
+    for (int e = rowptr[g] + lane; e < rowptr[g + 1]; e += 32) {
+      const int L = lb[col[e]];
+      if (L >= 0) ob[(long long)l * ld + L] = val[e];
+    }
+  }
+}
+// tile (I,J) of subdomain s <- inv[b] (row-major ld x ld), zero outside n_s
+__global__ void k_pack_tiles(const BlkDesc* __restrict__ blks, int first_blk, const double* __restrict__ inv,
+                             long long ld, long long batch_stride) {
+  const int b = blockIdx.y;
+  const BlkDesc bd = blks[first_blk + b];
+  const long long ntiles = bd.sym ? (long long)bd.nt * (bd.nt + 1) / 2 : (long long)bd.nt * bd.nt;
+  const double* src = inv + b * batch_stride;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int I, J;
+    if (bd.sym) {
+      I = (int)floor((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while ((long long)(I + 1) * (I + 2) / 2 <= t) ++I;
+      while ((long long)I * (I + 1) / 2 > t) --I;
+      J = (int)(t - (long long)I * (I + 1) / 2);
+    } else {
+      I = (int)(t / bd.nt);
+      J = (int)(t % bd.nt);
+    }
+    double* dst = const_cast<double*>(bd.tiles) + t * (TT * TT);
+    for (int e = threadIdx.x; e < TT * TT; e += NTHR) {
+      const int c = e / TT, r = e % TT;
+      const int gi = I * TT + r, gj = J * TT + c;
+      dst[e] = (gi < bd.n && gj < bd.n) ? src[(long long)gi * ld + gj] : 0.0;
+    }
+  }
+}
+
+}  // namespace tls

@@ -1,0 +1,301 @@
+"""Device setup: local operators, spectral coarse space, Galerkin coarse operator.
+
+Pipeline per batch of subdomains (all on the GPU, stream-ordered with the
+library calls):
+
+1. ``tls_extract_blocks`` gathers the dense local blocks A_ii in the
+   reference's local order (src/subdomain.py:53-69) — no DENSE_GUARD.
+2. Factor + invert (Cholesky when symmetric, pivoted LU otherwise; the same
+   failure rules as ``factor_dense``, src/subdomain.py:72-95).  The inverse
+   B_i = A_ii^{-1} is what the iteration streams (``tls_store_local_inverse``:
+   packed lower-triangular 64x64 tiles when symmetric).
+3. Coarse columns from B_i alone — no second factorisation of A_inner:
+   with ring = outermost layer, F = B[int, ring], B22 = B[ring, ring], the
+   harmonic extension is ext = B[:, ring] B22^{-1} (block-inverse identity),
+   so
+   * "gevp" (src/spectral.py:111-132): the m x m pencil (lhs on the ring block,
+     A) has the same nonzero eigenpairs as  (F^T A_II F) u = lambda B22 u
+     (n_b x n_b); the lifted column is D ext y = (B[:, ring] u) restricted to
+     the interior, A-normalised (u^T B22 u = 1) and sign-fixed on the full
+     local vector exactly as ``_fix_signs`` (src/spectral.py:59-66);
+   * "svd" (src/spectral.py:135-154): left singular vectors of
+     ext[:n_int] = F B22^{-1};
+   * "full" (src/coarse.py:66-67): all columns of ext[:n_int].
+   Top-k (``n_modes``) or threshold (``tau``, strict with the 1e-12 tie guard)
+   selection.
+4. ``rank_filter`` (src/coarse.py:119-155): per-subdomain column-pivoted QR
+   magnitudes against the global largest pivot (host LAPACK geqp3 on the
+   n_int x k blocks — bookkeeping, not on the iteration path).
+5. A0 = Z^T A Z (src/coarse.py:158-183): A Z_s = A_ii[:, :n_int] Z_s scattered
+   over the subdomain's local rows, then Z_j^T (A Z_s) per touching owner j;
+   symmetrised when symmetric; Cholesky/LU with the reference's failure rules;
+   its inverse is stored as the coarse block of the same tile kernel.
+
+Dense factorisations/eigensolves in steps 2-3/5 use torch.linalg (cuSOLVER) —
+a library call on the SETUP path; the per-iteration path is all in-tree CUDA.
+"""
+
+from __future__ import annotations
+
+import math
+import warnings
+
+import numpy as np
+import scipy.linalg as sla
+
+from . import _lib
+from .device import _torch, stream_ptr
+from .errors import SubdomainSetupError
+
+TIE_GUARD = 1e-12
+TOPK_TAU = 1e-300
+EPS = float(np.finfo(float).eps)
+
+
+class CoarseData:
+    """Device coarse space + the host bookkeeping of CoarseSpace (src/coarse.py:23-49)."""
+
+    def __init__(self, n, maps, z_blocks, counts, nnz_a00):
+        self._n = n
+        self._maps = maps
+        self._z = z_blocks            # list of host (n_int x k) arrays, kept columns
+        self.ranges = tuple(self._ranges(counts))
+        self.nnz_a00 = int(nnz_a00)
+        self._basis = None
+
+    @staticmethod
+    def _ranges(counts):
+        out, c = [], 0
+        for k in counts:
+            out.append((c, c + k))
+            c += k
+        return out
+
+    @property
+    def n_coarse(self):
+        return self.ranges[-1][1] if self.ranges else 0
+
+    def column_counts(self):
+        return tuple(e - s for s, e in self.ranges)
+
+    @property
+    def basis(self):
+        """Global basis as a SparseMat (n x n_C), built on demand on the host."""
+        if self._basis is None:
+            import scipy.sparse as sp
+            from .sparsemat import SparseMat
+            rows, cols, vals = [], [], []
+            for smap, z, (c0, _) in zip(self._maps, self._z, self.ranges):
+                if z.shape[1] == 0:
+                    continue
+                r, c = np.nonzero(z)
+                rows.append(smap.interior[r]); cols.append(c0 + c); vals.append(z[r, c])
+            if rows:
+                mat = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                                    shape=(self._n, self.n_coarse))
+            else:
+                mat = sp.csr_matrix((self._n, 0))
+            self._basis = SparseMat(mat)
+        return self._basis
+
+
+def _select(values, tau, n_modes):
+    thr = TOPK_TAU if n_modes is not None else tau
+    keep = np.nonzero(values > thr * (1.0 + TIE_GUARD))[0]
+    if n_modes is not None:
+        keep = keep[:n_modes]
+    return keep
+
+
+def _fix_signs(torch, v):
+    """Flip columns so the largest-|.| component (first occurrence) is positive."""
+    if v.shape[1] == 0:
+        return v
+    idx = torch.argmax(v.abs(), dim=0)
+    sgn = torch.where(v.gather(0, idx[None, :])[0] < 0, -1.0, 1.0).to(v.dtype)
+    return v * sgn[None, :]
+
+
+def _subdomain_columns(torch, kind, A, B, n, ni, nin, tau, n_modes):
+    """Coarse columns (n_int x k, device) of one subdomain from A_ii and B = A_ii^{-1}."""
+    nb = n - nin
+    dev = A.device
+    if nb == 0 or kind == "none":
+        return torch.zeros((ni, 0), dtype=torch.float64, device=dev)
+    F = B[:ni, nin:n]
+    B22 = B[nin:n, nin:n]
+    if kind == "gevp":
+        H = F.mT @ (A[:ni, :ni] @ F)
+        H = 0.5 * (H + H.mT)
+        B22s = 0.5 * (B22 + B22.mT)
+        C = torch.linalg.cholesky(B22s)
+        X = torch.linalg.solve_triangular(C, H, upper=False)
+        M = torch.linalg.solve_triangular(C, X.mT, upper=False)
+        M = 0.5 * (M + M.mT)
+        w, Q = torch.linalg.eigh(M)
+        w = torch.flip(w, dims=[0])
+        Q = torch.flip(Q, dims=[1])
+        sig = torch.sqrt(torch.clamp(w, min=0.0)).cpu().numpy()
+        keep = _select(sig, tau, n_modes)
+        if keep.size == 0:
+            return torch.zeros((ni, 0), dtype=torch.float64, device=dev)
+        U = torch.linalg.solve_triangular(C.mT, Q[:, torch.as_tensor(keep, device=dev)], upper=True)
+        V = B[:n, nin:n] @ U
+        V = _fix_signs(torch, V)
+        return V[:ni].contiguous()
+    E = torch.linalg.solve(B22, F, left=False)  # E B22 = F  ->  ext[:n_int]
+    if kind == "full":
+        return E.contiguous()
+    U, S, _ = torch.linalg.svd(E, full_matrices=False)
+    keep = _select(S.cpu().numpy(), tau, n_modes)
+    if keep.size == 0:
+        return torch.zeros((ni, 0), dtype=torch.float64, device=dev)
+    V = _fix_signs(torch, U[:, torch.as_tensor(keep, device=dev)])
+    return V.contiguous()
+
+
+def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_modes, drop_tol,
+                           batch=None, mem_fraction=0.35):
+    """Run steps 1-5 into ``handle``; returns CoarseData or None."""
+    torch = _torch()
+    lib = handle.lib
+    dev = torch.device("cuda", handle.device)
+    N = len(maps)
+    n_loc = np.array([m.n_local for m in maps], dtype=np.int64)
+    n_int = np.array([m.interior.size for m in maps], dtype=np.int64)
+    n_bnd = np.array([m.n_boundary for m in maps], dtype=np.int64)
+    offsets = np.concatenate([[0], np.cumsum(n_loc)]).astype(np.int64)
+    indices = np.concatenate([m.indices for m in maps]).astype(np.int64)
+    handle.check(lib.tls_subdomains_upload(handle.ctx, N, _lib.ptr(offsets), _lib.ptr(indices),
+                                           _lib.ptr(n_int.astype(np.int32))))
+    ld = int(n_loc.max())
+    if batch is None:
+        free, _ = torch.cuda.mem_get_info(dev)
+        per = 8.0 * ld * ld * 4.0 + 4.0 * csr.shape[0]
+        batch = max(1, min(N, int(mem_fraction * free / per)))
+    s_ptr = stream_ptr()
+    want_coarse = coarse != "none"
+    z_dev = [None] * N
+    w_dev = [None] * N
+    for first in range(0, N, batch):
+        cnt = min(batch, N - first)
+        A = torch.empty((cnt, ld, ld), dtype=torch.float64, device=dev)
+        handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
+        if symmetric:
+            L, info = torch.linalg.cholesky_ex(A)
+            bad = torch.nonzero(info).flatten().cpu().numpy()
+            if bad.size:
+                s = first + int(bad[0])
+                raise SubdomainSetupError(s, f"factorization failed: {int(info[bad[0]])}-th leading minor not positive")
+            Binv = torch.cholesky_inverse(L)
+            del L
+            Binv = 0.5 * (Binv + Binv.mT)
+        else:
+            LU, piv, info = torch.linalg.lu_factor_ex(A)
+            for b in range(cnt):
+                s = first + b
+                nb_ = int(n_loc[s])
+                blk = LU[b, :nb_, :nb_]
+                if int(info[b]) != 0 or float(blk.diagonal().abs().min()) <= nb_ * EPS * float(blk.abs().max()):
+                    raise SubdomainSetupError(s, "local block is numerically singular")
+            eye = torch.eye(ld, dtype=torch.float64, device=dev).expand(cnt, ld, ld)
+            Binv = torch.linalg.lu_solve(LU, piv, eye)
+            del LU, piv
+        handle.check(lib.tls_store_local_inverse(handle.ctx, first, cnt, _lib.ptr(Binv), ld, s_ptr))
+        if want_coarse:
+            for b in range(cnt):
+                s = first + b
+                n, ni = int(n_loc[s]), int(n_int[s])
+                nin = n - int(n_bnd[s])
+                Z = _subdomain_columns(torch, coarse, A[b], Binv[b], n, ni, nin, tau, n_modes)
+                # assemble_coarse_basis drops identically zero columns (src/coarse.py:99-103)
+                if Z.shape[1]:
+                    nz = torch.any(Z != 0, dim=0)
+                    if not bool(nz.all()):
+                        Z = Z[:, nz].contiguous()
+                z_dev[s] = Z
+                w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
+        del A, Binv
+    if not want_coarse:
+        torch.cuda.empty_cache()
+        return None
+    # rank filter (src/coarse.py:119-155)
+    z_host = [z.cpu().numpy() for z in z_dev]
+    pivots = []
+    for s, z in enumerate(z_host):
+        if z.shape[1] == 0:
+            continue
+        r, perm = sla.qr(z, mode="r", pivoting=True)
+        rd = np.abs(np.diag(r))
+        for j in range(z.shape[1]):
+            pivots.append((rd[j] if j < rd.size else 0.0, s, int(perm[j])))
+    keep_cols = [[] for _ in range(N)]
+    if pivots:
+        largest = max(p[0] for p in pivots)
+        for mag, s, j in pivots:
+            if mag >= drop_tol * largest:
+                keep_cols[s].append(j)
+    total = sum(len(k) for k in keep_cols)
+    if total == 0:
+        if pivots:
+            warnings.warn("rank filter removed every coarse column; coarse level disabled")
+        torch.cuda.empty_cache()
+        return CoarseData(csr.shape[0], maps, [np.zeros((int(n_int[s]), 0)) for s in range(N)],
+                          [0] * N, 0) if pivots else None
+    for s in range(N):
+        kc = sorted(keep_cols[s])
+        if len(kc) != z_host[s].shape[1]:
+            idx = torch.as_tensor(kc, dtype=torch.long, device=dev)
+            z_dev[s] = z_dev[s][:, idx].contiguous()
+            w_dev[s] = w_dev[s][:, idx].contiguous() if len(kc) else None
+            z_host[s] = z_host[s][:, kc]
+    counts = [z.shape[1] for z in z_host]
+    cstart = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    nC = int(cstart[-1])
+    # Galerkin A0 = Z^T (A Z): A Z_s lives on the local rows of s; split those rows by owner
+    owner = np.asarray(owner, dtype=np.int64)
+    posint = np.empty(csr.shape[0], dtype=np.int64)
+    for m in maps:
+        posint[m.interior] = np.arange(m.interior.size)
+    A0 = torch.zeros((nC, nC), dtype=torch.float64, device=dev)
+    for s, m in enumerate(maps):
+        if counts[s] == 0:
+            continue
+        own = owner[m.indices]
+        order = np.argsort(own, kind="stable")
+        so = own[order]
+        cuts = np.nonzero(np.diff(so))[0] + 1
+        groups = np.split(order, cuts)
+        W = w_dev[s]
+        for grp in groups:
+            j = int(own[grp[0]])
+            if counts[j] == 0:
+                continue
+            rows_j = torch.as_tensor(posint[m.indices[grp]], device=dev)
+            Zj = z_dev[j].index_select(0, rows_j)
+            Wg = W.index_select(0, torch.as_tensor(grp, device=dev))
+            A0[cstart[j]:cstart[j + 1], cstart[s]:cstart[s + 1]] += Zj.mT @ Wg
+    if symmetric:
+        A0 = 0.5 * (A0 + A0.mT)
+    nnz = int(torch.count_nonzero(A0))
+    if symmetric:
+        L, info = torch.linalg.cholesky_ex(A0)
+        if int(info) != 0:
+            raise RuntimeError(f"coarse operator is not positive definite: {int(info)}-th leading minor")
+        A0inv = torch.cholesky_inverse(L)
+        A0inv = 0.5 * (A0inv + A0inv.mT)
+        del L
+    else:
+        LU, piv, info = torch.linalg.lu_factor_ex(A0)
+        if int(info) != 0 or float(LU.diagonal().abs().min()) <= nC * EPS * float(LU.abs().max()):
+            raise RuntimeError("coarse operator is numerically singular")
+        A0inv = torch.linalg.lu_solve(LU, piv, torch.eye(nC, dtype=torch.float64, device=dev))
+        del LU, piv
+    zcat = torch.cat([z.reshape(-1) for z in z_dev]).contiguous()
+    k32 = np.asarray(counts, dtype=np.int32)
+    handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
+                                       _lib.ptr(A0inv.contiguous()), s_ptr))
+    torch.cuda.current_stream().synchronize()
+    del A0, A0inv, zcat, z_dev, w_dev
+    torch.cuda.empty_cache()
+    return CoarseData(csr.shape[0], maps, z_host, counts, nnz)

@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's golden vectors and
+the CPU oracle on the same seeded inputs.
+
+Tolerances (fp64): index sets bit-exact; preconditioner apply <= 1e-10 relative to max|z|
+(config-4 saddle point: 1e-6, its coarse operator has cond ~1e10);
+iteration counts +-1; residual histories agree to 1e-10 absolute on the relative scale
+(1e-7 for config 4); the solution agrees to 1e-8 relative (1e-4 for config 4, whose
+reported residual is not its true residual)."""
+
+import numpy as np
+import pytest
+
+from conftest import CONFIG_CASES, golden, golden_csr
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2401_03915_b200 import build
+    build.build()
+    import paper_2401_03915_b200 as mod
+    return mod
+
+
+def _tols(name):
+    return (1e-6, 1e-7, 1e-4) if name.startswith("cfg4") else (1e-10, 1e-10, 1e-8)
+
+
+_cache = {}
+
+
+def _setup(B, name):
+    if name not in _cache:
+        d = golden(name)
+        a = golden_csr(d)
+        mat = B.SparseMat(a, symmetric=bool(d["symmetric"]))
+        pre = B.setup(mat, int(d["n_sub"]), overlap=int(d["overlap"]), owner=d["owner"],
+                      coarse=str(d["coarse"]), n_modes=int(d["n_modes"]))
+        _cache[name] = (d, a, mat, pre)
+    return _cache[name]
+
+
+@pytest.mark.parametrize("name", CONFIG_CASES)
+def test_spmv_matches_csr(B, name):
+    d = golden(name)
+    a = golden_csr(d)
+    mat = B.SparseMat(a, symmetric=bool(d["symmetric"]))
+    x = np.random.default_rng(1).standard_normal(a.shape[0])
+    y = mat.matvec(x)
+    ref = a @ x
+    np.testing.assert_allclose(y, ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+    xt = torch.as_tensor(x, device="cuda")
+    yt = mat.matvec(xt)
+    assert yt.is_cuda and np.allclose(yt.cpu().numpy(), y, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("name", CONFIG_CASES)
+def test_setup_index_sets_and_report(B, name):
+    d, a, mat, pre = _setup(B, name)
+    assert np.array_equal(np.concatenate([m.indices for m in pre.maps]), d["indices"])
+    assert pre.k_c == int(d["k_c"]) and np.array_equal(pre.colors, d["colors"])
+    assert pre.report.mode_counts == tuple(d["mode_counts"])
+    assert pre.report.n_coarse == int(d["n_coarse"])
+    assert (pre.one_level, pre.combine) == (str(d["one_level"]), str(d["combine"]))
+
+
+@pytest.mark.parametrize("name", CONFIG_CASES)
+def test_apply_matches_reference(B, name):
+    d, a, mat, pre = _setup(B, name)
+    tol_apply = _tols(name)[0]
+    for r, z, z1, zc in zip(d["r"], d["z"], d["z_one"], d["z_coarse"]):
+        np.testing.assert_allclose(pre.apply(r), z, rtol=0, atol=tol_apply * np.abs(z).max())
+        np.testing.assert_allclose(pre.apply_one_level(r), z1, rtol=0, atol=1e-10 * np.abs(z1).max())
+        np.testing.assert_allclose(pre.coarse_apply(r), zc, rtol=0, atol=tol_apply * np.abs(zc).max())
+
+
+@pytest.mark.parametrize("name", CONFIG_CASES)
+def test_solve_matches_reference(B, name):
+    d, a, mat, pre = _setup(B, name)
+    _, tol_hist, tol_x = _tols(name)
+    b = d["b"]
+    if str(d["solver"]) == "pcg":
+        x, rep = B.pcg(mat, pre, b, tol=float(d["tol"]), maxit=int(d["maxit"]))
+    else:
+        x, rep = B.gmres(mat, pre, b, tol=float(d["tol"]), maxit=int(d["maxit"]),
+                         restart=int(d["restart"]))
+    assert rep.converged == bool(d["converged"])
+    assert abs(rep.iterations - int(d["iterations"])) <= 1
+    k = min(rep.residuals.size, d["history"].size)
+    np.testing.assert_allclose(rep.residuals[:k], d["history"][:k], rtol=0, atol=tol_hist)
+    np.testing.assert_allclose(x, d["x"], rtol=0, atol=tol_x * np.abs(d["x"]).max())
+    true_res = np.linalg.norm(b - a @ x) / np.linalg.norm(b)
+    assert abs(true_res - float(d["true_residual"])) <= max(tol_hist, 1e-3 * float(d["true_residual"]))
+    assert rep.gpu_launches > 0
+
+
+def test_config1_headline_numbers(B):
+    d, a, mat, pre = _setup(B, "cfg1")
+    x, rep = B.pcg(mat, pre, d["b"], tol=1e-8)
+    assert rep.iterations == 20 and rep.converged
+    assert abs(rep.residuals[-1] - 4.376820e-09) < 1e-13
+
+
+def test_apply_is_deterministic(B):
+    d, a, mat, pre = _setup(B, "cfg2_m24")
+    r = d["r"][0]
+    z1, z2 = pre.apply(r), pre.apply(r)
+    assert np.array_equal(z1, z2)
+
+
+def test_apply_linear_and_symmetric(B):
+    """Size-independent properties: linearity, and ASM+additive is a symmetric operator."""
+    d, a, mat, pre = _setup(B, "cfg2_m24")
+    rng = np.random.default_rng(11)
+    u, v = rng.standard_normal(a.shape[0]), rng.standard_normal(a.shape[0])
+    zu, zv = pre.apply(u), pre.apply(v)
+    np.testing.assert_allclose(pre.apply(2.0 * u - 3.0 * v), 2.0 * zu - 3.0 * zv, rtol=0,
+                               atol=1e-12 * np.abs(zu).max() * 5)
+    assert pre.is_symmetric
+    assert abs(v @ zu - u @ zv) <= 1e-12 * abs(v @ zu) + 1e-14
+
+
+def test_torch_inputs_stay_on_device(B):
+    d, a, mat, pre = _setup(B, "cfg1")
+    r = torch.as_tensor(d["r"][0], device="cuda")
+    z = pre.apply(r)
+    assert z.is_cuda
+    np.testing.assert_allclose(z.cpu().numpy(), d["z"][0], rtol=0, atol=1e-10 * np.abs(d["z"][0]).max())
+    x, rep = B.pcg(mat, pre, torch.as_tensor(d["b"], device="cuda"), tol=1e-8)
+    assert x.is_cuda and rep.iterations == 20
+
+
+@pytest.mark.parametrize("combo", [f"{o}_{c}_{k}" for o in ("asm", "ras")
+                                   for c in ("none", "additive", "deflated")
+                                   for k in ("full", "gevp", "svd")])
+def test_all_variants_against_reference(B, combo):
+    """The 18 variant combinations of tests/test_precond.py:78-101 (poisson2d m=8, N=4)."""
+    d = golden("variants_p2d8")
+    a = golden_csr(d)
+    one, comb, kind = combo.split("_")
+    mat = B.SparseMat(a, symmetric=True)
+    pre = B.setup(mat, 4, overlap=2, tau=0.05, coarse=kind, one_level=one, combine=comb)
+    assert np.array_equal(pre.maps[0].indices, pre.maps[0].indices)
+    for r, z in zip(d["r"], d["z_" + combo]):
+        np.testing.assert_allclose(pre.apply(r), z, rtol=0, atol=1e-11 * np.abs(z).max())
+
+
+@pytest.mark.parametrize("m", [8, 12])
+def test_nonsymmetric_defaults_and_unrestarted_gmres(B, m):
+    d = golden(f"adv{m}")
+    a = golden_csr(d)
+    mat = B.SparseMat(a)
+    pre = B.setup(mat, 4, overlap=2, tau=0.05)
+    assert (pre.one_level, pre.combine, pre.report.coarse_kind) == ("ras", "deflated", "svd")
+    for r, z in zip(d["r"], d["z"]):
+        np.testing.assert_allclose(pre.apply(r), z, rtol=0, atol=1e-10 * np.abs(z).max())
+    x, rep = B.gmres(mat, pre, d["b"], tol=1e-10)
+    assert abs(rep.iterations - int(d["iterations"])) <= 1
+    np.testing.assert_allclose(x, d["x"], rtol=0, atol=1e-8 * np.abs(d["x"]).max())
+
+
+def test_tau_selection_config1(B):
+    d = golden("cfg1_tau")
+    a = golden_csr(d)
+    mat = B.SparseMat(a, symmetric=True)
+    pre = B.setup(mat, int(d["n_sub"]), overlap=1, owner=d["owner"])
+    assert pre.report.mode_counts == tuple(d["mode_counts"])
+    np.testing.assert_allclose(pre.apply(d["r"]), d["z"], rtol=0, atol=1e-10 * np.abs(d["z"]).max())
+    x, rep = B.pcg(mat, pre, d["b"])
+    assert abs(rep.iterations - int(d["iterations"])) <= 1
+
+
+@pytest.mark.parametrize("m", [30, 60])
+def test_weak_scaling_cases(B, m):
+    d = golden(f"weak_p2d{m}")
+    a = golden_csr(d)
+    mat = B.SparseMat(a, symmetric=True)
+    pre = B.setup(mat, int(d["n_sub"]), overlap=2, tau=0.1, owner=d["owner"])
+    x, rep = B.pcg(mat, pre, d["b"], tol=1e-10)
+    assert abs(rep.iterations - int(d["iterations"])) <= 1
+
+
+def test_krylov_behaviour(B):
+    import scipy.sparse as sp
+    d = golden("krylov")
+    lap = lambda n: B.SparseMat(sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1],
+                                         format="csr"), symmetric=True)
+    x, rep = B.pcg(lap(32), None, d["lap32_b"], tol=1e-10)
+    assert rep.converged and abs(rep.iterations - int(d["lap32_it"])) <= 1
+    np.testing.assert_allclose(x, d["lap32_x"], atol=1e-8)
+    x, rep = B.pcg(lap(200), None, d["lap200_b"], tol=1e-14, maxit=3)
+    assert rep.iterations == 3 and not rep.converged and rep.residuals.size == 4
+    x, rep = B.pcg(lap(10), None, np.zeros(10))
+    assert rep.converged and rep.iterations == 0 and np.all(x == 0) and rep.residuals.tolist() == [0.0]
+    with pytest.raises(B.BreakdownError) as info:
+        B.pcg(B.SparseMat.from_dense(np.diag([1.0, -1.0])), None, np.array([0.0, 1.0]), tol=1e-10)
+    assert info.value.iteration >= 1
+    a = golden_csr(d, "adv9_a_")
+    x, rep = B.gmres(B.SparseMat(a), None, d["adv9_b"], tol=1e-8)
+    assert abs(rep.iterations - int(d["adv9_it"])) <= 1
+    np.testing.assert_allclose(rep.residuals[:5], d["adv9_hist"][:5], rtol=1e-9)
+    x, rep = B.gmres(B.SparseMat.from_dense(d["happy_a"]), None, d["happy_b"], tol=1e-15, maxit=50)
+    assert rep.converged and rep.iterations <= 3
+    eye = B.SparseMat.identity(20)
+    bb = np.random.default_rng(6).standard_normal(20)
+    x, rep = B.gmres(eye, None, bb, tol=1e-12)
+    assert rep.iterations == 1 and rep.converged
+    np.testing.assert_allclose(x, bb, atol=1e-14)
+    with pytest.raises(ValueError, match="hard cap"):
+        B.gmres(lap(5), None, np.ones(5), maxit=1001)
+    x, rep = B.gmres(lap(8), None, np.zeros(8))
+    assert rep.converged and rep.iterations == 0
+
+
+def test_callbacks_and_condition_estimate(B):
+    import scipy.sparse as sp
+    n = 64
+    mat = B.SparseMat(sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1],
+                               format="csr"), symmetric=True)
+    b = np.random.default_rng(5).standard_normal(n)
+    seen = []
+    x, rep = B.pcg(mat, None, b, tol=1e-12, maxit=200, callback=lambda it, xk: seen.append((it, xk)),
+                   track_tridiagonal=True)
+    assert [s[0] for s in seen] == list(range(1, rep.iterations + 1))
+    np.testing.assert_allclose(seen[-1][1], x, atol=0)
+    exact = np.linalg.cond(mat.to_dense())
+    assert abs(rep.cond_estimate - exact) <= 1e-2 * exact
+    x2, rep2 = B.pcg(mat, None, b, tol=1e-12, maxit=200)
+    assert rep2.iterations == rep.iterations
+    np.testing.assert_array_equal(x2, x)
+    ks = []
+    d = golden("adv12")
+    a = golden_csr(d)
+    pre = B.setup(B.SparseMat(a), 4, overlap=2, tau=0.05)
+    B.gmres(B.SparseMat(a), pre, d["b"], tol=1e-10, callback=lambda k, _: ks.append(k))
+    assert ks == list(range(1, len(ks) + 1)) and len(ks) >= 1
+
+
+def test_single_subdomain_is_exact_inverse(B):
+    import scipy.sparse as sp
+    n = 20
+    mat = B.SparseMat(sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1],
+                               format="csr"), symmetric=True)
+    pre = B.setup(mat, 1, overlap=1, coarse="none")
+    r = np.random.default_rng(0).standard_normal(n)
+    np.testing.assert_allclose(pre.apply(r), np.linalg.solve(mat.to_dense(), r), rtol=1e-12)
+
+
+def test_identity_matrix_ras_is_identity(B):
+    mat = B.SparseMat.identity(16)
+    pre = B.setup(mat, 4, overlap=1, coarse="none", one_level="ras")
+    r = np.random.default_rng(1).standard_normal(16)
+    np.testing.assert_allclose(pre.apply(r), r, atol=1e-14)
