@@ -93,5 +93,9 @@ def ptr(t):
     if t is None:
         return None
     if hasattr(t, "data_ptr"):
+        if not t.is_contiguous():
+            raise ValueError("raw pointers need C-contiguous (row-major) tensors")
         return C.c_void_p(t.data_ptr())
+    if not t.flags["C_CONTIGUOUS"]:
+        raise ValueError("raw pointers need C-contiguous arrays")
     return C.c_void_p(t.ctypes.data)

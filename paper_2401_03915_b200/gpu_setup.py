@@ -166,8 +166,9 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     n_bnd = np.array([m.n_boundary for m in maps], dtype=np.int64)
     offsets = np.concatenate([[0], np.cumsum(n_loc)]).astype(np.int64)
     indices = np.concatenate([m.indices for m in maps]).astype(np.int64)
+    n_int32 = n_int.astype(np.int32)  # keep alive across the call (raw pointer below)
     handle.check(lib.tls_subdomains_upload(handle.ctx, N, _lib.ptr(offsets), _lib.ptr(indices),
-                                           _lib.ptr(n_int.astype(np.int32))))
+                                           _lib.ptr(n_int32)))
     ld = int(n_loc.max())
     if batch is None:
         free, _ = torch.cuda.mem_get_info(dev)
@@ -189,7 +190,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                 raise SubdomainSetupError(s, f"factorization failed: {int(info[bad[0]])}-th leading minor not positive")
             Binv = torch.cholesky_inverse(L)
             del L
-            Binv = 0.5 * (Binv + Binv.mT)
+            Binv = (0.5 * (Binv + Binv.mT)).contiguous()
         else:
             LU, piv, info = torch.linalg.lu_factor_ex(A)
             for b in range(cnt):
@@ -199,7 +200,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                 if int(info[b]) != 0 or float(blk.diagonal().abs().min()) <= nb_ * EPS * float(blk.abs().max()):
                     raise SubdomainSetupError(s, "local block is numerically singular")
             eye = torch.eye(ld, dtype=torch.float64, device=dev).expand(cnt, ld, ld)
-            Binv = torch.linalg.lu_solve(LU, piv, eye)
+            Binv = torch.linalg.lu_solve(LU, piv, eye).contiguous()  # lu_solve returns column-major
             del LU, piv
         handle.check(lib.tls_store_local_inverse(handle.ctx, first, cnt, _lib.ptr(Binv), ld, s_ptr))
         if want_coarse:
@@ -283,13 +284,13 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         if int(info) != 0:
             raise RuntimeError(f"coarse operator is not positive definite: {int(info)}-th leading minor")
         A0inv = torch.cholesky_inverse(L)
-        A0inv = 0.5 * (A0inv + A0inv.mT)
+        A0inv = (0.5 * (A0inv + A0inv.mT)).contiguous()
         del L
     else:
         LU, piv, info = torch.linalg.lu_factor_ex(A0)
         if int(info) != 0 or float(LU.diagonal().abs().min()) <= nC * EPS * float(LU.abs().max()):
             raise RuntimeError("coarse operator is numerically singular")
-        A0inv = torch.linalg.lu_solve(LU, piv, torch.eye(nC, dtype=torch.float64, device=dev))
+        A0inv = torch.linalg.lu_solve(LU, piv, torch.eye(nC, dtype=torch.float64, device=dev)).contiguous()
         del LU, piv
     zcat = torch.cat([z.reshape(-1) for z in z_dev]).contiguous()
     k32 = np.asarray(counts, dtype=np.int32)
