@@ -160,6 +160,10 @@ def main():
     config_case("cfg4_m32", a, sym, owner, nsub, 1, 20, "svd", "gmres", 1e-7, restart=50)
     a, sym, owner, nsub = P.CONFIGS[5].scaled(16, 8, angle_block=8).build()
     config_case("cfg5_m16", a, sym, owner, nsub, 1, 12, "gevp", "pcg", 1e-8)
+    # config-4 family with 64 subdomains: the reference's GMRES(50) stagnates
+    a, sym, owner, nsub = P.CONFIGS[4].scaled(64, 8).build()
+    config_case("cfg4_m64_stall", a, sym, owner, nsub, 1, 20, "svd", "gmres", 1e-7, restart=50,
+                maxit=100, n_apply=1)
 
     # reference default selection (tau) on config 1, its own setup()
     a, sym, owner, nsub = c1.build()

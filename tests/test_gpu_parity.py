@@ -256,3 +256,15 @@ def test_identity_matrix_ras_is_identity(B):
     pre = B.setup(mat, 4, overlap=1, coarse="none", one_level="ras")
     r = np.random.default_rng(1).standard_normal(16)
     np.testing.assert_allclose(pre.apply(r), r, atol=1e-14)
+
+
+def test_config4_family_stall_history(B):
+    """Non-converging GMRES(50) on the 64-subdomain saddle point: same stagnating history."""
+    d = golden("cfg4_m64_stall")
+    a = golden_csr(d)
+    mat = B.SparseMat(a)
+    pre = B.setup(mat, int(d["n_sub"]), overlap=1, owner=d["owner"], coarse="svd", n_modes=20)
+    np.testing.assert_allclose(pre.apply(d["r"][0]), d["z"][0], rtol=0, atol=1e-6 * np.abs(d["z"][0]).max())
+    x, rep = B.gmres(mat, pre, d["b"], tol=1e-7, maxit=100, restart=50)
+    assert rep.iterations == 100 and not rep.converged
+    np.testing.assert_allclose(rep.residuals, d["history"], rtol=0, atol=1e-6)

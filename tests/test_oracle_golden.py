@@ -98,3 +98,13 @@ def test_oracle_krylov_behaviour():
         O.pcg(sp.csr_matrix(np.diag([1.0, -1.0])), None, np.array([0.0, 1.0]), 1e-10)
     with pytest.raises(ValueError, match="hard cap"):
         O.gmres(lap(5), None, np.ones(5), maxit=1001)
+
+
+def test_oracle_config4_family_stalls_like_reference():
+    """GMRES(50) on the saddle-point family stagnates in the reference too (64 subdomains)."""
+    d = golden("cfg4_m64_stall")
+    a = golden_csr(d)
+    pre = O.OraclePreconditioner(a, False, d["owner"], int(d["n_sub"]), 1, coarse="svd", n_modes=20)
+    x, it, conv, hist = O.gmres_restarted(a, pre, d["b"], 1e-7, 100, 50)
+    assert it == 100 and not conv and not bool(d["converged"])
+    np.testing.assert_allclose(hist, d["history"], rtol=1e-9)
