@@ -132,6 +132,22 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
 int32_t tls_report(const tls_ctx* ctx, int64_t* n, int32_t* n_sub, int32_t* n_coarse,
                    int64_t* tile_bytes);
 
+/* ---- sharding across GPUs (build extension, the reference is single-process).
+ * A handle owns the contiguous slab [s_lo, s_hi) of the global subdomain list (call before
+ * tls_subdomains_upload, which still receives the global maps; extract/store/coarse-upload
+ * then take global subdomain ids of owned subdomains, coarse k[] for all subdomains and the
+ * basis of the owned ones).  Vectors, SpMV, dots and the coarse solve are replicated; every
+ * prolongation is rank-partial and completed by one in-place sum all-reduce per apply stage.
+ * NCCL communicators are CUDA-graph capturable; an in-process group (several handles on one
+ * GPU driven from host threads) runs the identical schedule for single-GPU validation. */
+typedef struct tls_group tls_group;
+int32_t tls_set_owned_range(tls_ctx* ctx, int32_t s_lo, int32_t s_hi);
+int32_t tls_nccl_unique_id(void* out, int32_t bytes);
+int32_t tls_comm_init_nccl(tls_ctx* ctx, const void* unique_id, int32_t nranks, int32_t rank);
+int32_t tls_group_create(int32_t nmembers, tls_group** out);
+void tls_group_destroy(tls_group* g);
+int32_t tls_comm_init_group(tls_ctx* ctx, tls_group* g, int32_t rank);
+
 /* ---- measurement: average device time (ms) of the dominant kernel (batched local
  * solve) over the last solve, timed with CUDA events on the launching stream, and
  * the algorithmic bytes one launch of it must move. */

@@ -63,6 +63,12 @@ SIGNATURES = {
     "tls_gmres": (_I32, [_P, _P, _P, _D, _I32, _I32, _I32, _P, C.POINTER(TlsStatus), ITER_CB, _P, _P]),
     "tls_report": (_I32, [_P, C.POINTER(_I64), C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I64)]),
     "tls_profile_local_solve": (_I32, [_P, _I32, C.POINTER(_D), C.POINTER(_D), _P]),
+    "tls_set_owned_range": (_I32, [_P, _I32, _I32]),
+    "tls_nccl_unique_id": (_I32, [_P, _I32]),
+    "tls_comm_init_nccl": (_I32, [_P, _P, _I32, _I32]),
+    "tls_group_create": (_I32, [_I32, C.POINTER(_P)]),
+    "tls_group_destroy": (None, [_P]),
+    "tls_comm_init_group": (_I32, [_P, _P, _I32]),
 }
 
 _lib = None

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "tls_b200.h"
+#include "tls_comm.h"
 #include "tls_kernels.cuh"
 
 using namespace tls;
@@ -101,6 +102,14 @@ struct tls_ctx {
   int gm_exec_cols[2] = {0, 0};
   int gm_exec_launches[2] = {0, 0};
   int launches = 0;  // kernels enqueued since the counter was reset
+  // ---- sharding: this handle owns global subdomains [own_lo, own_hi)
+  int own_lo = 0, own_hi = -1, nsub_global = 0;
+  Comm* comm = nullptr;
+};
+
+struct tls_group {
+  GroupShared shared;
+  explicit tls_group(int n) : shared(n) {}
 };
 
 #define CK(call)                                                                             \
@@ -240,9 +249,73 @@ static int enq_prolong(tls_ctx* ctx, cudaStream_t s, const double* qv, const dou
 
 static bool has_coarse(const tls_ctx* ctx) { return ctx->ncoarse > 0 && ctx->combine != TLS_NONE; }
 
+static bool sharded(const tls_ctx* ctx) { return ctx->comm != nullptr && ctx->comm->nranks > 1; }
+
+// the exchange step: in-place sum over the ranks (NCCL or in-process group)
+static int enq_allreduce(tls_ctx* ctx, cudaStream_t s, double* buf, long long count) {
+  if (!sharded(ctx)) return TLS_OK;
+  std::string err;
+  cudaError_t e = ctx->comm->allreduce_sum(buf, count, s, err);
+  if (e != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+  return TLS_OK;
+}
+
+// coarse coefficients c = Z^T r: this rank's columns, then the sum over ranks
+static int enq_restrict_all(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
+  if (sharded(ctx))
+    CK(cudaMemsetAsync(ctx->xloc + ctx->coarse_xoff, 0, sizeof(double) * ctx->ncoarse, s));
+  TRY(enq_restrict(ctx, s, r, done));
+  return enq_allreduce(ctx, s, ctx->xloc + ctx->coarse_xoff, ctx->ncoarse);
+}
+
+static int enq_dot(tls_ctx* ctx, cudaStream_t s, const double* a, const double* b, const int* done) {
+  k_dot<<<ctx->G, NTHR, 0, s>>>(ctx->n, a, b, ctx->part, done);
+  CKL();
+  return TLS_OK;
+}
+
+// Sharded schedule: every prolongation is rank-partial (own subdomains only) and is completed
+// by one all-reduce of the n-vector; vectors, SpMV, dots and the coarse solve are replicated.
+static int enq_apply_sharded(tls_ctx* ctx, cudaStream_t s, const double* r, double* z, bool dot,
+                             const int* done) {
+  const long long n = ctx->n;
+  if (!has_coarse(ctx)) {
+    TRY(enq_gather(ctx, s, r, done));
+    TRY(enq_solve(ctx, s, L_LOCAL, done));
+    TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, z, done)));
+    TRY(enq_allreduce(ctx, s, z, n));
+  } else if (ctx->combine == TLS_ADDITIVE) {
+    TRY(enq_gather(ctx, s, r, done));
+    TRY(enq_restrict_all(ctx, s, r, done));
+    TRY(enq_solve(ctx, s, L_ALL, done));
+    TRY((enq_prolong<1, 0>(ctx, s, nullptr, nullptr, nullptr, z, done)));
+    TRY(enq_allreduce(ctx, s, z, n));
+  } else {
+    TRY(enq_restrict_all(ctx, s, r, done));
+    TRY(enq_solve(ctx, s, L_COARSE, done));
+    TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t1, done)));
+    TRY(enq_allreduce(ctx, s, ctx->t1, n));
+    TRY((spmv_lpr<1, 0>(ctx, s, ctx->t1, ctx->t2, r, nullptr, done)));
+    TRY(enq_gather(ctx, s, ctx->t2, done));
+    TRY(enq_solve(ctx, s, L_LOCAL, done));
+    TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t3, done)));
+    TRY(enq_allreduce(ctx, s, ctx->t3, n));
+    TRY((spmv_lpr<0, 0>(ctx, s, ctx->t3, ctx->t4, nullptr, nullptr, done)));
+    TRY(enq_restrict_all(ctx, s, ctx->t4, done));
+    TRY(enq_solve(ctx, s, L_COARSE, done));
+    TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, z, done)));
+    TRY(enq_allreduce(ctx, s, z, n));
+    k_defl_combine<<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->t1, ctx->t3, z, done);
+    CKL();
+  }
+  if (dot) TRY(enq_dot(ctx, s, r, z, done));
+  return TLS_OK;
+}
+
 // z = M^{-1} r (src/precond.py:128-136).  dot: partial r.z into ctx->part (G partials).
 static int enq_apply(tls_ctx* ctx, cudaStream_t s, const double* r, double* z, bool dot,
                      const int* done) {
+  if (sharded(ctx)) return enq_apply_sharded(ctx, s, r, z, dot, done);
   if (!has_coarse(ctx)) {
     TRY(enq_gather(ctx, s, r, done));
     TRY(enq_solve(ctx, s, L_LOCAL, done));
@@ -329,6 +402,7 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   if (ctx->h_x) cudaFreeHost(ctx->h_x);
   dfree(ctx->ab);
   if (ctx->cap) cudaStreamDestroy(ctx->cap);
+  delete ctx->comm;
   delete ctx;
 }
 
@@ -376,21 +450,31 @@ int32_t tls_spmv(tls_ctx* ctx, const double* x, double* y, void* stream) {
   return spmv_lpr<0, 0>(ctx, (cudaStream_t)stream, x, y, nullptr, nullptr, nullptr);
 }
 
-int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub, const int64_t* offsets,
-                              const int64_t* indices, const int32_t* n_interior) {
-  if (!ctx || n_sub <= 0) return ctx ? fail(ctx, TLS_ERR_ARG, "n_sub must be positive") : TLS_ERR_ARG;
+int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t* offsets_g,
+                              const int64_t* indices_g, const int32_t* n_interior_g) {
+  if (!ctx || n_sub_global <= 0) return ctx ? fail(ctx, TLS_ERR_ARG, "n_sub must be positive") : TLS_ERR_ARG;
   if (!ctx->rowptr) return fail(ctx, TLS_ERR_STATE, "upload the matrix first");
   CK(cudaSetDevice(ctx->device));
+  // this handle keeps only its owned slab [own_lo, own_hi) of the global subdomain list
+  const int lo = ctx->own_lo, hi = ctx->own_hi < 0 ? n_sub_global : ctx->own_hi;
+  if (lo < 0 || hi > n_sub_global || lo >= hi) return fail(ctx, TLS_ERR_ARG, "owned subdomain range out of bounds");
+  ctx->nsub_global = n_sub_global;
+  ctx->own_hi = hi;
+  const int n_sub = hi - lo;
+  const int64_t base = offsets_g[lo];
   ctx->nsub = n_sub;
-  ctx->h_off.assign(offsets, offsets + n_sub + 1);
+  ctx->h_off.resize(n_sub + 1);
+  for (int s = 0; s <= n_sub; ++s) ctx->h_off[s] = offsets_g[lo + s] - base;
+  const int64_t* offsets = ctx->h_off.data();
   const int64_t tot = offsets[n_sub];
   ctx->h_idx.resize(tot);
   for (int64_t i = 0; i < tot; ++i) {
-    if (indices[i] < 0 || indices[i] >= ctx->n) return fail(ctx, TLS_ERR_DIM, "subdomain index out of range");
-    ctx->h_idx[i] = (int)indices[i];
+    const int64_t g = indices_g[base + i];
+    if (g < 0 || g >= ctx->n) return fail(ctx, TLS_ERR_DIM, "subdomain index out of range");
+    ctx->h_idx[i] = (int)g;
   }
   ctx->h_n.resize(n_sub);
-  ctx->h_nint.assign(n_interior, n_interior + n_sub);
+  ctx->h_nint.assign(n_interior_g + lo, n_interior_g + hi);
   ctx->max_n = 0;
   std::vector<long long> idxoff(n_sub);
   for (int s = 0; s < n_sub; ++s) {
@@ -432,10 +516,12 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub, const int64_t* offset
 
 int32_t tls_subdomain_max_size(const tls_ctx* ctx) { return ctx ? ctx->max_n : 0; }
 
-int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first, int32_t count, double* out, int64_t ld,
+int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first_g, int32_t count, double* out, int64_t ld,
                            void* stream) {
-  if (!ctx || first < 0 || count <= 0 || first + count > ctx->nsub)
-    return ctx ? fail(ctx, TLS_ERR_ARG, "bad subdomain range") : TLS_ERR_ARG;
+  if (!ctx) return TLS_ERR_ARG;
+  const int first = first_g - ctx->own_lo;
+  if (first < 0 || count <= 0 || first + count > ctx->nsub)
+    return fail(ctx, TLS_ERR_ARG, "subdomain range not owned by this handle");
   for (int s = first; s < first + count; ++s)
     if (ctx->h_n[s] > ld) return fail(ctx, TLS_ERR_ARG, "ld smaller than a local block");
   CK(cudaSetDevice(ctx->device));
@@ -455,10 +541,12 @@ int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first, int32_t count, double* o
   return TLS_OK;
 }
 
-int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first, int32_t count, const double* inv,
+int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first_g, int32_t count, const double* inv,
                                 int64_t ld, void* stream) {
-  if (!ctx || first < 0 || count <= 0 || first + count > ctx->nsub)
-    return ctx ? fail(ctx, TLS_ERR_ARG, "bad subdomain range") : TLS_ERR_ARG;
+  if (!ctx) return TLS_ERR_ARG;
+  const int first = first_g - ctx->own_lo;
+  if (first < 0 || count <= 0 || first + count > ctx->nsub)
+    return fail(ctx, TLS_ERR_ARG, "subdomain range not owned by this handle");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
   dim3 g(512, count);
@@ -480,10 +568,12 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
     ctx->ncoarse = 0;
     return TLS_OK;
   }
-  ctx->h_k.assign(k, k + ctx->nsub);
+  // k[] covers all global subdomains (column numbering); the basis holds the owned ones
+  ctx->h_k.assign(k + ctx->own_lo, k + ctx->own_hi);
   ctx->h_cstart.resize(ctx->nsub);
   ctx->h_zoff.resize(ctx->nsub);
   int c = 0;
+  for (int g = 0; g < ctx->own_lo; ++g) c += k[g];
   long long zo = 0;
   for (int i = 0; i < ctx->nsub; ++i) {
     ctx->h_cstart[i] = c;
@@ -491,6 +581,7 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
     c += ctx->h_k[i];
     zo += (long long)ctx->h_nint[i] * ctx->h_k[i];
   }
+  for (int g = ctx->own_hi; g < ctx->nsub_global; ++g) c += k[g];
   if (c != n_coarse) return fail(ctx, TLS_ERR_ARG, "sum of k differs from n_coarse");
   ctx->ncoarse = n_coarse;
   TRY(dalloc(ctx, ctx->d_Z, zo));
@@ -659,7 +750,8 @@ int32_t tls_apply_one_level(tls_ctx* ctx, const double* r, double* z, void* stre
   cudaStream_t s = (cudaStream_t)stream;
   TRY(enq_gather(ctx, s, r, nullptr));
   TRY(enq_solve(ctx, s, L_LOCAL, nullptr));
-  return enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, z, nullptr);
+  TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, z, nullptr)));
+  return enq_allreduce(ctx, s, z, ctx->n);
 }
 
 int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream) {
@@ -667,9 +759,10 @@ int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream)
   if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "no coarse space");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
-  TRY(enq_restrict(ctx, s, r, nullptr));
+  TRY(enq_restrict_all(ctx, s, r, nullptr));
   TRY(enq_solve(ctx, s, L_COARSE, nullptr));
-  return enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, z, nullptr);
+  TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, z, nullptr)));
+  return enq_allreduce(ctx, s, z, ctx->n);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -760,16 +853,19 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
   k_pcg_rz0<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
   CKL();
   CK(cudaMemcpyAsync(ctx->vp, ctx->vz, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  const bool host_loop = cb || (sharded(ctx) && !ctx->comm->capturable());
   if (maxit > 0) {
-    if (cb) {
+    if (host_loop) {
       // per-iteration host loop (callback(it, x.copy()), src/krylov.py:92-93)
       for (int it = 1; it <= maxit; ++it) {
         TRY(enq_pcg_iter(ctx, s, it % PCG_GRAPH_ITERS == 0, prec));
         CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (h.status == 2) break;
-        CK(cudaMemcpy(ctx->h_x, ctx->vx, sizeof(double) * n, cudaMemcpyDeviceToHost));
-        cb(user, h.it, ctx->h_x);
+        if (cb) {
+          CK(cudaMemcpy(ctx->h_x, ctx->vx, sizeof(double) * n, cudaMemcpyDeviceToHost));
+          cb(user, h.it, ctx->h_x);
+        }
         if (h.done) break;
       }
     } else {
@@ -963,13 +1059,13 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
   const double one = 1.0;
   CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
   GmState hs{};
-  if (cb) {
+  if (cb || (sharded(ctx) && !ctx->comm->capturable())) {
     for (int guard = 0; guard <= maxit; ++guard) {
       for (int j = 0; j < mcols; ++j) {
         TRY(enq_gm_step(ctx, s, j, prec));
         CK(cudaMemcpyAsync(&hs, ctx->gm, sizeof(GmState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        cb(user, hs.total + hs.k, nullptr);
+        if (cb) cb(user, hs.total + hs.k, nullptr);
         if (hs.cycle_stop) break;
       }
       TRY(enq_gm_cycle_end(ctx, s, prec));
@@ -1052,6 +1148,79 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   cudaEventDestroy(e1);
   if (avg_ms) *avg_ms = ms / reps;
   if (algorithmic_bytes) *algorithmic_bytes = ctx->algo_local + (which == L_ALL ? ctx->algo_coarse : 0.0);
+  return TLS_OK;
+}
+
+// ---- sharding -------------------------------------------------------------------------------
+int32_t tls_set_owned_range(tls_ctx* ctx, int32_t s_lo, int32_t s_hi) {
+  if (!ctx || s_lo < 0 || s_hi <= s_lo) return ctx ? fail(ctx, TLS_ERR_ARG, "bad owned range") : TLS_ERR_ARG;
+  ctx->own_lo = s_lo;
+  ctx->own_hi = s_hi;
+  return TLS_OK;
+}
+
+int32_t tls_nccl_unique_id(void* out, int32_t bytes) {
+  std::string err;
+  if (!out || bytes < (int32_t)sizeof(ncclUniqueId)) return TLS_ERR_ARG;
+  if (!nccl_api().load(err)) return TLS_ERR_STATE;
+  ncclUniqueId id;
+  if (nccl_api().get_id(&id) != ncclSuccess) return TLS_ERR_CUDA;
+  memcpy(out, &id, sizeof(id));
+  return TLS_OK;
+}
+
+int32_t tls_comm_init_nccl(tls_ctx* ctx, const void* unique_id, int32_t nranks, int32_t rank) {
+  if (!ctx || !unique_id || nranks < 1 || rank < 0 || rank >= nranks)
+    return ctx ? fail(ctx, TLS_ERR_ARG, "bad communicator arguments") : TLS_ERR_ARG;
+  std::string err;
+  if (!nccl_api().load(err)) return fail(ctx, TLS_ERR_STATE, err);
+  CK(cudaSetDevice(ctx->device));
+  auto* c = new NcclComm();
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  ncclResult_t r = nccl_api().init_rank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(ctx, TLS_ERR_CUDA, std::string("ncclCommInitRank: ") + nccl_api().errstr(r));
+  }
+  c->rank = rank;
+  c->nranks = nranks;
+  delete ctx->comm;
+  ctx->comm = c;
+  destroy_graphs(ctx);
+  return TLS_OK;
+}
+
+int32_t tls_group_create(int32_t nmembers, tls_group** out) {
+  if (!out || nmembers < 1 || nmembers > MAX_GROUP) return TLS_ERR_ARG;
+  auto* g = new tls_group(nmembers);
+  for (int r = 0; r < nmembers; ++r) {
+    if (cudaEventCreateWithFlags(&g->shared.ev_in[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->shared.ev_out[r], cudaEventDisableTiming) != cudaSuccess) {
+      delete g;
+      return TLS_ERR_CUDA;
+    }
+  }
+  *out = g;
+  return TLS_OK;
+}
+
+void tls_group_destroy(tls_group* g) {
+  if (!g) return;
+  for (auto e : g->shared.ev_in) if (e) cudaEventDestroy(e);
+  for (auto e : g->shared.ev_out) if (e) cudaEventDestroy(e);
+  delete g;
+}
+
+int32_t tls_comm_init_group(tls_ctx* ctx, tls_group* g, int32_t rank) {
+  if (!ctx || !g || rank < 0 || rank >= g->shared.n) return ctx ? fail(ctx, TLS_ERR_ARG, "bad group rank") : TLS_ERR_ARG;
+  auto* c = new GroupComm();
+  c->g = &g->shared;
+  c->rank = rank;
+  c->nranks = g->shared.n;
+  delete ctx->comm;
+  ctx->comm = c;
+  destroy_graphs(ctx);
   return TLS_OK;
 }
 

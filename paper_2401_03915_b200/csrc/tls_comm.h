@@ -1,0 +1,167 @@
+// tls_comm.h — the one exchange step of the sharded path: an in-place sum all-reduce of fp64
+// buffers across the ranks that own disjoint subdomain slabs.
+//
+//  * NcclComm   — one process per GPU; NCCL (libnccl.so.2, dlopen'ed so the library also loads on
+//                 hosts without NCCL) over NVLink/NVSwitch; stream-ordered and CUDA-graph
+//                 capturable, so the all-reduces live inside the replayed PCG/GMRES graphs.
+//  * GroupComm  — R ranks inside ONE process on one device (host threads + stream events + a
+//                 fixed-order sum kernel).  Used to validate the sharded schedule end-to-end on a
+//                 single GPU; never spins on device flags (kernels only start after their stream
+//                 waits are satisfied), not capturable (host barrier per reduction).
+#pragma once
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace tls {
+
+constexpr int MAX_GROUP = 16;
+
+struct Comm {
+  int rank = 0, nranks = 1;
+  virtual ~Comm() {}
+  virtual cudaError_t allreduce_sum(double* buf, long long count, cudaStream_t s, std::string& err) = 0;
+  virtual bool capturable() const = 0;
+};
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init_rank = nullptr;
+  decltype(&ncclAllReduce) allreduce = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclGetErrorString) errstr = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("dlopen libnccl.so.2: ") + dlerror();
+      return false;
+    }
+    get_id = (decltype(get_id))dlsym(h, "ncclGetUniqueId");
+    init_rank = (decltype(init_rank))dlsym(h, "ncclCommInitRank");
+    allreduce = (decltype(allreduce))dlsym(h, "ncclAllReduce");
+    destroy = (decltype(destroy))dlsym(h, "ncclCommDestroy");
+    errstr = (decltype(errstr))dlsym(h, "ncclGetErrorString");
+    if (!get_id || !init_rank || !allreduce || !destroy || !errstr) {
+      err = "libnccl.so.2 lacks required symbols";
+      return false;
+    }
+    return true;
+  }
+};
+
+inline NcclApi& nccl_api() {
+  static NcclApi api;
+  return api;
+}
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  ~NcclComm() override {
+    if (comm) nccl_api().destroy(comm);
+  }
+  cudaError_t allreduce_sum(double* buf, long long count, cudaStream_t s, std::string& err) override {
+    ncclResult_t r = nccl_api().allreduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, comm, s);
+    if (r != ncclSuccess) {
+      err = std::string("ncclAllReduce: ") + nccl_api().errstr(r);
+      return cudaErrorUnknown;
+    }
+    return cudaSuccess;
+  }
+  bool capturable() const override { return true; }
+};
+
+// ---------------------------------------------------------------- in-process group
+struct GroupPtrs {
+  const double* p[MAX_GROUP];
+};
+
+__global__ void k_group_sum(GroupPtrs ptrs, int n, long long count, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s += ptrs.p[r][i];  // fixed rank order -> deterministic
+    out[i] = s;
+  }
+}
+
+struct GroupShared {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<double*> bufs;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  explicit GroupShared(int n_) : n(n_), bufs(n_, nullptr), ev_in(n_, nullptr), ev_out(n_, nullptr) {}
+  bool broken = false;
+  // false when a peer never arrives (it failed before reaching the exchange): the group is
+  // then broken and every later exchange fails fast instead of hanging the process.
+  bool barrier(int timeout_s = 120) {
+    std::unique_lock<std::mutex> lk(m);
+    if (broken) return false;
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(timeout_s), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+
+struct GroupComm : Comm {
+  GroupShared* g = nullptr;
+  double* tmp = nullptr;
+  long long tmp_cap = 0;
+  ~GroupComm() override {
+    if (tmp) cudaFree(tmp);
+  }
+  cudaError_t allreduce_sum(double* buf, long long count, cudaStream_t s, std::string& err) override {
+    cudaError_t e;
+    if (count > tmp_cap) {
+      if (tmp) cudaFree(tmp);
+      if ((e = cudaMalloc((void**)&tmp, sizeof(double) * count)) != cudaSuccess) return e;
+      tmp_cap = count;
+    }
+    g->bufs[rank] = buf;
+    if ((e = cudaEventRecord(g->ev_in[rank], s)) != cudaSuccess) return e;
+    if (!g->barrier()) {  // every member's partial is enqueued
+      err = "in-process group: a peer rank did not reach the exchange";
+      return cudaErrorUnknown;
+    }
+    GroupPtrs ptrs{};
+    for (int r = 0; r < g->n; ++r) {
+      if ((e = cudaStreamWaitEvent(s, g->ev_in[r], 0)) != cudaSuccess) return e;
+      ptrs.p[r] = g->bufs[r];
+    }
+    const int grid = (int)std::min<long long>((count + 255) / 256, 1184);
+    k_group_sum<<<grid > 0 ? grid : 1, 256, 0, s>>>(ptrs, g->n, count, tmp);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(g->ev_out[rank], s)) != cudaSuccess) return e;
+    if (!g->barrier()) {  // every member has enqueued its reads of all partials
+      err = "in-process group: a peer rank did not reach the exchange";
+      return cudaErrorUnknown;
+    }
+    for (int r = 0; r < g->n; ++r)
+      if ((e = cudaStreamWaitEvent(s, g->ev_out[r], 0)) != cudaSuccess) return e;
+    return cudaMemcpyAsync(buf, tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, s);
+  }
+  bool capturable() const override { return false; }
+};
+
+}  // namespace tls

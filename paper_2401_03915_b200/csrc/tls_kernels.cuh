@@ -363,6 +363,14 @@ __global__ void __launch_bounds__(NTHR) k_prolong(int n, const int* __restrict__
   }
 }
 
+// deflated combination after the sharded all-reduces: z = (q + w) - Qu  (src/precond.py:136)
+__global__ void __launch_bounds__(NTHR) k_defl_combine(int n, const double* __restrict__ q,
+                                                       const double* __restrict__ w,
+                                                       double* __restrict__ z, const int* done) {
+  if (done && *done) return;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) z[i] = (q[i] + w[i]) - z[i];
+}
+
 // ---------------------------------------------------------------------------------------
 // K8  Krylov vector kernels and scalar steps (src/krylov.py:58-107)
 // ---------------------------------------------------------------------------------------

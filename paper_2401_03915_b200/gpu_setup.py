@@ -99,6 +99,24 @@ class CoarseData:
         return self._basis
 
 
+def warm_linalg(device=None):
+    """Initialise torch.linalg's lazily-loaded GPU backends once, from the calling thread
+    (their first use is not thread-safe; in-process rank groups call this before threading)."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    a = torch.eye(4, dtype=torch.float64, device=dev) * 2.0
+    L, _ = torch.linalg.cholesky_ex(a)
+    torch.cholesky_inverse(L)
+    LU, piv, _ = torch.linalg.lu_factor_ex(a)
+    torch.linalg.lu_solve(LU, piv, a)
+    torch.linalg.eigh(a)
+    torch.linalg.svd(a, full_matrices=False)
+    torch.linalg.solve(a, a, left=False)
+    torch.linalg.solve_triangular(L, a, upper=False)
+    torch.linalg.cholesky(a)
+    torch.cuda.synchronize(dev)
+
+
 def _select(values, tau, n_modes):
     thr = TOPK_TAU if n_modes is not None else tau
     keep = np.nonzero(values > thr * (1.0 + TIE_GUARD))[0]
@@ -154,9 +172,43 @@ def _subdomain_columns(torch, kind, A, B, n, ni, nin, tau, n_modes):
     return V.contiguous()
 
 
+def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
+    """Column blocks of A0 = Z^T (A Z) for the owned subdomains (src/coarse.py:158-168).
+
+    ``w_blocks[s]`` = A_ii[:, :n_int] Z_s on the local rows of s (A Z_s is supported there,
+    because every graph neighbour of an interior row lies in layer 1); rows are split by their
+    owner j and contracted with Z_j.  Returns the dense n_C x n_C matrix holding only the
+    column blocks of ``own`` (sum over ranks = A0).
+    """
+    torch = _torch()
+    cstart = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    nC = int(cstart[-1])
+    posint = np.empty(int(max(m.indices.max() for m in maps)) + 1, dtype=np.int64)
+    for m in maps:
+        posint[m.interior] = np.arange(m.interior.size)
+    A0 = torch.zeros((nC, nC), dtype=torch.float64, device=device)
+    for s in own:
+        if counts[s] == 0:
+            continue
+        m = maps[s]
+        own_rows = owner[m.indices]
+        order = np.argsort(own_rows, kind="stable")
+        cuts = np.nonzero(np.diff(own_rows[order]))[0] + 1
+        W = w_blocks[s]
+        for grp in np.split(order, cuts):
+            j = int(own_rows[grp[0]])
+            if counts[j] == 0:
+                continue
+            rows_j = torch.as_tensor(posint[m.indices[grp]], device=device)
+            Zj = z_blocks[j].index_select(0, rows_j)
+            Wg = W.index_select(0, torch.as_tensor(grp, device=device))
+            A0[cstart[j]:cstart[j + 1], cstart[s]:cstart[s + 1]] += Zj.mT @ Wg
+    return A0
+
+
 def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_modes, drop_tol,
-                           batch=None, mem_fraction=0.35):
-    """Run steps 1-5 into ``handle``; returns CoarseData or None."""
+                           batch=None, mem_fraction=0.35, shard=None):
+    """Run steps 1-5 into ``handle`` (this rank's slab when ``shard``); returns CoarseData or None."""
     torch = _torch()
     lib = handle.lib
     dev = torch.device("cuda", handle.device)
@@ -164,22 +216,31 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     n_loc = np.array([m.n_local for m in maps], dtype=np.int64)
     n_int = np.array([m.interior.size for m in maps], dtype=np.int64)
     n_bnd = np.array([m.n_boundary for m in maps], dtype=np.int64)
+    sharded = shard is not None and shard.nranks > 1
+    if sharded:
+        from .distributed import slab_ranges
+        lo, hi = slab_ranges(n_loc.astype(np.float64) ** 2, shard.nranks)[shard.rank]
+        shard.lo, shard.hi = lo, hi
+        handle.check(lib.tls_set_owned_range(handle.ctx, lo, hi))
+        shard.attach(handle)
+    else:
+        lo, hi = 0, N
     offsets = np.concatenate([[0], np.cumsum(n_loc)]).astype(np.int64)
     indices = np.concatenate([m.indices for m in maps]).astype(np.int64)
     n_int32 = n_int.astype(np.int32)  # keep alive across the call (raw pointer below)
     handle.check(lib.tls_subdomains_upload(handle.ctx, N, _lib.ptr(offsets), _lib.ptr(indices),
                                            _lib.ptr(n_int32)))
-    ld = int(n_loc.max())
+    ld = int(n_loc[lo:hi].max())
     if batch is None:
         free, _ = torch.cuda.mem_get_info(dev)
         per = 8.0 * ld * ld * 4.0 + 4.0 * csr.shape[0]
-        batch = max(1, min(N, int(mem_fraction * free / per)))
+        batch = max(1, min(hi - lo, int(mem_fraction * free / per)))
     s_ptr = stream_ptr()
     want_coarse = coarse != "none"
-    z_dev = [None] * N
-    w_dev = [None] * N
-    for first in range(0, N, batch):
-        cnt = min(batch, N - first)
+    z_dev = {}
+    w_dev = {}
+    for first in range(lo, hi, batch):
+        cnt = min(batch, hi - first)
         A = torch.empty((cnt, ld, ld), dtype=torch.float64, device=dev)
         handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
         if symmetric:
@@ -220,62 +281,65 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     if not want_coarse:
         torch.cuda.empty_cache()
         return None
-    # rank filter (src/coarse.py:119-155)
-    z_host = [z.cpu().numpy() for z in z_dev]
+    # rank filter (src/coarse.py:119-155): pivoted-QR magnitudes vs the GLOBAL largest pivot
+    own = range(lo, hi)
+    z_host = {s: z_dev[s].cpu().numpy() for s in own}
     pivots = []
-    for s, z in enumerate(z_host):
+    for s in own:
+        z = z_host[s]
         if z.shape[1] == 0:
             continue
         r, perm = sla.qr(z, mode="r", pivoting=True)
         rd = np.abs(np.diag(r))
         for j in range(z.shape[1]):
             pivots.append((rd[j] if j < rd.size else 0.0, s, int(perm[j])))
-    keep_cols = [[] for _ in range(N)]
-    if pivots:
-        largest = max(p[0] for p in pivots)
-        for mag, s, j in pivots:
-            if mag >= drop_tol * largest:
-                keep_cols[s].append(j)
-    total = sum(len(k) for k in keep_cols)
-    if total == 0:
-        if pivots:
-            warnings.warn("rank filter removed every coarse column; coarse level disabled")
-        torch.cuda.empty_cache()
-        return CoarseData(csr.shape[0], maps, [np.zeros((int(n_int[s]), 0)) for s in range(N)],
-                          [0] * N, 0) if pivots else None
-    for s in range(N):
+    largest = max((p[0] for p in pivots), default=0.0)
+    any_cols = float(len(pivots))
+    if sharded:
+        t = torch.tensor([largest, any_cols], dtype=torch.float64, device=dev)
+        shard.coll.allreduce(t, op="max")
+        largest, any_cols = float(t[0]), float(t[1])
+    keep_cols = {s: [] for s in own}
+    for mag, s, j in pivots:
+        if mag >= drop_tol * largest:
+            keep_cols[s].append(j)
+    for s in own:
         kc = sorted(keep_cols[s])
         if len(kc) != z_host[s].shape[1]:
             idx = torch.as_tensor(kc, dtype=torch.long, device=dev)
             z_dev[s] = z_dev[s][:, idx].contiguous()
             w_dev[s] = w_dev[s][:, idx].contiguous() if len(kc) else None
             z_host[s] = z_host[s][:, kc]
-    counts = [z.shape[1] for z in z_host]
-    cstart = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    nC = int(cstart[-1])
-    # Galerkin A0 = Z^T (A Z): A Z_s lives on the local rows of s; split those rows by owner
+    counts_own = np.array([z_host[s].shape[1] for s in own], dtype=np.int64)
+    if sharded:
+        parts = shard.coll.allgather_list(torch.as_tensor(counts_own, device=dev))
+        counts = np.concatenate([p.cpu().numpy() for p in parts]).astype(np.int64)
+        flat = torch.cat([z_dev[s].reshape(-1) for s in own]) if len(own) else torch.zeros(0, device=dev)
+        zparts = shard.coll.allgather_list(flat.to(torch.float64))
+        z_all = {}
+        # unpack every rank's concatenated blocks in global subdomain order
+        from .distributed import slab_ranges
+        ranges = slab_ranges(n_loc.astype(np.float64) ** 2, shard.nranks)
+        for (rlo, rhi), zp in zip(ranges, zparts):
+            off = 0
+            for s in range(rlo, rhi):
+                sz = int(n_int[s]) * int(counts[s])
+                z_all[s] = zp[off:off + sz].reshape(int(n_int[s]), int(counts[s]))
+                off += sz
+    else:
+        counts = counts_own
+        z_all = z_dev
+    if counts.sum() == 0:
+        if any_cols > 0:
+            warnings.warn("rank filter removed every coarse column; coarse level disabled")
+        torch.cuda.empty_cache()
+        return CoarseData(csr.shape[0], maps, [np.zeros((int(n_int[s]), 0)) for s in range(N)],
+                          [0] * N, 0) if any_cols > 0 else None
+    nC = int(counts.sum())
     owner = np.asarray(owner, dtype=np.int64)
-    posint = np.empty(csr.shape[0], dtype=np.int64)
-    for m in maps:
-        posint[m.interior] = np.arange(m.interior.size)
-    A0 = torch.zeros((nC, nC), dtype=torch.float64, device=dev)
-    for s, m in enumerate(maps):
-        if counts[s] == 0:
-            continue
-        own = owner[m.indices]
-        order = np.argsort(own, kind="stable")
-        so = own[order]
-        cuts = np.nonzero(np.diff(so))[0] + 1
-        groups = np.split(order, cuts)
-        W = w_dev[s]
-        for grp in groups:
-            j = int(own[grp[0]])
-            if counts[j] == 0:
-                continue
-            rows_j = torch.as_tensor(posint[m.indices[grp]], device=dev)
-            Zj = z_dev[j].index_select(0, rows_j)
-            Wg = W.index_select(0, torch.as_tensor(grp, device=dev))
-            A0[cstart[j]:cstart[j + 1], cstart[s]:cstart[s + 1]] += Zj.mT @ Wg
+    A0 = assemble_a0_columns(maps, owner, z_all, w_dev, counts, own, dev)
+    if sharded:
+        shard.coll.allreduce(A0, op="sum")
     if symmetric:
         A0 = 0.5 * (A0 + A0.mT)
     nnz = int(torch.count_nonzero(A0))
@@ -292,11 +356,15 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             raise RuntimeError("coarse operator is numerically singular")
         A0inv = torch.linalg.lu_solve(LU, piv, torch.eye(nC, dtype=torch.float64, device=dev)).contiguous()
         del LU, piv
-    zcat = torch.cat([z.reshape(-1) for z in z_dev]).contiguous()
+    if sharded:  # one replicated coarse operator, bit-identical on every rank
+        shard.coll.broadcast(A0inv, src=0)
+    zcat = (torch.cat([z_dev[s].reshape(-1) for s in own]) if len(own) else
+            torch.zeros(1, dtype=torch.float64, device=dev)).contiguous()
     k32 = np.asarray(counts, dtype=np.int32)
     handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
-                                       _lib.ptr(A0inv.contiguous()), s_ptr))
+                                       _lib.ptr(A0inv), s_ptr))
     torch.cuda.current_stream().synchronize()
-    del A0, A0inv, zcat, z_dev, w_dev
+    z_list = [z_host[s] if s in z_host else z_all[s].cpu().numpy() for s in range(N)]
+    del A0, A0inv, zcat, z_dev, w_dev, z_all
     torch.cuda.empty_cache()
-    return CoarseData(csr.shape[0], maps, z_host, counts, nnz)
+    return CoarseData(csr.shape[0], maps, z_list, [int(c) for c in counts], nnz)

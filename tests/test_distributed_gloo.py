@@ -1,0 +1,117 @@
+"""Multi-rank host logic of the sharded path on CPU: world_size 2 over gloo (no GPU).
+
+Covers the slab decomposition, the collectives used by sharded setup (max pivot, variable-length
+all-gather of coarse blocks, broadcast of the NCCL id) and the sharded Galerkin assembly: the sum
+over ranks of their A0 column blocks equals the single-process A0."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import golden, golden_csr
+from paper_2401_03915_b200 import distributed as Dd
+from paper_2401_03915_b200 import partition as Pt
+from paper_2401_03915_b200.gpu_setup import assemble_a0_columns
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _problem():
+    d = golden("cfg2_m16")
+    a = golden_csr(d)
+    g = Pt.symmetrized_graph(a)
+    maps = Pt.extend_overlap(g, Pt.Partition(int(d["n_sub"]), d["owner"]), 1)
+    rng = np.random.default_rng(42)
+    counts = np.array([3 + (s % 3) for s in range(len(maps))], dtype=np.int64)
+    z = {s: torch.as_tensor(rng.standard_normal((m.interior.size, counts[s]))) for s, m in enumerate(maps)}
+    w = {s: torch.as_tensor(rng.standard_normal((m.n_local, counts[s]))) for s, m in enumerate(maps)}
+    return d["owner"].astype(np.int64), maps, counts, z, w
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        coll = Dd.TorchCollective()
+        owner, maps, counts, z, w = _problem()
+        lo, hi = Dd.slab_ranges([m.n_local ** 2 for m in maps], world)[rank]
+        # collectives used by the sharded setup
+        t = torch.tensor([float(rank + 1), float(10 * rank)], dtype=torch.float64)
+        coll.allreduce(t, op="max")
+        got = coll.allgather_list(torch.arange(rank + 2, dtype=torch.float64))
+        blob = coll.broadcast_bytes(b"nccl-id-bytes" if rank == 0 else None)
+        # sharded Galerkin assembly: own column blocks, then the sum over ranks
+        zs = {s: z[s] for s in range(len(maps))}
+        part = assemble_a0_columns(maps, owner, zs, w, counts, range(lo, hi), torch.device("cpu"))
+        coll.allreduce(part, op="sum")
+        full = assemble_a0_columns(maps, owner, zs, w, counts, range(len(maps)), torch.device("cpu"))
+        out.put((rank, t.tolist(), [g.tolist() for g in got], blob, (lo, hi),
+                 float((part - full).abs().max()), float(full.abs().max())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_host_logic_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(2)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ranges = [r[4] for r in res]
+    assert ranges[0][0] == 0 and ranges[0][1] == ranges[1][0] and ranges[1][1] == 8
+    for rank, t, got, blob, _, err, scale in res:
+        assert t == [2.0, 10.0]
+        assert got == [[0.0, 1.0], [0.0, 1.0, 2.0]]
+        assert blob == b"nccl-id-bytes"
+        assert err <= 1e-14 * scale
+
+
+def test_slab_ranges_balanced_and_contiguous():
+    w = np.array([5, 1, 1, 1, 5, 1, 1, 1], dtype=float)
+    r = Dd.slab_ranges(w, 2)
+    assert r == [(0, 4), (4, 8)]
+    r3 = Dd.slab_ranges(np.ones(10), 3)
+    assert r3[0][0] == 0 and r3[-1][1] == 10
+    assert all(a[1] == b[0] for a, b in zip(r3, r3[1:]))
+    assert all(hi > lo for lo, hi in r3)
+    with pytest.raises(ValueError):
+        Dd.slab_ranges(np.ones(2), 3)
+
+
+def test_thread_collective_semantics():
+    import threading
+    colls = Dd.ThreadCollective.make(3)
+    res = [None] * 3
+
+    def body(i):
+        c = colls[i]
+        t = torch.tensor([float(i), float(-i)], dtype=torch.float64)
+        s = c.allreduce(t.clone(), "sum")
+        m = c.allreduce(t.clone(), "max")
+        g = c.allgather_list(torch.full((i + 1,), float(i)))
+        b = c.broadcast(torch.tensor([float(i)]), src=2)
+        res[i] = (s.tolist(), m.tolist(), [x.tolist() for x in g], b.tolist())
+
+    ts = [threading.Thread(target=body, args=(i,)) for i in range(3)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    for r in res:
+        assert r[0] == [3.0, -3.0] and r[1] == [2.0, 0.0]
+        assert r[2] == [[0.0], [1.0, 1.0], [2.0, 2.0, 2.0]] and r[3] == [2.0]
