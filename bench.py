@@ -319,6 +319,9 @@ def main():
                    "overlap": cfg.overlap, "modes_per_subdomain": cfg.n_modes, "solver": cfg.solver,
                    "tol": cfg.tol, "restart": cfg.restart,
                    "iterations_per_solve": rep.iterations, "n_coarse": pre.report.n_coarse,
+                   "local_operator": pre.local_kind,
+                   "min_cut_gap": (min(pre.coarse.cut_gaps.values()) if pre.coarse is not None
+                                   and getattr(pre.coarse, "cut_gaps", None) else None),
                    "final_rel_residual": float(rep.residuals[-1]), "true_rel_residual": true_res,
                    "setup_s": t_setup, "generate_s": t_gen,
                    "time_to_solution_s": t_setup + ms / args.steps / 1e3,

@@ -99,6 +99,16 @@ int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first, int32_t count, double* o
  * factor_dense solve closures (src/subdomain.py:72-95) used at src/precond.py:117-118. */
 int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first, int32_t count, const double* inv,
                                 int64_t ld, void* stream);
+/* Banded Cholesky local operators (SPD matrices; alternative to the inverse tiles).
+ * tls_set_local_kind(ctx, 1) before tls_subdomains_upload.  For a batch of owned subdomains:
+ * L = Cholesky factor of the block in factor order (row-major count x ld x ld, identity
+ * padded), dinv = inverses of its 64x64 diagonal tiles (count x nbmax x 64 x 64 row-major),
+ * perm (HOST, concatenated) = local index stored at each factor position, kcnt (HOST,
+ * concatenated) = panel tile count K_I of every 64-row block (band: L[I, I-K_I .. I]). */
+int32_t tls_set_local_kind(tls_ctx* ctx, int32_t kind);
+int32_t tls_store_local_band(tls_ctx* ctx, int32_t first, int32_t count, const double* L,
+                             int64_t ld, const double* dinv, int32_t nbmax, const int32_t* perm,
+                             const int32_t* kcnt, void* stream);
 /* Coarse space (src/coarse.py:23-49): per subdomain a dense block Z_s of shape
  * n_interior[s] x k[s] (row-major, device, concatenated in subdomain order), columns
  * [col_start[s], col_start[s]+k[s]) of the global basis; a0inv = (Z^T A Z)^{-1}

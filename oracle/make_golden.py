@@ -117,7 +117,7 @@ def csr_fields(a):
 
 
 def config_case(name, a, sym, owner, n_sub, overlap, n_modes, coarse, solver, tol, restart=None,
-                maxit=500, rhs_seed=0, n_apply=2):
+                maxit=500, rhs_seed=0, n_apply=2, store_matrix=True, gen=""):
     mat = T.SparseMat(a, symmetric=sym)
     one_level = "asm" if sym else "ras"
     combine = "additive" if sym else "deflated"
@@ -135,7 +135,8 @@ def config_case(name, a, sym, owner, n_sub, overlap, n_modes, coarse, solver, to
     else:
         x, it, conv, hist = gmres_restarted(mat, pre, b, tol, maxit, restart)
     true_res = float(np.linalg.norm(b - mat.matvec(x)) / np.linalg.norm(b))
-    save(name, **csr_fields(a), symmetric=sym, owner=np.asarray(owner, np.int64), n_sub=n_sub,
+    mfields = csr_fields(a) if store_matrix else {}
+    save(name, **mfields, gen=gen, symmetric=sym, owner=np.asarray(owner, np.int64), n_sub=n_sub,
          overlap=overlap, n_modes=n_modes, coarse=coarse, solver=solver, tol=tol,
          restart=-1 if restart is None else restart, maxit=maxit, b=b, r=np.array(rs), z=np.array(zs),
          z_one=np.array(z1), z_coarse=np.array(zc), x=x, iterations=it, converged=conv,
@@ -160,6 +161,11 @@ def main():
     config_case("cfg4_m32", a, sym, owner, nsub, 1, 20, "svd", "gmres", 1e-7, restart=50)
     a, sym, owner, nsub = P.CONFIGS[5].scaled(16, 8, angle_block=8).build()
     config_case("cfg5_m16", a, sym, owner, nsub, 1, 12, "gevp", "pcg", 1e-8)
+    # many subdomains / several setup batches: 216 subdomains of 8^3 (matrix regenerated in tests)
+    cfg = P.CONFIGS[2].scaled(48, 8)
+    a, sym, owner, nsub = cfg.build()
+    config_case("cfg2_m48", a, sym, owner, nsub, 1, 16, "gevp", "pcg", 1e-8, n_apply=1,
+                store_matrix=False, gen="2:48:8")
     # config-4 family with 64 subdomains: the reference's GMRES(50) stagnates
     a, sym, owner, nsub = P.CONFIGS[4].scaled(64, 8).build()
     config_case("cfg4_m64_stall", a, sym, owner, nsub, 1, 20, "svd", "gmres", 1e-7, restart=50,

@@ -102,6 +102,14 @@ struct tls_ctx {
   int gm_exec_cols[2] = {0, 0};
   int gm_exec_launches[2] = {0, 0};
   int launches = 0;  // kernels enqueued since the counter was reset
+  // ---- banded Cholesky local operators (local_kind == 1)
+  int local_kind = 0;                 // 0: packed inverse tiles, 1: band factors
+  std::vector<BandDesc> h_band;
+  BandDesc* d_band = nullptr;
+  std::vector<void*> band_allocs;
+  std::vector<int> h_perm;            // per owned subdomain: perm[p] = local index at position p
+  double band_bytes = 0.0;            // stored factor bytes (read twice per apply)
+  size_t band_smem = 0;
   // ---- sharding: this handle owns global subdomains [own_lo, own_hi)
   int own_lo = 0, own_hi = -1, nsub_global = 0;
   Comm* comm = nullptr;
@@ -206,6 +214,12 @@ static int spmv_lpr(tls_ctx* ctx, cudaStream_t s, const double* x, double* y, co
 enum { L_LOCAL = 0, L_COARSE = 1, L_ALL = 2 };
 
 static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done) {
+  if (ctx->local_kind == 1 && which != L_COARSE) {
+    k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done);
+    CKL();
+    if (which == L_LOCAL) return TLS_OK;
+    which = L_COARSE;
+  }
   int u0 = 0, nu = 0, o0 = 0, no = 0;
   if (which == L_LOCAL) { nu = ctx->nu_local; no = ctx->no_local; }
   if (which == L_COARSE) { u0 = ctx->nu_local; nu = ctx->nu_coarse; o0 = ctx->no_local; no = ctx->no_coarse; }
@@ -398,6 +412,8 @@ void tls_ctx_destroy(tls_ctx* ctx) {
                      &ctx->V, &ctx->H, &ctx->cs, &ctx->sn, &ctx->gv, &ctx->yv, &ctx->h1, &ctx->h2};
   for (double** v : vecs) dfree(*v);
   dfree(ctx->pcg); dfree(ctx->gm);
+  for (void* pb : ctx->band_allocs) cudaFree(pb);
+  dfree(ctx->d_band);
   if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
   if (ctx->h_x) cudaFreeHost(ctx->h_x);
   dfree(ctx->ab);
@@ -502,9 +518,29 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     xo += (long long)nt * TT;
   }
   ctx->Xloc = xo;
-  ctx->tile_doubles = tiles * TT * TT;
+  ctx->tile_doubles = ctx->local_kind == 1 ? 0 : tiles * TT * TT;
   dfree(ctx->tiles);
   TRY(dalloc(ctx, ctx->tiles, ctx->tile_doubles));
+  if (ctx->local_kind == 1) {
+    ctx->h_band.assign(n_sub, BandDesc{});
+    int maxnb = 0;
+    for (int s = 0; s < n_sub; ++s) {
+      ctx->h_band[s].n = ctx->h_n[s];
+      ctx->h_band[s].nb = ctx->h_blk[s].nt;
+      ctx->h_band[s].xoff = ctx->h_blk[s].xoff;
+      maxnb = std::max(maxnb, ctx->h_blk[s].nt);
+    }
+    TRY(upload(ctx, ctx->d_band, ctx->h_band.data(), n_sub));
+    ctx->band_smem = sizeof(double) * ((size_t)maxnb * TT + 8 * TT + TT);
+    // the attribute is per function (process-wide): only ever raise it
+    static size_t smem_set = 0;
+    if (ctx->band_smem > smem_set) {
+      CK(cudaFuncSetAttribute(k_band_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->band_smem));
+      smem_set = ctx->band_smem;
+    }
+    ctx->h_perm.assign(tot, -1);
+    ctx->band_bytes = 0.0;
+  }
   for (int s = 0; s < n_sub; ++s) ctx->h_blk[s].tiles = ctx->tiles + tbase[s] * TT * TT;
   TRY(upload(ctx, ctx->d_blk, ctx->h_blk.data(), n_sub + 1));
   ctx->stored.assign(n_sub, 0);
@@ -547,6 +583,7 @@ int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first_g, int32_t count, co
   const int first = first_g - ctx->own_lo;
   if (first < 0 || count <= 0 || first + count > ctx->nsub)
     return fail(ctx, TLS_ERR_ARG, "subdomain range not owned by this handle");
+  if (ctx->local_kind != 0) return fail(ctx, TLS_ERR_STATE, "handle stores band factors, not inverses");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
   dim3 g(512, count);
@@ -639,15 +676,25 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   if (one_level != TLS_ASM && one_level != TLS_RAS) return fail(ctx, TLS_ERR_ARG, "unknown one-level kind");
   if (combine < TLS_NONE || combine > TLS_DEFLATED) return fail(ctx, TLS_ERR_ARG, "unknown combination");
   for (int s = 0; s < ctx->nsub; ++s)
-    if (!ctx->stored[s]) return fail(ctx, TLS_ERR_STATE, "local inverse of subdomain " + std::to_string(s) + " missing");
+    if (!ctx->stored[s])
+      return fail(ctx, TLS_ERR_STATE, "local operator of subdomain " + std::to_string(s + ctx->own_lo) + " missing");
   CK(cudaSetDevice(ctx->device));
   ctx->one_level = one_level;
   ctx->combine = ctx->ncoarse > 0 ? combine : TLS_NONE;
   const int nsub = ctx->nsub, n = ctx->n;
   // padded local layout
+  // local position of local index l (band mode stores the local vector in its factor order)
+  std::vector<int> posl(ctx->h_idx.size());
+  for (int s = 0; s < nsub; ++s)
+    for (int l = 0; l < ctx->h_n[s]; ++l)
+      posl[ctx->h_off[s] + l] = ctx->local_kind == 1 ? -1 : l;
+  if (ctx->local_kind == 1)
+    for (int s = 0; s < nsub; ++s)
+      for (int p = 0; p < ctx->h_n[s]; ++p) posl[ctx->h_off[s] + ctx->h_perm[ctx->h_off[s] + p]] = p;
   std::vector<int> gidx(ctx->Xloc, -1);
   for (int s = 0; s < nsub; ++s)
-    for (int l = 0; l < ctx->h_n[s]; ++l) gidx[ctx->h_blk[s].xoff + l] = ctx->h_idx[ctx->h_off[s] + l];
+    for (int l = 0; l < ctx->h_n[s]; ++l)
+      gidx[ctx->h_blk[s].xoff + posl[ctx->h_off[s] + l]] = ctx->h_idx[ctx->h_off[s] + l];
   TRY(upload(ctx, ctx->d_gidx, gidx.data(), ctx->Xloc));
   ctx->coarse_xoff = ctx->Xloc;
   ctx->X = ctx->Xloc + (ctx->ncoarse > 0 ? (long long)ctx->h_blk[nsub].nt * TT : 0);
@@ -661,10 +708,14 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   std::vector<int> red;
   int slot = 0;
   ctx->algo_local = 0.0;
-  for (int s = 0; s < nsub; ++s) {
+  for (int s = 0; s < nsub && ctx->local_kind == 0; ++s) {
     plan_block(s, ctx->h_blk[s].nt, ctx->sym, slot, units, outs, red);
     const double ns = ctx->h_n[s];
     ctx->algo_local += ctx->sym ? 8.0 * ns * (ns + 1) / 2 + 8.0 * ns : 8.0 * ns * ns + 8.0 * ns;
+  }
+  if (ctx->local_kind == 1) {  // two sweeps over the stored factor + x in, y out
+    ctx->algo_local = 2.0 * ctx->band_bytes;
+    for (int s = 0; s < nsub; ++s) ctx->algo_local += 16.0 * ctx->h_n[s];
   }
   ctx->nu_local = (int)units.size();
   ctx->no_local = (int)outs.size();
@@ -695,7 +746,7 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
     const int lim = one_level == TLS_RAS ? ctx->h_nint[s] : ctx->h_n[s];
     for (int l = 0; l < lim; ++l) {
       const int g = ctx->h_idx[ctx->h_off[s] + l];
-      pos[fill[g]++] = (int)(ctx->h_blk[s].xoff + l);
+      pos[fill[g]++] = (int)(ctx->h_blk[s].xoff + posl[ctx->h_off[s] + l]);
     }
   }
   TRY(upload(ctx, ctx->d_pull_ptr, cnt.data(), n + 1));
@@ -1133,11 +1184,13 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
-  CKL();
-  CK(cudaEventRecord(e0, s));
-  for (int i = 0; i < reps; ++i) {
-    k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
+  const bool band = ctx->local_kind == 1;
+  for (int i = 0; i <= reps; ++i) {
+    if (i == 1) CK(cudaEventRecord(e0, s));
+    if (band)
+      k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr);
+    else
+      k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
     CKL();
   }
   CK(cudaEventRecord(e1, s));
@@ -1147,7 +1200,86 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (avg_ms) *avg_ms = ms / reps;
-  if (algorithmic_bytes) *algorithmic_bytes = ctx->algo_local + (which == L_ALL ? ctx->algo_coarse : 0.0);
+  if (algorithmic_bytes)
+    *algorithmic_bytes = ctx->algo_local + (which == L_ALL && !band ? ctx->algo_coarse : 0.0);
+  return TLS_OK;
+}
+
+// ---- banded local factors ---------------------------------------------------------------------
+int32_t tls_set_local_kind(tls_ctx* ctx, int32_t kind) {
+  if (!ctx || (kind != 0 && kind != 1)) return ctx ? fail(ctx, TLS_ERR_ARG, "local kind is 0 (inverse tiles) or 1 (band)") : TLS_ERR_ARG;
+  if (ctx->nsub) return fail(ctx, TLS_ERR_STATE, "set the local kind before tls_subdomains_upload");
+  ctx->local_kind = kind;
+  return TLS_OK;
+}
+
+int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const double* L,
+                             int64_t ld, const double* dinv, int32_t nbmax, const int32_t* perm,
+                             const int32_t* kcnt, void* stream) {
+  if (!ctx) return TLS_ERR_ARG;
+  if (ctx->local_kind != 1) return fail(ctx, TLS_ERR_STATE, "handle is not in band mode");
+  if (!ctx->sym) return fail(ctx, TLS_ERR_ARG, "band factors need a symmetric matrix (Cholesky)");
+  const int first = first_g - ctx->own_lo;
+  if (first < 0 || count <= 0 || first + count > ctx->nsub)
+    return fail(ctx, TLS_ERR_ARG, "subdomain range not owned by this handle");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  // step offsets of the batch: one allocation for data, one for offsets, one for counts
+  std::vector<long long> offs;
+  std::vector<int> ks;
+  std::vector<long long> dstart(count), ostart(count);
+  long long tot = 0;
+  int kp = 0;
+  for (int b = 0; b < count; ++b) {
+    const int sl = first + b, nb = ctx->h_band[sl].nb;
+    if (nb > nbmax) return fail(ctx, TLS_ERR_ARG, "nbmax smaller than a subdomain's block count");
+    if (ctx->h_n[sl] > ld) return fail(ctx, TLS_ERR_ARG, "ld smaller than a local block");
+    dstart[b] = tot;
+    ostart[b] = (long long)offs.size();
+    for (int I = 0; I < nb; ++I) {
+      const int K = kcnt[kp + I];
+      if (K < 0 || K > I) return fail(ctx, TLS_ERR_ARG, "band panel count out of range");
+      offs.push_back(tot - dstart[b]);
+      ks.push_back(K);
+      tot += (long long)(K + 1) * TT * TT;
+    }
+    kp += nb;
+  }
+  double* data = nullptr;
+  long long* d_off = nullptr;
+  int* d_k = nullptr;
+  if (cudaMalloc((void**)&data, sizeof(double) * tot) != cudaSuccess ||
+      cudaMalloc((void**)&d_off, sizeof(long long) * offs.size()) != cudaSuccess ||
+      cudaMalloc((void**)&d_k, sizeof(int) * ks.size()) != cudaSuccess)
+    return fail(ctx, TLS_ERR_OOM, "band storage allocation failed");
+  ctx->band_allocs.push_back(data);
+  ctx->band_allocs.push_back(d_off);
+  ctx->band_allocs.push_back(d_k);
+  ctx->dev_bytes += (int64_t)(sizeof(double) * tot + sizeof(long long) * offs.size() + sizeof(int) * ks.size());
+  CK(cudaMemcpy(d_off, offs.data(), sizeof(long long) * offs.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_k, ks.data(), sizeof(int) * ks.size(), cudaMemcpyHostToDevice));
+  long long pp = 0;
+  for (int b = 0; b < count; ++b) {
+    const int sl = first + b;
+    BandDesc& bd = ctx->h_band[sl];
+    bd.data = data + dstart[b];
+    bd.step_off = d_off + ostart[b];
+    bd.kcnt = d_k + ostart[b];
+    ctx->band_bytes += 8.0 * (double)((b + 1 < count ? dstart[b + 1] : tot) - dstart[b]);
+    const int n = ctx->h_n[sl];
+    for (int p = 0; p < n; ++p) {
+      const int l = perm[pp + p];
+      if (l < 0 || l >= n) return fail(ctx, TLS_ERR_ARG, "band permutation out of range");
+      ctx->h_perm[ctx->h_off[sl] + p] = l;
+    }
+    pp += n;
+  }
+  CK(cudaMemcpy(ctx->d_band + first, ctx->h_band.data() + first, sizeof(BandDesc) * count, cudaMemcpyHostToDevice));
+  dim3 g(std::min(nbmax, 256), count);
+  k_pack_band<<<g, NTHR, 0, s>>>(ctx->d_band, first, L, ld, dinv, nbmax);
+  CKL();
+  for (int i = first; i < first + count; ++i) ctx->stored[i] = 1;
+  ctx->finalized = false;
   return TLS_OK;
 }
 

@@ -725,4 +725,147 @@ __global__ void k_pack_tiles(const BlkDesc* __restrict__ blks, int first_blk, co
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K3b  banded Cholesky local solves y_i = A_ii^{-1} r_i = L^{-T} L^{-1} r_i for SPD blocks
+// (the cho_solve closure of src/subdomain.py:80-82, same factorisation, other row order).
+// The local rows are ordered lexicographically by global index (a plane sweep for grid
+// operators), so the Cholesky factor lives in a band of ~one grid plane.  Per 64-row block I
+// the factor is stored as one contiguous "step": K_I panel tiles L[I, I-K_I .. I-1] and the
+// inverse of the diagonal tile (64x64 fp64, column-major).  One CTA per subdomain keeps the
+// whole local vector in shared memory and sweeps: forward u_I = D_I^{-1}(v_I - panel.u) with
+// row partials (lane-local, cross-warp smem sum), backward y_J = D_J^{-T} v_J and
+// v_{J-k} -= L_{J,J-k}^T y_J with column partials completed inside the warp (warp_reduce8).
+// Both sweeps stream every stored byte once; the loads do not depend on the solve, only the
+// FMAs do, and 4 CTAs per SM overlap one CTA's barriers with the others' loads.
+// ---------------------------------------------------------------------------------------
+struct BandDesc {
+  const double* data;          // steps of this subdomain
+  const long long* step_off;   // nb offsets (doubles) into data
+  const int* kcnt;             // nb panel tile counts
+  long long xoff;              // offset of the local vector in xloc / yloc
+  int n, nb, pad0, pad1;
+};
+
+__global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restrict__ bands,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ y, const int* done) {
+  if (done && *done) return;
+  extern __shared__ __align__(16) double sm[];
+  const BandDesc b = bands[blockIdx.x];
+  const int npad = b.nb * TT;
+  double* v = sm;                  // npad
+  double* red = sm + npad;         // 8 x 64
+  double* t = red + 8 * TT;        // 64
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c0 = warp * 8;
+  for (int i = threadIdx.x; i < npad; i += NTHR) v[i] = x[b.xoff + i];
+  __syncthreads();
+  // forward sweep: L u = x
+  for (int I = 0; I < b.nb; ++I) {
+    const double* blk = b.data + b.step_off[I];
+    const int K = b.kcnt[I];
+    double ra0 = 0.0, ra1 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
+      double2 w[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) w[kk] = ldg_stream2(tp + kk * TT);
+      const double* uj = v + (I - K + k) * TT + c0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) { ra0 += w[kk].x * uj[kk]; ra1 += w[kk].y * uj[kk]; }
+    }
+    red[warp * TT + 2 * lane] = ra0;
+    red[warp * TT + 2 * lane + 1] = ra1;
+    __syncthreads();
+    if (threadIdx.x < TT) {
+      double sacc = v[I * TT + threadIdx.x];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc -= red[w * TT + threadIdx.x];
+      t[threadIdx.x] = sacc;
+    }
+    __syncthreads();
+    {
+      const double* dp = blk + (long long)K * TT * TT + c0 * TT + 2 * lane;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double2 w = ldg_stream2(dp + kk * TT);
+        d0 += w.x * t[c0 + kk];
+        d1 += w.y * t[c0 + kk];
+      }
+      red[warp * TT + 2 * lane] = d0;
+      red[warp * TT + 2 * lane + 1] = d1;
+    }
+    __syncthreads();
+    if (threadIdx.x < TT) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc += red[w * TT + threadIdx.x];
+      v[I * TT + threadIdx.x] = sacc;
+    }
+    __syncthreads();
+  }
+  // backward sweep: L^T y = u
+  const int colsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  for (int J = b.nb - 1; J >= 0; --J) {
+    const double* blk = b.data + b.step_off[J];
+    const int K = b.kcnt[J];
+    {
+      const double* dp = blk + (long long)K * TT * TT + c0 * TT + 2 * lane;
+      const double u0 = v[J * TT + 2 * lane], u1 = v[J * TT + 2 * lane + 1];
+      double cp[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double2 w = ldg_stream2(dp + kk * TT);
+        cp[kk] = w.x * u0 + w.y * u1;
+      }
+      const double yv = warp_reduce8(cp, lane);
+      __syncthreads();  // every warp has read v_J
+      if ((lane & 3) == 0) v[J * TT + c0 + colsel] = yv;
+      __syncthreads();
+    }
+    const double y0 = v[J * TT + 2 * lane], y1 = v[J * TT + 2 * lane + 1];
+    for (int k = 0; k < K; ++k) {
+      const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
+      double cp[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double2 w = ldg_stream2(tp + kk * TT);
+        cp[kk] = w.x * y0 + w.y * y1;
+      }
+      const double val = warp_reduce8(cp, lane);
+      if ((lane & 3) == 0) v[(J - K + k) * TT + c0 + colsel] -= val;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
+}
+
+// pack band steps of one subdomain batch: L (row-major ld x ld, lexicographic order, identity
+// padding) and the inverted diagonal tiles dinv (nbmax x 64 x 64 row-major per subdomain)
+__global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, const double* __restrict__ L,
+                            long long ld, const double* __restrict__ dinv, int nbmax) {
+  const int bi = blockIdx.y;
+  const BandDesc bd = bands[first_band + bi];
+  const double* Lb = L + (long long)bi * ld * ld;
+  const double* Db = dinv + (long long)bi * nbmax * TT * TT;
+  for (int I = blockIdx.x; I < bd.nb; I += gridDim.x) {
+    const int K = bd.kcnt[I];
+    double* dst = const_cast<double*>(bd.data) + bd.step_off[I];
+    for (int k = 0; k <= K; ++k) {
+      const int J = I - K + k;
+      for (int e = threadIdx.x; e < TT * TT; e += NTHR) {
+        const int c = e / TT, r = e % TT;
+        double val;
+        if (k < K) {
+          const long long gi = (long long)I * TT + r, gj = (long long)J * TT + c;
+          val = (gi < ld && gj < ld) ? Lb[gi * ld + gj] : 0.0;
+        } else {
+          val = Db[(long long)I * TT * TT + r * TT + c];
+        }
+        dst[(long long)k * TT * TT + e] = val;
+      }
+    }
+  }
+}
+
 }  // namespace tls

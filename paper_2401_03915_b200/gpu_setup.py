@@ -134,14 +134,26 @@ def _fix_signs(torch, v):
     return v * sgn[None, :]
 
 
-def _subdomain_columns(torch, kind, A, B, n, ni, nin, tau, n_modes):
-    """Coarse columns (n_int x k, device) of one subdomain from A_ii and B = A_ii^{-1}."""
+def _cut_gap(values, keep):
+    """Relative gap between the last selected and the first rejected value (inf if none)."""
+    if keep.size == 0 or keep[-1] + 1 >= values.size or values[keep[-1]] <= 0:
+        return float("inf")
+    return float((values[keep[-1]] - values[keep[-1] + 1]) / values[keep[-1]])
+
+
+def _subdomain_columns(torch, kind, A, Bring, n, ni, nin, tau, n_modes):
+    """Coarse columns (n_int x k, device) of one subdomain, and the selection's cut gap.
+
+    ``A`` = dense A_ii (local order), ``Bring`` = A_ii^{-1}[:, ring] (n x n_b, local order).
+    The cut gap (sigma_k - sigma_{k+1}) / sigma_k measures how well-posed the selected span
+    is: a gap near rounding level means the top-k cut splits a multiplet.
+    """
     nb = n - nin
     dev = A.device
     if nb == 0 or kind == "none":
-        return torch.zeros((ni, 0), dtype=torch.float64, device=dev)
-    F = B[:ni, nin:n]
-    B22 = B[nin:n, nin:n]
+        return torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf")
+    F = Bring[:ni]
+    B22 = Bring[nin:n]
     if kind == "gevp":
         H = F.mT @ (A[:ni, :ni] @ F)
         H = 0.5 * (H + H.mT)
@@ -156,20 +168,52 @@ def _subdomain_columns(torch, kind, A, B, n, ni, nin, tau, n_modes):
         sig = torch.sqrt(torch.clamp(w, min=0.0)).cpu().numpy()
         keep = _select(sig, tau, n_modes)
         if keep.size == 0:
-            return torch.zeros((ni, 0), dtype=torch.float64, device=dev)
+            return torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf")
         U = torch.linalg.solve_triangular(C.mT, Q[:, torch.as_tensor(keep, device=dev)], upper=True)
-        V = B[:n, nin:n] @ U
+        V = Bring @ U
         V = _fix_signs(torch, V)
-        return V[:ni].contiguous()
+        return V[:ni].contiguous(), _cut_gap(sig, keep)
     E = torch.linalg.solve(B22, F, left=False)  # E B22 = F  ->  ext[:n_int]
     if kind == "full":
-        return E.contiguous()
+        return E.contiguous(), float("inf")
     U, S, _ = torch.linalg.svd(E, full_matrices=False)
-    keep = _select(S.cpu().numpy(), tau, n_modes)
+    sv = S.cpu().numpy()
+    keep = _select(sv, tau, n_modes)
     if keep.size == 0:
-        return torch.zeros((ni, 0), dtype=torch.float64, device=dev)
+        return torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf")
     V = _fix_signs(torch, U[:, torch.as_tensor(keep, device=dev)])
-    return V.contiguous()
+    return V.contiguous(), _cut_gap(sv, keep)
+
+
+def _band_factor(torch, A, idx_list, n_list, ld):
+    """Lexicographic factor order, band profile, Cholesky and diagonal-tile inverses of a batch.
+
+    Returns (L_P, Dinv, perms, kcnts, info): L_P[b] is the Cholesky factor of A[b] with rows and
+    columns in ascending global-index order (a plane sweep for grid operators, so L is banded),
+    kcnts[b][I] the number of 64-wide panel tiles left of the diagonal in block-row I.
+    """
+    cnt = A.shape[0]
+    dev = A.device
+    nbk = ld // 64
+    P = torch.arange(ld, device=dev).repeat(cnt, 1)
+    perms = []
+    for b in range(cnt):
+        perm = np.argsort(idx_list[b], kind="stable").astype(np.int64)
+        perms.append(perm.astype(np.int32))
+        P[b, : n_list[b]] = torch.as_tensor(perm, device=dev)
+    AP = torch.gather(A, 1, P[:, :, None].expand(cnt, ld, ld))
+    AP = torch.gather(AP, 2, P[:, None, :].expand(cnt, ld, ld)).contiguous()
+    first = torch.argmax((AP != 0).to(torch.int8), dim=2)           # row profile f(i)
+    bmin = first.view(cnt, nbk, 64).min(dim=2).values // 64
+    kc = (torch.arange(nbk, device=dev)[None, :] - bmin).clamp(min=0).cpu().numpy().astype(np.int32)
+    L, info = torch.linalg.cholesky_ex(AP)
+    del AP
+    L = L.contiguous()  # cuSOLVER returns column-major
+    Ld = L.view(cnt, nbk, 64, nbk, 64).diagonal(dim1=1, dim2=3).permute(0, 3, 1, 2)
+    eye = torch.eye(64, dtype=torch.float64, device=dev).expand(cnt, nbk, 64, 64)
+    Dinv = torch.linalg.solve_triangular(Ld, eye, upper=False).contiguous()
+    kcnts = [kc[b, : -(-n_list[b] // 64)] for b in range(cnt)]
+    return L, Dinv, perms, kcnts, info, P
 
 
 def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
@@ -207,8 +251,12 @@ def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
 
 
 def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_modes, drop_tol,
-                           batch=None, mem_fraction=0.35, shard=None):
-    """Run steps 1-5 into ``handle`` (this rank's slab when ``shard``); returns CoarseData or None."""
+                           batch=None, mem_fraction=0.35, shard=None, local="auto"):
+    """Run steps 1-5 into ``handle`` (this rank's slab when ``shard``); returns CoarseData or None.
+
+    ``local``: "inverse" (packed A_ii^{-1} tiles), "band" (banded Cholesky factors; SPD only) or
+    "auto" (band for symmetric matrices, inverse otherwise).
+    """
     torch = _torch()
     lib = handle.lib
     dev = torch.device("cuda", handle.device)
@@ -225,12 +273,23 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         shard.attach(handle)
     else:
         lo, hi = 0, N
+    if local == "auto":
+        local = "band" if symmetric else "inverse"
+    if local not in ("band", "inverse"):
+        raise ValueError(f"unknown local operator kind {local!r}")
+    if local == "band" and not symmetric:
+        raise ValueError("banded Cholesky local operators need a symmetric matrix")
+    band = local == "band"
+    if band:
+        handle.check(lib.tls_set_local_kind(handle.ctx, 1))
     offsets = np.concatenate([[0], np.cumsum(n_loc)]).astype(np.int64)
     indices = np.concatenate([m.indices for m in maps]).astype(np.int64)
     n_int32 = n_int.astype(np.int32)  # keep alive across the call (raw pointer below)
     handle.check(lib.tls_subdomains_upload(handle.ctx, N, _lib.ptr(offsets), _lib.ptr(indices),
                                            _lib.ptr(n_int32)))
     ld = int(n_loc[lo:hi].max())
+    if band:
+        ld = -(-ld // 64) * 64
     if batch is None:
         free, _ = torch.cuda.mem_get_info(dev)
         per = 8.0 * ld * ld * 4.0 + 4.0 * csr.shape[0]
@@ -239,10 +298,47 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     want_coarse = coarse != "none"
     z_dev = {}
     w_dev = {}
+    gaps = {}
     for first in range(lo, hi, batch):
         cnt = min(batch, hi - first)
         A = torch.empty((cnt, ld, ld), dtype=torch.float64, device=dev)
         handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
+        if band:
+            idx_list = [maps[first + b].indices for b in range(cnt)]
+            n_list = [int(n_loc[first + b]) for b in range(cnt)]
+            L, Dinv, perms, kcnts, info, P = _band_factor(torch, A, idx_list, n_list, ld)
+            bad = torch.nonzero(info).flatten().cpu().numpy()
+            if bad.size:
+                s = first + int(bad[0])
+                raise SubdomainSetupError(s, "factorization failed: the local block is not positive definite")
+            perm_cat = np.concatenate(perms).astype(np.int32)
+            k_cat = np.concatenate(kcnts).astype(np.int32)
+            handle.check(lib.tls_store_local_band(handle.ctx, first, cnt, _lib.ptr(L), ld, _lib.ptr(Dinv),
+                                                  ld // 64, _lib.ptr(perm_cat), _lib.ptr(k_cat), s_ptr))
+            torch.cuda.current_stream().synchronize()  # the host arrays above stay alive until here
+            del Dinv
+            if want_coarse:
+                for b in range(cnt):
+                    s = first + b
+                    n, ni = int(n_loc[s]), int(n_int[s])
+                    nin = n - int(n_bnd[s])
+                    if n == nin:
+                        Bring = torch.zeros((n, 0), dtype=torch.float64, device=dev)
+                    else:
+                        pinv = torch.empty(ld, dtype=torch.long, device=dev)
+                        pinv[P[b]] = torch.arange(ld, device=dev)
+                        E = torch.zeros((ld, n - nin), dtype=torch.float64, device=dev)
+                        E[pinv[nin:n], torch.arange(n - nin, device=dev)] = 1.0
+                        Bring = torch.cholesky_solve(E, L[b])[pinv[:n]]
+                    Z, gaps[s] = _subdomain_columns(torch, coarse, A[b], Bring, n, ni, nin, tau, n_modes)
+                    if Z.shape[1]:
+                        nz = torch.any(Z != 0, dim=0)
+                        if not bool(nz.all()):
+                            Z = Z[:, nz].contiguous()
+                    z_dev[s] = Z
+                    w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
+            del A, L
+            continue
         if symmetric:
             L, info = torch.linalg.cholesky_ex(A)
             bad = torch.nonzero(info).flatten().cpu().numpy()
@@ -269,7 +365,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                 s = first + b
                 n, ni = int(n_loc[s]), int(n_int[s])
                 nin = n - int(n_bnd[s])
-                Z = _subdomain_columns(torch, coarse, A[b], Binv[b], n, ni, nin, tau, n_modes)
+                Z, gaps[s] = _subdomain_columns(torch, coarse, A[b], Binv[b, :n, nin:n], n, ni, nin, tau,
+                                                n_modes)
                 # assemble_coarse_basis drops identically zero columns (src/coarse.py:99-103)
                 if Z.shape[1]:
                     nz = torch.any(Z != 0, dim=0)
@@ -367,4 +464,6 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     z_list = [z_host[s] if s in z_host else z_all[s].cpu().numpy() for s in range(N)]
     del A0, A0inv, zcat, z_dev, w_dev, z_all
     torch.cuda.empty_cache()
-    return CoarseData(csr.shape[0], maps, z_list, [int(c) for c in counts], nnz)
+    cd = CoarseData(csr.shape[0], maps, z_list, [int(c) for c in counts], nnz)
+    cd.cut_gaps = gaps  # owned subdomains only
+    return cd

@@ -12,6 +12,8 @@ import pytest
 
 from conftest import CONFIG_CASES, golden, golden_csr
 
+CASES = CONFIG_CASES + ["cfg2_m48"]
+
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
@@ -39,8 +41,9 @@ def _setup(B, name):
         d = golden(name)
         a = golden_csr(d)
         mat = B.SparseMat(a, symmetric=bool(d["symmetric"]))
+        # small batches so that multi-batch setup is exercised on every case
         pre = B.setup(mat, int(d["n_sub"]), overlap=int(d["overlap"]), owner=d["owner"],
-                      coarse=str(d["coarse"]), n_modes=int(d["n_modes"]))
+                      coarse=str(d["coarse"]), n_modes=int(d["n_modes"]), batch=5)
         _cache[name] = (d, a, mat, pre)
     return _cache[name]
 
@@ -59,7 +62,7 @@ def test_spmv_matches_csr(B, name):
     assert yt.is_cuda and np.allclose(yt.cpu().numpy(), y, rtol=0, atol=0)
 
 
-@pytest.mark.parametrize("name", CONFIG_CASES)
+@pytest.mark.parametrize("name", CASES)
 def test_setup_index_sets_and_report(B, name):
     d, a, mat, pre = _setup(B, name)
     assert np.array_equal(np.concatenate([m.indices for m in pre.maps]), d["indices"])
@@ -69,7 +72,7 @@ def test_setup_index_sets_and_report(B, name):
     assert (pre.one_level, pre.combine) == (str(d["one_level"]), str(d["combine"]))
 
 
-@pytest.mark.parametrize("name", CONFIG_CASES)
+@pytest.mark.parametrize("name", CASES)
 def test_apply_matches_reference(B, name):
     d, a, mat, pre = _setup(B, name)
     tol_apply = _tols(name)[0]
@@ -79,7 +82,7 @@ def test_apply_matches_reference(B, name):
         np.testing.assert_allclose(pre.coarse_apply(r), zc, rtol=0, atol=tol_apply * np.abs(zc).max())
 
 
-@pytest.mark.parametrize("name", CONFIG_CASES)
+@pytest.mark.parametrize("name", CASES)
 def test_solve_matches_reference(B, name):
     d, a, mat, pre = _setup(B, name)
     _, tol_hist, tol_x = _tols(name)
@@ -268,3 +271,23 @@ def test_config4_family_stall_history(B):
     x, rep = B.gmres(mat, pre, d["b"], tol=1e-7, maxit=100, restart=50)
     assert rep.iterations == 100 and not rep.converged
     np.testing.assert_allclose(rep.residuals, d["history"], rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_m24", "cfg5_m16"])
+def test_band_and_inverse_local_operators_agree(B, name):
+    """The two stored local operators (banded Cholesky sweeps vs packed inverse tiles)."""
+    d = golden(name)
+    a = golden_csr(d)
+    mat = B.SparseMat(a, symmetric=True)
+    kw = dict(overlap=int(d["overlap"]), owner=d["owner"], coarse=str(d["coarse"]), n_modes=int(d["n_modes"]))
+    pb = B.setup(mat, int(d["n_sub"]), local="band", **kw)
+    pi = B.setup(mat, int(d["n_sub"]), local="inverse", **kw)
+    assert pb.local_kind == "band" and pi.local_kind == "inverse"
+    for r, z1 in zip(d["r"], d["z_one"]):
+        zb, zi = pb.apply_one_level(r), pi.apply_one_level(r)
+        np.testing.assert_allclose(zb, z1, rtol=0, atol=1e-11 * np.abs(z1).max())
+        np.testing.assert_allclose(zb, zi, rtol=0, atol=1e-11 * np.abs(z1).max())
+    xb, rb = B.pcg(mat, pb, d["b"], tol=float(d["tol"]))
+    xi, ri = B.pcg(mat, pi, d["b"], tol=float(d["tol"]))
+    assert abs(rb.iterations - ri.iterations) <= 1
+    assert pb.device_bytes() < pi.device_bytes() or a.shape[0] < 5000

@@ -22,7 +22,7 @@ def test_config1_generator_is_reference_matrix():
     assert np.array_equal(owner, d["owner"])
 
 
-@pytest.mark.parametrize("name", CONFIG_CASES)
+@pytest.mark.parametrize("name", CONFIG_CASES + ["cfg2_m48"])
 def test_overlap_and_coloring_bit_exact(name):
     d = golden(name)
     a = golden_csr(d)
