@@ -111,9 +111,9 @@ def _max_over_ranks(value, world, torch):
     return float(t.item())
 
 
-def _traffic_from_profile(config_id):
+def _traffic_from_profile(config_id, kernel):
     """DRAM bytes per launch of the local-solve kernel from the committed ncu summary."""
-    path = os.path.join(REPO, "profiles", f"ncu_symv_cfg{config_id}.json")
+    path = os.path.join(REPO, "profiles", f"ncu_{kernel}_cfg{config_id}.json")
     try:
         with open(path) as fh:
             return float(json.load(fh)["dram_bytes_per_launch"])
@@ -306,7 +306,7 @@ def main():
                                           C.c_void_p(stream.cuda_stream)))
     peak, peak_kind = _peaks()
     achieved = algo.value / (avg_ms.value * 1e-3) / 1e9
-    traffic = _traffic_from_profile(cfg.cid)
+    traffic = _traffic_from_profile(cfg.cid, "band" if pre.local_kind == "band" else "symv")
     # true residual of the final solve
     xr = x.cpu().numpy()
     true_res = float(np.linalg.norm(b_host - a @ xr) / np.linalg.norm(b_host))
@@ -331,7 +331,9 @@ def main():
                                    else "1 GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_symv_tiles (batched local + coarse inverse tiles)",
+                     "kernel": ("k_band_solve (banded Cholesky forward+backward sweeps, all subdomains)"
+                                if pre.local_kind == "band" else
+                                "k_symv_tiles (batched local + coarse inverse tiles)"),
                      "algorithmic_bytes_per_launch": algo.value, "avg_launch_ms": avg_ms.value},
         "e2e": e2e,
         "gpu_launches": launches,

@@ -38,6 +38,8 @@ a library call on the SETUP path; the per-iteration path is all in-tree CUDA.
 from __future__ import annotations
 
 import math
+import os
+import time
 import warnings
 
 import numpy as np
@@ -47,6 +49,7 @@ from . import _lib
 from .device import _torch, stream_ptr
 from .errors import SubdomainSetupError
 
+VERBOSE = bool(int(os.environ.get("TLS_VERBOSE", "0")))
 TIE_GUARD = 1e-12
 TOPK_TAU = 1e-300
 EPS = float(np.finfo(float).eps)
@@ -115,6 +118,19 @@ def warm_linalg(device=None):
     torch.linalg.solve_triangular(L, a, upper=False)
     torch.linalg.cholesky(a)
     torch.cuda.synchronize(dev)
+
+
+def _log(t0, msg):
+    if VERBOSE:
+        print(f"[tls setup {time.perf_counter() - t0:7.1f}s] {msg}", flush=True)
+
+
+def _symmetrize_lower_inplace(torch, A, bs=4096):
+    """A[lower incl. diagonal blocks] <- 0.5 (A + A^T) without a dense temporary copy."""
+    n = A.shape[0]
+    for i0 in range(0, n, bs):
+        i1 = min(i0 + bs, n)
+        A[i0:i1, :i1] = 0.5 * (A[i0:i1, :i1] + A[:i1, i0:i1].mT)
 
 
 def _select(values, tau, n_modes):
@@ -299,8 +315,13 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     z_dev = {}
     w_dev = {}
     gaps = {}
+    t0 = time.perf_counter()
+    _log(t0, f"subdomains [{lo},{hi}) of {N}, local={local}, ld={ld}, batch={batch}")
     for first in range(lo, hi, batch):
         cnt = min(batch, hi - first)
+        if first > lo:
+            torch.cuda.empty_cache()  # band storage is cudaMalloc'ed by the library per batch
+            _log(t0, f"batch at {first}")
         A = torch.empty((cnt, ld, ld), dtype=torch.float64, device=dev)
         handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
         if band:
@@ -434,27 +455,37 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                           [0] * N, 0) if any_cols > 0 else None
     nC = int(counts.sum())
     owner = np.asarray(owner, dtype=np.int64)
+    torch.cuda.empty_cache()
+    _log(t0, f"local operators done; assembling A0 ({nC} x {nC})")
     A0 = assemble_a0_columns(maps, owner, z_all, w_dev, counts, own, dev)
+    del w_dev
     if sharded:
         shard.coll.allreduce(A0, op="sum")
+    nnz = int(torch.count_nonzero(A0))  # the pattern of Z^T A Z is symmetric
+    _log(t0, "A0 assembled; factorising")
     if symmetric:
-        A0 = 0.5 * (A0 + A0.mT)
-    nnz = int(torch.count_nonzero(A0))
-    if symmetric:
+        # symmetrise (src/coarse.py:169-170) the lower triangle Cholesky reads, in place
+        _symmetrize_lower_inplace(torch, A0)
         L, info = torch.linalg.cholesky_ex(A0)
+        del A0
         if int(info) != 0:
             raise RuntimeError(f"coarse operator is not positive definite: {int(info)}-th leading minor")
-        A0inv = torch.cholesky_inverse(L)
-        A0inv = (0.5 * (A0inv + A0inv.mT)).contiguous()
+        torch.cuda.empty_cache()
+        # the packed-tile store reads the lower triangle (and full diagonal tiles) only
+        A0inv = torch.cholesky_inverse(L).contiguous()
         del L
+        A0 = None
     else:
         LU, piv, info = torch.linalg.lu_factor_ex(A0)
+        del A0
+        A0 = None
         if int(info) != 0 or float(LU.diagonal().abs().min()) <= nC * EPS * float(LU.abs().max()):
             raise RuntimeError("coarse operator is numerically singular")
         A0inv = torch.linalg.lu_solve(LU, piv, torch.eye(nC, dtype=torch.float64, device=dev)).contiguous()
         del LU, piv
     if sharded:  # one replicated coarse operator, bit-identical on every rank
         shard.coll.broadcast(A0inv, src=0)
+    _log(t0, "coarse operator inverted; uploading")
     zcat = (torch.cat([z_dev[s].reshape(-1) for s in own]) if len(own) else
             torch.zeros(1, dtype=torch.float64, device=dev)).contiguous()
     k32 = np.asarray(counts, dtype=np.int32)
@@ -462,7 +493,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                                        _lib.ptr(A0inv), s_ptr))
     torch.cuda.current_stream().synchronize()
     z_list = [z_host[s] if s in z_host else z_all[s].cpu().numpy() for s in range(N)]
-    del A0, A0inv, zcat, z_dev, w_dev, z_all
+    del A0, A0inv, zcat, z_dev, z_all
     torch.cuda.empty_cache()
     cd = CoarseData(csr.shape[0], maps, z_list, [int(c) for c in counts], nnz)
     cd.cut_gaps = gaps  # owned subdomains only
