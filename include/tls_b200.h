@@ -110,7 +110,8 @@ int32_t tls_store_local_band(tls_ctx* ctx, int32_t first, int32_t count, const d
                              int64_t ld, const double* dinv, int32_t nbmax, const int32_t* perm,
                              const int32_t* kcnt, void* stream);
 /* Coarse space (src/coarse.py:23-49): per subdomain a dense block Z_s of shape
- * n_interior[s] x k[s] (row-major, device, concatenated in subdomain order), columns
+ * n_interior[s] x k[s] stored column by column (k[s] x n_interior[s] row-major, device,
+ * concatenated in subdomain order), columns
  * [col_start[s], col_start[s]+k[s]) of the global basis; a0inv = (Z^T A Z)^{-1}
  * (row-major n_coarse^2, device).  k == NULL or n_coarse == 0 disables the coarse level. */
 int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, const double* basis,

@@ -76,7 +76,7 @@ struct tls_ctx {
   int* d_gidx = nullptr;
   int *d_pull_ptr = nullptr, *d_pull_pos = nullptr;
   long long* d_zrow = nullptr;
-  int *d_zk = nullptr, *d_zc = nullptr;
+  int *d_zk = nullptr, *d_zc = nullptr, *d_zst = nullptr;
   double *xloc = nullptr, *yloc = nullptr, *slots = nullptr;
   int64_t nslots = 0;
   double algo_local = 0.0, algo_coarse = 0.0;
@@ -104,6 +104,7 @@ struct tls_ctx {
   int launches = 0;  // kernels enqueued since the counter was reset
   // ---- banded Cholesky local operators (local_kind == 1)
   int local_kind = 0;                 // 0: packed inverse tiles, 1: band factors
+  size_t restrict_smem = 0;
   std::vector<BandDesc> h_band;
   BandDesc* d_band = nullptr;
   std::vector<void*> band_allocs;
@@ -243,7 +244,7 @@ static int enq_gather(tls_ctx* ctx, cudaStream_t s, const double* r, const int* 
 }
 
 static int enq_restrict(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
-  k_restrict<<<ctx->nsub, NTHR, 0, s>>>(ctx->d_sub_idxoff, ctx->d_idx, ctx->d_nint, ctx->d_zoff,
+  k_restrict<<<ctx->nsub, NTHR, ctx->restrict_smem, s>>>(ctx->d_sub_idxoff, ctx->d_idx, ctx->d_nint, ctx->d_zoff,
                                         ctx->d_kcnt, ctx->d_cstart, ctx->d_Z, r,
                                         ctx->xloc + ctx->coarse_xoff, done);
   CKL();
@@ -254,7 +255,7 @@ template <int MODE, int DOT>
 static int enq_prolong(tls_ctx* ctx, cudaStream_t s, const double* qv, const double* wv,
                        const double* rdot, double* z, const int* done) {
   k_prolong<MODE, DOT><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->d_pull_ptr, ctx->d_pull_pos, ctx->yloc,
-                                               ctx->d_zrow, ctx->d_zk, ctx->d_zc, ctx->d_Z,
+                                               ctx->d_zrow, ctx->d_zst, ctx->d_zk, ctx->d_zc, ctx->d_Z,
                                                ctx->yloc + ctx->coarse_xoff, qv, wv, rdot, z,
                                                ctx->part, done);
   CKL();
@@ -406,7 +407,7 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   dfree(ctx->d_blk); dfree(ctx->tiles); dfree(ctx->d_Z); dfree(ctx->ctiles); dfree(ctx->d_zoff);
   dfree(ctx->d_kcnt); dfree(ctx->d_cstart); dfree(ctx->d_units); dfree(ctx->d_outs); dfree(ctx->d_red);
   dfree(ctx->d_gidx); dfree(ctx->d_pull_ptr); dfree(ctx->d_pull_pos); dfree(ctx->d_zrow);
-  dfree(ctx->d_zk); dfree(ctx->d_zc); dfree(ctx->xloc); dfree(ctx->yloc); dfree(ctx->slots);
+  dfree(ctx->d_zk); dfree(ctx->d_zc); dfree(ctx->d_zst); dfree(ctx->xloc); dfree(ctx->yloc); dfree(ctx->slots);
   double** vecs[] = {&ctx->t1, &ctx->t2, &ctx->t3, &ctx->t4, &ctx->t5, &ctx->t6, &ctx->t7, &ctx->vb,
                      &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz, &ctx->hist, &ctx->part,
                      &ctx->V, &ctx->H, &ctx->cs, &ctx->sn, &ctx->gv, &ctx->yv, &ctx->h1, &ctx->h2};
@@ -518,6 +519,16 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     xo += (long long)nt * TT;
   }
   ctx->Xloc = xo;
+  {
+    int mi = 1;
+    for (int s = 0; s < n_sub; ++s) mi = std::max(mi, ctx->h_nint[s]);
+    ctx->restrict_smem = sizeof(double) * (size_t)mi;
+    static size_t rsmem_set = 48 * 1024;
+    if (ctx->restrict_smem > rsmem_set) {
+      CK(cudaFuncSetAttribute(k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->restrict_smem));
+      rsmem_set = ctx->restrict_smem;
+    }
+  }
   ctx->tile_doubles = ctx->local_kind == 1 ? 0 : tiles * TT * TT;
   dfree(ctx->tiles);
   TRY(dalloc(ctx, ctx->tiles, ctx->tile_doubles));
@@ -637,7 +648,7 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
   cb.tiles = ctx->ctiles;
   ctx->h_blk[ctx->nsub] = cb;
   CK(cudaMemcpy(ctx->d_blk, ctx->h_blk.data(), sizeof(BlkDesc) * (ctx->nsub + 1), cudaMemcpyHostToDevice));
-  dim3 g(512, 1);
+  dim3 g((unsigned)std::min<int64_t>(ntiles, 8192), 1);
   k_pack_tiles<<<g, NTHR, 0, s>>>(ctx->d_blk, ctx->nsub, a0inv, n_coarse, 0);
   CKL();
   return TLS_OK;
@@ -753,13 +764,14 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   TRY(upload(ctx, ctx->d_pull_pos, pos.data(), (int64_t)pos.size()));
   // coarse prolongation rows: node g in the interior of s at position p -> Z_s[p, :]
   std::vector<long long> zrow(n, -1);
-  std::vector<int> zk(n, 0), zc(n, 0);
+  std::vector<int> zk(n, 0), zc(n, 0), zst(n, 0);
   if (ctx->ncoarse > 0) {
     for (int s = 0; s < nsub; ++s) {
       if (ctx->h_k[s] == 0) continue;
       for (int p = 0; p < ctx->h_nint[s]; ++p) {
         const int g = ctx->h_idx[ctx->h_off[s] + p];
-        zrow[g] = ctx->h_zoff[s] + (long long)p * ctx->h_k[s];
+        zrow[g] = ctx->h_zoff[s] + p;  // column-major block: element (p, t) at + t * n_int
+        zst[g] = ctx->h_nint[s];
         zk[g] = ctx->h_k[s];
         zc[g] = ctx->h_cstart[s];
       }
@@ -769,6 +781,7 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   }
   TRY(upload(ctx, ctx->d_zrow, zrow.data(), n));
   TRY(upload(ctx, ctx->d_zk, zk.data(), n));
+  TRY(upload(ctx, ctx->d_zst, zst.data(), n));
   TRY(upload(ctx, ctx->d_zc, zc.data(), n));
   if (ctx->ncoarse == 0) {
     std::vector<int> zero(nsub, 0);

@@ -130,9 +130,9 @@ __global__ void __launch_bounds__(NTHR) k_gather(long long m, const int* __restr
 // ---------------------------------------------------------------------------------------
 // K5  coarse restriction c = Z^T r (CoarseSpace.restrict, src/coarse.py:40-41).  Z is
 //     block-diagonal by subdomain with interior support (src/coarse.py:1-7): one CTA per
-//     subdomain, Z_s row-major n_int x k.  c lands in the coarse segment of xloc.
+//     subdomain, Z_s stored column by column (k x n_int, each column contiguous) so every
+//     load instruction is coalesced.  c lands in the coarse segment of xloc.
 // ---------------------------------------------------------------------------------------
-constexpr int KCH = 16;  // columns per pass
 __global__ void __launch_bounds__(NTHR) k_restrict(const long long* __restrict__ sub_idxoff,
                                                    const int* __restrict__ idx,
                                                    const int* __restrict__ nint,
@@ -143,39 +143,30 @@ __global__ void __launch_bounds__(NTHR) k_restrict(const long long* __restrict__
                                                    const double* __restrict__ r,
                                                    double* __restrict__ c, const int* done) {
   if (done && *done) return;
-  __shared__ double sh[NTHR / 32][KCH];
+  extern __shared__ __align__(16) double rs[];  // r on this subdomain's interior
   const int s = blockIdx.x;
   const int ks = kcnt[s], ni = nint[s];
   if (ks == 0) return;
   const int* id = idx + sub_idxoff[s];
-  const double* zs = Z + zoff[s];
+  for (int p = threadIdx.x; p < ni; p += NTHR) rs[p] = __ldg(r + __ldg(id + p));
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k0 = 0; k0 < ks; k0 += KCH) {
-    double acc[KCH];
-#pragma unroll
-    for (int k = 0; k < KCH; ++k) acc[k] = 0.0;
-    for (int p = threadIdx.x; p < ni; p += NTHR) {
-      const double rv = __ldg(r + __ldg(id + p));
-      const double* zr = zs + (long long)p * ks + k0;
-#pragma unroll
-      for (int k = 0; k < KCH; ++k)
-        if (k0 + k < ks) acc[k] += __ldg(zr + k) * rv;
+  const double* zs = Z + zoff[s];
+  for (int col = warp; col < ks; col += NTHR / 32) {
+    const double* zc = zs + (long long)col * ni;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int p = lane;
+    for (; p + 96 < ni; p += 128) {  // 4 independent coalesced loads in flight per lane
+      a0 += __ldg(zc + p) * rs[p];
+      a1 += __ldg(zc + p + 32) * rs[p + 32];
+      a2 += __ldg(zc + p + 64) * rs[p + 64];
+      a3 += __ldg(zc + p + 96) * rs[p + 96];
     }
+    for (; p < ni; p += 32) a0 += __ldg(zc + p) * rs[p];
+    double v = (a0 + a1) + (a2 + a3);
 #pragma unroll
-    for (int k = 0; k < KCH; ++k) {
-      double v = acc[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-      if (lane == 0) sh[warp][k] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < KCH && k0 + threadIdx.x < ks) {
-      double v = 0.0;
-#pragma unroll
-      for (int w = 0; w < NTHR / 32; ++w) v += sh[w][threadIdx.x];
-      c[cstart[s] + k0 + threadIdx.x] = v;
-    }
-    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    if (lane == 0) c[cstart[s] + col] = v;
   }
 }
 
@@ -324,6 +315,7 @@ __global__ void __launch_bounds__(NTHR) k_prolong(int n, const int* __restrict__
                                                   const int* __restrict__ pull_pos,
                                                   const double* __restrict__ yloc,
                                                   const long long* __restrict__ zrow,
+                                                  const int* __restrict__ zst,
                                                   const int* __restrict__ zk,
                                                   const int* __restrict__ zc,
                                                   const double* __restrict__ Z,
@@ -345,8 +337,8 @@ __global__ void __launch_bounds__(NTHR) k_prolong(int n, const int* __restrict__
     if (MODE >= 1) {
       const long long zo = __ldg(zrow + g);
       if (zo >= 0) {
-        const int k = __ldg(zk + g), c0 = __ldg(zc + g);
-        for (int t = 0; t < k; ++t) cz += __ldg(Z + zo + t) * __ldg(yc + c0 + t);
+        const int k = __ldg(zk + g), c0 = __ldg(zc + g), st = __ldg(zst + g);
+        for (int t = 0; t < k; ++t) cz += __ldg(Z + zo + (long long)t * st) * __ldg(yc + c0 + t);
       }
     }
     double out;
@@ -698,9 +690,11 @@ __global__ void k_extract(int count, const long long* __restrict__ sub_idxoff,
     }
   }
 }
-// tile (I,J) of subdomain s <- inv[b] (row-major ld x ld), zero outside n_s
+// tile (I,J) of subdomain s <- inv[b] (row-major ld x ld), zero outside n_s.  One CTA per tile:
+// coalesced row reads into shared memory, column-major (tile layout) coalesced writes.
 __global__ void k_pack_tiles(const BlkDesc* __restrict__ blks, int first_blk, const double* __restrict__ inv,
                              long long ld, long long batch_stride) {
+  __shared__ double tile[TT][TT + 1];
   const int b = blockIdx.y;
   const BlkDesc bd = blks[first_blk + b];
   const long long ntiles = bd.sym ? (long long)bd.nt * (bd.nt + 1) / 2 : (long long)bd.nt * bd.nt;
@@ -716,11 +710,17 @@ __global__ void k_pack_tiles(const BlkDesc* __restrict__ blks, int first_blk, co
       I = (int)(t / bd.nt);
       J = (int)(t % bd.nt);
     }
+    __syncthreads();
+    for (int e = threadIdx.x; e < TT * TT; e += NTHR) {
+      const int r = e / TT, c = e % TT;  // row-major walk: consecutive threads, consecutive columns
+      const int gi = I * TT + r, gj = J * TT + c;
+      tile[r][c] = (gi < bd.n && gj < bd.n) ? src[(long long)gi * ld + gj] : 0.0;
+    }
+    __syncthreads();
     double* dst = const_cast<double*>(bd.tiles) + t * (TT * TT);
     for (int e = threadIdx.x; e < TT * TT; e += NTHR) {
-      const int c = e / TT, r = e % TT;
-      const int gi = I * TT + r, gj = J * TT + c;
-      dst[e] = (gi < bd.n && gj < bd.n) ? src[(long long)gi * ld + gj] : 0.0;
+      const int c = e / TT, r = e % TT;  // column-major tile layout
+      dst[e] = tile[r][c];
     }
   }
 }

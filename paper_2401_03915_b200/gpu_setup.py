@@ -201,6 +201,116 @@ def _subdomain_columns(torch, kind, A, Bring, n, ni, nin, tau, n_modes):
     return V.contiguous(), _cut_gap(sv, keep)
 
 
+def _orth(torch, X):
+    """Batched orthonormalisation: CholeskyQR2 (two GEMM + p x p Cholesky passes)."""
+    for _ in range(2):
+        G = X.mT @ X
+        R, info = torch.linalg.cholesky_ex(G, upper=True)
+        if bool((info != 0).any()):  # numerically rank-deficient block: Householder fallback
+            return torch.linalg.qr(X).Q
+        X = torch.linalg.solve_triangular(R, X, upper=True, left=False)
+    return X
+
+
+def topk_subspace(torch, M, k, tol=1e-14, maxit=400, seed=20240103):
+    """Top-k eigenpairs (descending) of a batch of symmetric PSD matrices M (b, m, m).
+
+    Block subspace iteration on p = max(2k, k+8) vectors with the squared operator (two
+    batched GEMMs per sweep), CholeskyQR2 re-orthonormalisation and Rayleigh-Ritz; stops when
+    every wanted Ritz pair has residual ||M x - theta x|| <= tol * theta_1.  This is the batched
+    replacement of the dense generalized eigensolve of src/spectral.py:69-85 for a fixed number
+    of modes; small matrices go to a dense batched eigh.
+    """
+    b, m, _ = M.shape
+    p = min(m, max(2 * k, k + 8))
+    if m <= max(96, 2 * p):
+        w, Q = torch.linalg.eigh(M)
+        return torch.flip(w, dims=[-1])[:, :k], torch.flip(Q, dims=[-1])[:, :, :k], 0
+    gen = torch.Generator(device=M.device)
+    gen.manual_seed(seed)
+    X = _orth(torch, torch.randn((b, m, p), generator=gen, dtype=M.dtype, device=M.device))
+    scale = None
+    for it in range(1, maxit + 1):
+        X = _orth(torch, M @ (M @ X))
+        if it % 4 == 0 or it == maxit:
+            MX = M @ X
+            T = X.mT @ MX
+            # the p x p projected problem is tiny: solve it on the host (batched GPU eigh loops
+            # one cuSOLVER call per matrix once p > 32)
+            th, S = torch.linalg.eigh((0.5 * (T + T.mT)).cpu())
+            th = torch.flip(th, dims=[-1])[:, :k].to(M.device)
+            S = torch.flip(S, dims=[-1])[:, :, :k].to(M.device)
+            Xk = X @ S
+            R = MX @ S - Xk * th[:, None, :]
+            if scale is None:
+                scale = th[:, :1].abs().clamp(min=1e-300)
+            res = (R.norm(dim=1) / scale).max()
+            if float(res) <= tol:
+                return th, Xk, it
+    return th, Xk, maxit
+
+
+def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes):
+    """Coarse columns of a batch of band-factored subdomains, batched by shape.
+
+    Returns per subdomain (Z, cut_gap); gevp with a fixed mode count runs the batched subspace
+    iteration, everything else the per-subdomain dense path.
+    """
+    cnt = A.shape[0]
+    ld = A.shape[1]
+    dev = A.device
+    out = [None] * cnt
+    groups = {}
+    for b in range(cnt):
+        groups.setdefault((ns[b], nis[b], nins[b]), []).append(b)
+    for (n, ni, nin), bs in groups.items():
+        nbr = n - nin
+        bi = torch.as_tensor(bs, device=dev)
+        if nbr == 0 or kind == "none":
+            for b in bs:
+                out[b] = (torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf"))
+            continue
+        Pg = P.index_select(0, bi)
+        pinv = torch.empty_like(Pg)
+        pinv.scatter_(1, Pg, torch.arange(ld, device=dev).expand_as(Pg))
+        E = torch.zeros((len(bs), ld, nbr), dtype=torch.float64, device=dev)
+        rows = pinv[:, nin:n]                                       # (g, nbr) factor positions of the ring
+        E.view(len(bs), -1)[torch.arange(len(bs), device=dev)[:, None],
+                            rows * nbr + torch.arange(nbr, device=dev)[None, :]] = 1.0
+        X = torch.cholesky_solve(E, L.index_select(0, bi))          # A_P^{-1} E  (factor order)
+        del E
+        Bring = torch.gather(X, 1, pinv[:, :n, None].expand(len(bs), n, nbr))  # local order
+        del X
+        if kind == "gevp" and n_modes is not None:
+            F = Bring[:, :ni]
+            B22 = Bring[:, nin:n]
+            Ag = A.index_select(0, bi)
+            H = F.mT @ (Ag[:, :ni, :ni] @ F)
+            H = 0.5 * (H + H.mT)
+            C, info = torch.linalg.cholesky_ex(0.5 * (B22 + B22.mT))
+            Xs = torch.linalg.solve_triangular(C, H, upper=False)
+            M = torch.linalg.solve_triangular(C, Xs.mT, upper=False)
+            M = 0.5 * (M + M.mT)
+            kk = min(n_modes + 1, nbr)
+            th, Q, _ = topk_subspace(torch, M, kk)
+            sig = torch.sqrt(torch.clamp(th, min=0.0)).cpu().numpy()
+            U = torch.linalg.solve_triangular(C.mT, Q, upper=True)
+            V = Bring @ U
+            idx = torch.argmax(V.abs(), dim=1)
+            sgn = torch.where(torch.gather(V, 1, idx[:, None, :])[:, 0, :] < 0, -1.0, 1.0)
+            V = V * sgn[:, None, :]
+            for j, b in enumerate(bs):
+                keep = _select(sig[j], tau, n_modes)
+                gap = _cut_gap(sig[j], keep)
+                out[b] = (V[j][:ni, torch.as_tensor(keep, device=dev)].contiguous(), gap)
+            del Ag, H, C, Xs, M, U, V
+        else:
+            for j, b in enumerate(bs):
+                out[b] = _subdomain_columns(torch, kind, A[b], Bring[j], n, ni, nin, tau, n_modes)
+        del Bring
+    return out
+
+
 def _band_factor(torch, A, idx_list, n_list, ld):
     """Lexicographic factor order, band profile, Cholesky and diagonal-tile inverses of a batch.
 
@@ -339,19 +449,15 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             torch.cuda.current_stream().synchronize()  # the host arrays above stay alive until here
             del Dinv
             if want_coarse:
+                cols = _coarse_band_batch(torch, coarse, A, L, P,
+                                          [int(n_loc[first + b]) for b in range(cnt)],
+                                          [int(n_int[first + b]) for b in range(cnt)],
+                                          [int(n_loc[first + b] - n_bnd[first + b]) for b in range(cnt)],
+                                          tau, n_modes)
                 for b in range(cnt):
                     s = first + b
                     n, ni = int(n_loc[s]), int(n_int[s])
-                    nin = n - int(n_bnd[s])
-                    if n == nin:
-                        Bring = torch.zeros((n, 0), dtype=torch.float64, device=dev)
-                    else:
-                        pinv = torch.empty(ld, dtype=torch.long, device=dev)
-                        pinv[P[b]] = torch.arange(ld, device=dev)
-                        E = torch.zeros((ld, n - nin), dtype=torch.float64, device=dev)
-                        E[pinv[nin:n], torch.arange(n - nin, device=dev)] = 1.0
-                        Bring = torch.cholesky_solve(E, L[b])[pinv[:n]]
-                    Z, gaps[s] = _subdomain_columns(torch, coarse, A[b], Bring, n, ni, nin, tau, n_modes)
+                    Z, gaps[s] = cols[b]
                     if Z.shape[1]:
                         nz = torch.any(Z != 0, dim=0)
                         if not bool(nz.all()):
@@ -486,7 +592,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     if sharded:  # one replicated coarse operator, bit-identical on every rank
         shard.coll.broadcast(A0inv, src=0)
     _log(t0, "coarse operator inverted; uploading")
-    zcat = (torch.cat([z_dev[s].reshape(-1) for s in own]) if len(own) else
+    # column-major blocks (k x n_int): coalesced restriction and prolongation loads
+    zcat = (torch.cat([z_dev[s].mT.contiguous().reshape(-1) for s in own]) if len(own) else
             torch.zeros(1, dtype=torch.float64, device=dev)).contiguous()
     k32 = np.asarray(counts, dtype=np.int32)
     handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
