@@ -37,6 +37,12 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "preconditioned Krylov iters/sec + time-to-solution (fp64); HBM GB/s vs peak"
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    """Progress to stderr (stdout carries only the JSON line)."""
+    print(f"[bench {time.perf_counter() - _T0:8.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 def _peaks():
@@ -125,7 +131,7 @@ def _traffic_from_profile(config_id, kernel):
 # CPU baseline (oracle port of the reference algorithm, bounded sample)
 # --------------------------------------------------------------------------------------------
 
-def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8):
+def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8, sym=True):
     """Per-iteration CPU time of the reference algorithm, measured on a bounded sample.
 
     Timed pieces (numpy/scipy = the reference's own kernels, all host threads):
@@ -157,7 +163,6 @@ def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8):
             layers.append(ring)
             front = ring
         maps[s] = (interior, layers)
-    sym = (a != a.T).nnz == 0
     subs = {s: O.OracleSubdomain(a, maps[s], sym) for s in pick}
     x = rng.standard_normal(n)
     reps = 3
@@ -173,13 +178,15 @@ def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8):
         np.add.at(out, sd.indices, y)
     t_local = (time.perf_counter() - t0) * nsub / len(pick)
     nC = nsub * n_modes
-    m = rng.standard_normal((nC, 64))
-    spd = m @ m.T + nC * np.eye(nC)
+    nCs = min(nC, 8192)  # dense coarse solve timed at <= 8192 and scaled by (n_C / size)^2
+    m = rng.standard_normal((nCs, 64))
+    spd = m @ m.T + nCs * np.eye(nCs)
     fac = sla.cho_factor(spd)
-    c = rng.standard_normal(nC)
+    c = rng.standard_normal(nCs)
     t0 = time.perf_counter()
     sla.cho_solve(fac, c)
-    t_coarse = time.perf_counter() - t0
+    t_coarse = (time.perf_counter() - t0) * (nC / nCs) ** 2
+    del spd, fac, m
     p, r, z, xx = (rng.standard_normal(n) for _ in range(4))
     t0 = time.perf_counter()
     float(p @ x); xx += 0.5 * p; r -= 0.5 * x; float(np.linalg.norm(r)); float(r @ z); p = z + 0.3 * p
@@ -187,9 +194,10 @@ def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8):
     t_iter = t_spmv + t_local + t_coarse + t_vec
     cores = os.cpu_count()
     return {"value": 1.0 / t_iter, "unit": "iters/s", "cores": cores, "kind": "port",
-            "sample": (f"cfg{cfg_id}: {len(pick)} of {nsub} subdomain Cholesky solves (n_i up to "
+            "sample": (f"cfg{cfg_id}: {len(pick)} of {nsub} subdomain {'Cholesky' if sym else 'LU'} solves (n_i up to "
                        f"{max(subs[s].n_local for s in pick)}) + scatter, scaled x{nsub / len(pick):.0f}; "
-                       f"full-size SpMV; n_C={nC} dense Cholesky solve; PCG vector ops; "
+                       f"full-size SpMV; n_C={nC} dense Cholesky solve"
+                       f"{'' if nC == nCs else f' (timed at {nCs}, scaled by (n_C/{nCs})^2)'}; PCG vector ops; "
                        f"one iteration = {t_iter * 1e3:.1f} ms on {cores} host threads"),
             "t_iter_s": t_iter}
 
@@ -217,10 +225,10 @@ def main():
         if rank != 0:
             return
         a, sym, owner, nsub = cfg.build()
-        cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes)
+        cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym)
         times = [cb["t_iter_s"]]
         for _ in range(max(0, args.steps - 1)):
-            times.append(cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes)["t_iter_s"])
+            times.append(cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym)["t_iter_s"])
         val = 1.0 / float(np.mean(times))
         cbo = {k: v for k, v in cb.items() if k != "t_iter_s"}
         cbo["value"] = val
@@ -245,8 +253,10 @@ def main():
     BLD.build()
 
     t0 = time.perf_counter()
+    log(f"generating {cfg.name}")
     a, sym, owner, nsub = cfg.build()
     t_gen = time.perf_counter() - t0
+    log(f"n={a.shape[0]} nnz={a.nnz}; setup")
     mat = B.SparseMat(a, symmetric=sym)
     shard = None
     if world > 1:
@@ -259,10 +269,12 @@ def main():
     n = a.shape[0]
     b_host = cfg.rhs(n)
     b_dev = torch.as_tensor(b_host, device="cuda")
-    solver = (lambda rhs: B.pcg(mat, pre, rhs, tol=cfg.tol)) if cfg.solver == "pcg" else \
-        (lambda rhs: B.gmres(mat, pre, rhs, tol=cfg.tol, restart=cfg.restart))
+    solver = (lambda rhs: B.pcg(mat, pre, rhs, tol=cfg.tol, maxit=cfg.maxit)) if cfg.solver == "pcg" else \
+        (lambda rhs: B.gmres(mat, pre, rhs, tol=cfg.tol, maxit=cfg.maxit, restart=cfg.restart))
+    log(f"setup {t_setup:.1f}s; warm-up")
     for _ in range(args.warmup):
         solver(b_dev)
+    log("timed solves")
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -282,6 +294,7 @@ def main():
     ms = e0.elapsed_time(e1)
     ms = _max_over_ranks(ms, world, torch)
     value = its / (ms / 1e3)
+    log("e2e solves")
     # end to end through the public API with pinned host buffers
     b_pin = torch.from_numpy(b_host.copy()).pin_memory()
     x_pin = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -317,7 +330,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": cfg.name, "n": n, "nnz": int(a.nnz), "subdomains": nsub,
                    "overlap": cfg.overlap, "modes_per_subdomain": cfg.n_modes, "solver": cfg.solver,
-                   "tol": cfg.tol, "restart": cfg.restart,
+                   "tol": cfg.tol, "restart": cfg.restart, "maxit": cfg.maxit,
                    "iterations_per_solve": rep.iterations, "n_coarse": pre.report.n_coarse,
                    "local_operator": pre.local_kind,
                    "min_cut_gap": (min(pre.coarse.cut_gaps.values()) if pre.coarse is not None
@@ -339,8 +352,9 @@ def main():
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    log("cpu baseline")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes)
+        cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym)
         cb.pop("t_iter_s")
         line["cpu_baseline"] = cb
     if rank == 0:

@@ -212,17 +212,33 @@ def _orth(torch, X):
     return X
 
 
-def topk_subspace(torch, M, k, tol=1e-14, maxit=400, seed=20240103):
+def _rayleigh_ritz(torch, M, X, k):
+    MX = M @ X
+    T = X.mT @ MX
+    # the p x p projected problem is tiny: solve it on the host (batched GPU eigh loops one
+    # cuSOLVER call per matrix once p > 32)
+    th_all, S = torch.linalg.eigh((0.5 * (T + T.mT)).cpu())
+    th_all = torch.flip(th_all, dims=[-1]).to(M.device)
+    S = torch.flip(S, dims=[-1]).to(M.device)
+    Xr = X @ S
+    MXr = MX @ S
+    return th_all, Xr, MXr
+
+
+def topk_subspace(torch, M, k, tol=1e-14, maxit=2000, seed=20240103, p=None):
     """Top-k eigenpairs (descending) of a batch of symmetric PSD matrices M (b, m, m).
 
-    Block subspace iteration on p = max(2k, k+8) vectors with the squared operator (two
-    batched GEMMs per sweep), CholeskyQR2 re-orthonormalisation and Rayleigh-Ritz; stops when
-    every wanted Ritz pair has residual ||M x - theta x|| <= tol * theta_1.  This is the batched
-    replacement of the dense generalized eigensolve of src/spectral.py:69-85 for a fixed number
-    of modes; small matrices go to a dense batched eigh.
+    Block subspace iteration with the squared operator (two batched GEMMs per sweep) on
+    p = max(3k, k + 16) vectors, CholeskyQR2 re-orthonormalisation and Rayleigh-Ritz every 4
+    sweeps; stops when every wanted Ritz pair has ||M x - theta x|| <= tol * theta_1 and raises
+    if that does not happen (never returns an unconverged span).  Batched replacement of the
+    dense generalized eigensolve of src/spectral.py:69-85 for a fixed number of modes; small
+    matrices go to a dense batched eigh.  (A Chebyshev filter was tried and rejected: with
+    theta_1 / theta_p >> 1 a useful degree amplifies the top modes ~1e19 x more than the k-th,
+    which destroys the lower wanted directions in fp64.)
     """
     b, m, _ = M.shape
-    p = min(m, max(2 * k, k + 8))
+    p = min(m, p or max(3 * k, k + 16))
     if m <= max(96, 2 * p):
         w, Q = torch.linalg.eigh(M)
         return torch.flip(w, dims=[-1])[:, :k], torch.flip(Q, dims=[-1])[:, :, :k], 0
@@ -230,27 +246,51 @@ def topk_subspace(torch, M, k, tol=1e-14, maxit=400, seed=20240103):
     gen.manual_seed(seed)
     X = _orth(torch, torch.randn((b, m, p), generator=gen, dtype=M.dtype, device=M.device))
     scale = None
+    res = float("inf")
     for it in range(1, maxit + 1):
         X = _orth(torch, M @ (M @ X))
-        if it % 4 == 0 or it == maxit:
-            MX = M @ X
-            T = X.mT @ MX
-            # the p x p projected problem is tiny: solve it on the host (batched GPU eigh loops
-            # one cuSOLVER call per matrix once p > 32)
-            th, S = torch.linalg.eigh((0.5 * (T + T.mT)).cpu())
-            th = torch.flip(th, dims=[-1])[:, :k].to(M.device)
-            S = torch.flip(S, dims=[-1])[:, :, :k].to(M.device)
-            Xk = X @ S
-            R = MX @ S - Xk * th[:, None, :]
+        if it % 4 == 0:
+            th_all, Xr, MXr = _rayleigh_ritz(torch, M, X, k)
             if scale is None:
-                scale = th[:, :1].abs().clamp(min=1e-300)
-            res = (R.norm(dim=1) / scale).max()
-            if float(res) <= tol:
-                return th, Xk, it
-    return th, Xk, maxit
+                scale = th_all[:, :1].abs().clamp(min=1e-300)
+            R = MXr[:, :, :k] - Xr[:, :, :k] * th_all[:, None, :k]
+            res = float((R.norm(dim=1) / scale).max())
+            if res <= tol:
+                return th_all[:, :k], Xr[:, :, :k], it
+            X = Xr  # continue from the Ritz basis (sorted, orthonormal)
+    raise RuntimeError(f"subspace iteration did not converge: residual {res:.2e} after {maxit} sweeps")
 
 
-def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes):
+def band_solve_multi(torch, L, Dinv, kc, E):
+    """X = (L L^T)^{-1} E for a batch of banded Cholesky factors and many right-hand sides.
+
+    Blocked banded forward/backward substitution over 64-row blocks with batched GEMMs: block
+    row I touches only the panel L[I, I-K .. I-1] (K = the batch's largest panel count there),
+    so the work is ~ n * bandwidth * nrhs instead of the dense n^2 * nrhs of cholesky_solve.
+    ``Dinv`` holds the inverted diagonal tiles; ``kc`` (host, (b, nb)) the panel counts.
+    """
+    b, ld, nrhs = E.shape
+    nb = ld // 64
+    kmax = kc.max(axis=0) if kc.size else np.zeros(nb, dtype=np.int64)
+    X = E.clone()
+    for I in range(nb):  # forward: X_I = D_I^{-1} (E_I - L[I, J0:I] X[J0:I])
+        r0, r1 = I * 64, (I + 1) * 64
+        K = int(kmax[I])
+        if K:
+            c0 = r0 - K * 64
+            X[:, r0:r1] -= L[:, r0:r1, c0:r0] @ X[:, c0:r0]
+        X[:, r0:r1] = Dinv[:, I] @ X[:, r0:r1]
+    for I in range(nb - 1, -1, -1):  # backward: X_I = D_I^{-T} X_I; X[J0:I] -= L[I, J0:I]^T X_I
+        r0, r1 = I * 64, (I + 1) * 64
+        X[:, r0:r1] = Dinv[:, I].mT @ X[:, r0:r1]
+        K = int(kmax[I])
+        if K:
+            c0 = r0 - K * 64
+            X[:, c0:r0] -= L[:, r0:r1, c0:r0].mT @ X[:, r0:r1]
+    return X
+
+
+def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=None, kc=None):
     """Coarse columns of a batch of band-factored subdomains, batched by shape.
 
     Returns per subdomain (Z, cut_gap); gevp with a fixed mode count runs the batched subspace
@@ -268,7 +308,7 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes):
         bi = torch.as_tensor(bs, device=dev)
         if nbr == 0 or kind == "none":
             for b in bs:
-                out[b] = (torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf"))
+                out[b] = (torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf"), None)
             continue
         Pg = P.index_select(0, bi)
         pinv = torch.empty_like(Pg)
@@ -277,7 +317,11 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes):
         rows = pinv[:, nin:n]                                       # (g, nbr) factor positions of the ring
         E.view(len(bs), -1)[torch.arange(len(bs), device=dev)[:, None],
                             rows * nbr + torch.arange(nbr, device=dev)[None, :]] = 1.0
-        X = torch.cholesky_solve(E, L.index_select(0, bi))          # A_P^{-1} E  (factor order)
+        if Dinv is not None:   # banded blocked solve (batched GEMMs on the band only)
+            X = band_solve_multi(torch, L.index_select(0, bi), Dinv.index_select(0, bi),
+                                 kc[bs], E)
+        else:
+            X = torch.cholesky_solve(E, L.index_select(0, bi))      # A_P^{-1} E  (factor order)
         del E
         Bring = torch.gather(X, 1, pinv[:, :n, None].expand(len(bs), n, nbr))  # local order
         del X
@@ -299,14 +343,24 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes):
             idx = torch.argmax(V.abs(), dim=1)
             sgn = torch.where(torch.gather(V, 1, idx[:, None, :])[:, 0, :] < 0, -1.0, 1.0)
             V = V * sgn[:, None, :]
-            for j, b in enumerate(bs):
-                keep = _select(sig[j], tau, n_modes)
-                gap = _cut_gap(sig[j], keep)
-                out[b] = (V[j][:ni, torch.as_tensor(keep, device=dev)].contiguous(), gap)
+            keeps = [_select(sig[j], tau, n_modes) for j in range(len(bs))]
+            kk0 = keeps[0].size
+            if all(kp.size == kk0 and np.array_equal(kp, np.arange(kk0)) for kp in keeps):
+                # common case (fixed mode count): one batched epilogue for the whole group
+                Zg = V[:, :ni, :kk0].contiguous()
+                Wg = Ag[:, :n, :ni] @ Zg
+                if kk0 and not bool((Zg != 0).any(dim=1).all()):
+                    Wg = None  # a zero column: let the caller drop it subdomain by subdomain
+                for j, b in enumerate(bs):
+                    out[b] = (Zg[j], _cut_gap(sig[j], keeps[j]), None if Wg is None else Wg[j])
+            else:
+                for j, b in enumerate(bs):
+                    out[b] = (V[j][:ni, torch.as_tensor(keeps[j], device=dev)].contiguous(),
+                              _cut_gap(sig[j], keeps[j]), None)
             del Ag, H, C, Xs, M, U, V
         else:
             for j, b in enumerate(bs):
-                out[b] = _subdomain_columns(torch, kind, A[b], Bring[j], n, ni, nin, tau, n_modes)
+                out[b] = _subdomain_columns(torch, kind, A[b], Bring[j], n, ni, nin, tau, n_modes) + (None,)
         del Bring
     return out
 
@@ -357,6 +411,9 @@ def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
     for m in maps:
         posint[m.interior] = np.arange(m.interior.size)
     A0 = torch.zeros((nC, nC), dtype=torch.float64, device=device)
+    # host planning: every (s, owner j) group of rows, as slices of two index arrays that are
+    # uploaded once (no per-group host->device transfers)
+    plan, rows_cat, grp_cat, off = [], [], [], 0
     for s in own:
         if counts[s] == 0:
             continue
@@ -364,15 +421,22 @@ def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
         own_rows = owner[m.indices]
         order = np.argsort(own_rows, kind="stable")
         cuts = np.nonzero(np.diff(own_rows[order]))[0] + 1
-        W = w_blocks[s]
         for grp in np.split(order, cuts):
             j = int(own_rows[grp[0]])
             if counts[j] == 0:
                 continue
-            rows_j = torch.as_tensor(posint[m.indices[grp]], device=device)
-            Zj = z_blocks[j].index_select(0, rows_j)
-            Wg = W.index_select(0, torch.as_tensor(grp, device=device))
-            A0[cstart[j]:cstart[j + 1], cstart[s]:cstart[s + 1]] += Zj.mT @ Wg
+            rows_cat.append(posint[m.indices[grp]])
+            grp_cat.append(grp)
+            plan.append((s, j, off, off + grp.size))
+            off += grp.size
+    if not plan:
+        return A0
+    rows_d = torch.as_tensor(np.concatenate(rows_cat), device=device)
+    grp_d = torch.as_tensor(np.concatenate(grp_cat), device=device)
+    for s, j, o0, o1 in plan:
+        Zj = z_blocks[j].index_select(0, rows_d[o0:o1])
+        Wg = w_blocks[s].index_select(0, grp_d[o0:o1])
+        A0[cstart[j]:cstart[j + 1], cstart[s]:cstart[s + 1]] += Zj.mT @ Wg
     return A0
 
 
@@ -447,24 +511,27 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             handle.check(lib.tls_store_local_band(handle.ctx, first, cnt, _lib.ptr(L), ld, _lib.ptr(Dinv),
                                                   ld // 64, _lib.ptr(perm_cat), _lib.ptr(k_cat), s_ptr))
             torch.cuda.current_stream().synchronize()  # the host arrays above stay alive until here
-            del Dinv
             if want_coarse:
+                kc_full = np.zeros((cnt, ld // 64), dtype=np.int64)
+                for b in range(cnt):
+                    kc_full[b, : kcnts[b].size] = kcnts[b]
                 cols = _coarse_band_batch(torch, coarse, A, L, P,
                                           [int(n_loc[first + b]) for b in range(cnt)],
                                           [int(n_int[first + b]) for b in range(cnt)],
                                           [int(n_loc[first + b] - n_bnd[first + b]) for b in range(cnt)],
-                                          tau, n_modes)
+                                          tau, n_modes, Dinv=Dinv, kc=kc_full)
                 for b in range(cnt):
                     s = first + b
                     n, ni = int(n_loc[s]), int(n_int[s])
-                    Z, gaps[s] = cols[b]
-                    if Z.shape[1]:
+                    Z, gaps[s], W = cols[b]
+                    if W is None and Z.shape[1]:
                         nz = torch.any(Z != 0, dim=0)
                         if not bool(nz.all()):
                             Z = Z[:, nz].contiguous()
+                        W = A[b, :n, :ni] @ Z
                     z_dev[s] = Z
-                    w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
-            del A, L
+                    w_dev[s] = W if Z.shape[1] else None
+            del A, L, Dinv
             continue
         if symmetric:
             L, info = torch.linalg.cholesky_ex(A)

@@ -359,6 +359,7 @@ class ProblemConfig:
     restart: int | None = None
     symmetric: bool = True
     extra: dict = field(default_factory=dict)
+    maxit: int = 500
 
     def build(self):
         """Return (scipy CSR, symmetric flag, owner, n_subdomains)."""
@@ -386,7 +387,7 @@ class ProblemConfig:
         ex = dict(self.extra); ex.update(extra)
         return ProblemConfig(self.cid, self.name + f"@m{m}", self.kind, m, part or self.part,
                              self.overlap, self.n_modes, self.solver, self.tol, self.restart,
-                             self.symmetric, ex)
+                             self.symmetric, ex, self.maxit)
 
 
 CONFIGS = {
@@ -397,5 +398,5 @@ CONFIGS = {
     4: ProblemConfig(4, "cfg4-mac-stokes-512", "mac_stokes2d", 512, 32, 1, 20, "gmres", 1e-7, restart=50,
                      symmetric=False, extra={"c": 1e-6}),
     5: ProblemConfig(5, "cfg5-aniso27-256", "aniso27", 256, 16, 1, 12, "pcg", 1e-8,
-                     extra={"seed": 0, "angle_block": 32}),
+                     extra={"seed": 0, "angle_block": 32}, maxit=3000),
 }

@@ -49,12 +49,17 @@ def test_batched_band_coarse_columns_match_dense_path(name, sel):
     ns = [m.n_local for m in ms]
     nis = [m.interior.size for m in ms]
     nins = [m.n_local - m.n_boundary for m in ms]
-    cols = G._coarse_band_batch(torch, "gevp", A, L, P, ns, nis, nins, 0.1, k)
+    kc = np.zeros((len(ms), ld // 64), dtype=np.int64)
+    for b in range(len(ms)):
+        kc[b, : kcnts[b].size] = kcnts[b]
+    cols = G._coarse_band_batch(torch, "gevp", A, L, P, ns, nis, nins, 0.1, k, Dinv=Dinv, kc=kc)
     for b, m in enumerate(ms):
         n, ni, nin = ns[b], nis[b], nins[b]
         Binv = torch.linalg.inv(A[b, :n, :n])
         Zd, gap_d = G._subdomain_columns(torch, "gevp", A[b], Binv[:, nin:n], n, ni, nin, 0.1, k)
-        Zb, gap_b = cols[b]
+        Zb, gap_b, Wb = cols[b]
+        if Wb is not None:
+            np.testing.assert_allclose(Wb.numpy(), (A[b, :n, :ni] @ Zb).numpy(), atol=1e-12 * float(Wb.abs().max()))
         assert Zb.shape == Zd.shape == (ni, k)
         qb, _ = torch.linalg.qr(Zb)
         qd, _ = torch.linalg.qr(Zd)
@@ -63,3 +68,16 @@ def test_batched_band_coarse_columns_match_dense_path(name, sel):
         assert abs(gap_b - gap_d) <= 1e-6 * max(gap_d, 1e-12)
         # the lifted columns agree up to sign conventions
         np.testing.assert_allclose(np.abs(Zb.numpy()), np.abs(Zd.numpy()), atol=1e-9 * float(Zd.abs().max()))
+
+
+def test_band_solve_multi_matches_dense():
+    d, ms, A, ld = _batch("cfg2_m24", [0, 13])
+    L, Dinv, perms, kcnts, info, P = G._band_factor(torch, A, [m.indices for m in ms],
+                                                    [m.n_local for m in ms], ld)
+    kc = np.zeros((len(ms), ld // 64), dtype=np.int64)
+    for b in range(len(ms)):
+        kc[b, : kcnts[b].size] = kcnts[b]
+    E = torch.randn(len(ms), ld, 37, dtype=torch.float64, generator=torch.Generator().manual_seed(3))
+    X = G.band_solve_multi(torch, L, Dinv, kc, E)
+    ref = torch.cholesky_solve(E, L)
+    assert float((X - ref).abs().max() / ref.abs().max()) < 1e-12

@@ -8,7 +8,11 @@ cid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 cfg = PR.CONFIGS[cid]
 a, sym, owner, nsub = cfg.build()
 mat = B.SparseMat(a, symmetric=sym)
-B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes)  # warm (cuSOLVER init)
+if "--no-warm" not in sys.argv:
+    B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes)  # warm (cuSOLVER init)
+else:
+    from paper_2401_03915_b200.gpu_setup import warm_linalg
+    warm_linalg()
 torch.cuda.synchronize()
 pr = cProfile.Profile()
 t0 = time.perf_counter()
@@ -18,5 +22,8 @@ torch.cuda.synchronize()
 pr.disable()
 print("setup", time.perf_counter() - t0)
 s = io.StringIO()
-pstats.Stats(pr, stream=s).sort_stats("cumulative").print_stats(45)
+pstats.Stats(pr, stream=s).sort_stats("cumulative").print_stats(60)
+s2 = io.StringIO()
+pstats.Stats(pr, stream=s2).sort_stats("tottime").print_stats(25)
+print(s2.getvalue())
 print(s.getvalue())
