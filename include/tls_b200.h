@@ -104,7 +104,8 @@ int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first, int32_t count, cons
  * L = Cholesky factor of the block in factor order (row-major count x ld x ld, identity
  * padded), dinv = inverses of its 64x64 diagonal tiles (count x nbmax x 64 x 64 row-major),
  * perm (HOST, concatenated) = local index stored at each factor position, kcnt (HOST,
- * concatenated) = panel tile count K_I of every 64-row block (band: L[I, I-K_I .. I]). */
+ * concatenated) = per 64-row block K_I | (z_I << 16): the band is L[I, I-K_I .. I] and its first
+ * z_I 8-column strips are identically zero (skipped by the solve). */
 int32_t tls_set_local_kind(tls_ctx* ctx, int32_t kind);
 int32_t tls_store_local_band(tls_ctx* ctx, int32_t first, int32_t count, const double* L,
                              int64_t ld, const double* dinv, int32_t nbmax, const int32_t* perm,

@@ -1242,6 +1242,7 @@ int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const
   std::vector<int> ks;
   std::vector<long long> dstart(count), ostart(count);
   long long tot = 0;
+  double need = 0.0;  // doubles the solve actually reads (zero strips skipped)
   int kp = 0;
   for (int b = 0; b < count; ++b) {
     const int sl = first + b, nb = ctx->h_band[sl].nb;
@@ -1250,11 +1251,12 @@ int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const
     dstart[b] = tot;
     ostart[b] = (long long)offs.size();
     for (int I = 0; I < nb; ++I) {
-      const int K = kcnt[kp + I];
-      if (K < 0 || K > I) return fail(ctx, TLS_ERR_ARG, "band panel count out of range");
+      const int code = kcnt[kp + I], K = code & 0xffff, fz = code >> 16;
+      if (K < 0 || K > I || fz < 0 || fz > 8 * K) return fail(ctx, TLS_ERR_ARG, "band panel code out of range");
       offs.push_back(tot - dstart[b]);
-      ks.push_back(K);
-      tot += (long long)(K + 1) * TT * TT;
+      ks.push_back(code);
+      tot += (long long)K * TT * TT + DIAG_PACK;
+      need += (double)((long long)K * TT * TT - (long long)fz * 8 * TT + DIAG_PACK);
     }
     kp += nb;
   }
@@ -1278,7 +1280,6 @@ int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const
     bd.data = data + dstart[b];
     bd.step_off = d_off + ostart[b];
     bd.kcnt = d_k + ostart[b];
-    ctx->band_bytes += 8.0 * (double)((b + 1 < count ? dstart[b + 1] : tot) - dstart[b]);
     const int n = ctx->h_n[sl];
     for (int p = 0; p < n; ++p) {
       const int l = perm[pp + p];
@@ -1287,6 +1288,7 @@ int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const
     }
     pp += n;
   }
+  ctx->band_bytes += 8.0 * need;
   CK(cudaMemcpy(ctx->d_band + first, ctx->h_band.data() + first, sizeof(BandDesc) * count, cudaMemcpyHostToDevice));
   dim3 g(std::min(nbmax, 256), count);
   k_pack_band<<<g, NTHR, 0, s>>>(ctx->d_band, first, L, ld, dinv, nbmax);

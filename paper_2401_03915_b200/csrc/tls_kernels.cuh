@@ -741,10 +741,19 @@ __global__ void k_pack_tiles(const BlkDesc* __restrict__ blks, int first_blk, co
 struct BandDesc {
   const double* data;          // steps of this subdomain
   const long long* step_off;   // nb offsets (doubles) into data
-  const int* kcnt;             // nb panel tile counts
+  const int* kcnt;             // nb codes: K_I | (first nonzero 8-column panel strip << 16)
   long long xoff;              // offset of the local vector in xloc / yloc
   int n, nb, pad0, pad1;
 };
+
+// bulk L2 prefetch (TMA engine, no registers): pull the next step's factor block into L2
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// inverted diagonal tile, lower triangular: warp w's 8-column strip is stored from row 8w on
+constexpr int DIAG_PACK = 2304;  // = sum_w 8 * (64 - 8w)
+__device__ __forceinline__ int diag_strip_off(int w) { return 512 * w - 32 * w * (w - 1); }
 
 __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restrict__ bands,
                                                         const double* __restrict__ x,
@@ -757,14 +766,23 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   double* red = sm + npad;         // 8 x 64
   double* t = red + 8 * TT;        // 64
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c0 = warp * 8;
+  const int dlen = TT - 8 * warp;                    // rows stored in this warp's diagonal strip
+  const bool drow = lane >= 4 * warp;                // rows 2l, 2l+1 inside the strip
+  const int doff = diag_strip_off(warp) + (2 * lane - 8 * warp);
   for (int i = threadIdx.x; i < npad; i += NTHR) v[i] = x[b.xoff + i];
+  const long long dend = b.step_off[b.nb - 1] + (long long)(b.kcnt[b.nb - 1] & 0xffff) * TT * TT + DIAG_PACK;
   __syncthreads();
-  // forward sweep: L u = x
+  // forward sweep: L u = x  (the factor is one contiguous stream in this order)
   for (int I = 0; I < b.nb; ++I) {
     const double* blk = b.data + b.step_off[I];
-    const int K = b.kcnt[I];
+    const int code = b.kcnt[I], K = code & 0xffff, fz = code >> 16;
     double ra0 = 0.0, ra1 = 0.0;
     for (int k = 0; k < K; ++k) {
+      if (threadIdx.x == 0) {  // one 32 KiB tile ahead of the stream, into L2
+        const long long pf = b.step_off[I] + (long long)(k + 2) * TT * TT;
+        if (pf < dend) prefetch_l2(b.data + pf, 8u * (unsigned)min((long long)TT * TT, dend - pf));
+      }
+      if (k * 8 + warp < fz) continue;               // strip left of the band profile: zeros
       const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
       double2 w[8];
 #pragma unroll
@@ -784,13 +802,15 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
     }
     __syncthreads();
     {
-      const double* dp = blk + (long long)K * TT * TT + c0 * TT + 2 * lane;
       double d0 = 0.0, d1 = 0.0;
+      if (drow) {
+        const double* dp = blk + (long long)K * TT * TT + doff;
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const double2 w = ldg_stream2(dp + kk * TT);
-        d0 += w.x * t[c0 + kk];
-        d1 += w.y * t[c0 + kk];
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = ldg_stream2(dp + kk * dlen);
+          d0 += w.x * t[c0 + kk];
+          d1 += w.y * t[c0 + kk];
+        }
       }
       red[warp * TT + 2 * lane] = d0;
       red[warp * TT + 2 * lane + 1] = d1;
@@ -808,15 +828,25 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   const int colsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
   for (int J = b.nb - 1; J >= 0; --J) {
     const double* blk = b.data + b.step_off[J];
-    const int K = b.kcnt[J];
+    const int code = b.kcnt[J], K = code & 0xffff, fz = code >> 16;
+    if (threadIdx.x == 0 && J > 0) {  // previous step: its diagonal strips and first panel tile
+      const int Kp = b.kcnt[J - 1] & 0xffff;
+      prefetch_l2(b.data + b.step_off[J - 1] + (long long)Kp * TT * TT, 8u * DIAG_PACK);
+      if (Kp) prefetch_l2(b.data + b.step_off[J - 1], 8u * TT * TT);
+    }
     {
-      const double* dp = blk + (long long)K * TT * TT + c0 * TT + 2 * lane;
       const double u0 = v[J * TT + 2 * lane], u1 = v[J * TT + 2 * lane + 1];
       double cp[8];
+      if (drow) {
+        const double* dp = blk + (long long)K * TT * TT + doff;
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const double2 w = ldg_stream2(dp + kk * TT);
-        cp[kk] = w.x * u0 + w.y * u1;
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = ldg_stream2(dp + kk * dlen);
+          cp[kk] = w.x * u0 + w.y * u1;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) cp[kk] = 0.0;
       }
       const double yv = warp_reduce8(cp, lane);
       __syncthreads();  // every warp has read v_J
@@ -825,6 +855,9 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
     }
     const double y0 = v[J * TT + 2 * lane], y1 = v[J * TT + 2 * lane + 1];
     for (int k = 0; k < K; ++k) {
+      if (threadIdx.x == 0 && k + 1 < K)
+        prefetch_l2(blk + (long long)(k + 1) * TT * TT, 8u * TT * TT);
+      if (k * 8 + warp < fz) continue;
       const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
       double cp[8];
 #pragma unroll
@@ -840,7 +873,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
 }
 
-// pack band steps of one subdomain batch: L (row-major ld x ld, lexicographic order, identity
+// pack band steps of one subdomain batch: L (row-major ld x ld, factor order, identity
 // padding) and the inverted diagonal tiles dinv (nbmax x 64 x 64 row-major per subdomain)
 __global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, const double* __restrict__ L,
                             long long ld, const double* __restrict__ dinv, int nbmax) {
@@ -849,20 +882,22 @@ __global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, 
   const double* Lb = L + (long long)bi * ld * ld;
   const double* Db = dinv + (long long)bi * nbmax * TT * TT;
   for (int I = blockIdx.x; I < bd.nb; I += gridDim.x) {
-    const int K = bd.kcnt[I];
+    const int K = bd.kcnt[I] & 0xffff;
     double* dst = const_cast<double*>(bd.data) + bd.step_off[I];
-    for (int k = 0; k <= K; ++k) {
+    for (int k = 0; k < K; ++k) {
       const int J = I - K + k;
       for (int e = threadIdx.x; e < TT * TT; e += NTHR) {
         const int c = e / TT, r = e % TT;
-        double val;
-        if (k < K) {
-          const long long gi = (long long)I * TT + r, gj = (long long)J * TT + c;
-          val = (gi < ld && gj < ld) ? Lb[gi * ld + gj] : 0.0;
-        } else {
-          val = Db[(long long)I * TT * TT + r * TT + c];
-        }
-        dst[(long long)k * TT * TT + e] = val;
+        const long long gi = (long long)I * TT + r, gj = (long long)J * TT + c;
+        dst[(long long)k * TT * TT + e] = (gi < ld && gj < ld) ? Lb[gi * ld + gj] : 0.0;
+      }
+    }
+    double* dd = dst + (long long)K * TT * TT;
+    for (int w = 0; w < 8; ++w) {
+      const int len = TT - 8 * w, off = diag_strip_off(w);
+      for (int e = threadIdx.x; e < 8 * len; e += NTHR) {
+        const int kk = e / len, r = 8 * w + e % len;
+        dd[off + e] = Db[(long long)I * TT * TT + r * TT + (8 * w + kk)];
       }
     }
   }

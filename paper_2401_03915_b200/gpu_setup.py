@@ -384,8 +384,12 @@ def _band_factor(torch, A, idx_list, n_list, ld):
     AP = torch.gather(A, 1, P[:, :, None].expand(cnt, ld, ld))
     AP = torch.gather(AP, 2, P[:, None, :].expand(cnt, ld, ld)).contiguous()
     first = torch.argmax((AP != 0).to(torch.int8), dim=2)           # row profile f(i)
-    bmin = first.view(cnt, nbk, 64).min(dim=2).values // 64
+    fmin = first.view(cnt, nbk, 64).min(dim=2).values
+    bmin = fmin // 64
     kc = (torch.arange(nbk, device=dev)[None, :] - bmin).clamp(min=0).cpu().numpy().astype(np.int32)
+    # leading all-zero 8-column strips of each panel (the factor keeps the profile of A_P)
+    fz = ((fmin % 64) // 8).cpu().numpy().astype(np.int32)
+    fz = np.where(kc > 0, fz, 0)
     L, info = torch.linalg.cholesky_ex(AP)
     del AP
     L = L.contiguous()  # cuSOLVER returns column-major
@@ -393,7 +397,8 @@ def _band_factor(torch, A, idx_list, n_list, ld):
     eye = torch.eye(64, dtype=torch.float64, device=dev).expand(cnt, nbk, 64, 64)
     Dinv = torch.linalg.solve_triangular(Ld, eye, upper=False).contiguous()
     kcnts = [kc[b, : -(-n_list[b] // 64)] for b in range(cnt)]
-    return L, Dinv, perms, kcnts, info, P
+    codes = [(kc[b] | (fz[b] << 16))[: -(-n_list[b] // 64)].astype(np.int32) for b in range(cnt)]
+    return L, Dinv, perms, kcnts, info, P, codes
 
 
 def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
@@ -501,13 +506,13 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         if band:
             idx_list = [maps[first + b].indices for b in range(cnt)]
             n_list = [int(n_loc[first + b]) for b in range(cnt)]
-            L, Dinv, perms, kcnts, info, P = _band_factor(torch, A, idx_list, n_list, ld)
+            L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, idx_list, n_list, ld)
             bad = torch.nonzero(info).flatten().cpu().numpy()
             if bad.size:
                 s = first + int(bad[0])
                 raise SubdomainSetupError(s, "factorization failed: the local block is not positive definite")
             perm_cat = np.concatenate(perms).astype(np.int32)
-            k_cat = np.concatenate(kcnts).astype(np.int32)
+            k_cat = np.concatenate(codes).astype(np.int32)
             handle.check(lib.tls_store_local_band(handle.ctx, first, cnt, _lib.ptr(L), ld, _lib.ptr(Dinv),
                                                   ld // 64, _lib.ptr(perm_cat), _lib.ptr(k_cat), s_ptr))
             torch.cuda.current_stream().synchronize()  # the host arrays above stay alive until here
