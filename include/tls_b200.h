@@ -106,10 +106,21 @@ int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first, int32_t count, cons
  * perm (HOST, concatenated) = local index stored at each factor position, kcnt (HOST,
  * concatenated) = per 64-row block K_I | (z_I << 16): the band is L[I, I-K_I .. I] and its first
  * z_I 8-column strips are identically zero (skipped by the solve). */
-int32_t tls_set_local_kind(tls_ctx* ctx, int32_t kind);
+int32_t tls_set_local_kind(tls_ctx* ctx, int32_t kind);  /* 0 inverse tiles, 1 band Cholesky, 2 band LU */
 int32_t tls_store_local_band(tls_ctx* ctx, int32_t first, int32_t count, const double* L,
                              int64_t ld, const double* dinv, int32_t nbmax, const int32_t* perm,
                              const int32_t* kcnt, void* stream);
+/* Banded LU local operators (general matrices, kind 2; the lu_solve closure of
+ * src/subdomain.py:83-89).  LU = packed getrf factors of the block in factor order (row-major
+ * count x ld x ld; strictly-lower part = L, upper part = U), ldinv / udinv = inverses of the
+ * unit-lower / upper 64x64 diagonal tiles, perm_in = local index gathered into each input
+ * position (factor order composed with the row pivots), perm_out = local index of each output
+ * position, lcode = K_I | (leading zero strips << 16) of L, ucode = R_I | (trailing zero strips
+ * << 16) of U (panel U[I, I+1 .. I+R_I]); all codes/permutations HOST, concatenated. */
+int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first, int32_t count, const double* LU,
+                                int64_t ld, const double* ldinv, const double* udinv, int32_t nbmax,
+                                const int32_t* perm_in, const int32_t* perm_out, const int32_t* lcode,
+                                const int32_t* ucode, void* stream);
 /* Coarse space (src/coarse.py:23-49): per subdomain a dense block Z_s of shape
  * n_interior[s] x k[s] stored column by column (k[s] x n_interior[s] row-major, device,
  * concatenated in subdomain order), columns

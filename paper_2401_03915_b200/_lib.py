@@ -66,6 +66,7 @@ SIGNATURES = {
     "tls_set_owned_range": (_I32, [_P, _I32, _I32]),
     "tls_set_local_kind": (_I32, [_P, _I32]),
     "tls_store_local_band": (_I32, [_P, _I32, _I32, _P, _I64, _P, _I32, _P, _P, _P]),
+    "tls_store_local_band_lu": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P, _I32, _P, _P, _P, _P, _P]),
     "tls_nccl_unique_id": (_I32, [_P, _I32]),
     "tls_comm_init_nccl": (_I32, [_P, _P, _I32, _I32]),
     "tls_group_create": (_I32, [_I32, C.POINTER(_P)]),

@@ -38,6 +38,8 @@ struct tls_ctx {
   std::string err;
   int64_t dev_bytes = 0;
   cudaStream_t cap = nullptr;
+  cudaStream_t aux = nullptr;                          // side branch (coarse chain overlap)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // ---- matrix (CSR, int32 indices)
   int n = 0;
   int64_t nnz = 0;
@@ -108,7 +110,8 @@ struct tls_ctx {
   std::vector<BandDesc> h_band;
   BandDesc* d_band = nullptr;
   std::vector<void*> band_allocs;
-  std::vector<int> h_perm;            // per owned subdomain: perm[p] = local index at position p
+  std::vector<int> h_perm;            // per owned subdomain: perm[p] = local index at output position p
+  std::vector<int> h_perm_in;         // LU: local index gathered into input position p (row pivots)
   double band_bytes = 0.0;            // stored factor bytes (read twice per apply)
   size_t band_smem = 0;
   // ---- sharding: this handle owns global subdomains [own_lo, own_hi)
@@ -215,7 +218,7 @@ static int spmv_lpr(tls_ctx* ctx, cudaStream_t s, const double* x, double* y, co
 enum { L_LOCAL = 0, L_COARSE = 1, L_ALL = 2 };
 
 static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done) {
-  if (ctx->local_kind == 1 && which != L_COARSE) {
+  if (ctx->local_kind >= 1 && which != L_COARSE) {
     k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done);
     CKL();
     if (which == L_LOCAL) return TLS_OK;
@@ -337,6 +340,21 @@ static int enq_apply(tls_ctx* ctx, cudaStream_t s, const double* r, double* z, b
     return dot ? enq_prolong<0, 1>(ctx, s, nullptr, nullptr, r, z, done)
                : enq_prolong<0, 0>(ctx, s, nullptr, nullptr, r, z, done);
   }
+  if (ctx->combine == TLS_ADDITIVE && ctx->local_kind == 1) {
+    // the coarse chain (restrict -> A0^{-1} tiles -> reduce) reads r and writes only the coarse
+    // segments, the band solve reads/writes only the local segments: run them side by side
+    // (a fork/join that CUDA-graph capture turns into parallel branches)
+    CK(cudaEventRecord(ctx->ev_fork, s));
+    CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    TRY(enq_restrict(ctx, ctx->aux, r, done));
+    TRY(enq_solve(ctx, ctx->aux, L_COARSE, done));
+    CK(cudaEventRecord(ctx->ev_join, ctx->aux));
+    TRY(enq_gather(ctx, s, r, done));
+    TRY(enq_solve(ctx, s, L_LOCAL, done));
+    CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    return dot ? enq_prolong<1, 1>(ctx, s, nullptr, nullptr, r, z, done)
+               : enq_prolong<1, 0>(ctx, s, nullptr, nullptr, r, z, done);
+  }
   if (ctx->combine == TLS_ADDITIVE) {
     TRY(enq_gather(ctx, s, r, done));
     TRY(enq_restrict(ctx, s, r, done));
@@ -383,6 +401,9 @@ int32_t tls_ctx_create(int32_t device, tls_ctx** out) {
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&ctx->h_flag, sizeof(int) * 4);
   if (e != cudaSuccess) {
     delete ctx;
@@ -419,6 +440,9 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   if (ctx->h_x) cudaFreeHost(ctx->h_x);
   dfree(ctx->ab);
   if (ctx->cap) cudaStreamDestroy(ctx->cap);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx->comm;
   delete ctx;
 }
@@ -529,10 +553,10 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
       rsmem_set = ctx->restrict_smem;
     }
   }
-  ctx->tile_doubles = ctx->local_kind == 1 ? 0 : tiles * TT * TT;
+  ctx->tile_doubles = ctx->local_kind >= 1 ? 0 : tiles * TT * TT;
   dfree(ctx->tiles);
   TRY(dalloc(ctx, ctx->tiles, ctx->tile_doubles));
-  if (ctx->local_kind == 1) {
+  if (ctx->local_kind >= 1) {
     ctx->h_band.assign(n_sub, BandDesc{});
     int maxnb = 0;
     for (int s = 0; s < n_sub; ++s) {
@@ -550,6 +574,7 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
       smem_set = ctx->band_smem;
     }
     ctx->h_perm.assign(tot, -1);
+    ctx->h_perm_in.assign(ctx->local_kind == 2 ? tot : 0, -1);
     ctx->band_bytes = 0.0;
   }
   for (int s = 0; s < n_sub; ++s) ctx->h_blk[s].tiles = ctx->tiles + tbase[s] * TT * TT;
@@ -698,14 +723,18 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   std::vector<int> posl(ctx->h_idx.size());
   for (int s = 0; s < nsub; ++s)
     for (int l = 0; l < ctx->h_n[s]; ++l)
-      posl[ctx->h_off[s] + l] = ctx->local_kind == 1 ? -1 : l;
-  if (ctx->local_kind == 1)
+      posl[ctx->h_off[s] + l] = ctx->local_kind >= 1 ? -1 : l;
+  if (ctx->local_kind >= 1)
     for (int s = 0; s < nsub; ++s)
       for (int p = 0; p < ctx->h_n[s]; ++p) posl[ctx->h_off[s] + ctx->h_perm[ctx->h_off[s] + p]] = p;
   std::vector<int> gidx(ctx->Xloc, -1);
   for (int s = 0; s < nsub; ++s)
     for (int l = 0; l < ctx->h_n[s]; ++l)
       gidx[ctx->h_blk[s].xoff + posl[ctx->h_off[s] + l]] = ctx->h_idx[ctx->h_off[s] + l];
+  if (ctx->local_kind == 2)  // LU input order: the pivoted rows (P^T r), output order stays perm
+    for (int s = 0; s < nsub; ++s)
+      for (int p = 0; p < ctx->h_n[s]; ++p)
+        gidx[ctx->h_blk[s].xoff + p] = ctx->h_idx[ctx->h_off[s] + ctx->h_perm_in[ctx->h_off[s] + p]];
   TRY(upload(ctx, ctx->d_gidx, gidx.data(), ctx->Xloc));
   ctx->coarse_xoff = ctx->Xloc;
   ctx->X = ctx->Xloc + (ctx->ncoarse > 0 ? (long long)ctx->h_blk[nsub].nt * TT : 0);
@@ -724,8 +753,8 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
     const double ns = ctx->h_n[s];
     ctx->algo_local += ctx->sym ? 8.0 * ns * (ns + 1) / 2 + 8.0 * ns : 8.0 * ns * ns + 8.0 * ns;
   }
-  if (ctx->local_kind == 1) {  // two sweeps over the stored factor + x in, y out
-    ctx->algo_local = 2.0 * ctx->band_bytes;
+  if (ctx->local_kind >= 1) {  // sweeps over the stored factors (band_bytes counts the reads) + x, y
+    ctx->algo_local = ctx->band_bytes;
     for (int s = 0; s < nsub; ++s) ctx->algo_local += 16.0 * ctx->h_n[s];
   }
   ctx->nu_local = (int)units.size();
@@ -1197,7 +1226,7 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  const bool band = ctx->local_kind == 1;
+  const bool band = ctx->local_kind >= 1;
   for (int i = 0; i <= reps; ++i) {
     if (i == 1) CK(cudaEventRecord(e0, s));
     if (band)
@@ -1220,7 +1249,8 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
 
 // ---- banded local factors ---------------------------------------------------------------------
 int32_t tls_set_local_kind(tls_ctx* ctx, int32_t kind) {
-  if (!ctx || (kind != 0 && kind != 1)) return ctx ? fail(ctx, TLS_ERR_ARG, "local kind is 0 (inverse tiles) or 1 (band)") : TLS_ERR_ARG;
+  if (!ctx || kind < 0 || kind > 2)
+    return ctx ? fail(ctx, TLS_ERR_ARG, "local kind is 0 (inverse tiles), 1 (band Cholesky) or 2 (band LU)") : TLS_ERR_ARG;
   if (ctx->nsub) return fail(ctx, TLS_ERR_STATE, "set the local kind before tls_subdomains_upload");
   ctx->local_kind = kind;
   return TLS_OK;
@@ -1230,7 +1260,7 @@ int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const
                              int64_t ld, const double* dinv, int32_t nbmax, const int32_t* perm,
                              const int32_t* kcnt, void* stream) {
   if (!ctx) return TLS_ERR_ARG;
-  if (ctx->local_kind != 1) return fail(ctx, TLS_ERR_STATE, "handle is not in band mode");
+  if (ctx->local_kind != 1) return fail(ctx, TLS_ERR_STATE, "handle is not in band-Cholesky mode");
   if (!ctx->sym) return fail(ctx, TLS_ERR_ARG, "band factors need a symmetric matrix (Cholesky)");
   const int first = first_g - ctx->own_lo;
   if (first < 0 || count <= 0 || first + count > ctx->nsub)
@@ -1288,10 +1318,115 @@ int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const
     }
     pp += n;
   }
-  ctx->band_bytes += 8.0 * need;
+  ctx->band_bytes += 2.0 * 8.0 * need;  // forward with L, backward with L^T
   CK(cudaMemcpy(ctx->d_band + first, ctx->h_band.data() + first, sizeof(BandDesc) * count, cudaMemcpyHostToDevice));
   dim3 g(std::min(nbmax, 256), count);
   k_pack_band<<<g, NTHR, 0, s>>>(ctx->d_band, first, L, ld, dinv, nbmax);
+  CKL();
+  for (int i = first; i < first + count; ++i) ctx->stored[i] = 1;
+  ctx->finalized = false;
+  return TLS_OK;
+}
+
+// one step stream (K/R tiles + packed diagonal strips per block) for a batch: returns offsets
+static int band_layout(tls_ctx* ctx, int first, int count, const int32_t* codes, bool upper,
+                       std::vector<long long>& dstart, std::vector<long long>& offs,
+                       std::vector<int>& ks, long long& tot, double& need) {
+  dstart.assign(count, 0);
+  offs.clear();
+  ks.clear();
+  tot = 0;
+  need = 0.0;
+  int kp = 0;
+  for (int b = 0; b < count; ++b) {
+    const int sl = first + b, nb = ctx->h_band[sl].nb;
+    dstart[b] = tot;
+    std::vector<long long> local(nb);
+    // upper (U) steps are stored in backward-sweep order: block nb-1 first
+    for (int q = 0; q < nb; ++q) {
+      const int I = upper ? nb - 1 - q : q;
+      const int code = codes[kp + I], K = code & 0xffff, z = code >> 16;
+      const int lim = upper ? nb - 1 - I : I;
+      if (K < 0 || K > lim || z < 0 || z > 8 * K) return fail(ctx, TLS_ERR_ARG, "band panel code out of range");
+      local[I] = tot - dstart[b];
+      tot += (long long)K * TT * TT + DIAG_PACK;
+      need += (double)((long long)K * TT * TT - (long long)z * 8 * TT + DIAG_PACK);
+    }
+    for (int I = 0; I < nb; ++I) {
+      offs.push_back(local[I]);
+      ks.push_back(codes[kp + I]);
+    }
+    kp += nb;
+  }
+  return TLS_OK;
+}
+
+static int band_alloc(tls_ctx* ctx, long long tot, const std::vector<long long>& offs,
+                      const std::vector<int>& ks, double** data, long long** d_off, int** d_k) {
+  if (cudaMalloc((void**)data, sizeof(double) * tot) != cudaSuccess ||
+      cudaMalloc((void**)d_off, sizeof(long long) * offs.size()) != cudaSuccess ||
+      cudaMalloc((void**)d_k, sizeof(int) * ks.size()) != cudaSuccess)
+    return fail(ctx, TLS_ERR_OOM, "band storage allocation failed");
+  ctx->band_allocs.push_back(*data);
+  ctx->band_allocs.push_back(*d_off);
+  ctx->band_allocs.push_back(*d_k);
+  ctx->dev_bytes += (int64_t)(sizeof(double) * tot + sizeof(long long) * offs.size() + sizeof(int) * ks.size());
+  CK(cudaMemcpy(*d_off, offs.data(), sizeof(long long) * offs.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(*d_k, ks.data(), sizeof(int) * ks.size(), cudaMemcpyHostToDevice));
+  return TLS_OK;
+}
+
+int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first_g, int32_t count, const double* LU,
+                                int64_t ld, const double* ldinv, const double* udinv, int32_t nbmax,
+                                const int32_t* perm_in, const int32_t* perm_out, const int32_t* lcode,
+                                const int32_t* ucode, void* stream) {
+  if (!ctx) return TLS_ERR_ARG;
+  if (ctx->local_kind != 2) return fail(ctx, TLS_ERR_STATE, "handle is not in band-LU mode");
+  const int first = first_g - ctx->own_lo;
+  if (first < 0 || count <= 0 || first + count > ctx->nsub)
+    return fail(ctx, TLS_ERR_ARG, "subdomain range not owned by this handle");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int b = 0; b < count; ++b) {
+    const int sl = first + b;
+    if (ctx->h_band[sl].nb > nbmax || ctx->h_n[sl] > ld) return fail(ctx, TLS_ERR_ARG, "batch dimensions too small");
+  }
+  std::vector<long long> dsL, offL, dsU, offU;
+  std::vector<int> kL, kU;
+  long long totL, totU;
+  double needL, needU;
+  TRY(band_layout(ctx, first, count, lcode, false, dsL, offL, kL, totL, needL));
+  TRY(band_layout(ctx, first, count, ucode, true, dsU, offU, kU, totU, needU));
+  double *dL, *dU;
+  long long *oL, *oU;
+  int *cL, *cU;
+  TRY(band_alloc(ctx, totL, offL, kL, &dL, &oL, &cL));
+  TRY(band_alloc(ctx, totU, offU, kU, &dU, &oU, &cU));
+  long long pp = 0, op = 0;
+  for (int b = 0; b < count; ++b) {
+    const int sl = first + b, n = ctx->h_n[sl];
+    BandDesc& bd = ctx->h_band[sl];
+    bd.data = dL + dsL[b];
+    bd.step_off = oL + op;
+    bd.kcnt = cL + op;
+    bd.udata = dU + dsU[b];
+    bd.ustep_off = oU + op;
+    bd.ucnt = cU + op;
+    op += bd.nb;
+    for (int p = 0; p < n; ++p) {
+      const int lo = perm_out[pp + p], li = perm_in[pp + p];
+      if (lo < 0 || lo >= n || li < 0 || li >= n) return fail(ctx, TLS_ERR_ARG, "band permutation out of range");
+      ctx->h_perm[ctx->h_off[sl] + p] = lo;
+      ctx->h_perm_in[ctx->h_off[sl] + p] = li;
+    }
+    pp += n;
+  }
+  ctx->band_bytes += 8.0 * (needL + needU);  // forward with L, backward with U
+  CK(cudaMemcpy(ctx->d_band + first, ctx->h_band.data() + first, sizeof(BandDesc) * count, cudaMemcpyHostToDevice));
+  dim3 g(std::min(nbmax, 256), count);
+  k_pack_band<<<g, NTHR, 0, s>>>(ctx->d_band, first, LU, ld, ldinv, nbmax);
+  CKL();
+  k_pack_band_u<<<g, NTHR, 0, s>>>(ctx->d_band, first, LU, ld, udinv, nbmax);
   CKL();
   for (int i = first; i < first + count; ++i) ctx->stored[i] = 1;
   ctx->finalized = false;

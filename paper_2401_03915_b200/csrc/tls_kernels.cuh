@@ -739,11 +739,15 @@ __global__ void k_pack_tiles(const BlkDesc* __restrict__ blks, int first_blk, co
 // FMAs do, and 4 CTAs per SM overlap one CTA's barriers with the others' loads.
 // ---------------------------------------------------------------------------------------
 struct BandDesc {
-  const double* data;          // steps of this subdomain
+  const double* data;          // L steps of this subdomain (forward order)
   const long long* step_off;   // nb offsets (doubles) into data
   const int* kcnt;             // nb codes: K_I | (first nonzero 8-column panel strip << 16)
   long long xoff;              // offset of the local vector in xloc / yloc
   int n, nb, pad0, pad1;
+  // LU only (nonsymmetric blocks): U steps stored in backward-sweep order (block nb-1 first)
+  const double* udata;         // null for Cholesky (backward sweep uses L^T)
+  const long long* ustep_off;  // nb offsets, indexed by block row I
+  const int* ucnt;             // nb codes: R_I | (number of all-zero trailing strips << 16)
 };
 
 // bulk L2 prefetch (TMA engine, no registers): pull the next step's factor block into L2
@@ -754,6 +758,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 // inverted diagonal tile, lower triangular: warp w's 8-column strip is stored from row 8w on
 constexpr int DIAG_PACK = 2304;  // = sum_w 8 * (64 - 8w)
 __device__ __forceinline__ int diag_strip_off(int w) { return 512 * w - 32 * w * (w - 1); }
+// inverted diagonal tile, upper triangular: warp w's strip keeps rows 0 .. 8w+7
+__device__ __forceinline__ int udiag_strip_off(int w) { return 32 * w * w + 32 * w; }
 
 __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restrict__ bands,
                                                         const double* __restrict__ x,
@@ -823,6 +829,66 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
       v[I * TT + threadIdx.x] = sacc;
     }
     __syncthreads();
+  }
+  if (b.udata) {
+    // backward sweep with U (LU): y_I = U_II^{-1} (u_I - sum_k U[I, I+1+k] y_{I+1+k}), row partials
+    const int ulen = 8 * warp + 8;                   // rows stored in this warp's upper strip
+    const bool urow = lane <= 4 * warp + 3;
+    const int uoff = udiag_strip_off(warp) + 2 * lane;
+    const long long uend = b.ustep_off[0] + (long long)(b.ucnt[0] & 0xffff) * TT * TT + DIAG_PACK;
+    for (int I = b.nb - 1; I >= 0; --I) {
+      const double* blk = b.udata + b.ustep_off[I];
+      const int code = b.ucnt[I], R = code & 0xffff, tz = code >> 16;
+      double ra0 = 0.0, ra1 = 0.0;
+      for (int k = 0; k < R; ++k) {
+        if (threadIdx.x == 0) {
+          const long long pf = b.ustep_off[I] + (long long)(k + 2) * TT * TT;
+          if (pf < uend) prefetch_l2(b.udata + pf, 8u * (unsigned)min((long long)TT * TT, uend - pf));
+        }
+        if (k * 8 + warp >= 8 * R - tz) continue;    // strip right of the band profile: zeros
+        const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
+        double2 w[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) w[kk] = ldg_stream2(tp + kk * TT);
+        const double* yj = v + (I + 1 + k) * TT + c0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) { ra0 += w[kk].x * yj[kk]; ra1 += w[kk].y * yj[kk]; }
+      }
+      red[warp * TT + 2 * lane] = ra0;
+      red[warp * TT + 2 * lane + 1] = ra1;
+      __syncthreads();
+      if (threadIdx.x < TT) {
+        double sacc = v[I * TT + threadIdx.x];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sacc -= red[w * TT + threadIdx.x];
+        t[threadIdx.x] = sacc;
+      }
+      __syncthreads();
+      {
+        double d0 = 0.0, d1 = 0.0;
+        if (urow) {
+          const double* dp = blk + (long long)R * TT * TT + uoff;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const double2 w = ldg_stream2(dp + kk * ulen);
+            d0 += w.x * t[c0 + kk];
+            d1 += w.y * t[c0 + kk];
+          }
+        }
+        red[warp * TT + 2 * lane] = d0;
+        red[warp * TT + 2 * lane + 1] = d1;
+      }
+      __syncthreads();
+      if (threadIdx.x < TT) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sacc += red[w * TT + threadIdx.x];
+        v[I * TT + threadIdx.x] = sacc;
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
+    return;
   }
   // backward sweep: L^T y = u
   const int colsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
@@ -897,6 +963,36 @@ __global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, 
       const int len = TT - 8 * w, off = diag_strip_off(w);
       for (int e = threadIdx.x; e < 8 * len; e += NTHR) {
         const int kk = e / len, r = 8 * w + e % len;
+        dd[off + e] = Db[(long long)I * TT * TT + r * TT + (8 * w + kk)];
+      }
+    }
+  }
+}
+
+// pack the U steps of one LU batch: U (row-major ld x ld, upper part of the packed LU) and
+// the inverted upper diagonal tiles udinv (nbmax x 64 x 64 row-major per subdomain)
+__global__ void k_pack_band_u(const BandDesc* __restrict__ bands, int first_band, const double* __restrict__ LU,
+                              long long ld, const double* __restrict__ udinv, int nbmax) {
+  const int bi = blockIdx.y;
+  const BandDesc bd = bands[first_band + bi];
+  const double* Ub = LU + (long long)bi * ld * ld;
+  const double* Db = udinv + (long long)bi * nbmax * TT * TT;
+  for (int I = blockIdx.x; I < bd.nb; I += gridDim.x) {
+    const int R = bd.ucnt[I] & 0xffff;
+    double* dst = const_cast<double*>(bd.udata) + bd.ustep_off[I];
+    for (int k = 0; k < R; ++k) {
+      const int J = I + 1 + k;
+      for (int e = threadIdx.x; e < TT * TT; e += NTHR) {
+        const int c = e / TT, r = e % TT;
+        const long long gi = (long long)I * TT + r, gj = (long long)J * TT + c;
+        dst[(long long)k * TT * TT + e] = (gi < ld && gj < ld) ? Ub[gi * ld + gj] : 0.0;
+      }
+    }
+    double* dd = dst + (long long)R * TT * TT;
+    for (int w = 0; w < 8; ++w) {
+      const int len = 8 * w + 8, off = udiag_strip_off(w);
+      for (int e = threadIdx.x; e < 8 * len; e += NTHR) {
+        const int kk = e / len, r = e % len;
         dd[off + e] = Db[(long long)I * TT * TT + r * TT + (8 * w + kk)];
       }
     }

@@ -365,24 +365,157 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
     return out
 
 
-def _band_factor(torch, A, idx_list, n_list, ld):
-    """Lexicographic factor order, band profile, Cholesky and diagonal-tile inverses of a batch.
+def _profile_bytes(adj, perm):
+    """Bytes of the 64-blocked band panels of a factor with row order ``perm``."""
+    n = perm.size
+    pos = np.empty(n, dtype=np.int64)
+    pos[perm] = np.arange(n)
+    coo = adj.tocoo()
+    f = pos.copy()
+    np.minimum.at(f, coo.row, pos[coo.col])
+    f_by_pos = np.empty(n, dtype=np.int64)
+    f_by_pos[pos] = f
+    nb = -(-n // 64)
+    pad = np.concatenate([f_by_pos, np.arange(n, nb * 64)])
+    bmin = pad.reshape(nb, 64).min(axis=1)
+    K = np.arange(nb) - bmin // 64
+    return float(K.sum() * 64 * 64 * 8 + nb * 2304 * 8)
 
-    Returns (L_P, Dinv, perms, kcnts, info): L_P[b] is the Cholesky factor of A[b] with rows and
-    columns in ascending global-index order (a plane sweep for grid operators, so L is banded),
-    kcnts[b][I] the number of 64-wide panel tiles left of the diagonal in block-row I.
+
+def local_orders(adj_csr, maps, kind):
+    """Factor row order of every subdomain: "lex" = ascending global index (a plane sweep for
+    grid operators), "rcm" = reverse Cuthill-McKee of the local graph."""
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+    out = []
+    for m in maps:
+        if kind == "lex":
+            out.append(np.argsort(m.indices, kind="stable").astype(np.int64))
+        else:
+            sub = adj_csr[m.indices][:, m.indices].tocsr()
+            out.append(np.asarray(reverse_cuthill_mckee(sub, symmetric_mode=True), dtype=np.int64))
+    return out
+
+
+def choose_local_order(adj_csr, maps, symmetric, forced=False):
+    """Pick lex or RCM by the band bytes on sample subdomains; None (unless ``forced``) when the
+    dense inverse is cheaper to stream (then the inverse-tile path is used)."""
+    sample = sorted({0, len(maps) // 2, len(maps) - 1})
+    best = None
+    for kind in ("lex", "rcm"):
+        tot = inv = 0.0
+        for s in sample:
+            m = maps[s]
+            adj = adj_csr[m.indices][:, m.indices]
+            perm = local_orders(adj_csr, [m], kind)[0]
+            band = _profile_bytes(adj, perm)
+            # Cholesky: L read twice; LU: L and U (about twice the lower profile) once each
+            tot += 2.0 * band
+            n = m.n_local
+            inv += (8.0 * n * (n + 1) / 2) if symmetric else 8.0 * n * n
+        if best is None or tot < best[1]:
+            best = (kind, tot, inv)
+    kind, tot, inv = best
+    return (kind if forced or tot < 0.8 * inv else None), tot / inv
+
+
+def lu_growth(torch, csr, maps, perm_kind, adj_csr, device, sample=None):
+    """Largest pivot growth max|U| / max|A| of the banded LU on sample subdomains.
+
+    Partial pivoting in a bandwidth-reducing order can grow the factors of saddle-point blocks
+    (the tiny pressure block is eliminated early); the reference factors in its own local order.
+    A large growth makes the band-LU solve less accurate, so "auto" keeps the inverse tiles then.
+    """
+    sample = sample or sorted({0, len(maps) // 2, len(maps) - 1})
+    worst = 1.0
+    for s in sample:
+        m = maps[s]
+        perm = local_orders(adj_csr, [m], perm_kind)[0]
+        blk = csr[m.indices[perm]][:, m.indices[perm]].toarray()
+        A = torch.as_tensor(blk, device=device)
+        LU, piv, info = torch.linalg.lu_factor_ex(A)
+        worst = max(worst, float(torch.triu(LU).abs().max() / A.abs().max()))
+    return worst
+
+
+def _lex_perm(torch, A, perms, n_list, ld):
+    cnt = A.shape[0]
+    dev = A.device
+    P = torch.arange(ld, device=dev).repeat(cnt, 1)
+    for b in range(cnt):
+        P[b, : n_list[b]] = torch.as_tensor(perms[b], device=dev)
+    AP = torch.gather(A, 1, P[:, :, None].expand(cnt, ld, ld))
+    AP = torch.gather(AP, 2, P[:, None, :].expand(cnt, ld, ld)).contiguous()
+    return AP, P, perms
+
+
+def _band_lu_factor(torch, A, perm_list, n_list, ld):
+    """Banded LU (partial pivoting) of a batch in lexicographic factor order.
+
+    Returns (LU, piv, Ldinv, Udinv, perm_in, perm_out, lcodes, ucodes, info, P): getrf of
+    A_P = P_piv L U; the row interchanges stay inside the band, so L (row profile) and U (last
+    nonzero per row) keep narrow profiles; perm_in composes the factor order with the pivots.
     """
     cnt = A.shape[0]
     dev = A.device
     nbk = ld // 64
-    P = torch.arange(ld, device=dev).repeat(cnt, 1)
-    perms = []
+    AP, P, perms = _lex_perm(torch, A, perm_list, n_list, ld)
+    LU, piv, info = torch.linalg.lu_factor_ex(AP)
+    del AP
+    LU = LU.contiguous()
+    nzm = LU != 0
+    ar = torch.arange(ld, device=dev)
+    lower = nzm & (ar[None, :] < ar[:, None])[None]
+    has = lower.any(dim=2)
+    firstL = torch.where(has, torch.argmax(lower.to(torch.int8), dim=2), ar[None, :].expand(cnt, ld))
+    upper = nzm & (ar[None, :] >= ar[:, None])[None]
+    lastU = ld - 1 - torch.argmax(torch.flip(upper, dims=[2]).to(torch.int8), dim=2)
+    lastU = torch.maximum(lastU, ar[None, :].expand(cnt, ld))
+    del nzm, lower, upper
+    fmin = firstL.view(cnt, nbk, 64).min(dim=2).values
+    gmax = lastU.view(cnt, nbk, 64).max(dim=2).values
+    Ib = torch.arange(nbk, device=dev)[None, :]
+    K = (Ib - fmin // 64).clamp(min=0)
+    fz = torch.where(K > 0, (fmin % 64) // 8, torch.zeros_like(K))
+    R = (gmax // 64 - Ib).clamp(min=0)
+    nzs = (gmax - (Ib + 1) * 64) // 8 + 1                 # nonzero strips of the right panel
+    tz = torch.where(R > 0, 8 * R - nzs, torch.zeros_like(R))
+    lc = (K | (fz << 16)).cpu().numpy().astype(np.int32)
+    uc = (R | (tz << 16)).cpu().numpy().astype(np.int32)
+    Ld = LU.view(cnt, nbk, 64, nbk, 64).diagonal(dim1=1, dim2=3).permute(0, 3, 1, 2)
+    eye = torch.eye(64, dtype=torch.float64, device=dev).expand(cnt, nbk, 64, 64)
+    Ldinv = torch.linalg.solve_triangular(Ld, eye, upper=False, unitriangular=True).contiguous()
+    Udinv = torch.linalg.solve_triangular(Ld, eye, upper=True).contiguous()
+    piv_h = piv.cpu().numpy()
+    perm_in, perm_out, lcodes, ucodes = [], [], [], []
     for b in range(cnt):
-        perm = np.argsort(idx_list[b], kind="stable").astype(np.int64)
-        perms.append(perm.astype(np.int32))
-        P[b, : n_list[b]] = torch.as_tensor(perm, device=dev)
-    AP = torch.gather(A, 1, P[:, :, None].expand(cnt, ld, ld))
-    AP = torch.gather(AP, 2, P[:, None, :].expand(cnt, ld, ld)).contiguous()
+        n = n_list[b]
+        nb = -(-n // 64)
+        q = np.arange(ld)
+        for i, j in enumerate(piv_h[b] - 1):          # LAPACK interchanges, in order
+            if j != i:
+                q[i], q[j] = q[j], q[i]
+        if q[:n].max() >= n:
+            raise RuntimeError("pivoting left the subdomain block")
+        perm_out.append(perms[b].astype(np.int32))
+        perm_in.append(perms[b][q[:n]].astype(np.int32))
+        lcodes.append(lc[b, :nb])
+        ucodes.append(uc[b, :nb])
+    return LU, piv, Ldinv, Udinv, perm_in, perm_out, lcodes, ucodes, info, P
+
+
+def _band_factor(torch, A, perm_list, n_list, ld):
+    """Lexicographic factor order, band profile, Cholesky and diagonal-tile inverses of a batch.
+
+    Returns (L_P, Dinv, perms, kcnts, info, P, codes): L_P[b] is the Cholesky factor of A[b] with
+    rows and columns in factor order (``perm_list[b]``: ascending global index or RCM), so L is
+    banded; kcnts[b][I] = panel tiles left of the diagonal in block-row I; codes add the leading
+    all-zero 8-column strips.
+    """
+    cnt = A.shape[0]
+    dev = A.device
+    nbk = ld // 64
+    AP, P, perms = _lex_perm(torch, A, perm_list, n_list, ld)
+    perms = [p.astype(np.int32) for p in perms]
     first = torch.argmax((AP != 0).to(torch.int8), dim=2)           # row profile f(i)
     fmin = first.view(cnt, nbk, 64).min(dim=2).values
     bmin = fmin // 64
@@ -468,15 +601,31 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         shard.attach(handle)
     else:
         lo, hi = 0, N
-    if local == "auto":
-        local = "band" if symmetric else "inverse"
-    if local not in ("band", "inverse"):
+    if local not in ("auto", "band", "inverse"):
         raise ValueError(f"unknown local operator kind {local!r}")
-    if local == "band" and not symmetric:
-        raise ValueError("banded Cholesky local operators need a symmetric matrix")
-    band = local == "band"
+    forced = local == "band"
+    band = local in ("auto", "band")
+    order_kind = None
     if band:
-        handle.check(lib.tls_set_local_kind(handle.ctx, 1))
+        from .partition import symmetrized_graph as _sg
+        g = _sg(csr)
+        import scipy.sparse as sp
+        adj = sp.csr_matrix((np.ones(g.adjacency.size), g.adjacency, g.indptr), shape=csr.shape)
+        adj = (adj + sp.identity(csr.shape[0], format="csr")).tocsr()
+        order_kind, ratio = choose_local_order(adj, maps, symmetric, forced)
+        _log(time.perf_counter(), f"band order {order_kind} (band/inverse bytes {ratio:.2f})")
+        if order_kind is None:
+            band = False  # "auto": no ordering beats streaming the dense inverse
+        elif not symmetric and not forced:
+            growth = lu_growth(torch, csr, maps, order_kind, adj, dev)
+            _log(time.perf_counter(), f"band LU pivot growth {growth:.2e}")
+            if growth > 1.0e3:
+                band = False  # keep the inverse tiles (factored in the reference's local order)
+    band_lu = band and not symmetric
+    handle.local_kind = ("band-lu" if band_lu else "band") if band else "inverse"
+    handle.local_order = order_kind
+    if band:
+        handle.check(lib.tls_set_local_kind(handle.ctx, 2 if band_lu else 1))
     offsets = np.concatenate([[0], np.cumsum(n_loc)]).astype(np.int64)
     indices = np.concatenate([m.indices for m in maps]).astype(np.int64)
     n_int32 = n_int.astype(np.int32)  # keep alive across the call (raw pointer below)
@@ -484,7 +633,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                                            _lib.ptr(n_int32)))
     ld = int(n_loc[lo:hi].max())
     if band:
-        ld = -(-ld // 64) * 64
+        ld = -(-ld // 64) * 64  # factor tiles are 64 x 64
     if batch is None:
         free, _ = torch.cuda.mem_get_info(dev)
         per = 8.0 * ld * ld * 4.0 + 4.0 * csr.shape[0]
@@ -503,10 +652,51 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             _log(t0, f"batch at {first}")
         A = torch.empty((cnt, ld, ld), dtype=torch.float64, device=dev)
         handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
-        if band:
-            idx_list = [maps[first + b].indices for b in range(cnt)]
+        if band_lu:
+            perm_list = local_orders(adj, [maps[first + b] for b in range(cnt)], order_kind)
             n_list = [int(n_loc[first + b]) for b in range(cnt)]
-            L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, idx_list, n_list, ld)
+            LU, piv, Ldinv, Udinv, pin, pout, lcodes, ucodes, info, P = _band_lu_factor(
+                torch, A, perm_list, n_list, ld)
+            for b in range(cnt):  # the reference's singularity rule (src/subdomain.py:86-88)
+                nb_ = n_list[b]
+                blk = LU[b, :nb_, :nb_]
+                if int(info[b]) != 0 or float(blk.diagonal().abs().min()) <= nb_ * EPS * float(blk.abs().max()):
+                    raise SubdomainSetupError(first + b, "local block is numerically singular")
+            pin_c = np.concatenate(pin).astype(np.int32)
+            pout_c = np.concatenate(pout).astype(np.int32)
+            lc_c = np.concatenate(lcodes).astype(np.int32)
+            uc_c = np.concatenate(ucodes).astype(np.int32)
+            handle.check(lib.tls_store_local_band_lu(handle.ctx, first, cnt, _lib.ptr(LU), ld, _lib.ptr(Ldinv),
+                                                     _lib.ptr(Udinv), ld // 64, _lib.ptr(pin_c),
+                                                     _lib.ptr(pout_c), _lib.ptr(lc_c), _lib.ptr(uc_c), s_ptr))
+            torch.cuda.current_stream().synchronize()
+            del Ldinv, Udinv
+            if want_coarse:
+                for b in range(cnt):
+                    s = first + b
+                    n, ni = int(n_loc[s]), int(n_int[s])
+                    nin = n - int(n_bnd[s])
+                    if n == nin:
+                        Bring = torch.zeros((n, 0), dtype=torch.float64, device=dev)
+                    else:
+                        pinv = torch.empty(ld, dtype=torch.long, device=dev)
+                        pinv[P[b]] = torch.arange(ld, device=dev)
+                        E = torch.zeros((ld, n - nin), dtype=torch.float64, device=dev)
+                        E[pinv[nin:n], torch.arange(n - nin, device=dev)] = 1.0
+                        Bring = torch.linalg.lu_solve(LU[b], piv[b], E)[pinv[:n]]
+                    Z, gaps[s] = _subdomain_columns(torch, coarse, A[b], Bring, n, ni, nin, tau, n_modes)
+                    if Z.shape[1]:
+                        nz = torch.any(Z != 0, dim=0)
+                        if not bool(nz.all()):
+                            Z = Z[:, nz].contiguous()
+                    z_dev[s] = Z
+                    w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
+            del A, LU, piv
+            continue
+        if band:
+            perm_list = local_orders(adj, [maps[first + b] for b in range(cnt)], order_kind)
+            n_list = [int(n_loc[first + b]) for b in range(cnt)]
+            L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld)
             bad = torch.nonzero(info).flatten().cpu().numpy()
             if bad.size:
                 s = first + int(bad[0])

@@ -43,7 +43,7 @@ def test_topk_subspace_matches_dense_eigh():
 def test_batched_band_coarse_columns_match_dense_path(name, sel):
     d, ms, A, ld = _batch(name, sel)
     k = int(d["n_modes"])
-    L, Dinv, perms, kcnts, info, P, codes = G._band_factor(torch, A, [m.indices for m in ms],
+    L, Dinv, perms, kcnts, info, P, codes = G._band_factor(torch, A, [np.argsort(m.indices, kind="stable") for m in ms],
                                                     [m.n_local for m in ms], ld)
     assert int(info.abs().sum()) == 0
     ns = [m.n_local for m in ms]
@@ -72,7 +72,7 @@ def test_batched_band_coarse_columns_match_dense_path(name, sel):
 
 def test_band_solve_multi_matches_dense():
     d, ms, A, ld = _batch("cfg2_m24", [0, 13])
-    L, Dinv, perms, kcnts, info, P, codes = G._band_factor(torch, A, [m.indices for m in ms],
+    L, Dinv, perms, kcnts, info, P, codes = G._band_factor(torch, A, [np.argsort(m.indices, kind="stable") for m in ms],
                                                     [m.n_local for m in ms], ld)
     kc = np.zeros((len(ms), ld // 64), dtype=np.int64)
     for b in range(len(ms)):
