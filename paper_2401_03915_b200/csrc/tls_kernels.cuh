@@ -758,6 +758,63 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 // inverted diagonal tile, lower triangular: warp w's 8-column strip is stored from row 8w on
 constexpr int DIAG_PACK = 2304;  // = sum_w 8 * (64 - 8w)
 __device__ __forceinline__ int diag_strip_off(int w) { return 512 * w - 32 * w * (w - 1); }
+// L2 prefetch of item j of step I of an L stream in forward order (item j < K_I: panel tile j
+// without its leading zero strips, j == K_I: the packed diagonal), spilling into later steps.
+__device__ __forceinline__ void prefetch_fwd_item(const BandDesc& b, int I, int j) {
+  while (I < b.nb) {
+    const int code = b.kcnt[I], K = code & 0xffff, fz = code >> 16;
+    if (j <= K) {
+      const double* base = b.data + b.step_off[I];
+      if (j == K) {
+        prefetch_l2(base + (long long)K * TT * TT, 8u * DIAG_PACK);
+      } else {
+        const int z = j == 0 ? min(fz, 8) : 0;
+        if (z < 8) prefetch_l2(base + (long long)j * TT * TT + z * 8 * TT, 8u * (unsigned)((8 - z) * 8 * TT));
+      }
+      return;
+    }
+    j -= K + 1;
+    ++I;
+  }
+}
+// backward (Cholesky L^T) order per step J: diagonal first, then panel tiles 0..K-1; steps descend
+__device__ __forceinline__ void prefetch_bwd_item(const BandDesc& b, int J, int j) {
+  while (J >= 0) {
+    const int code = b.kcnt[J], K = code & 0xffff, fz = code >> 16;
+    if (j <= K) {
+      const double* base = b.data + b.step_off[J];
+      if (j == 0) {
+        prefetch_l2(base + (long long)K * TT * TT, 8u * DIAG_PACK);
+      } else {
+        const int t = j - 1, z = t == 0 ? min(fz, 8) : 0;
+        if (z < 8) prefetch_l2(base + (long long)t * TT * TT + z * 8 * TT, 8u * (unsigned)((8 - z) * 8 * TT));
+      }
+      return;
+    }
+    j -= K + 1;
+    --J;
+  }
+}
+// backward (LU, U stream) order per step I: panel tiles 0..R-1 (trailing zero strips dropped),
+// then the packed diagonal; steps descend
+__device__ __forceinline__ void prefetch_u_item(const BandDesc& b, int I, int j) {
+  while (I >= 0) {
+    const int code = b.ucnt[I], R = code & 0xffff, tz = code >> 16;
+    if (j <= R) {
+      const double* base = b.udata + b.ustep_off[I];
+      if (j == R) {
+        prefetch_l2(base + (long long)R * TT * TT, 8u * DIAG_PACK);
+      } else {
+        const int keep = j == R - 1 ? 8 - min(tz, 8) : 8;
+        if (keep > 0) prefetch_l2(base + (long long)j * TT * TT, 8u * (unsigned)(keep * 8 * TT));
+      }
+      return;
+    }
+    j -= R + 1;
+    --I;
+  }
+}
+
 // inverted diagonal tile, upper triangular: warp w's strip keeps rows 0 .. 8w+7
 __device__ __forceinline__ int udiag_strip_off(int w) { return 32 * w * w + 32 * w; }
 
@@ -776,7 +833,6 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   const bool drow = lane >= 4 * warp;                // rows 2l, 2l+1 inside the strip
   const int doff = diag_strip_off(warp) + (2 * lane - 8 * warp);
   for (int i = threadIdx.x; i < npad; i += NTHR) v[i] = x[b.xoff + i];
-  const long long dend = b.step_off[b.nb - 1] + (long long)(b.kcnt[b.nb - 1] & 0xffff) * TT * TT + DIAG_PACK;
   __syncthreads();
   // forward sweep: L u = x  (the factor is one contiguous stream in this order)
   for (int I = 0; I < b.nb; ++I) {
@@ -784,10 +840,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
     const int code = b.kcnt[I], K = code & 0xffff, fz = code >> 16;
     double ra0 = 0.0, ra1 = 0.0;
     for (int k = 0; k < K; ++k) {
-      if (threadIdx.x == 0) {  // one 32 KiB tile ahead of the stream, into L2
-        const long long pf = b.step_off[I] + (long long)(k + 2) * TT * TT;
-        if (pf < dend) prefetch_l2(b.data + pf, 8u * (unsigned)min((long long)TT * TT, dend - pf));
-      }
+      if (threadIdx.x == 0) prefetch_fwd_item(b, I, k + 2);  // two items ahead, into L2
       if (k * 8 + warp < fz) continue;               // strip left of the band profile: zeros
       const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
       double2 w[8];
@@ -797,6 +850,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) { ra0 += w[kk].x * uj[kk]; ra1 += w[kk].y * uj[kk]; }
     }
+    if (threadIdx.x == 0) prefetch_fwd_item(b, I, K + 2);
     red[warp * TT + 2 * lane] = ra0;
     red[warp * TT + 2 * lane + 1] = ra1;
     __syncthreads();
@@ -835,16 +889,12 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
     const int ulen = 8 * warp + 8;                   // rows stored in this warp's upper strip
     const bool urow = lane <= 4 * warp + 3;
     const int uoff = udiag_strip_off(warp) + 2 * lane;
-    const long long uend = b.ustep_off[0] + (long long)(b.ucnt[0] & 0xffff) * TT * TT + DIAG_PACK;
     for (int I = b.nb - 1; I >= 0; --I) {
       const double* blk = b.udata + b.ustep_off[I];
       const int code = b.ucnt[I], R = code & 0xffff, tz = code >> 16;
       double ra0 = 0.0, ra1 = 0.0;
       for (int k = 0; k < R; ++k) {
-        if (threadIdx.x == 0) {
-          const long long pf = b.ustep_off[I] + (long long)(k + 2) * TT * TT;
-          if (pf < uend) prefetch_l2(b.udata + pf, 8u * (unsigned)min((long long)TT * TT, uend - pf));
-        }
+        if (threadIdx.x == 0) prefetch_u_item(b, I, k + 2);
         if (k * 8 + warp >= 8 * R - tz) continue;    // strip right of the band profile: zeros
         const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
         double2 w[8];
@@ -854,6 +904,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) { ra0 += w[kk].x * yj[kk]; ra1 += w[kk].y * yj[kk]; }
       }
+      if (threadIdx.x == 0) prefetch_u_item(b, I, R + 2);
       red[warp * TT + 2 * lane] = ra0;
       red[warp * TT + 2 * lane + 1] = ra1;
       __syncthreads();
@@ -895,11 +946,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   for (int J = b.nb - 1; J >= 0; --J) {
     const double* blk = b.data + b.step_off[J];
     const int code = b.kcnt[J], K = code & 0xffff, fz = code >> 16;
-    if (threadIdx.x == 0 && J > 0) {  // previous step: its diagonal strips and first panel tile
-      const int Kp = b.kcnt[J - 1] & 0xffff;
-      prefetch_l2(b.data + b.step_off[J - 1] + (long long)Kp * TT * TT, 8u * DIAG_PACK);
-      if (Kp) prefetch_l2(b.data + b.step_off[J - 1], 8u * TT * TT);
-    }
+    if (threadIdx.x == 0) prefetch_bwd_item(b, J, 2);
     {
       const double u0 = v[J * TT + 2 * lane], u1 = v[J * TT + 2 * lane + 1];
       double cp[8];
@@ -921,8 +968,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
     }
     const double y0 = v[J * TT + 2 * lane], y1 = v[J * TT + 2 * lane + 1];
     for (int k = 0; k < K; ++k) {
-      if (threadIdx.x == 0 && k + 1 < K)
-        prefetch_l2(blk + (long long)(k + 1) * TT * TT, 8u * TT * TT);
+      if (threadIdx.x == 0) prefetch_bwd_item(b, J, k + 3);
       if (k * 8 + warp < fz) continue;
       const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
       double cp[8];
