@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -202,6 +203,7 @@ static int spmv_lpr(tls_ctx* ctx, cudaStream_t s, const double* x, double* y, co
                                                part, done);                                       \
     break;
   switch (ctx->lpr) {
+    SPMV_CASE(1)
     SPMV_CASE(2)
     SPMV_CASE(4)
     SPMV_CASE(8)
@@ -465,8 +467,14 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
   TRY(upload(ctx, ctx->col, indices, nnz));
   TRY(upload(ctx, ctx->val, data, nnz));
   const double avg = nrows ? (double)nnz / (double)nrows : 1.0;
-  int l = 2;
-  while (l < 32 && l < avg) l *= 2;
+  // lanes per row ~ nnz/row / 7 (measured on B200: 7-point rows run best one thread per row,
+  // 27-point rows with 4 lanes; tools/bench_spmv.py)
+  int l = 1;
+  while (l < 32 && 7 * l < avg) l *= 2;
+  if (const char* e = getenv("TLS_SPMV_LPR")) {  // tuning override (1, 2, 4, 8, 16, 32)
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) l = v;
+  }
   ctx->lpr = l;
   ctx->G = grid_for(nrows, NTHR);
   ctx->Gs = grid_for(nrows, NTHR / l);

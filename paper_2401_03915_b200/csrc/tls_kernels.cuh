@@ -75,7 +75,8 @@ __device__ __forceinline__ double sum_partials(const double* __restrict__ p, int
 // K1  CSR SpMV  (replaces scipy csr_matvec behind SparseMat.matvec, src/sparsemat.py:125-129)
 //   MODE 0: y = A x          MODE 1: y = b - A x       (src/krylov.py:88-89 replacement)
 //   DOT  0: none   1: partial sum x.y   2: partial sum y.y
-// LPR lanes per row, grid-stride over row groups with a fixed grid -> deterministic partials.
+// LPR lanes per row (1 = thread per row), grid-stride over row groups with a fixed grid ->
+// deterministic partials.
 // ---------------------------------------------------------------------------------------
 template <int LPR, int MODE, int DOT>
 __global__ void __launch_bounds__(NTHR) k_spmv(int n, const int* __restrict__ rowptr,
