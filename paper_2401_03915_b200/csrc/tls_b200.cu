@@ -62,6 +62,7 @@ struct tls_ctx {
   std::vector<int> stored;  // which subdomains have their inverse stored
   // ---- coarse
   int ncoarse = 0;
+  int kmax = 1;
   std::vector<int> h_k, h_cstart;
   std::vector<long long> h_zoff;
   double *d_Z = nullptr, *ctiles = nullptr;
@@ -664,6 +665,8 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
   }
   for (int g = ctx->own_hi; g < ctx->nsub_global; ++g) c += k[g];
   if (c != n_coarse) return fail(ctx, TLS_ERR_ARG, "sum of k differs from n_coarse");
+  ctx->kmax = 1;
+  for (int i = 0; i < ctx->nsub; ++i) ctx->kmax = std::max(ctx->kmax, ctx->h_k[i]);
   ctx->ncoarse = n_coarse;
   TRY(dalloc(ctx, ctx->d_Z, zo));
   if (zo) CK(cudaMemcpyAsync(ctx->d_Z, basis, sizeof(double) * zo, cudaMemcpyDeviceToDevice, s));
@@ -687,26 +690,32 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
   return TLS_OK;
 }
 
-// Units and reduction lists for one block (see k_symv_tiles).
-static void plan_block(int blk, int nt, int sym, int& slot, std::vector<Unit>& units,
+// Units and reduction lists for one block (see k_symv_tiles): units of ur tile-rows x UW
+// tile-cols (ur <= UR); symmetric blocks only plan units touching the lower triangle.
+static void plan_block(int blk, int nt, int sym, int ur, int& slot, std::vector<Unit>& units,
                        std::vector<OutTile>& outs, std::vector<int>& red) {
-  const int np = (nt + UR - 1) / UR, nq = (nt + UW - 1) / UW;
-  std::vector<int> uid((size_t)np * nq, -1);
+  const int np = (nt + ur - 1) / ur, nq = (nt + UW - 1) / UW;
   std::vector<int> uslot((size_t)np * nq, -1);
-  for (int p = 0; p < np; ++p)
-    for (int q = 0; q < (sym ? p + 1 : nq); ++q) {
+  for (int p = 0; p < np; ++p) {
+    const int i0 = p * ur, ni = std::min(ur, nt - i0);
+    for (int q = 0; q < nq; ++q) {
+      const int j0 = q * UW, nj = std::min(UW, nt - j0);
+      if (sym && j0 > i0 + ni - 1) break;  // entirely above the diagonal
       uslot[(size_t)p * nq + q] = slot;
-      units.push_back(Unit{blk, p, q, slot});
+      units.push_back(Unit{blk, i0, j0, slot, (short)ni, (short)nj, 0, 0});
       slot += SLOTS_PER_UNIT;
     }
+  }
   for (int J = 0; J < nt; ++J) {
     OutTile ot{blk, J, (int)red.size(), 0};
-    const int p = J / UR;
-    for (int q = 0; q < (sym ? p + 1 : nq); ++q) red.push_back(uslot[(size_t)p * nq + q] + (J - p * UR));
-    if (sym) {
+    const int p = J / ur;
+    for (int q = 0; q < nq; ++q)  // row partials of tile-row J
+      if (uslot[(size_t)p * nq + q] >= 0) red.push_back(uslot[(size_t)p * nq + q] + (J - p * ur));
+    if (sym) {  // column partials of tile-col J from units strictly below it
       const int q = J / UW;
-      for (int pp = q; pp < np; ++pp) {
-        const int imax = std::min((pp + 1) * UR, nt) - 1;
+      for (int pp = 0; pp < np; ++pp) {
+        if (uslot[(size_t)pp * nq + q] < 0) continue;
+        const int imax = std::min((pp + 1) * ur, nt) - 1;
         if (imax > J) red.push_back(uslot[(size_t)pp * nq + q] + UR + (J - q * UW));
       }
     }
@@ -757,7 +766,7 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   int slot = 0;
   ctx->algo_local = 0.0;
   for (int s = 0; s < nsub && ctx->local_kind == 0; ++s) {
-    plan_block(s, ctx->h_blk[s].nt, ctx->sym, slot, units, outs, red);
+    plan_block(s, ctx->h_blk[s].nt, ctx->sym, UR, slot, units, outs, red);
     const double ns = ctx->h_n[s];
     ctx->algo_local += ctx->sym ? 8.0 * ns * (ns + 1) / 2 + 8.0 * ns : 8.0 * ns * ns + 8.0 * ns;
   }
@@ -770,7 +779,8 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   ctx->nu_coarse = ctx->no_coarse = 0;
   ctx->algo_coarse = 0.0;
   if (ctx->ncoarse > 0) {
-    plan_block(nsub, ctx->h_blk[nsub].nt, ctx->sym, slot, units, outs, red);
+    // the coarse operator is ONE block: thinner units (2 tile-rows) to fill the machine
+    plan_block(nsub, ctx->h_blk[nsub].nt, ctx->sym, 2, slot, units, outs, red);
     ctx->nu_coarse = (int)units.size() - ctx->nu_local;
     ctx->no_coarse = (int)outs.size() - ctx->no_local;
     const double nc = ctx->ncoarse;

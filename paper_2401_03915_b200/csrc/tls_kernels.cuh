@@ -22,7 +22,7 @@ struct BlkDesc {                // one dense local operator (a subdomain or the 
   long long xoff;               // offset of its local vector in xloc / yloc (multiple of TT)
   int n, nt, sym, pad_;
 };
-struct Unit { int blk, p, q, slot; };       // tile-rows [p*UR, +UR) x tile-cols [q*UW, +UW)
+struct Unit { int blk, i0, j0, slot; short ni, nj, pad0, pad1; };  // tile-rows [i0, i0+ni) x cols [j0, j0+nj)
 struct OutTile { int blk, J, beg, end; };   // reduce slots red[beg:end] into y tile J of blk
 
 struct PcgState {
@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_symv_tiles(const BlkDesc* __restric
   const Unit un = units[blockIdx.x];
   const BlkDesc b = blks[un.blk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int I0 = un.p * UR, J0 = un.q * UW;
-  const int nI = min(UR, b.nt - I0), nJ = min(UW, b.nt - J0);
+  const int I0 = un.i0, J0 = un.j0;
+  const int nI = un.ni, nJ = un.nj;
   for (int t = threadIdx.x; t < UR * TT; t += NTHR) {
     xr[t] = t < nI * TT ? x[b.xoff + (long long)I0 * TT + t] : 0.0;
     xc[t] = t < nJ * TT ? x[b.xoff + (long long)J0 * TT + t] : 0.0;
