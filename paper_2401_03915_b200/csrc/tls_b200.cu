@@ -250,7 +250,8 @@ static int enq_gather(tls_ctx* ctx, cudaStream_t s, const double* r, const int* 
 }
 
 static int enq_restrict(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
-  k_restrict<<<ctx->nsub, NTHR, ctx->restrict_smem, s>>>(ctx->d_sub_idxoff, ctx->d_idx, ctx->d_nint, ctx->d_zoff,
+  k_restrict<<<ctx->nsub, 32 * std::min(std::max(ctx->kmax, 8), 32), ctx->restrict_smem, s>>>(
+      ctx->d_sub_idxoff, ctx->d_idx, ctx->d_nint, ctx->d_zoff,
                                         ctx->d_kcnt, ctx->d_cstart, ctx->d_Z, r,
                                         ctx->xloc + ctx->coarse_xoff, done);
   CKL();

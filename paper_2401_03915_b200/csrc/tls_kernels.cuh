@@ -134,7 +134,9 @@ __global__ void __launch_bounds__(NTHR) k_gather(long long m, const int* __restr
 //     subdomain, Z_s stored column by column (k x n_int, each column contiguous) so every
 //     load instruction is coalesced.  c lands in the coarse segment of xloc.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHR) k_restrict(const long long* __restrict__ sub_idxoff,
+// one warp per coarse column (blockDim = 32 * max k, up to 1024): r_int is gathered once per
+// subdomain into shared memory and every column is streamed by its own warp
+__global__ void __launch_bounds__(1024) k_restrict(const long long* __restrict__ sub_idxoff,
                                                    const int* __restrict__ idx,
                                                    const int* __restrict__ nint,
                                                    const long long* __restrict__ zoff,
@@ -149,11 +151,11 @@ __global__ void __launch_bounds__(NTHR) k_restrict(const long long* __restrict__
   const int ks = kcnt[s], ni = nint[s];
   if (ks == 0) return;
   const int* id = idx + sub_idxoff[s];
-  for (int p = threadIdx.x; p < ni; p += NTHR) rs[p] = __ldg(r + __ldg(id + p));
+  for (int p = threadIdx.x; p < ni; p += blockDim.x) rs[p] = __ldg(r + __ldg(id + p));
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* zs = Z + zoff[s];
-  for (int col = warp; col < ks; col += NTHR / 32) {
+  for (int col = warp; col < ks; col += nw) {
     const double* zc = zs + (long long)col * ni;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int p = lane;
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(NTHR) k_prolong(int n, const int* __restrict__
       const long long zo = __ldg(zrow + g);
       if (zo >= 0) {
         const int k = __ldg(zk + g), c0 = __ldg(zc + g), st = __ldg(zst + g);
+#pragma unroll 4
         for (int t = 0; t < k; ++t) cz += __ldg(Z + zo + (long long)t * st) * __ldg(yc + c0 + t);
       }
     }
