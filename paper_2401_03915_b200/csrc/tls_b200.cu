@@ -7,6 +7,8 @@
 // so one host sync happens per 25 PCG iterations / per GMRES cycle instead of per kernel.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_segmented_sort.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -608,18 +610,31 @@ int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first_g, int32_t count, double*
     if (ctx->h_n[s] > ld) return fail(ctx, TLS_ERR_ARG, "ld smaller than a local block");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
-  int* loc = nullptr;
-  CK(cudaMallocAsync((void**)&loc, sizeof(int) * (size_t)count * ctx->n, s));
-  CK(cudaMemsetAsync(loc, 0xff, sizeof(int) * (size_t)count * ctx->n, s));
+  const long long base = ctx->h_off[first];
+  const int items = (int)(ctx->h_off[first + count] - base);
+  int *beg = nullptr, *pos = nullptr, *skey = nullptr, *sval = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp_bytes, ctx->d_idx + base, skey, pos, sval, items,
+                                         count, beg, beg + count, s));
+  CK(cudaMallocAsync((void**)&beg, sizeof(int) * 2 * (size_t)count, s));
+  CK(cudaMallocAsync((void**)&pos, sizeof(int) * 3 * (size_t)items, s));
+  CK(cudaMallocAsync(&tmp, tmp_bytes + 16, s));
+  skey = pos + items;
+  sval = pos + 2 * (size_t)items;
   CK(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)count * ld * ld, s));
   dim3 g1(grid_for(ctx->max_n, NTHR) / 4 + 1, count);
-  k_loc_map<<<g1, NTHR, 0, s>>>(count, ctx->d_sub_idxoff, ctx->d_sub_n, ctx->d_idx, first, ctx->n, loc);
+  k_seg_prep<<<g1, NTHR, 0, s>>>(count, ctx->d_sub_idxoff, ctx->d_sub_n, first, beg, beg + count, pos);
   CKL();
+  CK(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, ctx->d_idx + base, skey, pos, sval, items, count, beg,
+                                         beg + count, s));
   dim3 g2(std::max<int>(1, (int)std::min<int64_t>((ld + 7) / 8, 4096)), count);
-  k_extract<<<g2, NTHR, 0, s>>>(count, ctx->d_sub_idxoff, ctx->d_sub_n, ctx->d_idx, first, ctx->n,
-                                loc, ctx->rowptr, ctx->col, ctx->val, out, ld);
+  k_extract<<<g2, NTHR, 0, s>>>(count, ctx->d_sub_idxoff, ctx->d_sub_n, ctx->d_idx, first, skey, sval,
+                                ctx->rowptr, ctx->col, ctx->val, out, ld);
   CKL();
-  CK(cudaFreeAsync(loc, s));
+  CK(cudaFreeAsync(tmp, s));
+  CK(cudaFreeAsync(pos, s));
+  CK(cudaFreeAsync(beg, s));
   return TLS_OK;
 }
 

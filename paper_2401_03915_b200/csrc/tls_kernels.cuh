@@ -659,26 +659,42 @@ __global__ void k_gm_cycle_begin(GmState* st, const double* part, int np, double
 // ---------------------------------------------------------------------------------------
 // Setup kernels (src/subdomain.py:53-69 extraction; tile packing of local inverses)
 // ---------------------------------------------------------------------------------------
-__global__ void k_loc_map(int count, const long long* __restrict__ sub_idxoff,
-                          const int* __restrict__ sub_n, const int* __restrict__ idx, int first,
-                          long long n, int* __restrict__ loc) {
+// local-index lookup for the extraction: the batch's global index lists are sorted per
+// subdomain (keys) together with their local positions (vals); a CSR column is then found by a
+// binary search in its subdomain's sorted list -- no n-sized map per subdomain.
+__global__ void k_seg_prep(int count, const long long* __restrict__ sub_idxoff, const int* __restrict__ sub_n,
+                           int first, int* __restrict__ beg, int* __restrict__ end, int* __restrict__ pos) {
   const int b = blockIdx.y;
   const int s = first + b;
-  const int ns = sub_n[s];
-  const int* id = idx + sub_idxoff[s];
-  for (int l = blockIdx.x * NTHR + threadIdx.x; l < ns; l += gridDim.x * NTHR)
-    loc[(long long)b * n + id[l]] = l;
+  const long long base = sub_idxoff[first];
+  const int o = (int)(sub_idxoff[s] - base), ns = sub_n[s];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    beg[b] = o;
+    end[b] = o + ns;
+  }
+  for (int l = blockIdx.x * NTHR + threadIdx.x; l < ns; l += gridDim.x * NTHR) pos[o + l] = l;
+}
+__device__ __forceinline__ int seg_find(const int* __restrict__ keys, int n, int c) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (keys[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < n && keys[lo] == c) ? lo : -1;
 }
 __global__ void k_extract(int count, const long long* __restrict__ sub_idxoff,
                           const int* __restrict__ sub_n, const int* __restrict__ idx, int first,
-                          long long n, const int* __restrict__ loc, const int* __restrict__ rowptr,
-                          const int* __restrict__ col, const double* __restrict__ val,
-                          double* __restrict__ out, long long ld) {
+                          const int* __restrict__ skey, const int* __restrict__ sval,
+                          const int* __restrict__ rowptr, const int* __restrict__ col,
+                          const double* __restrict__ val, double* __restrict__ out, long long ld) {
   const int b = blockIdx.y;
   const int s = first + b;
   const int ns = sub_n[s];
   const int* id = idx + sub_idxoff[s];
-  const int* lb = loc + (long long)b * n;
+  const int o = (int)(sub_idxoff[s] - sub_idxoff[first]);
+  const int* kb = skey + o;
+  const int* vb = sval + o;
   double* ob = out + (long long)b * ld * ld;
   const int warp = (blockIdx.x * NTHR + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nwarps = gridDim.x * (NTHR / 32);
@@ -689,8 +705,8 @@ __global__ void k_extract(int count, const long long* __restrict__ sub_idxoff,
     }
     const int g = id[l];
     for (int e = rowptr[g] + lane; e < rowptr[g + 1]; e += 32) {
-      const int L = lb[col[e]];
-      if (L >= 0) ob[(long long)l * ld + L] = val[e];
+      const int q = seg_find(kb, ns, col[e]);
+      if (q >= 0) ob[(long long)l * ld + vb[q]] = val[e];
     }
   }
 }

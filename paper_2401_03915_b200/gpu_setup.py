@@ -120,6 +120,19 @@ def warm_linalg(device=None):
     torch.cuda.synchronize(dev)
 
 
+_STAGE = {}
+
+
+def _stage(name, t_prev):
+    """Accumulate synchronized stage times (verbose mode only); returns the new timestamp."""
+    if not VERBOSE:
+        return t_prev
+    _torch().cuda.synchronize()
+    t = time.perf_counter()
+    _STAGE[name] = _STAGE.get(name, 0.0) + (t - t_prev)
+    return t
+
+
 def _log(t0, msg):
     if VERBOSE:
         print(f"[tls setup {time.perf_counter() - t0:7.1f}s] {msg}", flush=True)
@@ -233,9 +246,8 @@ def topk_subspace(torch, M, k, tol=1e-14, maxit=2000, seed=20240103, p=None):
     sweeps; stops when every wanted Ritz pair has ||M x - theta x|| <= tol * theta_1 and raises
     if that does not happen (never returns an unconverged span).  Batched replacement of the
     dense generalized eigensolve of src/spectral.py:69-85 for a fixed number of modes; small
-    matrices go to a dense batched eigh.  (A Chebyshev filter was tried and rejected: with
-    theta_1 / theta_p >> 1 a useful degree amplifies the top modes ~1e19 x more than the k-th,
-    which destroys the lower wanted directions in fp64.)
+    matrices go to a dense batched eigh.  Converges like (theta_{p+1} / theta_k)^2 per sweep:
+    slow on flat spectra, where ``topk_chebyshev`` (the setup's default) needs ~4x fewer products.
     """
     b, m, _ = M.shape
     p = min(m, p or max(3 * k, k + 16))
@@ -259,6 +271,63 @@ def topk_subspace(torch, M, k, tol=1e-14, maxit=2000, seed=20240103, p=None):
                 return th_all[:, :k], Xr[:, :, :k], it
             X = Xr  # continue from the Ritz basis (sorted, orthonormal)
     raise RuntimeError(f"subspace iteration did not converge: residual {res:.2e} after {maxit} sweeps")
+
+
+def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rmax=32.0, dmax=16):
+    """Top-k eigenpairs (descending) of a batch of symmetric PSD matrices M (b, m, m).
+
+    Chebyshev-filtered subspace iteration: each outer step applies T_d((M - c) / e) to the
+    current Ritz block, with [0, a] (a = the smallest Ritz value of the block, per matrix) mapped
+    onto [-1, 1], then CholeskyQR2 and Rayleigh-Ritz (p x p, host).  Each matrix gets its own
+    degree d_b (the batch runs max d_b products; a matrix whose degree is reached stops
+    updating), chosen so the filter's dynamic range over its wanted Ritz values,
+    T_d(x_1) / T_d(x_k), stays below min(rmax, residual / (64 eps)): the k-th direction then
+    keeps ~eps * range relative precision, below the current residual (an unbounded degree
+    amplifies the top modes ~1e19 x more than the k-th and wipes the lower wanted directions out
+    in fp64).  Same stopping rule as ``topk_subspace``; raises when it does not converge.
+    Returns (theta, X, block products).
+    """
+    b, m, _ = M.shape
+    p = min(m, p or max(3 * k, k + 16))
+    if m <= max(96, 2 * p):
+        w, Q = torch.linalg.eigh(M)
+        return torch.flip(w, dims=[-1])[:, :k], torch.flip(Q, dims=[-1])[:, :, :k], 0
+    gen = torch.Generator(device=M.device)
+    gen.manual_seed(seed)
+    X = _orth(torch, torch.randn((b, m, p), generator=gen, dtype=M.dtype, device=M.device))
+    X = _orth(torch, M @ (M @ X))
+    th, X, MX = _rayleigh_ritz(torch, M, X, p)
+    scale = th[:, :1].abs().clamp(min=1e-300)
+    res = float("inf")
+    products = 3
+    for it in range(1, maxit + 1):
+        R = MX[:, :, :k] - X[:, :, :k] * th[:, None, :k]
+        res_b = (R.norm(dim=1) / scale).amax(dim=1)                     # (b,)
+        res = float(res_b.max())
+        if res <= tol:
+            return th[:, :k], X[:, :, :k], products
+        a = th[:, p - 1].clamp(min=0.0)
+        e = (0.5 * a).clamp(min=1e-300)
+        x1 = ((th[:, 0] - e) / e).clamp(min=1.0 + 1e-12)
+        xk = ((th[:, k - 1] - e) / e).clamp(min=1.0 + 1e-12)
+        per = (torch.acosh(x1) - torch.acosh(xk)).clamp(min=1e-12)
+        rng = (res_b / (64.0 * EPS)).clamp(min=2.0, max=rmax)
+        d_b = torch.floor(torch.log(rng) / per).clamp(min=1, max=dmax)
+        d = int(d_b.max())
+        c = e[:, None, None]
+        inv_e = (1.0 / e)[:, None, None]
+        Y0 = X
+        Y1 = (MX - c * X) * inv_e
+        for j in range(2, d + 1):
+            Y2 = 2.0 * (M @ Y1 - c * Y1) * inv_e - Y0
+            live = (d_b >= j)[:, None, None]
+            Y0 = torch.where(live, Y1, Y0)
+            Y1 = torch.where(live, Y2, Y1)
+        products += d
+        X = _orth(torch, Y1)
+        th, X, MX = _rayleigh_ritz(torch, M, X, p)
+        products += 1
+    raise RuntimeError(f"Chebyshev subspace iteration did not converge: residual {res:.2e} after {maxit} steps")
 
 
 def band_solve_multi(torch, L, Dinv, kc, E):
@@ -290,6 +359,37 @@ def band_solve_multi(torch, L, Dinv, kc, E):
     return X
 
 
+def _harmonic_h(torch, Ag, Bring, n, ni):
+    """H = F^T A_II F for F = Bring[:ni] without the dense (ni x ni) A_II product.
+
+    Interior rows of A Bring vanish (Bring = A^{-1} restricted to the ring columns, and the ring
+    lies outside the interior), so A_II F = -A[:ni, ni:n] Bring[ni:n].  Only the interior rows
+    adjacent to the overlap have a nonzero there; their sparse rows (at most D nonzeros, taken
+    with topk from the dense block) times Bring give those rows of A_II F, and
+    H = -F[R]^T (A[R, ni:n] Bring[ni:n]) costs |R| * nbr^2 instead of ni^2 * nbr + ni * nbr^2.
+    """
+    g = Ag.shape[0]
+    Gb = Ag[:, :ni, ni:n]
+    nnz = (Gb != 0).sum(dim=2)                                       # (g, ni)
+    D = int(nnz.max()) if nnz.numel() else 0
+    if D == 0:
+        return torch.zeros((g, Bring.shape[2], Bring.shape[2]), dtype=Bring.dtype, device=Bring.device)
+    cntR = (nnz > 0).sum(dim=1)
+    Rm = int(cntR.max())
+    R = torch.argsort((nnz == 0).to(torch.int8), dim=1, stable=True)[:, :Rm]   # rows with a nonzero
+    Gr = torch.gather(Gb, 1, R[:, :, None].expand(g, Rm, n - ni))
+    _, cols = torch.topk(Gr.abs(), D, dim=2)
+    vals = torch.gather(Gr, 2, cols)                                 # signed entries (0 pads)
+    del Gr
+    nbr = Bring.shape[2]
+    Blay = Bring[:, ni:n]
+    Y = torch.zeros((g, Rm, nbr), dtype=Bring.dtype, device=Bring.device)
+    for d in range(D):
+        Y.addcmul_(vals[:, :, d:d + 1], torch.gather(Blay, 1, cols[:, :, d:d + 1].expand(g, Rm, nbr)))
+    Fr = torch.gather(Bring[:, :ni], 1, R[:, :, None].expand(g, Rm, nbr))
+    return -(Fr.mT @ Y)
+
+
 def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=None, kc=None):
     """Coarse columns of a batch of band-factored subdomains, batched by shape.
 
@@ -317,6 +417,7 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
         rows = pinv[:, nin:n]                                       # (g, nbr) factor positions of the ring
         E.view(len(bs), -1)[torch.arange(len(bs), device=dev)[:, None],
                             rows * nbr + torch.arange(nbr, device=dev)[None, :]] = 1.0
+        ts = _stage("coarse: ring rhs", time.perf_counter() if VERBOSE else 0.0)
         if Dinv is not None:   # banded blocked solve (batched GEMMs on the band only)
             X = band_solve_multi(torch, L.index_select(0, bi), Dinv.index_select(0, bi),
                                  kc[bs], E)
@@ -325,18 +426,22 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
         del E
         Bring = torch.gather(X, 1, pinv[:, :n, None].expand(len(bs), n, nbr))  # local order
         del X
+        ts = _stage("coarse: ring solve", ts)
         if kind == "gevp" and n_modes is not None:
             F = Bring[:, :ni]
             B22 = Bring[:, nin:n]
             Ag = A.index_select(0, bi)
-            H = F.mT @ (Ag[:, :ni, :ni] @ F)
+            H = _harmonic_h(torch, Ag, Bring, n, ni)
             H = 0.5 * (H + H.mT)
+            ts = _stage("coarse: H = F^T A_II F", ts)
             C, info = torch.linalg.cholesky_ex(0.5 * (B22 + B22.mT))
             Xs = torch.linalg.solve_triangular(C, H, upper=False)
             M = torch.linalg.solve_triangular(C, Xs.mT, upper=False)
             M = 0.5 * (M + M.mT)
             kk = min(n_modes + 1, nbr)
-            th, Q, _ = topk_subspace(torch, M, kk)
+            ts = _stage("coarse: pencil reduction", ts)
+            th, Q, _ = topk_chebyshev(torch, M, kk)
+            ts = _stage("coarse: subspace iteration", ts)
             sig = torch.sqrt(torch.clamp(th, min=0.0)).cpu().numpy()
             U = torch.linalg.solve_triangular(C.mT, Q, upper=True)
             V = Bring @ U
@@ -358,6 +463,7 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
                     out[b] = (V[j][:ni, torch.as_tensor(keeps[j], device=dev)].contiguous(),
                               _cut_gap(sig[j], keeps[j]), None)
             del Ag, H, C, Xs, M, U, V
+            ts = _stage("coarse: epilogue", ts)
         else:
             for j, b in enumerate(bs):
                 out[b] = _subdomain_columns(torch, kind, A[b], Bring[j], n, ni, nin, tau, n_modes) + (None,)
@@ -503,6 +609,38 @@ def _band_lu_factor(torch, A, perm_list, n_list, ld):
     return LU, piv, Ldinv, Udinv, perm_in, perm_out, lcodes, ucodes, info, P
 
 
+def _band_cholesky_inplace(torch, AP, kmax):
+    """Blocked right-looking Cholesky of a batch of banded SPD matrices, in place (lower).
+
+    ``kmax[I]`` = the batch's largest panel count left of the diagonal in block row I (64-row
+    blocks); the factor keeps the row profile of AP (no fill outside the envelope), so step J
+    only touches block rows J+1 .. rmax[J] = max{I : I - kmax[I] <= J}: a 64 x 64 batched
+    Cholesky, one batched TRSM on the panel below it and one batched GEMM update of the trailing
+    band square -- ~n * bandwidth^2 flops instead of the dense n^3 / 3.  Entries above the
+    diagonal are zeroed at the end.  Returns (L, info) with info[b] = 1-based row of the first
+    non-positive pivot (0 = success), like ``torch.linalg.cholesky_ex``.
+    """
+    cnt, ld, _ = AP.shape
+    nbk = ld // 64
+    kmax = np.asarray(kmax, dtype=np.int64)
+    rows = np.arange(nbk)
+    info = torch.zeros(cnt, dtype=torch.int32, device=AP.device)
+    for J in range(nbk):
+        j0, j1 = J * 64, (J + 1) * 64
+        reach = rows[(rows > J) & (rows - kmax <= J)]
+        r1 = (int(reach.max()) + 1) * 64 if reach.size else j1
+        D = AP[:, j0:j1, j0:j1]
+        Ljj, inf = torch.linalg.cholesky_ex(D)
+        info = torch.where((info == 0) & (inf > 0), inf + j0, info)
+        D.copy_(Ljj)
+        if r1 > j1:
+            P = AP[:, j1:r1, j0:j1]
+            P.copy_(torch.linalg.solve_triangular(Ljj.mT, P, upper=True, left=False))
+            AP[:, j1:r1, j1:r1].baddbmm_(P, P.mT, alpha=-1.0)
+    AP.masked_fill_(torch.ones(ld, ld, dtype=torch.bool, device=AP.device).triu_(1), 0.0)
+    return AP, info
+
+
 def _band_factor(torch, A, perm_list, n_list, ld):
     """Lexicographic factor order, band profile, Cholesky and diagonal-tile inverses of a batch.
 
@@ -523,9 +661,7 @@ def _band_factor(torch, A, perm_list, n_list, ld):
     # leading all-zero 8-column strips of each panel (the factor keeps the profile of A_P)
     fz = ((fmin % 64) // 8).cpu().numpy().astype(np.int32)
     fz = np.where(kc > 0, fz, 0)
-    L, info = torch.linalg.cholesky_ex(AP)
-    del AP
-    L = L.contiguous()  # cuSOLVER returns column-major
+    L, info = _band_cholesky_inplace(torch, AP, kc.max(axis=0))
     Ld = L.view(cnt, nbk, 64, nbk, 64).diagonal(dim1=1, dim2=3).permute(0, 3, 1, 2)
     eye = torch.eye(64, dtype=torch.float64, device=dev).expand(cnt, nbk, 64, 64)
     Dinv = torch.linalg.solve_triangular(Ld, eye, upper=False).contiguous()
@@ -576,6 +712,21 @@ def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
         Wg = w_blocks[s].index_select(0, grp_d[o0:o1])
         A0[cstart[j]:cstart[j + 1], cstart[s]:cstart[s + 1]] += Zj.mT @ Wg
     return A0
+
+
+def _band_bytes(codes):
+    """Device bytes the library allocates for band panels with these codes (band_layout)."""
+    k = (np.asarray(codes, dtype=np.int64) & 0xFFFF)
+    return 8 * int((k * 4096 + 2304).sum()) + 12 * k.size
+
+
+def _make_room(torch, dev, nbytes, slack=1 << 29):
+    """Return torch's cached blocks to the driver only when the library's next cudaMalloc of
+    ``nbytes`` would not fit (emptying the cache every batch costs a re-map of the batch
+    buffers)."""
+    free, _ = torch.cuda.mem_get_info(dev)
+    if free < nbytes + slack:
+        torch.cuda.empty_cache()
 
 
 def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_modes, drop_tol,
@@ -645,12 +796,13 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     gaps = {}
     t0 = time.perf_counter()
     _log(t0, f"subdomains [{lo},{hi}) of {N}, local={local}, ld={ld}, batch={batch}")
+    a_buf = torch.empty((min(batch, hi - lo), ld, ld), dtype=torch.float64, device=dev)
     for first in range(lo, hi, batch):
         cnt = min(batch, hi - first)
         if first > lo:
-            torch.cuda.empty_cache()  # band storage is cudaMalloc'ed by the library per batch
             _log(t0, f"batch at {first}")
-        A = torch.empty((cnt, ld, ld), dtype=torch.float64, device=dev)
+        tb0 = time.perf_counter() if VERBOSE else 0.0
+        A = a_buf[:cnt]
         handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
         if band_lu:
             perm_list = local_orders(adj, [maps[first + b] for b in range(cnt)], order_kind)
@@ -666,6 +818,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             pout_c = np.concatenate(pout).astype(np.int32)
             lc_c = np.concatenate(lcodes).astype(np.int32)
             uc_c = np.concatenate(ucodes).astype(np.int32)
+            _make_room(torch, dev, _band_bytes(lc_c) + _band_bytes(uc_c))
             handle.check(lib.tls_store_local_band_lu(handle.ctx, first, cnt, _lib.ptr(LU), ld, _lib.ptr(Ldinv),
                                                      _lib.ptr(Udinv), ld // 64, _lib.ptr(pin_c),
                                                      _lib.ptr(pout_c), _lib.ptr(lc_c), _lib.ptr(uc_c), s_ptr))
@@ -694,18 +847,23 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             del A, LU, piv
             continue
         if band:
+            tb = _stage("extract", tb0)
             perm_list = local_orders(adj, [maps[first + b] for b in range(cnt)], order_kind)
+            tb = _stage("orders (host)", tb)
             n_list = [int(n_loc[first + b]) for b in range(cnt)]
             L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld)
+            tb = _stage("band factor", tb)
             bad = torch.nonzero(info).flatten().cpu().numpy()
             if bad.size:
                 s = first + int(bad[0])
                 raise SubdomainSetupError(s, "factorization failed: the local block is not positive definite")
             perm_cat = np.concatenate(perms).astype(np.int32)
             k_cat = np.concatenate(codes).astype(np.int32)
+            _make_room(torch, dev, _band_bytes(k_cat))
             handle.check(lib.tls_store_local_band(handle.ctx, first, cnt, _lib.ptr(L), ld, _lib.ptr(Dinv),
                                                   ld // 64, _lib.ptr(perm_cat), _lib.ptr(k_cat), s_ptr))
             torch.cuda.current_stream().synchronize()  # the host arrays above stay alive until here
+            tb = _stage("band pack", tb)
             if want_coarse:
                 kc_full = np.zeros((cnt, ld // 64), dtype=np.int64)
                 for b in range(cnt):
@@ -764,6 +922,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                 z_dev[s] = Z
                 w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
         del A, Binv
+    del a_buf
     if not want_coarse:
         torch.cuda.empty_cache()
         return None
@@ -824,6 +983,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     nC = int(counts.sum())
     owner = np.asarray(owner, dtype=np.int64)
     torch.cuda.empty_cache()
+    if VERBOSE:
+        _log(t0, "stage times: " + ", ".join(f"{k} {v:.2f}s" for k, v in _STAGE.items()))
     _log(t0, f"local operators done; assembling A0 ({nC} x {nC})")
     A0 = assemble_a0_columns(maps, owner, z_all, w_dev, counts, own, dev)
     del w_dev

@@ -39,6 +39,22 @@ def test_topk_subspace_matches_dense_eigh():
         assert float(sv.min()) > 1 - 1e-12
 
 
+@pytest.mark.parametrize("decay", ["flat", "fast"])
+def test_topk_chebyshev_matches_dense_eigh(decay):
+    torch.manual_seed(1)
+    m, k = 400, 13
+    Q, _ = torch.linalg.qr(torch.randn(2, m, m, dtype=torch.float64))
+    i = torch.arange(m, dtype=torch.float64)
+    lam = torch.exp(-0.003 * i) if decay == "flat" else torch.logspace(0, -12, m, dtype=torch.float64)
+    M = Q @ torch.diag_embed(lam.expand(2, m)) @ Q.mT
+    th, X, mv = G.topk_chebyshev(torch, M, k)
+    assert mv > 0
+    np.testing.assert_allclose(th.numpy(), lam[:k].expand(2, k).numpy(), rtol=1e-12)
+    for b in range(2):
+        sv = torch.linalg.svdvals(X[b].mT @ Q[b][:, :k])
+        assert float(sv.min()) > 1 - 1e-12
+
+
 @pytest.mark.parametrize("name,sel", [("cfg2_m24", [0, 4, 13, 26]), ("cfg5_m16", [0, 3, 7])])
 def test_batched_band_coarse_columns_match_dense_path(name, sel):
     d, ms, A, ld = _batch(name, sel)
@@ -81,3 +97,20 @@ def test_band_solve_multi_matches_dense():
     X = G.band_solve_multi(torch, L, Dinv, kc, E)
     ref = torch.cholesky_solve(E, L)
     assert float((X - ref).abs().max() / ref.abs().max()) < 1e-12
+
+
+def test_band_cholesky_matches_dense_and_flags_indefinite():
+    d, ms, A, ld = _batch("cfg5_m16", [0, 3, 7])
+    perm_list = [np.argsort(m.indices, kind="stable") for m in ms]
+    n_list = [m.n_local for m in ms]
+    AP, P, _ = G._lex_perm(torch, A, perm_list, n_list, ld)
+    L, Dinv, perms, kcnts, info, P2, codes = G._band_factor(torch, A, perm_list, n_list, ld)
+    assert int(info.abs().sum()) == 0
+    assert float(torch.triu(L, 1).abs().max()) == 0.0
+    ref = torch.linalg.cholesky(AP)
+    assert float((L - ref).abs().max() / ref.abs().max()) < 1e-12
+    # an indefinite block is reported with the 1-based failing row, like cholesky_ex
+    B = A.clone()
+    B[1, 70, 70] = -10.0
+    _, _, _, _, info, _, _ = G._band_factor(torch, B, perm_list, n_list, ld)
+    assert int(info[0]) == 0 and int(info[1]) > 0 and int(info[2]) == 0
