@@ -273,19 +273,22 @@ def topk_subspace(torch, M, k, tol=1e-14, maxit=2000, seed=20240103, p=None):
     raise RuntimeError(f"subspace iteration did not converge: residual {res:.2e} after {maxit} sweeps")
 
 
-def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rmax=32.0, dmax=16):
+def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rmax=1e8, dmax=16,
+                   trace=None):
     """Top-k eigenpairs (descending) of a batch of symmetric PSD matrices M (b, m, m).
 
-    Chebyshev-filtered subspace iteration: each outer step applies T_d((M - c) / e) to the
-    current Ritz block, with [0, a] (a = the smallest Ritz value of the block, per matrix) mapped
-    onto [-1, 1], then CholeskyQR2 and Rayleigh-Ritz (p x p, host).  Each matrix gets its own
-    degree d_b (the batch runs max d_b products; a matrix whose degree is reached stops
-    updating), chosen so the filter's dynamic range over its wanted Ritz values,
-    T_d(x_1) / T_d(x_k), stays below min(rmax, residual / (64 eps)): the k-th direction then
-    keeps ~eps * range relative precision, below the current residual (an unbounded degree
-    amplifies the top modes ~1e19 x more than the k-th and wipes the lower wanted directions out
-    in fp64).  Same stopping rule as ``topk_subspace``; raises when it does not converge.
-    Returns (theta, X, block products).
+    Chebyshev-filtered subspace iteration: each outer step applies T_d((M - c) / e) to the Ritz
+    block (columns = current Ritz vectors), with [0, a] (a = the block's smallest Ritz value, per
+    matrix) mapped onto [-1, 1]; the filtered columns are normalised, re-orthonormalised
+    (CholeskyQR2) and Rayleigh-Ritz'ed (p x p).  Every matrix gets its own degree d_b (the batch
+    runs the largest d_b among unconverged matrices; a matrix whose degree is reached stops
+    updating), capped so the filter's spread over its wanted Ritz values,
+    R = T_d(x_1) / T_d(x_k), stays below ``rmax``.  Because each column starts as a Ritz vector,
+    column i's pull toward the top modes is (its residual) x R, not R: the columns stay far from
+    collinear and the k-th keeps ~eps * (1 + residual * R) relative precision.  (From a random
+    block an uncapped degree amplifies the top modes ~1e19 x more than the k-th and collapses the
+    block.)  Same stopping rule as ``topk_subspace``; raises when it does not converge.  Returns
+    (theta, X, block products).
     """
     b, m, _ = M.shape
     p = min(m, p or max(3 * k, k + 16))
@@ -311,19 +314,22 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
         x1 = ((th[:, 0] - e) / e).clamp(min=1.0 + 1e-12)
         xk = ((th[:, k - 1] - e) / e).clamp(min=1.0 + 1e-12)
         per = (torch.acosh(x1) - torch.acosh(xk)).clamp(min=1e-12)
-        rng = (res_b / (64.0 * EPS)).clamp(min=2.0, max=rmax)
-        d_b = torch.floor(torch.log(rng) / per).clamp(min=1, max=dmax)
+        d_b = torch.floor(np.log(rmax) / per).clamp(min=1, max=dmax)
+        d_b = torch.where(res_b > tol, d_b, torch.zeros_like(d_b))       # converged: leave as is
         d = int(d_b.max())
+        if trace is not None:
+            trace.append((d, res, int((res_b > tol).sum()), float(per.max())))
         c = e[:, None, None]
         inv_e = (1.0 / e)[:, None, None]
         Y0 = X
-        Y1 = (MX - c * X) * inv_e
+        Y1 = torch.where((d_b >= 1)[:, None, None], (MX - c * X) * inv_e, X)
         for j in range(2, d + 1):
             Y2 = 2.0 * (M @ Y1 - c * Y1) * inv_e - Y0
             live = (d_b >= j)[:, None, None]
             Y0 = torch.where(live, Y1, Y0)
             Y1 = torch.where(live, Y2, Y1)
         products += d
+        Y1 = Y1 / Y1.norm(dim=1, keepdim=True).clamp(min=1e-300)
         X = _orth(torch, Y1)
         th, X, MX = _rayleigh_ritz(torch, M, X, p)
         products += 1
@@ -491,13 +497,15 @@ def _profile_bytes(adj, perm):
 def local_orders(adj_csr, maps, kind):
     """Factor row order of every subdomain: "lex" = ascending global index (a plane sweep for
     grid operators), "rcm" = reverse Cuthill-McKee of the local graph."""
+    import scipy.sparse as sp
     from scipy.sparse.csgraph import reverse_cuthill_mckee
     out = []
     for m in maps:
         if kind == "lex":
             out.append(np.argsort(m.indices, kind="stable").astype(np.int64))
         else:
-            sub = adj_csr[m.indices][:, m.indices].tocsr()
+            sub = adj_csr[m.indices][:, m.indices]
+            sub = (sub + sp.identity(sub.shape[0], dtype=sub.dtype, format="csr")).tocsr()
             out.append(np.asarray(reverse_cuthill_mckee(sub, symmetric_mode=True), dtype=np.int64))
     return out
 
@@ -730,7 +738,7 @@ def _make_room(torch, dev, nbytes, slack=1 << 29):
 
 
 def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_modes, drop_tol,
-                           batch=None, mem_fraction=0.35, shard=None, local="auto"):
+                           batch=None, mem_fraction=0.35, shard=None, local="auto", graph=None):
     """Run steps 1-5 into ``handle`` (this rank's slab when ``shard``); returns CoarseData or None.
 
     ``local``: "inverse" (packed A_ii^{-1} tiles), "band" (banded Cholesky factors; SPD only) or
@@ -758,11 +766,12 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     band = local in ("auto", "band")
     order_kind = None
     if band:
-        from .partition import symmetrized_graph as _sg
-        g = _sg(csr)
         import scipy.sparse as sp
-        adj = sp.csr_matrix((np.ones(g.adjacency.size), g.adjacency, g.indptr), shape=csr.shape)
-        adj = (adj + sp.identity(csr.shape[0], format="csr")).tocsr()
+        if graph is None:
+            from .partition import symmetrized_graph as _sg
+            graph = _sg(csr, symmetric=symmetric)
+        adj = sp.csr_matrix((np.ones(graph.adjacency.size, dtype=np.int8), graph.adjacency, graph.indptr),
+                            shape=csr.shape)
         order_kind, ratio = choose_local_order(adj, maps, symmetric, forced)
         _log(time.perf_counter(), f"band order {order_kind} (band/inverse bytes {ratio:.2f})")
         if order_kind is None:
@@ -1019,6 +1028,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     zcat = (torch.cat([z_dev[s].mT.contiguous().reshape(-1) for s in own]) if len(own) else
             torch.zeros(1, dtype=torch.float64, device=dev)).contiguous()
     k32 = np.asarray(counts, dtype=np.int32)
+    torch.cuda.empty_cache()  # the library cudaMalloc's the packed coarse operator (~4 nC^2 bytes)
     handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
                                        _lib.ptr(A0inv), s_ptr))
     torch.cuda.current_stream().synchronize()

@@ -115,11 +115,27 @@ class Graph:
         return self.adjacency[base + np.arange(total, dtype=np.int64)]
 
 
-def symmetrized_graph(csr):
-    """Edge {i,j}, i != j, iff |a_ij| > 0 or |a_ji| > 0 (src/sparsemat.py:180-195)."""
+def symmetrized_graph(csr, symmetric=False):
+    """Edge {i,j}, i != j, iff |a_ij| > 0 or |a_ji| > 0 (src/sparsemat.py:180-195).
+
+    ``symmetric``: the caller guarantees a == a^T exactly (``SparseMat`` verifies its flag), so
+    the symmetrised pattern is the pattern itself: the nonzero off-diagonal entries are kept in
+    place (one pass, no transpose or sparse add; same result).
+    """
     a = sp.csr_matrix(csr)
     if a.shape[0] != a.shape[1]:
         raise ValueError("sparsity graph requires a square matrix")
+    if symmetric:
+        if not a.has_sorted_indices:
+            a = a.sorted_indices()
+        n = a.shape[0]
+        rows = np.repeat(np.arange(n, dtype=np.int32), np.diff(a.indptr))
+        keep = (a.data != 0) & (a.indices != rows)
+        del rows
+        ck = np.zeros(keep.size + 1, dtype=np.int64)
+        np.cumsum(keep, out=ck[1:])
+        indptr = ck[a.indptr]
+        return Graph(indptr, a.indices[keep].astype(np.int64))
     pat = sp.csr_matrix((np.abs(a.data), a.indices.copy(), a.indptr.copy()), shape=a.shape)
     pat.eliminate_zeros()
     pat = (pat + pat.T).tocsr()

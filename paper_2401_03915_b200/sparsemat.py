@@ -160,7 +160,7 @@ def symmetrized_graph(matrix):
     m = as_sparsemat(matrix)
     if m.nrows != m.ncols:
         raise ValueError("sparsity graph requires a square matrix")
-    return _sym_graph(m.scipy())
+    return _sym_graph(m.scipy(), symmetric=m.symmetric)
 
 
 __all__ = ["SparseMat", "Graph", "symmetrized_graph", "as_sparsemat", "DENSE_GUARD"]

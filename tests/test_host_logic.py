@@ -66,6 +66,28 @@ def test_stored_zeros_are_not_edges():
     assert g.neighbors(0).tolist() == [] and g.neighbors(1).tolist() == [2]
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_symmetric_fast_path_matches_general_graph(seed):
+    rng = np.random.default_rng(seed)
+    n = 300
+    a = sp.random(n, n, density=0.03, random_state=seed, format="csr")
+    a = (a + a.T).tocsr()
+    a.setdiag(rng.standard_normal(n))
+    a = a.tocsr()
+    a.data[rng.random(a.data.size) < 0.1] = 0.0       # explicit stored zeros (symmetric ones too)
+    a = (0.5 * (a + a.T)).tocsr()
+    a.sort_indices()
+    assert (a != a.T).nnz == 0
+    g0 = Pt.symmetrized_graph(a)
+    g1 = Pt.symmetrized_graph(a, symmetric=True)
+    assert np.array_equal(g0.indptr, g1.indptr) and np.array_equal(g0.adjacency, g1.adjacency)
+    for name in ["cfg1", "cfg2_m16", "cfg5_m16"]:
+        d = golden(name)
+        b = golden_csr(d)
+        h0, h1 = Pt.symmetrized_graph(b), Pt.symmetrized_graph(b, symmetric=True)
+        assert np.array_equal(h0.indptr, h1.indptr) and np.array_equal(h0.adjacency, h1.adjacency)
+
+
 def test_partition_validation():
     with pytest.raises(ValueError):
         Pt.Partition(2, np.array([0, 0]))

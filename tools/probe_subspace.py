@@ -61,8 +61,10 @@ def main():
     for p in [int(x) for x in a.ps.split(",")]:
         torch.cuda.synchronize()
         t = time.perf_counter()
-        th2, X2, mv = G.topk_chebyshev(torch, M, k, p=p or None)
+        tr = []
+        th2, X2, mv = G.topk_chebyshev(torch, M, k, p=p or None, trace=tr)
         torch.cuda.synchronize()
+        print("  steps (d, res, active, per_max):", " ".join(f"({d},{r:.0e},{n},{pm:.2f})" for d, r, n, pm in tr))
         err = float((th2 - th).abs().max() / th[:, :1].abs().min())
         print(f"chebyshev p={p or 'default'}: {mv} block products, {1e3 * (time.perf_counter() - t):.1f} ms, "
               f"theta err {err:.1e}", flush=True)
