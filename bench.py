@@ -8,13 +8,16 @@ A "step" is one full PCG solve of that system from x0 = 0 (the hot path: SpMV + 
 Schwarz apply + Krylov reductions, every iteration).  value = Krylov iterations per second
 over the K timed solves (inputs resident in HBM); ms_per_step = time-to-solution of one solve.
 e2e = the same metric through the public API (``pcg`` on a pinned host RHS, host<->device
-copies inside the timed region).  The operator (60 GB of packed local inverses) is far larger
-than the 126 MB L2, so no explicit flush is needed between steps.
+copies inside the timed region).  The operator (6.5 GB of banded local factors for configuration
+2, 95 GB for configuration 5) is far larger than the 126 MB L2, so no explicit flush is needed
+between steps.
 
 N>1 (torchrun, one process per GPU): the SAME system is sharded by subdomain slabs across the
-ranks (strong scaling): each rank stores and solves only its slab's local operators; vectors,
-SpMV, dots and the coarse solve are replicated; the rank-partial prolongations are summed by an
-NCCL all-reduce inside the captured solve graph.  Timing is the max over ranks.
+ranks (strong scaling): each rank owns a slab of subdomains and their rows (renumbered rank by
+rank) and computes only those: SpMV rows, local solves, its rows of A0^{-1} c, prolongation,
+vector updates.  Inside the captured solve graph NCCL carries the halo of ghost rows
+(point-to-point with the neighbouring slabs), the ASM reverse halo, and sum all-reduces of the
+dot-product partials and of Z^T r.  Timing is the max over ranks.
 
 --impl reference: the reference's CPU algorithm (oracle port; the reference is pure Python
 and does not travel to the GPU box) on the box's host cores, on a bounded sample of the same
@@ -339,8 +342,8 @@ def main():
                    "setup_s": t_setup, "generate_s": t_gen,
                    "time_to_solution_s": t_setup + ms / args.steps / 1e3,
                    "device_bytes": pre.device_bytes(),
-                   "l2": "operator (packed local inverses) >> 126 MB L2; no flush needed",
-                   "parallelism": (f"subdomain slabs x{world} (NCCL all-reduce)" if world > 1
+                   "l2": "operator (local factors + coarse inverse) >> 126 MB L2; no flush needed",
+                   "parallelism": (f"subdomain/row slabs x{world} (NCCL halo + all-reduce)" if world > 1
                                    else "1 GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

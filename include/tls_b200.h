@@ -156,15 +156,30 @@ int32_t tls_report(const tls_ctx* ctx, int64_t* n, int32_t* n_sub, int32_t* n_co
                    int64_t* tile_bytes);
 
 /* ---- sharding across GPUs (build extension, the reference is single-process).
- * A handle owns the contiguous slab [s_lo, s_hi) of the global subdomain list (call before
- * tls_subdomains_upload, which still receives the global maps; extract/store/coarse-upload
- * then take global subdomain ids of owned subdomains, coarse k[] for all subdomains and the
- * basis of the owned ones).  Vectors, SpMV, dots and the coarse solve are replicated; every
- * prolongation is rank-partial and completed by one in-place sum all-reduce per apply stage.
- * NCCL communicators are CUDA-graph capturable; an in-process group (several handles on one
- * GPU driven from host threads) runs the identical schedule for single-GPU validation. */
+ * Each rank owns a contiguous slab [s_lo, s_hi) of the global subdomain list and the rows
+ * those subdomains own.  tls_set_row_partition (before tls_matrix_upload) renumbers the rows
+ * rank by rank (new_of_old[g] = internal row of caller row g; rank q owns internal rows
+ * [row_starts[q], row_starts[q+1])); the library then stores P A P^T and maps every subdomain
+ * index through new_of_old.  Vectors at the ABI stay in the caller's numbering (inputs full,
+ * outputs completed on every rank).  Inside a solve each rank computes only its owned rows:
+ * SpMV, local solves of its subdomains, its rows of A0^{-1} c, prolongation, vector updates.
+ * Exchanges: a halo of ghost rows (tls_set_halo: rows each peer sends / this rank receives, in
+ * ascending internal order), the ASM overlap contributions to rows of other ranks
+ * (tls_set_remote_contrib: what this rank receives, (global subdomain, internal row) in the
+ * sender's (subdomain, local index) order -- the sender side is derived by the library), sum
+ * all-reduces of the dot-product partials and of c = Z^T r.  tls_set_owned_range before
+ * tls_subdomains_upload (which still receives the global maps; extract/store/coarse-upload then
+ * take global subdomain ids of owned subdomains, coarse k[] for all subdomains and the basis of
+ * the owned ones).  NCCL communicators are CUDA-graph capturable; an in-process group (several
+ * handles on one GPU driven from host threads) runs the identical schedule for validation. */
 typedef struct tls_group tls_group;
 int32_t tls_set_owned_range(tls_ctx* ctx, int32_t s_lo, int32_t s_hi);
+int32_t tls_set_row_partition(tls_ctx* ctx, int64_t n, const int32_t* new_of_old, int32_t nranks,
+                              const int32_t* row_starts, int32_t rank);
+int32_t tls_set_halo(tls_ctx* ctx, int32_t npeers, const int32_t* peers, const int32_t* send_counts,
+                     const int32_t* send_rows, const int32_t* recv_counts, const int32_t* recv_rows);
+int32_t tls_set_remote_contrib(tls_ctx* ctx, int32_t npeers, const int32_t* peers,
+                               const int32_t* counts, const int32_t* subs, const int32_t* rows);
 int32_t tls_nccl_unique_id(void* out, int32_t bytes);
 int32_t tls_comm_init_nccl(tls_ctx* ctx, const void* unique_id, int32_t nranks, int32_t rank);
 int32_t tls_group_create(int32_t nmembers, tls_group** out);

@@ -64,6 +64,9 @@ SIGNATURES = {
     "tls_report": (_I32, [_P, C.POINTER(_I64), C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I64)]),
     "tls_profile_local_solve": (_I32, [_P, _I32, C.POINTER(_D), C.POINTER(_D), _P]),
     "tls_set_owned_range": (_I32, [_P, _I32, _I32]),
+    "tls_set_row_partition": (_I32, [_P, _I64, _P, _I32, _P, _I32]),
+    "tls_set_halo": (_I32, [_P, _I32, _P, _P, _P, _P, _P]),
+    "tls_set_remote_contrib": (_I32, [_P, _I32, _P, _P, _P, _P]),
     "tls_set_local_kind": (_I32, [_P, _I32]),
     "tls_store_local_band": (_I32, [_P, _I32, _I32, _P, _I64, _P, _I32, _P, _P, _P]),
     "tls_store_local_band_lu": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P, _I32, _P, _P, _P, _P, _P]),

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -118,9 +119,20 @@ struct tls_ctx {
   std::vector<int> h_perm_in;         // LU: local index gathered into input position p (row pivots)
   double band_bytes = 0.0;            // stored factor bytes (read twice per apply)
   size_t band_smem = 0;
-  // ---- sharding: this handle owns global subdomains [own_lo, own_hi)
+  // ---- sharding: this handle owns global subdomains [own_lo, own_hi) and the
+  // rows [r0, r1) of the internal numbering (rows renumbered rank by rank: nofo[g] = internal id
+  // of caller row g; identity and [0, n) on one GPU)
   int own_lo = 0, own_hi = -1, nsub_global = 0;
   Comm* comm = nullptr;
+  int r0 = 0, r1 = -1;
+  std::vector<int> h_nofo;            // empty: identity numbering
+  std::vector<int> row_starts;        // per rank [row_starts[q], row_starts[q+1])
+  int* d_nofo = nullptr;
+  XPlan halo;                         // ghost rows (SpMV columns + overlap rows) from their owners
+  XPlan rev;                          // ASM overlap contributions to rows owned by other ranks
+  std::vector<int> rc_peer, rc_cnt, rc_sub, rc_row;  // remote contributions received (in order)
+  long long Xrecv = 0;                // tail of yloc holding the received contributions
+  double *pin = nullptr, *pout = nullptr;  // caller-numbering staging vectors
 };
 
 struct tls_group {
@@ -179,6 +191,17 @@ static int upload(tls_ctx* ctx, T*& d, const T* h, int64_t count) {
   return TLS_OK;
 }
 
+// The dynamic shared-memory limit is a per-function, process-wide attribute: only ever raise it,
+// under a lock (several handles may be set up concurrently from host threads).
+static cudaError_t raise_smem(const void* fn, size_t bytes, size_t& current) {
+  static std::mutex m;
+  std::lock_guard<std::mutex> lk(m);
+  if (bytes <= current) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) current = bytes;
+  return e;
+}
+
 static int grid_for(int64_t work, int per_block) {
   int64_t g = (work + per_block - 1) / per_block;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, MAX_GRID));
@@ -196,14 +219,15 @@ static void destroy_graphs(tls_ctx* ctx) {
 // ---------------------------------------------------------------------------------------------
 // enqueue helpers
 // ---------------------------------------------------------------------------------------------
+// rows [r0, r1): all rows on one GPU, the owned range on the sharded path
 template <int MODE, int DOT>
 static int spmv_lpr(tls_ctx* ctx, cudaStream_t s, const double* x, double* y, const double* b,
                     double* part, const int* done) {
   const int grid = ctx->Gs;
-#define SPMV_CASE(L)                                                                              \
-  case L:                                                                                         \
-    k_spmv<L, MODE, DOT><<<grid, NTHR, 0, s>>>(ctx->n, ctx->rowptr, ctx->col, ctx->val, x, y, b, \
-                                               part, done);                                       \
+#define SPMV_CASE(L)                                                                                 \
+  case L:                                                                                            \
+    k_spmv<L, MODE, DOT><<<grid, NTHR, 0, s>>>(ctx->r0, ctx->r1, ctx->rowptr, ctx->col, ctx->val, x, y, \
+                                               b, part, done);                                       \
     break;
   switch (ctx->lpr) {
     SPMV_CASE(1)
@@ -260,13 +284,15 @@ static int enq_restrict(tls_ctx* ctx, cudaStream_t s, const double* r, const int
   return TLS_OK;
 }
 
+// rows [r0, r1) only (all rows on one GPU); row-indexed arrays are offset, yloc / yc are not
 template <int MODE, int DOT>
 static int enq_prolong(tls_ctx* ctx, cudaStream_t s, const double* qv, const double* wv,
                        const double* rdot, double* z, const int* done) {
-  k_prolong<MODE, DOT><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->d_pull_ptr, ctx->d_pull_pos, ctx->yloc,
-                                               ctx->d_zrow, ctx->d_zst, ctx->d_zk, ctx->d_zc, ctx->d_Z,
-                                               ctx->yloc + ctx->coarse_xoff, qv, wv, rdot, z,
-                                               ctx->part, done);
+  const int r0 = ctx->r0;
+  k_prolong<MODE, DOT><<<ctx->G, NTHR, 0, s>>>(
+      ctx->r1 - r0, ctx->d_pull_ptr + r0, ctx->d_pull_pos, ctx->yloc, ctx->d_zrow + r0, ctx->d_zst + r0,
+      ctx->d_zk + r0, ctx->d_zc + r0, ctx->d_Z, ctx->yloc + ctx->coarse_xoff, qv ? qv + r0 : nullptr,
+      wv ? wv + r0 : nullptr, rdot ? rdot + r0 : nullptr, z + r0, ctx->part, done);
   CKL();
   return TLS_OK;
 }
@@ -275,13 +301,51 @@ static bool has_coarse(const tls_ctx* ctx) { return ctx->ncoarse > 0 && ctx->com
 
 static bool sharded(const tls_ctx* ctx) { return ctx->comm != nullptr && ctx->comm->nranks > 1; }
 
-// the exchange step: in-place sum over the ranks (NCCL or in-process group)
+static int nown(const tls_ctx* ctx) { return ctx->r1 - ctx->r0; }
+
+// in-place sum over the ranks (NCCL or in-process group); no-op on one GPU
 static int enq_allreduce(tls_ctx* ctx, cudaStream_t s, double* buf, long long count) {
   if (!sharded(ctx)) return TLS_OK;
   std::string err;
   cudaError_t e = ctx->comm->allreduce_sum(buf, count, s, err);
   if (e != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
   return TLS_OK;
+}
+
+// the G (fixed, equal on every rank) partial sums of a dot product, summed over the ranks
+static int enq_allreduce_part(tls_ctx* ctx, cudaStream_t s, int np) {
+  return enq_allreduce(ctx, s, ctx->part, np);
+}
+
+// point-to-point exchange: pack src rows, send/recv, unpack into dst.  Every rank calls every
+// exchange of the schedule (possibly with an empty plan) so the collective order matches.
+static int enq_exchange(tls_ctx* ctx, cudaStream_t s, XPlan& x, const double* src, double* dst,
+                        const int* done) {
+  if (!sharded(ctx)) return TLS_OK;
+  if (x.stot > 0) {
+    k_xpack<<<grid_for(x.stot, NTHR), NTHR, 0, s>>>(x.stot, x.d_sidx, src, x.sbuf, done);
+    CKL();
+  }
+  std::string err;
+  cudaError_t e = ctx->comm->exchange(x, s, err);
+  if (e != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+  if (x.rtot > 0) {
+    k_xunpack<<<grid_for(x.rtot, NTHR), NTHR, 0, s>>>(x.rtot, x.d_ridx, x.rbuf, dst, done);
+    CKL();
+  }
+  return TLS_OK;
+}
+
+// ghost rows of v (rows other ranks own that this rank's SpMV rows / subdomains read)
+static int enq_halo(tls_ctx* ctx, cudaStream_t s, double* v, const int* done) {
+  return enq_exchange(ctx, s, ctx->halo, v, v, done);
+}
+
+// ASM: local-solve outputs on rows owned by other ranks travel to the owners, who add them in
+// ascending subdomain order (their pull maps point into the received tail of yloc)
+static int enq_rev(tls_ctx* ctx, cudaStream_t s, const int* done) {
+  if (ctx->one_level != TLS_ASM) return TLS_OK;
+  return enq_exchange(ctx, s, ctx->rev, ctx->yloc, ctx->yloc, done);
 }
 
 // coarse coefficients c = Z^T r: this rank's columns, then the sum over ranks
@@ -293,104 +357,103 @@ static int enq_restrict_all(tls_ctx* ctx, cudaStream_t s, const double* r, const
 }
 
 static int enq_dot(tls_ctx* ctx, cudaStream_t s, const double* a, const double* b, const int* done) {
-  k_dot<<<ctx->G, NTHR, 0, s>>>(ctx->n, a, b, ctx->part, done);
+  k_dot<<<ctx->G, NTHR, 0, s>>>(nown(ctx), a + ctx->r0, b + ctx->r0, ctx->part, done);
   CKL();
-  return TLS_OK;
+  return enq_allreduce_part(ctx, s, ctx->G);
 }
 
-// Sharded schedule: every prolongation is rank-partial (own subdomains only) and is completed
-// by one all-reduce of the n-vector; vectors, SpMV, dots and the coarse solve are replicated.
-static int enq_apply_sharded(tls_ctx* ctx, cudaStream_t s, const double* r, double* z, bool dot,
-                             const int* done) {
-  const long long n = ctx->n;
+// z = M^{-1} r (src/precond.py:128-136) on the owned rows.  r must be valid on the owned rows;
+// r_full: its ghost rows are valid too (no halo needed).  dot: r.z partials (summed over the
+// ranks) in ctx->part (G of them).
+static int enq_apply(tls_ctx* ctx, cudaStream_t s, double* r, double* z, bool dot, const int* done,
+                     bool r_full = false) {
   if (!has_coarse(ctx)) {
+    if (!r_full) TRY(enq_halo(ctx, s, r, done));
     TRY(enq_gather(ctx, s, r, done));
     TRY(enq_solve(ctx, s, L_LOCAL, done));
-    TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, z, done)));
-    TRY(enq_allreduce(ctx, s, z, n));
-  } else if (ctx->combine == TLS_ADDITIVE) {
-    TRY(enq_gather(ctx, s, r, done));
-    TRY(enq_restrict_all(ctx, s, r, done));
-    TRY(enq_solve(ctx, s, L_ALL, done));
-    TRY((enq_prolong<1, 0>(ctx, s, nullptr, nullptr, nullptr, z, done)));
-    TRY(enq_allreduce(ctx, s, z, n));
-  } else {
-    TRY(enq_restrict_all(ctx, s, r, done));
-    TRY(enq_solve(ctx, s, L_COARSE, done));
-    TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t1, done)));
-    TRY(enq_allreduce(ctx, s, ctx->t1, n));
-    TRY((spmv_lpr<1, 0>(ctx, s, ctx->t1, ctx->t2, r, nullptr, done)));
-    TRY(enq_gather(ctx, s, ctx->t2, done));
-    TRY(enq_solve(ctx, s, L_LOCAL, done));
-    TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t3, done)));
-    TRY(enq_allreduce(ctx, s, ctx->t3, n));
-    TRY((spmv_lpr<0, 0>(ctx, s, ctx->t3, ctx->t4, nullptr, nullptr, done)));
-    TRY(enq_restrict_all(ctx, s, ctx->t4, done));
-    TRY(enq_solve(ctx, s, L_COARSE, done));
-    TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, z, done)));
-    TRY(enq_allreduce(ctx, s, z, n));
-    k_defl_combine<<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->t1, ctx->t3, z, done);
-    CKL();
-  }
-  if (dot) TRY(enq_dot(ctx, s, r, z, done));
-  return TLS_OK;
-}
-
-// z = M^{-1} r (src/precond.py:128-136).  dot: partial r.z into ctx->part (G partials).
-static int enq_apply(tls_ctx* ctx, cudaStream_t s, const double* r, double* z, bool dot,
-                     const int* done) {
-  if (sharded(ctx)) return enq_apply_sharded(ctx, s, r, z, dot, done);
-  if (!has_coarse(ctx)) {
-    TRY(enq_gather(ctx, s, r, done));
-    TRY(enq_solve(ctx, s, L_LOCAL, done));
-    return dot ? enq_prolong<0, 1>(ctx, s, nullptr, nullptr, r, z, done)
-               : enq_prolong<0, 0>(ctx, s, nullptr, nullptr, r, z, done);
-  }
-  if (ctx->combine == TLS_ADDITIVE && ctx->local_kind == 1) {
-    // the coarse chain (restrict -> A0^{-1} tiles -> reduce) reads r and writes only the coarse
-    // segments, the band solve reads/writes only the local segments: run them side by side
-    // (a fork/join that CUDA-graph capture turns into parallel branches)
+    TRY(enq_rev(ctx, s, done));
+    TRY(dot ? enq_prolong<0, 1>(ctx, s, nullptr, nullptr, r, z, done)
+            : enq_prolong<0, 0>(ctx, s, nullptr, nullptr, r, z, done));
+  } else if (ctx->combine == TLS_ADDITIVE && ctx->local_kind >= 1) {
+    if (!r_full) TRY(enq_halo(ctx, s, r, done));
+    // the coarse chain (restrict -> [sum over ranks] -> A0^{-1} tiles -> reduce) reads r and
+    // writes only the coarse segments, the band solve reads/writes only the local segments: run
+    // them side by side (a fork/join that CUDA-graph capture turns into parallel branches)
     CK(cudaEventRecord(ctx->ev_fork, s));
     CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-    TRY(enq_restrict(ctx, ctx->aux, r, done));
+    TRY(enq_restrict_all(ctx, ctx->aux, r, done));
     TRY(enq_solve(ctx, ctx->aux, L_COARSE, done));
     CK(cudaEventRecord(ctx->ev_join, ctx->aux));
     TRY(enq_gather(ctx, s, r, done));
     TRY(enq_solve(ctx, s, L_LOCAL, done));
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-    return dot ? enq_prolong<1, 1>(ctx, s, nullptr, nullptr, r, z, done)
-               : enq_prolong<1, 0>(ctx, s, nullptr, nullptr, r, z, done);
-  }
-  if (ctx->combine == TLS_ADDITIVE) {
+    TRY(enq_rev(ctx, s, done));
+    TRY(dot ? enq_prolong<1, 1>(ctx, s, nullptr, nullptr, r, z, done)
+            : enq_prolong<1, 0>(ctx, s, nullptr, nullptr, r, z, done));
+  } else if (ctx->combine == TLS_ADDITIVE) {
+    if (!r_full) TRY(enq_halo(ctx, s, r, done));
     TRY(enq_gather(ctx, s, r, done));
-    TRY(enq_restrict(ctx, s, r, done));
+    TRY(enq_restrict_all(ctx, s, r, done));
     TRY(enq_solve(ctx, s, L_ALL, done));
-    return dot ? enq_prolong<1, 1>(ctx, s, nullptr, nullptr, r, z, done)
-               : enq_prolong<1, 0>(ctx, s, nullptr, nullptr, r, z, done);
+    TRY(enq_rev(ctx, s, done));
+    TRY(dot ? enq_prolong<1, 1>(ctx, s, nullptr, nullptr, r, z, done)
+            : enq_prolong<1, 0>(ctx, s, nullptr, nullptr, r, z, done));
+  } else {
+    // deflated: q = Q r; w = M1 (r - A q); z = q + w - Q A w  (only the owned rows of r are read
+    // directly; q and w get their ghost rows by halo before each SpMV / gather)
+    TRY(enq_restrict_all(ctx, s, r, done));
+    TRY(enq_solve(ctx, s, L_COARSE, done));
+    TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t1, done)));
+    TRY(enq_halo(ctx, s, ctx->t1, done));
+    TRY((spmv_lpr<1, 0>(ctx, s, ctx->t1, ctx->t2, r, nullptr, done)));
+    TRY(enq_halo(ctx, s, ctx->t2, done));
+    TRY(enq_gather(ctx, s, ctx->t2, done));
+    TRY(enq_solve(ctx, s, L_LOCAL, done));
+    TRY(enq_rev(ctx, s, done));
+    TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t3, done)));
+    TRY(enq_halo(ctx, s, ctx->t3, done));
+    TRY((spmv_lpr<0, 0>(ctx, s, ctx->t3, ctx->t4, nullptr, nullptr, done)));
+    TRY(enq_restrict_all(ctx, s, ctx->t4, done));
+    TRY(enq_solve(ctx, s, L_COARSE, done));
+    TRY(dot ? enq_prolong<3, 1>(ctx, s, ctx->t1, ctx->t3, r, z, done)
+            : enq_prolong<3, 0>(ctx, s, ctx->t1, ctx->t3, r, z, done));
   }
-  // deflated: q = Q r; w = M1 (r - A q); z = q + w - Q A w
-  TRY(enq_restrict(ctx, s, r, done));
-  TRY(enq_solve(ctx, s, L_COARSE, done));
-  TRY(enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t1, done));
-  TRY((spmv_lpr<1, 0>(ctx, s, ctx->t1, ctx->t2, r, nullptr, done)));
-  TRY(enq_gather(ctx, s, ctx->t2, done));
-  TRY(enq_solve(ctx, s, L_LOCAL, done));
-  TRY(enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t3, done));
-  TRY((spmv_lpr<0, 0>(ctx, s, ctx->t3, ctx->t4, nullptr, nullptr, done)));
-  TRY(enq_restrict(ctx, s, ctx->t4, done));
-  TRY(enq_solve(ctx, s, L_COARSE, done));
-  return dot ? enq_prolong<3, 1>(ctx, s, ctx->t1, ctx->t3, r, z, done)
-             : enq_prolong<3, 0>(ctx, s, ctx->t1, ctx->t3, r, z, done);
+  return dot ? enq_allreduce_part(ctx, s, ctx->G) : TLS_OK;
 }
 
 static int enq_identity(tls_ctx* ctx, cudaStream_t s, const double* r, double* z, bool dot,
                         const int* done) {
+  const int r0 = ctx->r0;
   if (dot)
-    k_copy_dot<1><<<ctx->G, NTHR, 0, s>>>(ctx->n, r, z, ctx->part, done);
+    k_copy_dot<1><<<ctx->G, NTHR, 0, s>>>(nown(ctx), r + r0, z + r0, ctx->part, done);
   else
-    k_copy_dot<0><<<ctx->G, NTHR, 0, s>>>(ctx->n, r, z, ctx->part, done);
+    k_copy_dot<0><<<ctx->G, NTHR, 0, s>>>(nown(ctx), r + r0, z + r0, ctx->part, done);
   CKL();
+  return dot ? enq_allreduce_part(ctx, s, ctx->G) : TLS_OK;
+}
+
+// Caller-numbering vectors at the C ABI.  One GPU: used in place.  Sharded: v_in is permuted
+// into the internal numbering (all rows, so no halo is needed), the operator writes its owned
+// rows of ctx->pout, and out = the sum over ranks of the owned rows scattered back.
+static int api_in(tls_ctx* ctx, cudaStream_t s, const double* v_in, double** v_int) {
+  if (ctx->h_nofo.empty()) {
+    *v_int = const_cast<double*>(v_in);
+    return TLS_OK;
+  }
+  k_perm_in<<<grid_for(ctx->n, NTHR), NTHR, 0, s>>>(ctx->n, ctx->d_nofo, v_in, ctx->pin);
+  CKL();
+  *v_int = ctx->pin;
   return TLS_OK;
+}
+static double* api_out_buf(tls_ctx* ctx, double* out) { return ctx->h_nofo.empty() ? out : ctx->pout; }
+static int api_out(tls_ctx* ctx, cudaStream_t s, const double* v_int, double* out) {
+  if (ctx->h_nofo.empty()) {
+    if (v_int != out) CK(cudaMemcpyAsync(out, v_int, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, s));
+    return TLS_OK;
+  }
+  k_perm_out<<<grid_for(ctx->n, NTHR), NTHR, 0, s>>>(ctx->n, ctx->d_nofo, ctx->r0, ctx->r1, v_int, out);
+  CKL();
+  return enq_allreduce(ctx, s, out, ctx->n);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -437,8 +500,12 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   dfree(ctx->d_zk); dfree(ctx->d_zc); dfree(ctx->d_zst); dfree(ctx->xloc); dfree(ctx->yloc); dfree(ctx->slots);
   double** vecs[] = {&ctx->t1, &ctx->t2, &ctx->t3, &ctx->t4, &ctx->t5, &ctx->t6, &ctx->t7, &ctx->vb,
                      &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz, &ctx->hist, &ctx->part,
-                     &ctx->V, &ctx->H, &ctx->cs, &ctx->sn, &ctx->gv, &ctx->yv, &ctx->h1, &ctx->h2};
+                     &ctx->V, &ctx->H, &ctx->cs, &ctx->sn, &ctx->gv, &ctx->yv, &ctx->h1, &ctx->h2,
+                     &ctx->pin, &ctx->pout, &ctx->halo.sbuf, &ctx->halo.rbuf, &ctx->rev.sbuf,
+                     &ctx->rev.rbuf};
   for (double** v : vecs) dfree(*v);
+  dfree(ctx->d_nofo); dfree(ctx->halo.d_sidx); dfree(ctx->halo.d_ridx); dfree(ctx->rev.d_sidx);
+  dfree(ctx->rev.d_ridx);
   dfree(ctx->pcg); dfree(ctx->gm);
   for (void* pb : ctx->band_allocs) cudaFree(pb);
   dfree(ctx->d_band);
@@ -462,14 +529,40 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
   if (!ctx || nrows <= 0 || nrows > INT32_MAX || nnz < 0 || nnz >= INT32_MAX)
     return ctx ? fail(ctx, TLS_ERR_ARG, "matrix size out of the supported int32 range") : TLS_ERR_ARG;
   CK(cudaSetDevice(ctx->device));
+  const bool renum = !ctx->h_nofo.empty();
+  if (renum && (int64_t)ctx->h_nofo.size() != nrows)
+    return fail(ctx, TLS_ERR_DIM, "row partition and matrix sizes differ");
   ctx->n = (int)nrows;
   ctx->nnz = nnz;
   ctx->sym = symmetric ? 1 : 0;
   std::vector<int> rp(nrows + 1);
-  for (int64_t i = 0; i <= nrows; ++i) rp[i] = (int)indptr[i];
-  TRY(upload(ctx, ctx->rowptr, rp.data(), nrows + 1));
-  TRY(upload(ctx, ctx->col, indices, nnz));
-  TRY(upload(ctx, ctx->val, data, nnz));
+  if (!renum) {
+    for (int64_t i = 0; i <= nrows; ++i) rp[i] = (int)indptr[i];
+    TRY(upload(ctx, ctx->rowptr, rp.data(), nrows + 1));
+    TRY(upload(ctx, ctx->col, indices, nnz));
+    TRY(upload(ctx, ctx->val, data, nnz));
+    ctx->r0 = 0;
+    ctx->r1 = (int)nrows;
+  } else {
+    // P A P^T in the internal numbering; each row keeps its entries in the caller's order, so
+    // every row sum (SpMV) is bit-identical to the unpermuted one
+    std::vector<int> oldof(nrows);
+    for (int64_t g = 0; g < nrows; ++g) oldof[ctx->h_nofo[g]] = (int)g;
+    rp[0] = 0;
+    for (int64_t i = 0; i < nrows; ++i) rp[i + 1] = rp[i] + (int)(indptr[oldof[i] + 1] - indptr[oldof[i]]);
+    std::vector<int> pc(nnz);
+    std::vector<double> pv(nnz);
+    for (int64_t i = 0; i < nrows; ++i) {
+      const int64_t b = indptr[oldof[i]], e = indptr[oldof[i] + 1];
+      for (int64_t k = b; k < e; ++k) {
+        pc[rp[i] + (k - b)] = ctx->h_nofo[indices[k]];
+        pv[rp[i] + (k - b)] = data[k];
+      }
+    }
+    TRY(upload(ctx, ctx->rowptr, rp.data(), nrows + 1));
+    TRY(upload(ctx, ctx->col, pc.data(), nnz));
+    TRY(upload(ctx, ctx->val, pv.data(), nnz));
+  }
   const double avg = nrows ? (double)nnz / (double)nrows : 1.0;
   // lanes per row ~ nnz/row / 7 (measured on B200: 7-point rows run best one thread per row,
   // 27-point rows with 4 lanes; tools/bench_spmv.py)
@@ -482,14 +575,18 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
   ctx->lpr = l;
   ctx->G = grid_for(nrows, NTHR);
   ctx->Gs = grid_for(nrows, NTHR / l);
+  if (renum) ctx->G = ctx->Gs = MAX_GRID;  // equal partial counts on every rank (summed elementwise)
   const int64_t need = std::max<int64_t>(ctx->G, ctx->Gs);
   if (need > ctx->part_cap) {
     TRY(dalloc(ctx, ctx->part, need));
     ctx->part_cap = need;
   }
   double** vecs[] = {&ctx->t1, &ctx->t2, &ctx->t3, &ctx->t4, &ctx->t5, &ctx->t6, &ctx->t7,
-                     &ctx->vb, &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz};
-  for (double** v : vecs) TRY(dalloc(ctx, *v, nrows));
+                     &ctx->vb, &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz, &ctx->pin, &ctx->pout};
+  for (double** v : vecs) {
+    TRY(dalloc(ctx, *v, nrows));
+    CK(cudaMemset(*v, 0, sizeof(double) * nrows));  // ghost rows are read (x 0) before any halo
+  }
   if (ctx->h_x) cudaFreeHost(ctx->h_x);
   CK(cudaMallocHost((void**)&ctx->h_x, sizeof(double) * nrows));
   destroy_graphs(ctx);
@@ -500,7 +597,12 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
 int32_t tls_spmv(tls_ctx* ctx, const double* x, double* y, void* stream) {
   if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "no matrix uploaded") : TLS_ERR_ARG;
   CK(cudaSetDevice(ctx->device));
-  return spmv_lpr<0, 0>(ctx, (cudaStream_t)stream, x, y, nullptr, nullptr, nullptr);
+  cudaStream_t s = (cudaStream_t)stream;
+  double* xi;
+  TRY(api_in(ctx, s, x, &xi));
+  double* yi = api_out_buf(ctx, y);
+  TRY((spmv_lpr<0, 0>(ctx, s, xi, yi, nullptr, nullptr, nullptr)));
+  return api_out(ctx, s, yi, y);
 }
 
 int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t* offsets_g,
@@ -524,7 +626,7 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
   for (int64_t i = 0; i < tot; ++i) {
     const int64_t g = indices_g[base + i];
     if (g < 0 || g >= ctx->n) return fail(ctx, TLS_ERR_DIM, "subdomain index out of range");
-    ctx->h_idx[i] = (int)g;
+    ctx->h_idx[i] = ctx->h_nofo.empty() ? (int)g : ctx->h_nofo[g];  // internal numbering
   }
   ctx->h_n.resize(n_sub);
   ctx->h_nint.assign(n_interior_g + lo, n_interior_g + hi);
@@ -560,10 +662,7 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     for (int s = 0; s < n_sub; ++s) mi = std::max(mi, ctx->h_nint[s]);
     ctx->restrict_smem = sizeof(double) * (size_t)mi;
     static size_t rsmem_set = 48 * 1024;
-    if (ctx->restrict_smem > rsmem_set) {
-      CK(cudaFuncSetAttribute(k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->restrict_smem));
-      rsmem_set = ctx->restrict_smem;
-    }
+    CK(raise_smem((const void*)k_restrict, ctx->restrict_smem, rsmem_set));
   }
   ctx->tile_doubles = ctx->local_kind >= 1 ? 0 : tiles * TT * TT;
   dfree(ctx->tiles);
@@ -579,12 +678,8 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     }
     TRY(upload(ctx, ctx->d_band, ctx->h_band.data(), n_sub));
     ctx->band_smem = sizeof(double) * ((size_t)maxnb * TT + 8 * TT + TT);
-    // the attribute is per function (process-wide): only ever raise it
     static size_t smem_set = 0;
-    if (ctx->band_smem > smem_set) {
-      CK(cudaFuncSetAttribute(k_band_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->band_smem));
-      smem_set = ctx->band_smem;
-    }
+    CK(raise_smem((const void*)k_band_solve, ctx->band_smem, smem_set));
     ctx->h_perm.assign(tot, -1);
     ctx->h_perm_in.assign(ctx->local_kind == 2 ? tot : 0, -1);
     ctx->band_bytes = 0.0;
@@ -771,10 +866,15 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   TRY(upload(ctx, ctx->d_gidx, gidx.data(), ctx->Xloc));
   ctx->coarse_xoff = ctx->Xloc;
   ctx->X = ctx->Xloc + (ctx->ncoarse > 0 ? (long long)ctx->h_blk[nsub].nt * TT : 0);
+  const bool part = !ctx->h_nofo.empty();
+  const bool asm_ = one_level == TLS_ASM;
+  ctx->Xrecv = 0;
+  if (part && asm_)
+    for (int c : ctx->rc_cnt) ctx->Xrecv += c;
   TRY(dalloc(ctx, ctx->xloc, ctx->X));
-  TRY(dalloc(ctx, ctx->yloc, ctx->X));
+  TRY(dalloc(ctx, ctx->yloc, ctx->X + ctx->Xrecv));
   CK(cudaMemset(ctx->xloc, 0, sizeof(double) * ctx->X));
-  CK(cudaMemset(ctx->yloc, 0, sizeof(double) * ctx->X));
+  CK(cudaMemset(ctx->yloc, 0, sizeof(double) * (ctx->X + ctx->Xrecv)));
   // work units + reduction lists
   std::vector<Unit> units;
   std::vector<OutTile> outs;
@@ -797,10 +897,46 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   if (ctx->ncoarse > 0) {
     // the coarse operator is ONE block: thinner units (2 tile-rows) to fill the machine
     plan_block(nsub, ctx->h_blk[nsub].nt, ctx->sym, 2, slot, units, outs, red);
-    ctx->nu_coarse = (int)units.size() - ctx->nu_local;
-    ctx->no_coarse = (int)outs.size() - ctx->no_local;
     const double nc = ctx->ncoarse;
     ctx->algo_coarse = ctx->sym ? 8.0 * nc * (nc + 1) / 2 + 8.0 * nc : 8.0 * nc * nc + 8.0 * nc;
+    if (part) {
+      // sharded: only the output tiles of this rank's coarse rows (its subdomains' columns, the
+      // only entries of A0^{-1} c its prolongation reads) and the units that feed them; each
+      // kept tile reduces the same slots in the same order as on one GPU
+      const long long c0 = ctx->h_cstart[0], c1 = ctx->h_cstart[nsub - 1] + ctx->h_k[nsub - 1];
+      std::vector<OutTile> kept_outs;
+      std::vector<int> kept_red;
+      std::vector<char> used((size_t)slot / SLOTS_PER_UNIT + 1, 0);
+      for (size_t o = ctx->no_local; o < outs.size(); ++o) {
+        const OutTile& ot = outs[o];
+        if (c1 <= c0 || (long long)ot.J * TT >= c1 || (long long)(ot.J + 1) * TT <= c0) continue;
+        OutTile nt{ot.blk, ot.J, (int)(red.size() + kept_red.size()), 0};
+        for (int e = ot.beg; e < ot.end; ++e) {
+          kept_red.push_back(red[e]);
+          used[red[e] / SLOTS_PER_UNIT] = 1;
+        }
+        nt.end = (int)(red.size() + kept_red.size());
+        kept_outs.push_back(nt);
+      }
+      // the kept reduction lists go behind all existing ones (their beg/end already say so)
+      outs.resize(ctx->no_local);
+      outs.insert(outs.end(), kept_outs.begin(), kept_outs.end());
+      red.insert(red.end(), kept_red.begin(), kept_red.end());
+      std::vector<Unit> ku(units.begin(), units.begin() + ctx->nu_local);
+      double tiles_read = 0.0;
+      for (size_t u = ctx->nu_local; u < units.size(); ++u) {
+        const Unit& un = units[u];
+        if (!used[un.slot / SLOTS_PER_UNIT]) continue;
+        ku.push_back(un);
+        for (int I = un.i0; I < un.i0 + un.ni; ++I)
+          for (int J = un.j0; J < un.j0 + un.nj; ++J)
+            if (!ctx->sym || J <= I) tiles_read += 1.0;
+      }
+      units.swap(ku);
+      ctx->algo_coarse = tiles_read * TT * TT * 8.0 + 16.0 * (double)(c1 - c0);
+    }
+    ctx->nu_coarse = (int)units.size() - ctx->nu_local;
+    ctx->no_coarse = (int)outs.size() - ctx->no_local;
   }
   TRY(upload(ctx, ctx->d_units, units.data(), (int64_t)units.size()));
   TRY(upload(ctx, ctx->d_outs, outs.data(), (int64_t)outs.size()));
@@ -809,19 +945,85 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   TRY(dalloc(ctx, ctx->slots, (int64_t)slot * TT));
   // prolongation pull map: contributions to node g in ascending subdomain order (np.add.at)
   std::vector<int> cnt(n + 1, 0);
-  for (int s = 0; s < nsub; ++s) {
-    const int lim = one_level == TLS_RAS ? ctx->h_nint[s] : ctx->h_n[s];
-    for (int l = 0; l < lim; ++l) cnt[ctx->h_idx[ctx->h_off[s] + l] + 1]++;
-  }
-  for (int g = 0; g < n; ++g) cnt[g + 1] += cnt[g];
-  std::vector<int> pos(cnt[n]);
-  std::vector<int> fill(cnt.begin(), cnt.end() - 1);
-  for (int s = 0; s < nsub; ++s) {
-    const int lim = one_level == TLS_RAS ? ctx->h_nint[s] : ctx->h_n[s];
-    for (int l = 0; l < lim; ++l) {
-      const int g = ctx->h_idx[ctx->h_off[s] + l];
-      pos[fill[g]++] = (int)(ctx->h_blk[s].xoff + posl[ctx->h_off[s] + l]);
+  std::vector<int> pos;
+  if (!part) {
+    for (int s = 0; s < nsub; ++s) {
+      const int lim = one_level == TLS_RAS ? ctx->h_nint[s] : ctx->h_n[s];
+      for (int l = 0; l < lim; ++l) cnt[ctx->h_idx[ctx->h_off[s] + l] + 1]++;
     }
+    for (int g = 0; g < n; ++g) cnt[g + 1] += cnt[g];
+    pos.resize(cnt[n]);
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int s = 0; s < nsub; ++s) {
+      const int lim = one_level == TLS_RAS ? ctx->h_nint[s] : ctx->h_n[s];
+      for (int l = 0; l < lim; ++l) {
+        const int g = ctx->h_idx[ctx->h_off[s] + l];
+        pos[fill[g]++] = (int)(ctx->h_blk[s].xoff + posl[ctx->h_off[s] + l]);
+      }
+    }
+  } else {
+    // owned rows only; contributions of other ranks' subdomains arrive in the yloc tail (the
+    // reverse halo) and are merged in ascending subdomain order; contributions of this rank's
+    // subdomains to other ranks' rows are sent to their owners in (subdomain, local index) order
+    struct Ent { int row, sub; long long pos; };
+    std::vector<Ent> ent;
+    const int nr = (int)ctx->row_starts.size() - 1;
+    std::vector<std::vector<int>> sendpos(nr);
+    for (int s = 0; s < nsub; ++s) {
+      const int lim = asm_ ? ctx->h_n[s] : ctx->h_nint[s];
+      for (int l = 0; l < lim; ++l) {
+        const int g = ctx->h_idx[ctx->h_off[s] + l];
+        const long long p = ctx->h_blk[s].xoff + posl[ctx->h_off[s] + l];
+        if (g >= ctx->r0 && g < ctx->r1) {
+          ent.push_back(Ent{g, ctx->own_lo + s, p});
+        } else {
+          const int q = (int)(std::upper_bound(ctx->row_starts.begin(), ctx->row_starts.end(), g) -
+                              ctx->row_starts.begin()) - 1;
+          sendpos[q].push_back((int)p);
+        }
+      }
+    }
+    if (asm_) {
+      long long k = 0;
+      for (size_t b = 0; b < ctx->rc_peer.size(); ++b)
+        for (int e = 0; e < ctx->rc_cnt[b]; ++e, ++k) {
+          const int g = ctx->rc_row[k];
+          if (g < ctx->r0 || g >= ctx->r1) return fail(ctx, TLS_ERR_ARG, "remote contribution to a row not owned");
+          ent.push_back(Ent{g, ctx->rc_sub[k], ctx->X + k});
+        }
+    }
+    std::stable_sort(ent.begin(), ent.end(),
+                     [](const Ent& a, const Ent& b) { return a.row != b.row ? a.row < b.row : a.sub < b.sub; });
+    for (const Ent& e : ent) cnt[e.row + 1]++;
+    for (int g = 0; g < n; ++g) cnt[g + 1] += cnt[g];
+    pos.resize(ent.size());
+    for (size_t i = 0; i < ent.size(); ++i) pos[i] = (int)ent[i].pos;
+    // reverse-halo plan
+    XPlan& x = ctx->rev;
+    x.peers.clear(); x.scnt.clear(); x.rcnt.clear(); x.soff.clear(); x.roff.clear();
+    std::vector<int> sidx, ridx;
+    for (int q = 0; q < nr; ++q) {
+      long long rc = 0;
+      for (size_t b = 0; b < ctx->rc_peer.size(); ++b)
+        if (asm_ && ctx->rc_peer[b] == q) rc = ctx->rc_cnt[b];
+      if (sendpos[q].empty() && rc == 0) continue;
+      x.peers.push_back(q);
+      x.soff.push_back((long long)sidx.size());
+      x.scnt.push_back((int)sendpos[q].size());
+      sidx.insert(sidx.end(), sendpos[q].begin(), sendpos[q].end());
+      x.roff.push_back((long long)ridx.size());
+      x.rcnt.push_back((int)rc);
+      long long k0 = 0;
+      for (size_t b = 0; b < ctx->rc_peer.size() && ctx->rc_peer[b] != q; ++b) k0 += ctx->rc_cnt[b];
+      for (long long e = 0; e < rc; ++e) ridx.push_back((int)(ctx->X + k0 + e));
+    }
+    if (!asm_ && !sidx.empty()) return fail(ctx, TLS_ERR_STATE, "RAS interior row owned by another rank");
+    x.stot = (long long)sidx.size();
+    x.rtot = (long long)ridx.size();
+    TRY(upload(ctx, x.d_sidx, sidx.data(), x.stot));
+    TRY(upload(ctx, x.d_ridx, ridx.data(), x.rtot));
+    TRY(dalloc(ctx, x.sbuf, x.stot));
+    TRY(dalloc(ctx, x.rbuf, x.rtot));
   }
   TRY(upload(ctx, ctx->d_pull_ptr, cnt.data(), n + 1));
   TRY(upload(ctx, ctx->d_pull_pos, pos.data(), (int64_t)pos.size()));
@@ -868,17 +1070,26 @@ static int need_final(tls_ctx* ctx) {
 int32_t tls_precond_apply(tls_ctx* ctx, const double* r, double* z, void* stream) {
   TRY(need_final(ctx));
   CK(cudaSetDevice(ctx->device));
-  return enq_apply(ctx, (cudaStream_t)stream, r, z, false, nullptr);
+  cudaStream_t s = (cudaStream_t)stream;
+  double* ri;
+  TRY(api_in(ctx, s, r, &ri));
+  double* zi = api_out_buf(ctx, z);
+  TRY(enq_apply(ctx, s, ri, zi, false, nullptr, true));
+  return api_out(ctx, s, zi, z);
 }
 
 int32_t tls_apply_one_level(tls_ctx* ctx, const double* r, double* z, void* stream) {
   TRY(need_final(ctx));
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
-  TRY(enq_gather(ctx, s, r, nullptr));
+  double* ri;
+  TRY(api_in(ctx, s, r, &ri));
+  double* zi = api_out_buf(ctx, z);
+  TRY(enq_gather(ctx, s, ri, nullptr));
   TRY(enq_solve(ctx, s, L_LOCAL, nullptr));
-  TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, z, nullptr)));
-  return enq_allreduce(ctx, s, z, ctx->n);
+  TRY(enq_rev(ctx, s, nullptr));
+  TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, zi, nullptr)));
+  return api_out(ctx, s, zi, z);
 }
 
 int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream) {
@@ -886,10 +1097,13 @@ int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream)
   if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "no coarse space");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
-  TRY(enq_restrict_all(ctx, s, r, nullptr));
+  double* ri;
+  TRY(api_in(ctx, s, r, &ri));
+  double* zi = api_out_buf(ctx, z);
+  TRY(enq_restrict_all(ctx, s, ri, nullptr));
   TRY(enq_solve(ctx, s, L_COARSE, nullptr));
-  TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, z, nullptr)));
-  return enq_allreduce(ctx, s, z, ctx->n);
+  TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, zi, nullptr)));
+  return api_out(ctx, s, zi, z);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -898,18 +1112,26 @@ int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream)
 static int enq_pcg_iter(tls_ctx* ctx, cudaStream_t s, bool replace, bool prec) {
   PcgState* st = ctx->pcg;
   const int* done = &st->done;
+  const int r0 = ctx->r0, no = nown(ctx);
+  TRY(enq_halo(ctx, s, ctx->vp, done));
   TRY((spmv_lpr<0, 1>(ctx, s, ctx->vp, ctx->vap, nullptr, ctx->part, done)));
+  TRY(enq_allreduce_part(ctx, s, ctx->Gs));
   k_pcg_alpha<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->ab);
   CKL();
   if (!replace) {
-    k_pcg_update<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, ctx->vx, ctx->vr, ctx->vp, ctx->vap, ctx->part, 1);
+    k_pcg_update<<<ctx->G, NTHR, 0, s>>>(no, st, ctx->vx + r0, ctx->vr + r0, ctx->vp + r0, ctx->vap + r0,
+                                         ctx->part, 1);
     CKL();
+    TRY(enq_allreduce_part(ctx, s, ctx->G));
     k_pcg_hist<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->G, ctx->hist);
     CKL();
   } else {
-    k_pcg_update<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, ctx->vx, ctx->vr, ctx->vp, ctx->vap, ctx->part, 0);
+    k_pcg_update<<<ctx->G, NTHR, 0, s>>>(no, st, ctx->vx + r0, ctx->vr + r0, ctx->vp + r0, ctx->vap + r0,
+                                         ctx->part, 0);
     CKL();
+    TRY(enq_halo(ctx, s, ctx->vx, done));
     TRY((spmv_lpr<1, 2>(ctx, s, ctx->vx, ctx->vr, ctx->vb, ctx->part, done)));
+    TRY(enq_allreduce_part(ctx, s, ctx->Gs));
     k_pcg_hist<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->hist);
     CKL();
   }
@@ -919,7 +1141,7 @@ static int enq_pcg_iter(tls_ctx* ctx, cudaStream_t s, bool replace, bool prec) {
     TRY(enq_identity(ctx, s, ctx->vr, ctx->vz, true, done));
   k_pcg_beta<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->G, ctx->ab);
   CKL();
-  k_pcg_pupdate<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, ctx->vp, ctx->vz);
+  k_pcg_pupdate<<<ctx->G, NTHR, 0, s>>>(no, st, ctx->vp + r0, ctx->vz + r0);
   CKL();
   return TLS_OK;
 }
@@ -947,16 +1169,20 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
   TRY(ensure_hist(ctx, maxit));
   const int launches0 = ctx->launches;
   tls_status stt{};
-  // init: x = 0, r = b, ||b||
-  CK(cudaMemcpyAsync(ctx->vb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(ctx->vr, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  // init: x = 0, r = b (all rows, internal numbering), ||b||
+  if (ctx->h_nofo.empty()) {
+    CK(cudaMemcpyAsync(ctx->vb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    k_perm_in<<<grid_for(n, NTHR), NTHR, 0, s>>>(n, ctx->d_nofo, b, ctx->vb);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(ctx->vr, ctx->vb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   CK(cudaMemsetAsync(ctx->vx, 0, sizeof(double) * n, s));
   PcgState h{};
   h.tol = tol;
   h.maxit = maxit;
   CK(cudaMemcpyAsync(ctx->pcg, &h, sizeof(PcgState), cudaMemcpyHostToDevice, s));
-  k_dot<<<ctx->G, NTHR, 0, s>>>(n, ctx->vb, ctx->vb, ctx->part, nullptr);
-  CKL();
+  TRY(enq_dot(ctx, s, ctx->vb, ctx->vb, nullptr));
   k_pcg_init<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
   CKL();
   CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
@@ -974,7 +1200,7 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
   const double one = 1.0;
   CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
   if (prec)
-    TRY(enq_apply(ctx, s, ctx->vr, ctx->vz, true, nullptr));
+    TRY(enq_apply(ctx, s, ctx->vr, ctx->vz, true, nullptr, true));
   else
     TRY(enq_identity(ctx, s, ctx->vr, ctx->vz, true, nullptr));
   k_pcg_rz0<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
@@ -990,7 +1216,9 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
         CK(cudaStreamSynchronize(s));
         if (h.status == 2) break;
         if (cb) {
-          CK(cudaMemcpy(ctx->h_x, ctx->vx, sizeof(double) * n, cudaMemcpyDeviceToHost));
+          TRY(api_out(ctx, s, ctx->vx, ctx->pout));
+          CK(cudaStreamSynchronize(s));
+          CK(cudaMemcpy(ctx->h_x, ctx->pout, sizeof(double) * n, cudaMemcpyDeviceToHost));
           cb(user, h.it, ctx->h_x);
         }
         if (h.done) break;
@@ -1023,7 +1251,7 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
     }
   }
   CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  TRY(api_out(ctx, s, ctx->vx, x));
   CK(cudaStreamSynchronize(s));
   const int its = h.it;
   CK(cudaMemcpy(history, ctx->hist, sizeof(double) * (its + 1), cudaMemcpyDeviceToHost));
@@ -1051,54 +1279,63 @@ static int enq_gm_step(tls_ctx* ctx, cudaStream_t s, int j, bool prec) {
   GmState* st = ctx->gm;
   const int* stop = &st->cycle_stop;
   const long long ldv = ctx->n;
-  const double* vj = ctx->V + (long long)j * ldv;
+  const int r0 = ctx->r0, no = nown(ctx);
+  double* vj = ctx->V + (long long)j * ldv;
   double* w = ctx->t6;
   if (prec) {
     TRY(enq_apply(ctx, s, vj, ctx->t5, false, stop));
+    TRY(enq_halo(ctx, s, ctx->t5, stop));
     TRY((spmv_lpr<0, 0>(ctx, s, ctx->t5, w, nullptr, nullptr, stop)));
   } else {
+    TRY(enq_halo(ctx, s, vj, stop));
     TRY((spmv_lpr<0, 0>(ctx, s, vj, w, nullptr, nullptr, stop)));
   }
   const int nc = j + 1;
   double* hs[2] = {ctx->h1, ctx->h2};
   for (int pass = 0; pass < 2; ++pass) {
-    k_gm_gemvt<<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->V, ldv, nc, w, ctx->part, stop);
+    k_gm_gemvt<<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, w + r0, ctx->part, stop);
     CKL();
     k_gm_hreduce<<<nc, NTHR, 0, s>>>(ctx->part, ctx->G, hs[pass], stop);
     CKL();
+    TRY(enq_allreduce(ctx, s, hs[pass], nc));
     if (pass == 0)
-      k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->V, ldv, nc, st, hs[pass], w, ctx->part, 1, stop);
+      k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, st, hs[pass], w + r0, ctx->part, 1, stop);
     else
-      k_gm_gemvn<1><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->V, ldv, nc, st, hs[pass], w, ctx->part, 1, stop);
+      k_gm_gemvn<1><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, st, hs[pass], w + r0, ctx->part, 1, stop);
     CKL();
   }
+  TRY(enq_allreduce_part(ctx, s, ctx->G));
   k_gm_givens<<<1, NTHR, 0, s>>>(st, j, ctx->gm_cols + 1, ctx->H, ctx->h1, ctx->h2, ctx->part, ctx->G,
                                  ctx->cs, ctx->sn, ctx->gv, ctx->hist);
   CKL();
-  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, w, ctx->V + (long long)(j + 1) * ldv, 0);
+  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(no, st, w + r0, ctx->V + (long long)(j + 1) * ldv + r0, 0);
   CKL();
   return TLS_OK;
 }
 
 static int enq_gm_cycle_end(tls_ctx* ctx, cudaStream_t s, bool prec) {
   GmState* st = ctx->gm;
+  const int r0 = ctx->r0, no = nown(ctx);
   k_gm_trisolve<<<1, 32, 0, s>>>(st, ctx->gm_cols + 1, ctx->H, ctx->gv, ctx->yv);
   CKL();
-  k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->V, ctx->n, -1, st, ctx->yv, ctx->t7, nullptr, 0, nullptr);
+  k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ctx->n, -1, st, ctx->yv, ctx->t7 + r0, nullptr, 0,
+                                        nullptr);
   CKL();
   if (prec) {
     TRY(enq_apply(ctx, s, ctx->t7, ctx->t5, false, nullptr));
-    k_axpy1<<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->vx, ctx->t5, nullptr);
+    k_axpy1<<<ctx->G, NTHR, 0, s>>>(no, ctx->vx + r0, ctx->t5 + r0, nullptr);
   } else {
-    k_axpy1<<<ctx->G, NTHR, 0, s>>>(ctx->n, ctx->vx, ctx->t7, nullptr);
+    k_axpy1<<<ctx->G, NTHR, 0, s>>>(no, ctx->vx + r0, ctx->t7 + r0, nullptr);
   }
   CKL();
   k_gm_cycle_end<<<1, 32, 0, s>>>(st);
   CKL();
+  TRY(enq_halo(ctx, s, ctx->vx, &st->done));
   TRY((spmv_lpr<1, 2>(ctx, s, ctx->vx, ctx->vr, ctx->vb, ctx->part, &st->done)));
+  TRY(enq_allreduce_part(ctx, s, ctx->Gs));
   k_gm_cycle_begin<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->gv, ctx->gm_cols);
   CKL();
-  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(ctx->n, st, ctx->vr, ctx->V, 1);
+  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(no, st, ctx->vr + r0, ctx->V + r0, 1);
   CKL();
   return TLS_OK;
 }
@@ -1107,6 +1344,7 @@ static int ensure_gm(tls_ctx* ctx, int mcols) {
   if (mcols == ctx->gm_cols && ctx->V) return TLS_OK;
   const int64_t n = ctx->n;
   TRY(dalloc(ctx, ctx->V, n * (mcols + 1)));
+  CK(cudaMemset(ctx->V, 0, sizeof(double) * n * (mcols + 1)));
   TRY(dalloc(ctx, ctx->H, (int64_t)(mcols + 1) * (mcols + 1)));
   TRY(dalloc(ctx, ctx->cs, mcols + 1));
   TRY(dalloc(ctx, ctx->sn, mcols + 1));
@@ -1156,12 +1394,16 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
   h.restart = restarted ? restart : 0;
   h.restarted = restarted ? 1 : 0;
   CK(cudaMemcpyAsync(ctx->gm, &h, sizeof(GmState), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(ctx->vb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(ctx->vr, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (ctx->h_nofo.empty()) {
+    CK(cudaMemcpyAsync(ctx->vb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    k_perm_in<<<grid_for(n, NTHR), NTHR, 0, s>>>(n, ctx->d_nofo, b, ctx->vb);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(ctx->vr, ctx->vb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   CK(cudaMemsetAsync(ctx->vx, 0, sizeof(double) * n, s));
   CK(cudaMemsetAsync(ctx->H, 0, sizeof(double) * (size_t)(mcols + 1) * (mcols + 1), s));
-  k_dot<<<ctx->G, NTHR, 0, s>>>(n, ctx->vb, ctx->vb, ctx->part, nullptr);
-  CKL();
+  TRY(enq_dot(ctx, s, ctx->vb, ctx->vb, nullptr));
   // reuse pcg init to get ||b|| then seed the first cycle
   k_pcg_init<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
   CKL();
@@ -1181,7 +1423,7 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
   CK(cudaMemcpyAsync(ctx->gm, &h, sizeof(GmState), cudaMemcpyHostToDevice, s));
   k_gm_cycle_begin<<<1, NTHR, 0, s>>>(ctx->gm, ctx->part, ctx->G, ctx->gv, mcols);
   CKL();
-  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(n, ctx->gm, ctx->vr, ctx->V, 1);
+  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(nown(ctx), ctx->gm, ctx->vr + ctx->r0, ctx->V + ctx->r0, 1);
   CKL();
   const double one = 1.0;
   CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
@@ -1229,7 +1471,7 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
     }
   }
   CK(cudaMemcpyAsync(&hs, ctx->gm, sizeof(GmState), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(x, ctx->vx, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  TRY(api_out(ctx, s, ctx->vx, x));
   CK(cudaStreamSynchronize(s));
   CK(cudaMemcpy(history, ctx->hist, sizeof(double) * (hs.total + 1), cudaMemcpyDeviceToHost));
   stt.iterations = hs.total;
@@ -1468,6 +1710,84 @@ int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first_g, int32_t count, co
 }
 
 // ---- sharding -------------------------------------------------------------------------------
+int32_t tls_set_row_partition(tls_ctx* ctx, int64_t n, const int32_t* new_of_old, int32_t nranks,
+                              const int32_t* row_starts, int32_t rank) {
+  if (!ctx) return TLS_ERR_ARG;
+  if (ctx->rowptr) return fail(ctx, TLS_ERR_STATE, "set the row partition before tls_matrix_upload");
+  if (n <= 0 || n > INT32_MAX || !new_of_old || nranks < 1 || !row_starts || rank < 0 || rank >= nranks)
+    return fail(ctx, TLS_ERR_ARG, "bad row partition");
+  if (row_starts[0] != 0 || row_starts[nranks] != n) return fail(ctx, TLS_ERR_ARG, "row ranges must cover [0, n)");
+  for (int q = 0; q < nranks; ++q)
+    if (row_starts[q + 1] < row_starts[q]) return fail(ctx, TLS_ERR_ARG, "row ranges must be ascending");
+  std::vector<char> seen(n, 0);
+  for (int64_t g = 0; g < n; ++g) {
+    const int v = new_of_old[g];
+    if (v < 0 || v >= n || seen[v]) return fail(ctx, TLS_ERR_ARG, "new_of_old is not a permutation");
+    seen[v] = 1;
+  }
+  CK(cudaSetDevice(ctx->device));
+  ctx->h_nofo.assign(new_of_old, new_of_old + n);
+  ctx->row_starts.assign(row_starts, row_starts + nranks + 1);
+  ctx->r0 = row_starts[rank];
+  ctx->r1 = row_starts[rank + 1];
+  TRY(upload(ctx, ctx->d_nofo, ctx->h_nofo.data(), n));
+  return TLS_OK;
+}
+
+// halo plan: per peer (ascending), the owned rows this rank sends and the ghost rows it receives
+// (internal numbering, both sides in ascending row order)
+int32_t tls_set_halo(tls_ctx* ctx, int32_t npeers, const int32_t* peers, const int32_t* send_counts,
+                     const int32_t* send_rows, const int32_t* recv_counts, const int32_t* recv_rows) {
+  if (!ctx) return TLS_ERR_ARG;
+  if (ctx->h_nofo.empty()) return fail(ctx, TLS_ERR_STATE, "no row partition");
+  if (npeers < 0) return fail(ctx, TLS_ERR_ARG, "bad peer count");
+  CK(cudaSetDevice(ctx->device));
+  XPlan& x = ctx->halo;
+  x.peers.assign(peers, peers + npeers);
+  x.scnt.assign(send_counts, send_counts + npeers);
+  x.rcnt.assign(recv_counts, recv_counts + npeers);
+  x.soff.assign(npeers, 0);
+  x.roff.assign(npeers, 0);
+  long long so = 0, ro = 0;
+  for (int k = 0; k < npeers; ++k) {
+    if (x.scnt[k] < 0 || x.rcnt[k] < 0) return fail(ctx, TLS_ERR_ARG, "negative halo count");
+    x.soff[k] = so;
+    x.roff[k] = ro;
+    so += x.scnt[k];
+    ro += x.rcnt[k];
+  }
+  for (long long i = 0; i < so; ++i)
+    if (send_rows[i] < ctx->r0 || send_rows[i] >= ctx->r1) return fail(ctx, TLS_ERR_ARG, "halo sends a row not owned");
+  for (long long i = 0; i < ro; ++i)
+    if (recv_rows[i] < 0 || recv_rows[i] >= ctx->n || (recv_rows[i] >= ctx->r0 && recv_rows[i] < ctx->r1))
+      return fail(ctx, TLS_ERR_ARG, "halo receives an owned or out-of-range row");
+  x.stot = so;
+  x.rtot = ro;
+  TRY(upload(ctx, x.d_sidx, send_rows, so));
+  TRY(upload(ctx, x.d_ridx, recv_rows, ro));
+  TRY(dalloc(ctx, x.sbuf, so));
+  TRY(dalloc(ctx, x.rbuf, ro));
+  destroy_graphs(ctx);
+  return TLS_OK;
+}
+
+// ASM overlap contributions this rank receives: per peer (ascending), `counts` entries of
+// (global subdomain, internal row) in the sender's (subdomain, local index) order
+int32_t tls_set_remote_contrib(tls_ctx* ctx, int32_t npeers, const int32_t* peers, const int32_t* counts,
+                               const int32_t* subs, const int32_t* rows) {
+  if (!ctx) return TLS_ERR_ARG;
+  if (ctx->h_nofo.empty()) return fail(ctx, TLS_ERR_STATE, "no row partition");
+  if (npeers < 0) return fail(ctx, TLS_ERR_ARG, "bad peer count");
+  ctx->rc_peer.assign(peers, peers + npeers);
+  ctx->rc_cnt.assign(counts, counts + npeers);
+  long long tot = 0;
+  for (int k = 0; k < npeers; ++k) tot += counts[k];
+  ctx->rc_sub.assign(subs, subs + tot);
+  ctx->rc_row.assign(rows, rows + tot);
+  ctx->finalized = false;
+  return TLS_OK;
+}
+
 int32_t tls_set_owned_range(tls_ctx* ctx, int32_t s_lo, int32_t s_hi) {
   if (!ctx || s_lo < 0 || s_hi <= s_lo) return ctx ? fail(ctx, TLS_ERR_ARG, "bad owned range") : TLS_ERR_ARG;
   ctx->own_lo = s_lo;

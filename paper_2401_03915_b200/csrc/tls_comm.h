@@ -1,5 +1,7 @@
-// tls_comm.h — the one exchange step of the sharded path: an in-place sum all-reduce of fp64
-// buffers across the ranks that own disjoint subdomain slabs.
+// tls_comm.h — the exchange steps of the sharded path: in-place sum all-reduces
+// of small fp64 buffers (dot-product partials, coarse coefficients) and point-to-point exchanges
+// of halo rows (SpMV / overlap gathers) and of ASM overlap contributions (reverse halo) between
+// the ranks that own disjoint row ranges / subdomain slabs.
 //
 //  * NcclComm   — one process per GPU; NCCL (libnccl.so.2, dlopen'ed so the library also loads on
 //                 hosts without NCCL) over NVLink/NVSwitch; stream-ordered and CUDA-graph
@@ -13,6 +15,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <mutex>
@@ -23,10 +26,23 @@ namespace tls {
 
 constexpr int MAX_GROUP = 16;
 
+// One point-to-point exchange pattern: this rank sends sbuf[soff[k], +scnt[k]) to peers[k] and
+// receives rbuf[roff[k], +rcnt[k]) from peers[k] (same peer list on both sides, ascending).
+struct XPlan {
+  std::vector<int> peers, scnt, rcnt;
+  std::vector<long long> soff, roff;
+  long long stot = 0, rtot = 0;
+  int* d_sidx = nullptr;   // pack: sbuf[p] = src[d_sidx[p]]
+  int* d_ridx = nullptr;   // unpack: dst[d_ridx[p]] = rbuf[p]
+  double *sbuf = nullptr, *rbuf = nullptr;
+  bool empty() const { return peers.empty(); }
+};
+
 struct Comm {
   int rank = 0, nranks = 1;
   virtual ~Comm() {}
   virtual cudaError_t allreduce_sum(double* buf, long long count, cudaStream_t s, std::string& err) = 0;
+  virtual cudaError_t exchange(const XPlan& x, cudaStream_t s, std::string& err) = 0;
   virtual bool capturable() const = 0;
 };
 
@@ -38,6 +54,10 @@ struct NcclApi {
   decltype(&ncclAllReduce) allreduce = nullptr;
   decltype(&ncclCommDestroy) destroy = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
   bool load(std::string& err) {
     if (h) return true;
     h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -50,7 +70,12 @@ struct NcclApi {
     allreduce = (decltype(allreduce))dlsym(h, "ncclAllReduce");
     destroy = (decltype(destroy))dlsym(h, "ncclCommDestroy");
     errstr = (decltype(errstr))dlsym(h, "ncclGetErrorString");
-    if (!get_id || !init_rank || !allreduce || !destroy || !errstr) {
+    send = (decltype(send))dlsym(h, "ncclSend");
+    recv = (decltype(recv))dlsym(h, "ncclRecv");
+    group_start = (decltype(group_start))dlsym(h, "ncclGroupStart");
+    group_end = (decltype(group_end))dlsym(h, "ncclGroupEnd");
+    if (!get_id || !init_rank || !allreduce || !destroy || !errstr || !send || !recv || !group_start ||
+        !group_end) {
       err = "libnccl.so.2 lacks required symbols";
       return false;
     }
@@ -72,6 +97,23 @@ struct NcclComm : Comm {
     ncclResult_t r = nccl_api().allreduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, comm, s);
     if (r != ncclSuccess) {
       err = std::string("ncclAllReduce: ") + nccl_api().errstr(r);
+      return cudaErrorUnknown;
+    }
+    return cudaSuccess;
+  }
+  // grouped send/recv with every peer of the plan (one NCCL group = one fused launch)
+  cudaError_t exchange(const XPlan& x, cudaStream_t s, std::string& err) override {
+    NcclApi& api = nccl_api();
+    ncclResult_t r = api.group_start();
+    for (size_t k = 0; k < x.peers.size() && r == ncclSuccess; ++k) {
+      if (x.scnt[k] > 0) r = api.send(x.sbuf + x.soff[k], (size_t)x.scnt[k], ncclFloat64, x.peers[k], comm, s);
+      if (r == ncclSuccess && x.rcnt[k] > 0)
+        r = api.recv(x.rbuf + x.roff[k], (size_t)x.rcnt[k], ncclFloat64, x.peers[k], comm, s);
+    }
+    ncclResult_t r2 = api.group_end();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) {
+      err = std::string("ncclSend/ncclRecv: ") + api.errstr(r);
       return cudaErrorUnknown;
     }
     return cudaSuccess;
@@ -101,7 +143,11 @@ struct GroupShared {
   long long gen = 0;
   std::vector<double*> bufs;
   std::vector<cudaEvent_t> ev_in, ev_out;
-  explicit GroupShared(int n_) : n(n_), bufs(n_, nullptr), ev_in(n_, nullptr), ev_out(n_, nullptr) {}
+  std::vector<const double*> xbuf;          // exchange: every member's send buffer
+  std::vector<std::vector<long long>> xoff; // xoff[p][q]: offset of p's segment for q (-1: none)
+  explicit GroupShared(int n_)
+      : n(n_), bufs(n_, nullptr), ev_in(n_, nullptr), ev_out(n_, nullptr), xbuf(n_, nullptr),
+        xoff(n_, std::vector<long long>(n_, -1)) {}
   bool broken = false;
   // false when a peer never arrives (it failed before reaching the exchange): the group is
   // then broken and every later exchange fails fast instead of hanging the process.
@@ -160,6 +206,38 @@ struct GroupComm : Comm {
     for (int r = 0; r < g->n; ++r)
       if ((e = cudaStreamWaitEvent(s, g->ev_out[r], 0)) != cudaSuccess) return e;
     return cudaMemcpyAsync(buf, tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, s);
+  }
+  // every member publishes its send buffer; each copies its segments out of the peers' buffers
+  cudaError_t exchange(const XPlan& x, cudaStream_t s, std::string& err) override {
+    cudaError_t e;
+    std::fill(g->xoff[rank].begin(), g->xoff[rank].end(), -1LL);
+    for (size_t k = 0; k < x.peers.size(); ++k) g->xoff[rank][x.peers[k]] = x.scnt[k] > 0 ? x.soff[k] : -1;
+    g->xbuf[rank] = x.sbuf;
+    if ((e = cudaEventRecord(g->ev_in[rank], s)) != cudaSuccess) return e;
+    if (!g->barrier()) {
+      err = "in-process group: a peer rank did not reach the exchange";
+      return cudaErrorUnknown;
+    }
+    for (size_t k = 0; k < x.peers.size(); ++k) {
+      if (x.rcnt[k] == 0) continue;
+      const int p = x.peers[k];
+      if (g->xoff[p][rank] < 0) {
+        err = "in-process group: exchange plans disagree";
+        return cudaErrorUnknown;
+      }
+      if ((e = cudaStreamWaitEvent(s, g->ev_in[p], 0)) != cudaSuccess) return e;
+      if ((e = cudaMemcpyAsync(x.rbuf + x.roff[k], g->xbuf[p] + g->xoff[p][rank], sizeof(double) * x.rcnt[k],
+                               cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+        return e;
+    }
+    if ((e = cudaEventRecord(g->ev_out[rank], s)) != cudaSuccess) return e;
+    if (!g->barrier()) {  // every member has enqueued its reads of the send buffers
+      err = "in-process group: a peer rank did not reach the exchange";
+      return cudaErrorUnknown;
+    }
+    for (int r = 0; r < g->n; ++r)
+      if ((e = cudaStreamWaitEvent(s, g->ev_out[r], 0)) != cudaSuccess) return e;
+    return cudaSuccess;
   }
   bool capturable() const override { return false; }
 };

@@ -79,18 +79,19 @@ __device__ __forceinline__ double sum_partials(const double* __restrict__ p, int
 // deterministic partials.
 // ---------------------------------------------------------------------------------------
 template <int LPR, int MODE, int DOT>
-__global__ void __launch_bounds__(NTHR) k_spmv(int n, const int* __restrict__ rowptr,
+__global__ void __launch_bounds__(NTHR) k_spmv(int r0, int n, const int* __restrict__ rowptr,
                                                const int* __restrict__ col,
                                                const double* __restrict__ val,
                                                const double* __restrict__ x, double* __restrict__ y,
                                                const double* __restrict__ b,
                                                double* __restrict__ part, const int* done) {
+  // rows [r0, n): the whole matrix, or this rank's owned row range on the sharded path
   if (done && *done) return;
   __shared__ double sh[32];
   const int g = threadIdx.x / LPR, gl = threadIdx.x % LPR;
   const int rows_per_block = NTHR / LPR;
   double dacc = 0.0;
-  for (int row0 = blockIdx.x * rows_per_block; row0 < n; row0 += gridDim.x * rows_per_block) {
+  for (int row0 = r0 + blockIdx.x * rows_per_block; row0 < n; row0 += gridDim.x * rows_per_block) {
     const int row = row0 + g;
     double s = 0.0;
     if (row < n) {
@@ -357,6 +358,39 @@ __global__ void __launch_bounds__(NTHR) k_prolong(int n, const int* __restrict__
     const double t = block_sum(dacc, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = t;
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// Sharded path: the system is renumbered so every rank owns a contiguous row
+// range; vectors enter/leave in the caller's numbering, and the halo / reverse-halo exchanges
+// move only the rows a rank's SpMV, gathers and ASM prolongation touch.
+// ---------------------------------------------------------------------------------------
+// dst[nofo[g]] = src[g]  (caller numbering -> internal numbering, all rows)
+__global__ void __launch_bounds__(NTHR) k_perm_in(int n, const int* __restrict__ nofo,
+                                                  const double* __restrict__ src, double* __restrict__ dst) {
+  for (int g = blockIdx.x * NTHR + threadIdx.x; g < n; g += gridDim.x * NTHR) dst[__ldg(nofo + g)] = src[g];
+}
+// dst[g] = src[nofo[g]] for owned rows, 0 elsewhere (completed by a sum all-reduce)
+__global__ void __launch_bounds__(NTHR) k_perm_out(int n, const int* __restrict__ nofo, int r0, int r1,
+                                                   const double* __restrict__ src, double* __restrict__ dst) {
+  for (int g = blockIdx.x * NTHR + threadIdx.x; g < n; g += gridDim.x * NTHR) {
+    const int i = __ldg(nofo + g);
+    dst[g] = (i >= r0 && i < r1) ? src[i] : 0.0;
+  }
+}
+__global__ void __launch_bounds__(NTHR) k_xpack(long long m, const int* __restrict__ idx,
+                                                const double* __restrict__ src, double* __restrict__ buf,
+                                                const int* done) {
+  if (done && *done) return;
+  for (long long p = blockIdx.x * (long long)NTHR + threadIdx.x; p < m; p += (long long)gridDim.x * NTHR)
+    buf[p] = src[__ldg(idx + p)];
+}
+__global__ void __launch_bounds__(NTHR) k_xunpack(long long m, const int* __restrict__ idx,
+                                                  const double* __restrict__ buf, double* __restrict__ dst,
+                                                  const int* done) {
+  if (done && *done) return;
+  for (long long p = blockIdx.x * (long long)NTHR + threadIdx.x; p < m; p += (long long)gridDim.x * NTHR)
+    dst[__ldg(idx + p)] = buf[p];
 }
 
 // deflated combination after the sharded all-reduces: z = (q + w) - Qu  (src/precond.py:136)

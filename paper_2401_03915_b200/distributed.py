@@ -1,15 +1,22 @@
 """Sharding the hot path across GPUs.
 
 Decomposition: each rank owns a contiguous slab of subdomains (balanced by the bytes of their
-local operators).  Vectors, SpMV, dot products and the (replicated, small) coarse solve are
-computed redundantly on every rank; every prolongation is rank-partial and completed by ONE
-in-place sum all-reduce (NCCL over NVLink inside the captured solve graph).  Setup exchanges:
-global max pivot (rank filter), per-subdomain coarse counts, the coarse basis blocks and the
-column blocks of A0 = Z^T A Z.
+local operators) and the rows those subdomains own (Boolean PoU: every row has exactly one
+owner subdomain).  The rows are renumbered rank by rank (``RowPartition``) so each rank's rows
+form one contiguous internal range; every per-iteration kernel then runs on the owned rows only:
+SpMV, the local solves of its subdomains, its rows of A0^{-1} c, the prolongation, the Krylov
+vector updates.  Exchanges per operator (NCCL over NVLink, captured in the solve graphs):
+* halo: the ghost rows a rank reads (columns of its SpMV rows, overlap rows of its subdomains)
+  from their owners -- point-to-point, only between neighbouring slabs;
+* reverse halo (ASM only): local-solve outputs on rows owned by another rank go to the owner,
+  who adds them in ascending subdomain order (the np.add.at order of src/precond.py:121);
+* sum all-reduces of the dot-product partials (a few KB) and of c = Z^T r (n_C doubles).
+Setup exchanges: global max pivot (rank filter), per-subdomain coarse counts, the coarse basis
+blocks and the column blocks of A0 = Z^T A Z; the halo plans (needed-row lists).
 
 Two transports with the same interface:
 * ``TorchCollective`` — torch.distributed (NCCL on GPUs; gloo on CPU for the host-logic tests);
-  the solve-time all-reduce is an NCCL communicator inside libtls_b200.
+  the solve-time exchanges use an NCCL communicator inside libtls_b200.
 * ``ThreadCollective`` — R ranks inside one process (host threads) on one GPU; the library side
   uses an in-process group (tls_group).  Validates the sharded schedule end-to-end on 1 GPU.
 """
@@ -40,6 +47,121 @@ def slab_ranges(weights, nranks):
         cuts.append(c)
     cuts.append(n)
     return [(cuts[r], cuts[r + 1]) for r in range(nranks)]
+
+
+def row_partition(owner, n_loc, nranks):
+    """Rank of every subdomain and row, and the rank-by-rank row numbering.
+
+    Returns (slabs, new_of_old, row_starts): rank q owns subdomains slabs[q] = [lo, hi) and the
+    internal rows [row_starts[q], row_starts[q+1]); new_of_old[g] is the internal row of row g
+    (rows keep their relative order inside a rank)."""
+    owner = np.asarray(owner, dtype=np.int64)
+    slabs = slab_ranges(np.asarray(n_loc, dtype=np.float64) ** 2, nranks)
+    sub_rank = np.empty(len(n_loc), dtype=np.int64)
+    for q, (lo, hi) in enumerate(slabs):
+        sub_rank[lo:hi] = q
+    row_rank = sub_rank[owner]
+    old_of_new = np.argsort(row_rank, kind="stable")
+    new_of_old = np.empty_like(old_of_new)
+    new_of_old[old_of_new] = np.arange(old_of_new.size)
+    row_starts = np.concatenate([[0], np.cumsum(np.bincount(row_rank, minlength=nranks))])
+    return slabs, new_of_old.astype(np.int64), row_starts.astype(np.int64)
+
+
+def needed_rows(csr, maps, slab, new_of_old, r0, r1):
+    """Sorted internal ids of the ghost rows rank reads: columns of its SpMV rows and the
+    overlap rows of its subdomains that it does not own."""
+    lo, hi = slab
+    own_old = np.zeros(csr.shape[0], dtype=bool)
+    own_old[(new_of_old >= r0) & (new_of_old < r1)] = True
+    lens = np.diff(csr.indptr)
+    cols = csr.indices[np.repeat(own_old, lens)]
+    parts = [new_of_old[cols]] + [new_of_old[maps[s].indices] for s in range(lo, hi)]
+    allr = np.unique(np.concatenate(parts))
+    return allr[(allr < r0) | (allr >= r1)]
+
+
+def halo_lists(needs, rank, row_starts):
+    """From every rank's sorted needed rows: (peers, send_rows per peer, recv_rows per peer)."""
+    r0, r1 = int(row_starts[rank]), int(row_starts[rank + 1])
+    peers, send, recv = [], [], []
+    for q in range(len(needs)):
+        if q == rank:
+            continue
+        nq = needs[q]
+        s_q = nq[(nq >= r0) & (nq < r1)]
+        mine = needs[rank]
+        rq = mine[(mine >= row_starts[q]) & (mine < row_starts[q + 1])]
+        if s_q.size or rq.size:
+            peers.append(q)
+            send.append(s_q)
+            recv.append(rq)
+    return peers, send, recv
+
+
+def remote_contributions(maps, slabs, rank, new_of_old, row_starts):
+    """ASM overlap contributions rank receives: per peer (ascending) the (global subdomain,
+    internal row) pairs of the peer's subdomains on rows this rank owns, in the peer's
+    (subdomain, local index) order."""
+    r0, r1 = int(row_starts[rank]), int(row_starts[rank + 1])
+    peers, subs, rows = [], [], []
+    for q, (lo, hi) in enumerate(slabs):
+        if q == rank:
+            continue
+        idx = [new_of_old[maps[s].indices] for s in range(lo, hi)]
+        if not idx:
+            continue
+        sid = np.repeat(np.arange(lo, hi), [a.size for a in idx])
+        cat = np.concatenate(idx)
+        keep = (cat >= r0) & (cat < r1)
+        if keep.any():
+            peers.append(q)
+            subs.append(sid[keep])
+            rows.append(cat[keep])
+    return peers, subs, rows
+
+
+class RowPartition:
+    """One rank's share of the renumbered system and its exchange plans."""
+
+    def __init__(self, maps, owner, shard):
+        n_loc = np.array([m.n_local for m in maps], dtype=np.int64)
+        self.slabs, self.new_of_old, self.row_starts = row_partition(owner, n_loc, shard.nranks)
+        self.shard = shard
+        self.rank = shard.rank
+        self.r0 = int(self.row_starts[self.rank])
+        self.r1 = int(self.row_starts[self.rank + 1])
+
+    def set_numbering(self, handle):
+        """Before the matrix upload: the library stores P A P^T in the internal numbering."""
+        nofo = np.ascontiguousarray(self.new_of_old, dtype=np.int32)
+        rs = np.ascontiguousarray(self.row_starts, dtype=np.int32)
+        handle.check(handle.lib.tls_set_row_partition(handle.ctx, nofo.size, _lib.ptr(nofo),
+                                                      self.shard.nranks, _lib.ptr(rs), self.rank))
+
+    def install(self, handle, csr, maps, one_level):
+        """Exchange the needed-row lists and hand the halo / reverse-halo plans to the library."""
+        import torch
+        needs_me = needed_rows(csr, maps, self.slabs[self.rank], self.new_of_old, self.r0, self.r1)
+        dev = torch.device("cuda", handle.device)
+        parts = self.shard.coll.allgather_list(torch.as_tensor(needs_me, dtype=torch.int64, device=dev))
+        needs = [p.cpu().numpy() for p in parts]
+        peers, send, recv = halo_lists(needs, self.rank, self.row_starts)
+        i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)  # noqa: E731
+        cat = lambda xs: i32(np.concatenate(xs) if xs else np.zeros(0))  # noqa: E731
+        pe, sc, sr, rc, rr = (i32(peers), i32([x.size for x in send]), cat(send),
+                              i32([x.size for x in recv]), cat(recv))
+        handle.check(handle.lib.tls_set_halo(handle.ctx, pe.size, _lib.ptr(pe), _lib.ptr(sc), _lib.ptr(sr),
+                                             _lib.ptr(rc), _lib.ptr(rr)))
+        self.halo_rows = int(rr.size)
+        if one_level == "asm":
+            rp, rs, rw = remote_contributions(maps, self.slabs, self.rank, self.new_of_old, self.row_starts)
+        else:
+            rp, rs, rw = [], [], []
+        p2, c2, s2, w2 = i32(rp), i32([x.size for x in rs]), cat(rs), cat(rw)
+        handle.check(handle.lib.tls_set_remote_contrib(handle.ctx, p2.size, _lib.ptr(p2), _lib.ptr(c2),
+                                                       _lib.ptr(s2), _lib.ptr(w2)))
+        self.remote_rows = int(w2.size)
 
 
 class TorchCollective:

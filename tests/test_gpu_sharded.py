@@ -1,7 +1,9 @@
 """Sharded path validated on ONE GPU: R ranks in one process, each with its own
-library handle owning a slab of subdomains, exchanging through the in-process group transport
-(same schedule as NCCL: rank-partial prolongation + one sum all-reduce per apply stage).
-Results must equal the single-handle path and be identical on every rank."""
+library handle owning a slab of subdomains and its rows (renumbered rank by rank), exchanging
+through the in-process group transport (same schedule as NCCL: halo of ghost rows, reverse halo
+of ASM overlap contributions, sum all-reduces of dot partials and of Z^T r).  Applies agree with
+the single-handle path to rounding (the setup batches differ per rank, nothing else: same row
+sums, same prolongation order); solves match the reference and are identical on every rank."""
 
 import numpy as np
 import pytest
@@ -22,24 +24,34 @@ def B():
     return mod
 
 
-def _sharded_run(B, name, nranks, solve):
+def _sharded_run(B, name, nranks, solve, **kw):
     from paper_2401_03915_b200.distributed import LocalGroup
     d = dict(golden(name))  # materialise: NpzFile is not thread-safe
     a = golden_csr(d)
     grp = LocalGroup(nranks)
+    opts = dict(overlap=int(d["overlap"]), owner=d["owner"], coarse=str(d["coarse"]),
+                n_modes=int(d["n_modes"]))
+    opts.update(kw)
 
     def body(shard):
         stream = torch.cuda.Stream()
         with torch.cuda.stream(stream):
             mat = B.SparseMat(a, symmetric=bool(d["symmetric"]))
-            pre = B.setup(mat, int(d["n_sub"]), overlap=int(d["overlap"]), owner=d["owner"],
-                          coarse=str(d["coarse"]), n_modes=int(d["n_modes"]), shard=shard)
+            pre = B.setup(mat, int(d["n_sub"]), shard=shard, **opts)
             z = pre.apply(d["r"][0])
+            z1 = pre.apply_one_level(d["r"][0])
             x, rep = solve(B, mat, pre, d)
             stream.synchronize()
-            return pre.report, (shard.lo, shard.hi), z, x, rep
+            return pre.report, (shard.lo, shard.hi), z, x, rep, z1
 
-    return d, a, grp.run(body)
+    res = grp.run(body)
+    mat = B.SparseMat(a, symmetric=bool(d["symmetric"]))
+    single = B.setup(mat, int(d["n_sub"]), **opts)
+    zs, z1s = single.apply(d["r"][0]), single.apply_one_level(d["r"][0])
+    for r in res:  # same operator as one handle (setup batches differ: rounding-level only)
+        np.testing.assert_allclose(r[2], zs, rtol=0, atol=1e-12 * np.abs(zs).max())
+        np.testing.assert_allclose(r[5], z1s, rtol=0, atol=1e-12 * np.abs(z1s).max())
+    return d, a, res
 
 
 def _pcg(B, mat, pre, d):
@@ -56,7 +68,7 @@ def test_sharded_additive_pcg_matches_single(B, nranks):
     slabs = [r[1] for r in res]
     assert slabs[0][0] == 0 and slabs[-1][1] == int(d["n_sub"])
     assert all(x[1] == y[0] for x, y in zip(slabs, slabs[1:]))
-    for report, _, z, x, rep in res:
+    for report, _, z, x, rep, _z1 in res:
         assert report.mode_counts == tuple(d["mode_counts"]) and report.n_coarse == int(d["n_coarse"])
         np.testing.assert_allclose(z, d["z"][0], rtol=0, atol=1e-10 * np.abs(d["z"][0]).max())
         assert abs(rep.iterations - int(d["iterations"])) <= 1 and rep.converged
@@ -68,8 +80,50 @@ def test_sharded_additive_pcg_matches_single(B, nranks):
 
 def test_sharded_deflated_gmres_matches_single(B):
     d, a, res = _sharded_run(B, "cfg3_m64", 2, _gmres)
-    for report, _, z, x, rep in res:
+    for report, _, z, x, rep, _z1 in res:
         np.testing.assert_allclose(z, d["z"][0], rtol=0, atol=1e-10 * np.abs(d["z"][0]).max())
         assert abs(rep.iterations - int(d["iterations"])) <= 1 and rep.converged
         np.testing.assert_allclose(x, d["x"], rtol=0, atol=1e-8 * np.abs(d["x"]).max())
     assert np.array_equal(res[0][3], res[1][3])
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_sharded_one_level_asm_reverse_halo(B, nranks):
+    """coarse='none' ASM: every overlap row receives contributions from other ranks' subdomains
+    through the reverse halo; the sum order must stay ascending in the subdomain id."""
+    d, a, res = _sharded_run(B, "cfg2_m24", nranks,
+                             lambda B, mat, pre, d: B.pcg(mat, pre, d["b"], tol=1e-8, maxit=300),
+                             coarse="none")
+    for other in res[1:]:
+        assert np.array_equal(other[3], res[0][3]) and other[4].iterations == res[0][4].iterations
+    x, rep = res[0][3], res[0][4]
+    assert rep.converged
+    b = d["b"]
+    assert np.linalg.norm(b - a @ x) / np.linalg.norm(b) < 1e-8 * 1.01
+
+
+def test_sharded_callback_and_spmv(B):
+    """host-loop path (callback) and the SpMV entry point in caller numbering."""
+    from paper_2401_03915_b200.distributed import LocalGroup
+    d = dict(golden("cfg2_m24"))
+    a = golden_csr(d)
+    grp = LocalGroup(2)
+    v = np.random.default_rng(5).standard_normal(a.shape[0])
+
+    def body(shard):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            mat = B.SparseMat(a, symmetric=True)
+            pre = B.setup(mat, int(d["n_sub"]), overlap=int(d["overlap"]), owner=d["owner"],
+                          n_modes=int(d["n_modes"]), shard=shard)
+            seen = []
+            x, rep = B.pcg(mat, pre, d["b"], tol=float(d["tol"]), callback=lambda it, xk: seen.append(it))
+            y = pre.matvec(v)
+            stream.synchronize()
+            return seen, x, rep, y
+
+    res = grp.run(body)
+    for seen, x, rep, y in res:
+        assert seen == list(range(1, rep.iterations + 1))
+        np.testing.assert_allclose(x, d["x"], rtol=0, atol=1e-8 * np.abs(d["x"]).max())
+        assert np.array_equal(y, a @ v) or np.abs(y - a @ v).max() <= 1e-12 * np.abs(a @ v).max()
