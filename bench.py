@@ -104,6 +104,22 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+class _StdoutToStderr:
+    """Native libraries (MAGMA inside torch.linalg) print banners on fd 1; stdout must carry only
+    the JSON line, so fd 1 points at stderr while they run."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self._saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self._saved, 1)
+        os.close(self._saved)
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -128,6 +144,34 @@ def _traffic_from_profile(config_id, kernel):
             return float(json.load(fh)["dram_bytes_per_launch"])
     except Exception:
         return None
+
+
+def iteration_bytes(cfg, a, pre, local_bytes):
+    """Algorithmic HBM bytes of ONE Krylov iteration (SURVEY.md §8d formulas; the local solve
+    counts the factor bytes its sweeps must stream -- band profile read twice for Cholesky, L
+    and U once each for LU -- instead of dense blocks).  Every operand read once, every output
+    written once, per operator application:
+      SpMV   12 nnz + 4 (n+1) + 16 n
+      local  factor bytes + 24 sum(n_i) + 8 n      (sweeps + gather/scatter)
+      coarse 16 sum(n_int,s k_s) + 24 n + A0^{-1} bytes (packed triangle if SPD)
+      PCG    SpMV + local + coarse + 80 n + (SpMV + 24 n) / 25   (replacement every 25)
+      GMRES(m), deflated: 3 SpMV + local + 2 coarse + 8 n (m+1) + 72 n   (CGS2 averaged)"""
+    n, nnz = a.shape[0], int(a.nnz)
+    sum_ni = float(sum(m.n_local for m in pre.maps))
+    spmv = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n
+    local = float(local_bytes) + 8.0 * sum_ni + 8.0 * n
+    coarse = 0.0
+    nC = pre.report.n_coarse
+    if nC and pre.coarse is not None:
+        zk = float(sum(m.interior.size * k for m, k in zip(pre.maps, pre.coarse.column_counts())))
+        a0 = 8.0 * nC * (nC + 1) / 2 if pre.report.symmetric else 8.0 * nC * nC
+        coarse = 16.0 * zk + 24.0 * n + a0
+    if cfg.solver == "pcg":
+        total = spmv + local + coarse + 80.0 * n + (spmv + 24.0 * n) / 25.0
+    else:
+        m = cfg.restart or 50
+        total = 3.0 * spmv + local + 2.0 * coarse + 8.0 * n * (m + 1) + 72.0 * n
+    return total, {"spmv": spmv, "local": local, "coarse": coarse}
 
 
 # --------------------------------------------------------------------------------------------
@@ -266,8 +310,9 @@ def main():
         from paper_2401_03915_b200.distributed import world_shard
         shard = world_shard()
     t0 = time.perf_counter()
-    pre = B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes, shard=shard)
-    torch.cuda.synchronize()
+    with _StdoutToStderr():
+        pre = B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes, shard=shard)
+        torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     n = a.shape[0]
     b_host = cfg.rhs(n)
@@ -323,6 +368,14 @@ def main():
     peak, peak_kind = _peaks()
     achieved = algo.value / (avg_ms.value * 1e-3) / 1e9
     traffic = _traffic_from_profile(cfg.cid, "band" if pre.local_kind == "band" else "symv")
+    # whole-loop roofline: algorithmic bytes of one iteration x iterations/s
+    if pre.local_kind != "inverse":
+        local_algo = algo.value  # band factor bytes streamed + 16 sum(n_i)
+    else:  # inverse tiles (the profiled launch also covers the coarse block): packed A_ii^{-1}
+        ns = np.array([m.n_local for m in pre.maps], dtype=np.float64)
+        local_algo = float((8.0 * ns * (ns + 1) / 2 if sym else 8.0 * ns * ns).sum() + 16.0 * ns.sum())
+    it_bytes, it_parts = iteration_bytes(cfg, a, pre, local_algo)
+    loop_ach = it_bytes * value / 1e9
     # true residual of the final solve
     xr = x.cpu().numpy()
     true_res = float(np.linalg.norm(b_host - a @ xr) / np.linalg.norm(b_host))
@@ -351,6 +404,10 @@ def main():
                                 if pre.local_kind == "band" else
                                 "k_symv_tiles (batched local + coarse inverse tiles)"),
                      "algorithmic_bytes_per_launch": algo.value, "avg_launch_ms": avg_ms.value},
+        "loop_roofline": {"bound": "hbm", "achieved": loop_ach, "peak": peak * world, "unit": "GB/s",
+                          "frac": loop_ach / (peak * world), "bytes_per_iteration": it_bytes,
+                          "bytes_split": it_parts,
+                          "note": "whole preconditioned iteration (all kernels), bench.iteration_bytes"},
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
