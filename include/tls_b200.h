@@ -42,7 +42,9 @@ typedef enum {
   TLS_ERR_ARG = 6,        /* invalid argument / unsupported option                         */
   TLS_ERR_STATE = 7,      /* call order violated (e.g. apply before finalize)              */
   TLS_ERR_CUDA = 8,       /* CUDA runtime failure                                          */
-  TLS_ERR_OOM = 9         /* device allocation failed                                      */
+  TLS_ERR_OOM = 9,        /* device allocation failed                                      */
+  TLS_ERR_FORMAT = 10,    /* MatrixMarketError(lineno, message)  (src/sparsemat.py:20-25)  */
+  TLS_ERR_IO = 11         /* file could not be opened / written (OSError)                  */
 } tls_code;
 
 typedef enum { TLS_ASM = 0, TLS_RAS = 1 } tls_one_level;                       /* src/precond.py:34 */
@@ -191,6 +193,25 @@ int32_t tls_comm_init_group(tls_ctx* ctx, tls_group* g, int32_t rank);
  * the algorithmic bytes one launch of it must move. */
 int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms,
                                 double* algorithmic_bytes, void* stream);
+
+/* ---- Matrix Market ingest / output (src/sparsemat.py:201-372).
+ * Host-side, multithreaded.  tls_mm_parse / tls_mm_load parse text / a file (nthreads <= 0: all
+ * host threads) with the reference's dialect, validation order and error texts; on
+ * TLS_ERR_FORMAT the handle carries (line, message) of MatrixMarketError.  On success
+ * tls_mm_info gives the sizes and tls_mm_export copies the canonical CSR (sorted columns,
+ * duplicates summed, explicit zeros of coordinate files kept, symmetric lower storage expanded;
+ * array zeros dropped) into caller buffers of nrows+1 / nnz / nnz elements, ready for
+ * tls_matrix_upload.  Always release the handle with tls_mm_free (also after an error).
+ * tls_mm_write writes general coordinate format with %.17g values (write_matrix_market). */
+typedef struct tls_mm tls_mm;
+int32_t tls_mm_parse(const char* text, int64_t len, int32_t nthreads, tls_mm** out);
+int32_t tls_mm_load(const char* path, int32_t nthreads, tls_mm** out);
+int32_t tls_mm_info(const tls_mm* mm, int64_t* nrows, int64_t* ncols, int64_t* nnz, int32_t* symmetric,
+                    int64_t* err_line, const char** err_msg);
+int32_t tls_mm_export(const tls_mm* mm, int64_t* indptr, int32_t* indices, double* data);
+void tls_mm_free(tls_mm* mm);
+int32_t tls_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* indptr,
+                     const int32_t* indices, const double* data, int32_t nthreads);
 
 #ifdef __cplusplus
 }

@@ -18,6 +18,17 @@ from .partition import (
     partition_graph,
 )
 from .sparsemat import DENSE_GUARD, SparseMat, as_sparsemat, symmetrized_graph
+from .mmio import (
+    MatrixMarketError,
+    load_matrix_market,
+    load_vector,
+    read_matrix_market,
+    read_vector,
+    save_matrix_market,
+    save_vector,
+    write_matrix_market,
+    write_vector,
+)
 from .precond import Preconditioner, SetupReport, setup
 from .krylov import SolveReport, gmres, pcg
 from . import problems

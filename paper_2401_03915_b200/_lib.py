@@ -23,6 +23,8 @@ TLS_ERR_ARG = 6
 TLS_ERR_STATE = 7
 TLS_ERR_CUDA = 8
 TLS_ERR_OOM = 9
+TLS_ERR_FORMAT = 10
+TLS_ERR_IO = 11
 
 ONE_LEVEL = {"asm": 0, "ras": 1}
 COMBINE = {"none": 0, "additive": 1, "deflated": 2}
@@ -68,6 +70,13 @@ SIGNATURES = {
     "tls_set_halo": (_I32, [_P, _I32, _P, _P, _P, _P, _P]),
     "tls_set_remote_contrib": (_I32, [_P, _I32, _P, _P, _P, _P]),
     "tls_set_local_kind": (_I32, [_P, _I32]),
+    "tls_mm_parse": (_I32, [C.c_char_p, _I64, _I32, C.POINTER(_P)]),
+    "tls_mm_load": (_I32, [C.c_char_p, _I32, C.POINTER(_P)]),
+    "tls_mm_info": (_I32, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I32),
+                           C.POINTER(_I64), C.POINTER(C.c_char_p)]),
+    "tls_mm_export": (_I32, [_P, _P, _P, _P]),
+    "tls_mm_free": (None, [_P]),
+    "tls_mm_write": (_I32, [C.c_char_p, _I64, _I64, _P, _P, _P, _I32]),
     "tls_store_local_band": (_I32, [_P, _I32, _I32, _P, _I64, _P, _I32, _P, _P, _P]),
     "tls_store_local_band_lu": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P, _I32, _P, _P, _P, _P, _P]),
     "tls_nccl_unique_id": (_I32, [_P, _I32]),

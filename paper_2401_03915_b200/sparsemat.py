@@ -38,6 +38,18 @@ class SparseMat:
         self._handle = None
 
     @classmethod
+    def _canonical(cls, csr, symmetric=False):
+        """Wrap a CSR that is already canonical (sorted, duplicate-free, finite; symmetric by
+        construction when flagged) -- the native Matrix Market reader's output."""
+        self = cls.__new__(cls)
+        self._csr = csr
+        self.symmetric = bool(symmetric)
+        for arr in (csr.data, csr.indices, csr.indptr):
+            arr.flags.writeable = False
+        self._handle = None
+        return self
+
+    @classmethod
     def from_coo(cls, nrows, ncols, rows, cols, vals, symmetric=False):
         rows = np.asarray(rows, dtype=np.int64)
         cols = np.asarray(cols, dtype=np.int64)
