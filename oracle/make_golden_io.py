@@ -1,6 +1,7 @@
 """Golden fixtures for the file boundary (Matrix Market) by running the REFERENCE itself.
 
-    python oracle/make_golden_io.py     # writes tests/golden/mm_cases.json
+    python oracle/make_golden_io.py                 # writes tests/golden/mm_cases.json
+    python oracle/make_golden_io.py --experiments   # writes tests/golden/experiments.json
 
 Test infrastructure only (this container: /root/reference is imported read-only).  Every case is
 a Matrix Market / vector text and what the reference's ``read_matrix_market`` / ``read_vector``
@@ -146,5 +147,56 @@ def main():
     print(f"{len(cases)} matrix cases, {len(vec_cases)} vector cases -> {OUT}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--experiments" not in sys.argv:
     main()
+
+
+# -- run_experiment / CLI (src/harness.py:326-371) ---------------------------------------------
+EXP_OUT = os.path.join(REPO, "tests", "golden", "experiments.json")
+
+EXPERIMENTS = [
+    dict(kind="poisson2d", m=24, n_subdomains=4, overlap=2, tau=0.1, solver="cg"),
+    dict(kind="hetero2d", m=24, n_subdomains=9, overlap=1, tau=0.1, solver="cg", seed=3),
+    dict(kind="advection2d", m=24, n_subdomains=4, overlap=2, tau=0.1, solver="gmres"),
+    dict(kind="poisson3d", m=9, n_subdomains=8, overlap=1, tau=0.2, solver="cg", coarse="gevp",
+         one_level="ras", combine="deflated"),
+    dict(kind="poisson2d", m=24, n_subdomains=4, overlap=1, tau=0.1, solver="gmres", coarse="svd"),
+    dict(kind="poisson2d", m=24, n_subdomains=4, overlap=1, solver="cg", coarse="none", maxit=60),
+    dict(matrix="mm", rhs="vec", n_subdomains=4, overlap=1, tau=0.1, solver="cg"),
+]
+
+
+def experiments():
+    import tempfile
+    from tlschwarz import harness as Hh
+    out = []
+    tmp = tempfile.mkdtemp()
+    mat, _ = T.generate(T.ProblemSpec("hetero-diffusion2d", 22, channel_seed=5))
+    mm_text = SM.write_matrix_market(mat)
+    rhs = np.random.default_rng(9).uniform(-1, 1, mat.nrows)
+    vec_text = SM.write_vector(rhs)
+    for e in EXPERIMENTS:
+        kw = dict(e)
+        if kw.pop("matrix", None):
+            kw.pop("rhs")
+            mp, vp = os.path.join(tmp, "a.mtx"), os.path.join(tmp, "b.txt")
+            with open(mp, "w") as fh:
+                fh.write(mm_text)
+            with open(vp, "w") as fh:
+                fh.write(vec_text)
+            kw.update(matrix_path=mp, rhs_path=vp)
+        res = Hh.run_experiment(Hh.ExperimentConfig(report_path=os.path.join(tmp, "r.txt"), **kw))
+        with open(os.path.join(tmp, "r.txt.history")) as fh:
+            hist = fh.read()
+        out.append({"config": e, "report": res.precond.report.to_text(),
+                    "iterations": res.solve_report.iterations, "converged": bool(res.solve_report.converged),
+                    "residuals": [float(v) for v in res.solve_report.residuals],
+                    "cond_estimate": res.solve_report.cond_estimate, "x": [float(v) for v in res.x],
+                    "history_lines": len(hist.splitlines()), "bound_check": res.bound_check is not None})
+    with open(EXP_OUT, "w") as fh:
+        json.dump({"mm_text": mm_text, "vec_text": vec_text, "cases": out}, fh)
+    print(f"{len(out)} experiments -> {EXP_OUT}")
+
+
+if __name__ == "__main__" and "--experiments" in sys.argv:
+    experiments()

@@ -1,0 +1,68 @@
+"""run_experiment / CLI on the GPU backend vs the reference's own runs.
+
+tests/golden/experiments.json holds the reference's run_experiment results (generated problems of
+every kind, the deflated / svd / none variants, a Matrix Market matrix + rhs file pair): the
+SetupReport text must be identical, iterations and convergence equal, residual histories and the
+condition estimate within tolerance, iterates within 1e-8 relative."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "experiments.json")
+
+
+@pytest.fixture(scope="module")
+def H():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2401_03915_b200 import build
+    build.build()
+    from paper_2401_03915_b200 import harness
+    return harness
+
+
+def _config(H, e, tmp_path, gold):
+    kw = dict(e)
+    if kw.pop("matrix", None):
+        kw.pop("rhs")
+        mp, vp = tmp_path / "a.mtx", tmp_path / "b.txt"
+        mp.write_text(gold["mm_text"])
+        vp.write_text(gold["vec_text"])
+        kw.update(matrix_path=str(mp), rhs_path=str(vp))
+    return H.ExperimentConfig(report_path=str(tmp_path / "r.txt"), **kw)
+
+
+def test_run_experiment_matches_reference(H, tmp_path):
+    with open(GOLD) as fh:
+        gold = json.load(fh)
+    for case in gold["cases"]:
+        res = H.run_experiment(_config(H, case["config"], tmp_path, gold))
+        assert res.precond.report.to_text() == case["report"], case["config"]
+        rep = res.solve_report
+        assert rep.iterations == case["iterations"] and rep.converged == case["converged"], case["config"]
+        np.testing.assert_allclose(rep.residuals, case["residuals"], rtol=0, atol=1e-10)
+        if case["cond_estimate"] is not None:
+            assert abs(rep.cond_estimate - case["cond_estimate"]) <= 1e-6 * case["cond_estimate"]
+        x = np.asarray(case["x"])
+        np.testing.assert_allclose(res.x, x, rtol=0, atol=1e-8 * np.abs(x).max())
+        text = (tmp_path / "r.txt").read_text()
+        assert text == res.report_text and text.startswith(case["report"])
+        hist = (tmp_path / "r.txt.history").read_text().splitlines()
+        assert len(hist) == case["history_lines"] and hist[0] == "0 1"
+
+
+def test_cli_exit_codes(H, tmp_path, capsys):
+    from paper_2401_03915_b200 import cli
+    rc = cli.main(["--kind", "poisson2d", "--m", "20", "--N", "4", "--report", str(tmp_path / "c.txt")])
+    out = capsys.readouterr().out
+    assert rc == 0 and "converged = True" in out and "subdomains = 4" in out
+    rc = cli.main(["--kind", "poisson2d", "--m", "20", "--N", "4", "--coarse", "none", "--maxit", "2"])
+    assert rc == 3
+    rc = cli.main(["--matrix", str(tmp_path / "missing.mtx")])
+    assert rc == 1 and "error_type = " in capsys.readouterr().err

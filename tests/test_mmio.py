@@ -95,3 +95,23 @@ def test_large_parallel_parse_equals_serial(lib, tmp_path):
 def test_missing_file_raises_oserror(lib, tmp_path):
     with pytest.raises(OSError):
         P.load_matrix_market(str(tmp_path / "nope.mtx"))
+
+
+def test_cli_usage_error_without_gpu(capsys):
+    from paper_2401_03915_b200 import cli
+    assert cli.main([]) == 2
+    assert "need --matrix or --kind" in capsys.readouterr().err
+    args = cli.build_parser().parse_args(["--kind", "hetero2d", "--N", "9", "--delta", "1", "--one-level", "ras"])
+    cfg = cli.config_from_args(args)
+    assert (cfg.kind, cfg.n_subdomains, cfg.overlap, cfg.one_level, cfg.solver) == ("hetero2d", 9, 1, "ras", "cg")
+
+
+def test_generate_matches_reference_fixture_kinds():
+    """generate(): the reference's four model problems, rhs = A * ones on the host."""
+    from paper_2401_03915_b200 import harness as H
+    with pytest.raises(ValueError):
+        H.ProblemSpec("poisson4d", 8)
+    with pytest.raises(ValueError):
+        H.ProblemSpec("poisson2d", 2)
+    m, b = H.generate(H.ProblemSpec("advection2d", 6))
+    assert not m.symmetric and np.array_equal(b, m.scipy() @ np.ones(36))
