@@ -2,6 +2,7 @@
 
     python oracle/make_golden_io.py                 # writes tests/golden/mm_cases.json
     python oracle/make_golden_io.py --experiments   # writes tests/golden/experiments.json
+    python oracle/make_golden_io.py --pou           # writes tests/golden/pou.npz
 
 Test infrastructure only (this container: /root/reference is imported read-only).  Every case is
 a Matrix Market / vector text and what the reference's ``read_matrix_market`` / ``read_vector``
@@ -147,7 +148,7 @@ def main():
     print(f"{len(cases)} matrix cases, {len(vec_cases)} vector cases -> {OUT}")
 
 
-if __name__ == "__main__" and "--experiments" not in sys.argv:
+if __name__ == "__main__" and not {"--experiments", "--pou"} & set(sys.argv):
     main()
 
 
@@ -200,3 +201,50 @@ def experiments():
 
 if __name__ == "__main__" and "--experiments" in sys.argv:
     experiments()
+
+
+# -- partition-of-unity modes (src/spectral.py:93-108) -------------------
+POU_OUT = os.path.join(REPO, "tests", "golden", "pou.npz")
+
+POU_CASES = [
+    ("poisson2d", 16, 4, 2, 0.1, 1.5, "gevp"),
+    ("hetero-diffusion2d", 16, 4, 1, 0.1, 1.3, "gevp"),
+    ("poisson2d", 20, 9, 1, 0.1, 1.2, "full"),
+    ("poisson3d", 8, 8, 1, 0.2, 1.25, "gevp"),
+    ("poisson2d", 16, 4, 2, 0.1, 1.5, "svd"),
+    ("poisson2d", 16, 4, 1, 0.1, 50.0, "gevp"),   # threshold above every PoU value: none added
+]
+
+
+def pou():
+    arrs = {}
+    rng = np.random.default_rng(21)
+    for c, (kind, m, N, d, tau, nu, coarse) in enumerate(POU_CASES):
+        mat, b = T.generate(T.ProblemSpec(kind, m))
+        pre = T.setup(mat, N, overlap=d, tau=tau, nu=nu, coarse=coarse)
+        csr = mat.scipy()
+        r = rng.standard_normal(mat.nrows)
+        x, rep = T.pcg(mat, pre, b, tol=1e-10)
+        pou_counts = [pb.n_selected for pb in pre.pou_bases]
+        gaps = []
+        for pb in pre.pou_bases:  # distance of the threshold to the nearest PoU value
+            v = pb.all_values
+            gaps.append(float(np.min(np.abs(v - nu)) / nu))
+        Z = pre.coarse.basis.scipy().toarray()
+        cond_a0 = float(np.linalg.cond(Z.T @ (csr @ Z)))
+        p = f"c{c}_"
+        arrs.update({p + "cond_a0": cond_a0, p + "indptr": csr.indptr, p + "indices": csr.indices, p + "data": csr.data,
+                     p + "params": np.array([m, N, d, tau, nu]), p + "kind": np.array(kind),
+                     p + "coarse": np.array(coarse), p + "mode_counts": np.array(pre.report.mode_counts),
+                     p + "pou_counts": np.array(pou_counts), p + "n_coarse": pre.report.n_coarse,
+                     p + "r": r, p + "z": pre.apply(r), p + "b": b, p + "x": x,
+                     p + "iterations": rep.iterations, p + "residuals": rep.residuals,
+                     p + "min_gap": min(gaps)})
+        print(kind, coarse, nu, pre.report.mode_counts, pou_counts, rep.iterations, f"gap {min(gaps):.2e}",
+              f"cond(A0) {cond_a0:.2e}")
+    arrs["n_cases"] = len(POU_CASES)
+    np.savez_compressed(POU_OUT, **arrs)
+
+
+if __name__ == "__main__" and "--pou" in sys.argv:
+    pou()

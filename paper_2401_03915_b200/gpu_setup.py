@@ -170,6 +170,49 @@ def _cut_gap(values, keep):
     return float((values[keep[-1]] - values[keep[-1] + 1]) / values[keep[-1]])
 
 
+def _pou_columns(torch, A, n, ni, nu):
+    """Partition-of-unity modes (src/spectral.py:93-108, added by src/coarse.py:81-82) on the
+    device: the m x m pencil (D A D) u = lam A u with D = diag(pou_mask) reduces, for lam != 0,
+    to the n_int pencil A_II y = lam S_I y with S_I = A_II - A_IG A_GG^{-1} A_GI (the interior
+    Schur complement) and u = [y; -A_GG^{-1} A_GI y]; y^T S_I y = u^T A u = 1 is the reference's
+    normalisation.  Values descending, kept when lam > nu (1 + TIE_GUARD), signs fixed on the full
+    u, columns = D u = y (interior rows)."""
+    dev = A.device
+    if ni == n:  # no overlap rows: S_I = A_II, every lam = 1 <= nu
+        return torch.zeros((ni, 0), dtype=torch.float64, device=dev)
+    AII = A[:ni, :ni]
+    AIG = A[:ni, ni:n]
+    AGG = A[ni:n, ni:n]
+    LG = torch.linalg.cholesky(0.5 * (AGG + AGG.mT))
+    X = torch.cholesky_solve(AIG.mT.contiguous(), LG)        # A_GG^{-1} A_GI
+    S = AII - AIG @ X
+    LS = torch.linalg.cholesky(0.5 * (S + S.mT))
+    Y = torch.linalg.solve_triangular(LS, AII, upper=False)
+    C = torch.linalg.solve_triangular(LS, Y.mT, upper=False)
+    w, Q = torch.linalg.eigh(0.5 * (C + C.mT))
+    w = torch.flip(w, dims=[0]).cpu().numpy()
+    keep = np.nonzero(w > nu * (1.0 + TIE_GUARD))[0]
+    if keep.size == 0:
+        return torch.zeros((ni, 0), dtype=torch.float64, device=dev)
+    Q = torch.flip(Q, dims=[1])[:, torch.as_tensor(keep, device=dev)]
+    Yv = torch.linalg.solve_triangular(LS.mT, Q, upper=True)
+    U = _fix_signs(torch, torch.cat([Yv, -(X @ Yv)], dim=0))
+    return U[:ni].contiguous()
+
+
+def _with_pou(torch, Z, A, n, ni, nu):
+    """[harmonic columns, PoU columns] (src/coarse.py:72-84), all-zero columns dropped
+    (src/coarse.py:99-103)."""
+    if nu is None:
+        return Z
+    P = _pou_columns(torch, A, n, ni, nu)
+    if P.shape[1] == 0:
+        return Z
+    Z = torch.cat([Z, P], dim=1) if Z.shape[1] else P
+    nz = torch.any(Z != 0, dim=0)
+    return Z if bool(nz.all()) else Z[:, nz].contiguous()
+
+
 def _subdomain_columns(torch, kind, A, Bring, n, ni, nin, tau, n_modes):
     """Coarse columns (n_int x k, device) of one subdomain, and the selection's cut gap.
 
@@ -738,7 +781,7 @@ def _make_room(torch, dev, nbytes, slack=1 << 29):
 
 
 def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_modes, drop_tol,
-                           batch=None, mem_fraction=0.35, shard=None, local="auto", graph=None):
+                           batch=None, mem_fraction=0.35, shard=None, local="auto", graph=None, nu=None):
     """Run steps 1-5 into ``handle`` (this rank's slab when ``shard``); returns CoarseData or None.
 
     ``local``: "inverse" (packed A_ii^{-1} tiles), "band" (banded Cholesky factors; SPD only) or
@@ -851,6 +894,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                         nz = torch.any(Z != 0, dim=0)
                         if not bool(nz.all()):
                             Z = Z[:, nz].contiguous()
+                    Z = _with_pou(torch, Z, A[b], n, ni, nu)
                     z_dev[s] = Z
                     w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
             del A, LU, piv
@@ -891,6 +935,9 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                         if not bool(nz.all()):
                             Z = Z[:, nz].contiguous()
                         W = A[b, :n, :ni] @ Z
+                    if nu is not None:
+                        Z = _with_pou(torch, Z, A[b], n, ni, nu)
+                        W = A[b, :n, :ni] @ Z if Z.shape[1] else None
                     z_dev[s] = Z
                     w_dev[s] = W if Z.shape[1] else None
             del A, L, Dinv
@@ -928,6 +975,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                     nz = torch.any(Z != 0, dim=0)
                     if not bool(nz.all()):
                         Z = Z[:, nz].contiguous()
+                Z = _with_pou(torch, Z, A[b], n, ni, nu)
                 z_dev[s] = Z
                 w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
         del A, Binv

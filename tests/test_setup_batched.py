@@ -114,3 +114,34 @@ def test_band_cholesky_matches_dense_and_flags_indefinite():
     B[1, 70, 70] = -10.0
     _, _, _, _, info, _, _ = G._band_factor(torch, B, perm_list, n_list, ld)
     assert int(info[0]) == 0 and int(info[1]) > 0 and int(info[2]) == 0
+
+
+def test_pou_columns_equal_full_pencil():
+    """_pou_columns (reduced n_int pencil with the interior Schur complement) = the reference's
+    m x m pencil (D A D) u = lam A u (src/spectral.py:93-108): same selected values, same
+    columns D u (A-normalised, sign-fixed on the full vector)."""
+    import scipy.linalg as sla
+    from paper_2401_03915_b200.gpu_setup import _pou_columns
+    from paper_2401_03915_b200 import problems as PR
+    from paper_2401_03915_b200.partition import Partition, extend_overlap, symmetrized_graph
+    a = PR.poisson2d(12)
+    owner = PR.tile_owner_2d(12, 6)
+    maps = extend_overlap(symmetrized_graph(a, symmetric=True), Partition(4, owner), 2)
+    for smap in maps:
+        idx = smap.indices
+        A = a[idx][:, idx].toarray()
+        n, ni = A.shape[0], smap.interior.size
+        d = np.zeros(n)
+        d[:ni] = 1.0
+        vals, vecs = sla.eigh(A * np.outer(d, d), A)
+        vals, vecs = vals[::-1], vecs[:, ::-1]
+        nu = 1.3
+        keep = vals > nu * (1 + 1e-12)
+        ref = vecs[:, keep]
+        for j in range(ref.shape[1]):
+            k = int(np.argmax(np.abs(ref[:, j])))
+            if ref[k, j] < 0:
+                ref[:, j] = -ref[:, j]
+        got = _pou_columns(torch, torch.as_tensor(A), n, ni, nu).numpy()
+        assert got.shape[1] == ref.shape[1] and got.shape[1] > 0
+        np.testing.assert_allclose(got, ref[:ni], rtol=0, atol=1e-10 * np.abs(ref).max())
