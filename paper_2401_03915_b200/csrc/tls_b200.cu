@@ -119,6 +119,7 @@ struct tls_ctx {
   std::vector<int> h_perm_in;         // LU: local index gathered into input position p (row pivots)
   double band_bytes = 0.0;            // stored factor bytes (read twice per apply)
   size_t band_smem = 0;
+  int band_pf = 2;                    // L2 prefetch distance of k_band_solve (items)
   // ---- sharding: this handle owns global subdomains [own_lo, own_hi) and the
   // rows [r0, r1) of the internal numbering (rows renumbered rank by rank: nofo[g] = internal id
   // of caller row g; identity and [0, n) on one GPU)
@@ -248,7 +249,7 @@ enum { L_LOCAL = 0, L_COARSE = 1, L_ALL = 2 };
 
 static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done) {
   if (ctx->local_kind >= 1 && which != L_COARSE) {
-    k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done);
+    k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf);
     CKL();
     if (which == L_LOCAL) return TLS_OK;
     which = L_COARSE;
@@ -680,6 +681,12 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     ctx->band_smem = sizeof(double) * ((size_t)maxnb * TT + 8 * TT + TT);
     static size_t smem_set = 0;
     CK(raise_smem((const void*)k_band_solve, ctx->band_smem, smem_set));
+    // prefetch distance: 2 items when >= 3 subdomain CTAs share an SM, deeper otherwise
+    ctx->band_pf = n_sub >= 3 * 148 ? 2 : 4;
+    if (const char* e = getenv("TLS_BAND_PF")) {
+      const int v = atoi(e);
+      if (v >= 1 && v <= 16) ctx->band_pf = v;
+    }
     ctx->h_perm.assign(tot, -1);
     ctx->h_perm_in.assign(ctx->local_kind == 2 ? tot : 0, -1);
     ctx->band_bytes = 0.0;
@@ -1506,7 +1513,7 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   for (int i = 0; i <= reps; ++i) {
     if (i == 1) CK(cudaEventRecord(e0, s));
     if (band)
-      k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr);
+      k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr, ctx->band_pf);
     else
       k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
     CKL();

@@ -872,9 +872,12 @@ __device__ __forceinline__ void prefetch_u_item(const BandDesc& b, int I, int j)
 // inverted diagonal tile, upper triangular: warp w's strip keeps rows 0 .. 8w+7
 __device__ __forceinline__ int udiag_strip_off(int w) { return 32 * w * w + 32 * w; }
 
+// pf: L2 prefetch distance in items (2 when >= 3 CTAs share an SM; deeper when few subdomains
+// leave SMs with 1-2 CTAs and so fewer bytes in flight)
 __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restrict__ bands,
                                                         const double* __restrict__ x,
-                                                        double* __restrict__ y, const int* done) {
+                                                        double* __restrict__ y, const int* done,
+                                                        int pf) {
   if (done && *done) return;
   extern __shared__ __align__(16) double sm[];
   const BandDesc b = bands[blockIdx.x];
@@ -886,6 +889,8 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   const int dlen = TT - 8 * warp;                    // rows stored in this warp's diagonal strip
   const bool drow = lane >= 4 * warp;                // rows 2l, 2l+1 inside the strip
   const int doff = diag_strip_off(warp) + (2 * lane - 8 * warp);
+  if (threadIdx.x == 0)
+    for (int j = 2; j < pf; ++j) prefetch_fwd_item(b, 0, j);  // items >= 2 of the stream head
   for (int i = threadIdx.x; i < npad; i += NTHR) v[i] = x[b.xoff + i];
   __syncthreads();
   // forward sweep: L u = x  (the factor is one contiguous stream in this order)
@@ -894,7 +899,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
     const int code = b.kcnt[I], K = code & 0xffff, fz = code >> 16;
     double ra0 = 0.0, ra1 = 0.0;
     for (int k = 0; k < K; ++k) {
-      if (threadIdx.x == 0) prefetch_fwd_item(b, I, k + 2);  // two items ahead, into L2
+      if (threadIdx.x == 0) prefetch_fwd_item(b, I, k + pf);  // pf items ahead, into L2
       if (k * 8 + warp < fz) continue;               // strip left of the band profile: zeros
       const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
       double2 w[8];
@@ -904,7 +909,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) { ra0 += w[kk].x * uj[kk]; ra1 += w[kk].y * uj[kk]; }
     }
-    if (threadIdx.x == 0) prefetch_fwd_item(b, I, K + 2);
+    if (threadIdx.x == 0) prefetch_fwd_item(b, I, K + pf);
     red[warp * TT + 2 * lane] = ra0;
     red[warp * TT + 2 * lane + 1] = ra1;
     __syncthreads();
@@ -948,7 +953,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
       const int code = b.ucnt[I], R = code & 0xffff, tz = code >> 16;
       double ra0 = 0.0, ra1 = 0.0;
       for (int k = 0; k < R; ++k) {
-        if (threadIdx.x == 0) prefetch_u_item(b, I, k + 2);
+        if (threadIdx.x == 0) prefetch_u_item(b, I, k + pf);
         if (k * 8 + warp >= 8 * R - tz) continue;    // strip right of the band profile: zeros
         const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
         double2 w[8];
@@ -958,7 +963,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) { ra0 += w[kk].x * yj[kk]; ra1 += w[kk].y * yj[kk]; }
       }
-      if (threadIdx.x == 0) prefetch_u_item(b, I, R + 2);
+      if (threadIdx.x == 0) prefetch_u_item(b, I, R + pf);
       red[warp * TT + 2 * lane] = ra0;
       red[warp * TT + 2 * lane + 1] = ra1;
       __syncthreads();
@@ -1000,7 +1005,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   for (int J = b.nb - 1; J >= 0; --J) {
     const double* blk = b.data + b.step_off[J];
     const int code = b.kcnt[J], K = code & 0xffff, fz = code >> 16;
-    if (threadIdx.x == 0) prefetch_bwd_item(b, J, 2);
+    if (threadIdx.x == 0) prefetch_bwd_item(b, J, pf);
     {
       const double u0 = v[J * TT + 2 * lane], u1 = v[J * TT + 2 * lane + 1];
       double cp[8];
@@ -1022,7 +1027,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
     }
     const double y0 = v[J * TT + 2 * lane], y1 = v[J * TT + 2 * lane + 1];
     for (int k = 0; k < K; ++k) {
-      if (threadIdx.x == 0) prefetch_bwd_item(b, J, k + 3);
+      if (threadIdx.x == 0) prefetch_bwd_item(b, J, k + 1 + pf);
       if (k * 8 + warp < fz) continue;
       const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
       double cp[8];
