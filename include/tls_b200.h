@@ -193,6 +193,11 @@ int32_t tls_comm_init_group(tls_ctx* ctx, tls_group* g, int32_t rank);
  * the algorithmic bytes one launch of it must move. */
 int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms,
                                 double* algorithmic_bytes, void* stream);
+/* in-graph timing of the band local-solve kernel inside real PCG / GMRES solves: on = 1
+ * re-captures the solve graphs with CUDA event nodes around each band-solve node (and resets);
+ * tls_kernel_timing returns the mean duration of the launches that did work. */
+int32_t tls_set_kernel_timing(tls_ctx* ctx, int32_t on);
+int32_t tls_kernel_timing(const tls_ctx* ctx, double* avg_ms, int64_t* count);
 
 /* ---- Matrix Market ingest / output (src/sparsemat.py:201-372).
  * Host-side, multithreaded.  tls_mm_parse / tls_mm_load parse text / a file (nthreads <= 0: all

@@ -65,6 +65,8 @@ SIGNATURES = {
     "tls_gmres": (_I32, [_P, _P, _P, _D, _I32, _I32, _I32, _P, C.POINTER(TlsStatus), ITER_CB, _P, _P]),
     "tls_report": (_I32, [_P, C.POINTER(_I64), C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I64)]),
     "tls_profile_local_solve": (_I32, [_P, _I32, C.POINTER(_D), C.POINTER(_D), _P]),
+    "tls_set_kernel_timing": (_I32, [_P, _I32]),
+    "tls_kernel_timing": (_I32, [_P, C.POINTER(_D), C.POINTER(_I64)]),
     "tls_set_owned_range": (_I32, [_P, _I32, _I32]),
     "tls_set_row_partition": (_I32, [_P, _I64, _P, _I32, _P, _I32]),
     "tls_set_halo": (_I32, [_P, _I32, _P, _P, _P, _P, _P]),

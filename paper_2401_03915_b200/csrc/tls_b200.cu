@@ -109,6 +109,13 @@ struct tls_ctx {
   int gm_exec_cols[2] = {0, 0};
   int gm_exec_launches[2] = {0, 0};
   int launches = 0;  // kernels enqueued since the counter was reset
+  // ---- in-graph timing of the local-solve kernel (bench roofline over real solves)
+  bool ktime = false, capturing = false;
+  std::vector<cudaEvent_t> kt_a, kt_b;  // one pair per band-solve node of the captured graph
+  int kt_n = 0;                         // pairs recorded by the current capture
+  int kt_n_graph[2][2] = {{0, 0}, {0, 0}};  // [pcg|gmres][prec]: pairs in that graph
+  double kt_sum_ms = 0.0;
+  long long kt_count = 0;
   // ---- banded Cholesky local operators (local_kind == 1)
   int local_kind = 0;                 // 0: packed inverse tiles, 1: band factors
   size_t restrict_smem = 0;
@@ -208,6 +215,23 @@ static int grid_for(int64_t work, int per_block) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, MAX_GRID));
 }
 
+// after a replay of a timed graph: add the band-solve node durations; nodes whose kernel
+// returned at once (the solve had converged) take a few us and are not launches of the solve
+static void harvest_ktime(tls_ctx* ctx, int npairs) {
+  if (!ctx->ktime) return;
+  std::vector<float> ms(npairs, 0.f);
+  float mx = 0.f;
+  for (int i = 0; i < npairs; ++i) {
+    if (cudaEventElapsedTime(&ms[i], ctx->kt_a[i], ctx->kt_b[i]) != cudaSuccess) ms[i] = 0.f;
+    mx = std::max(mx, ms[i]);
+  }
+  for (int i = 0; i < npairs; ++i)
+    if (ms[i] > 0.25f * mx && ms[i] > 0.004f) {
+      ctx->kt_sum_ms += ms[i];
+      ctx->kt_count++;
+    }
+}
+
 static void destroy_graphs(tls_ctx* ctx) {
   for (int i = 0; i < 2; ++i) {
     if (ctx->pcg_exec[i]) cudaGraphExecDestroy(ctx->pcg_exec[i]);
@@ -249,8 +273,20 @@ enum { L_LOCAL = 0, L_COARSE = 1, L_ALL = 2 };
 
 static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done) {
   if (ctx->local_kind >= 1 && which != L_COARSE) {
+    const bool timed = ctx->ktime && ctx->capturing;
+    if (timed) {
+      while ((int)ctx->kt_a.size() <= ctx->kt_n) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        ctx->kt_a.push_back(a);
+        ctx->kt_b.push_back(b);
+      }
+      CK(cudaEventRecordWithFlags(ctx->kt_a[ctx->kt_n], s, cudaEventRecordExternal));
+    }
     k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf);
     CKL();
+    if (timed) CK(cudaEventRecordWithFlags(ctx->kt_b[ctx->kt_n++], s, cudaEventRecordExternal));
     if (which == L_LOCAL) return TLS_OK;
     which = L_COARSE;
   }
@@ -508,6 +544,8 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   dfree(ctx->d_nofo); dfree(ctx->halo.d_sidx); dfree(ctx->halo.d_ridx); dfree(ctx->rev.d_sidx);
   dfree(ctx->rev.d_ridx);
   dfree(ctx->pcg); dfree(ctx->gm);
+  for (auto e : ctx->kt_a) cudaEventDestroy(e);
+  for (auto e : ctx->kt_b) cudaEventDestroy(e);
   for (void* pb : ctx->band_allocs) cudaFree(pb);
   dfree(ctx->d_band);
   if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
@@ -681,8 +719,9 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     ctx->band_smem = sizeof(double) * ((size_t)maxnb * TT + 8 * TT + TT);
     static size_t smem_set = 0;
     CK(raise_smem((const void*)k_band_solve, ctx->band_smem, smem_set));
-    // prefetch distance: 2 items when >= 3 subdomain CTAs share an SM, deeper otherwise
-    ctx->band_pf = n_sub >= 3 * 148 ? 2 : 4;
+    // prefetch distance 2 items (measured: 4 and 6 lose 1-15% on configurations 2 and 3 --
+    // tools/sweep_pf.sh, profiles/pf_sweep_r01.txt)
+    ctx->band_pf = 2;
     if (const char* e = getenv("TLS_BAND_PF")) {
       const int v = atoi(e);
       if (v >= 1 && v <= 16) ctx->band_pf = v;
@@ -1236,9 +1275,13 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
         const int before = ctx->launches;
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal));
+        ctx->capturing = true;
+        ctx->kt_n = 0;
         int rc = TLS_OK;
         for (int i = 1; i <= PCG_GRAPH_ITERS && rc == TLS_OK; ++i)
           rc = enq_pcg_iter(ctx, ctx->cap, i == PCG_GRAPH_ITERS, prec);
+        ctx->capturing = false;
+        ctx->kt_n_graph[0][gi] = ctx->kt_n;
         cudaError_t ec = cudaStreamEndCapture(ctx->cap, &graph);
         if (rc != TLS_OK) return rc;
         if (ec != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
@@ -1253,6 +1296,7 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
         ctx->launches += ctx->pcg_exec_launches[gi];
         CK(cudaMemcpyAsync(ctx->h_flag, &ctx->pcg->done, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        harvest_ktime(ctx, ctx->kt_n_graph[0][gi]);
         if (ctx->h_flag[0]) break;
       }
     }
@@ -1457,9 +1501,13 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
       const int before = ctx->launches;
       cudaGraph_t graph;
       CK(cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal));
+      ctx->capturing = true;
+      ctx->kt_n = 0;
       int rc = TLS_OK;
       for (int j = 0; j < mcols && rc == TLS_OK; ++j) rc = enq_gm_step(ctx, ctx->cap, j, prec);
       if (rc == TLS_OK) rc = enq_gm_cycle_end(ctx, ctx->cap, prec);
+      ctx->capturing = false;
+      ctx->kt_n_graph[1][gi] = ctx->kt_n;
       cudaError_t ec = cudaStreamEndCapture(ctx->cap, &graph);
       if (rc != TLS_OK) return rc;
       if (ec != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
@@ -1474,6 +1522,7 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
       ctx->launches += ctx->gm_exec_launches[gi];
       CK(cudaMemcpyAsync(ctx->h_flag, &ctx->gm->done, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      harvest_ktime(ctx, ctx->kt_n_graph[1][gi]);
       if (ctx->h_flag[0]) break;
     }
   }
@@ -1527,6 +1576,26 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   if (avg_ms) *avg_ms = ms / reps;
   if (algorithmic_bytes)
     *algorithmic_bytes = ctx->algo_local + (which == L_ALL && !band ? ctx->algo_coarse : 0.0);
+  return TLS_OK;
+}
+
+// in-graph timing of the local-solve kernel: on = 1 re-captures the solve graphs with CUDA event
+// nodes around every band-solve node and resets the accumulators; *avg_ms = mean duration of
+// the launches that did work (early exits after convergence are not counted), *count = their number
+int32_t tls_set_kernel_timing(tls_ctx* ctx, int32_t on) {
+  if (!ctx) return TLS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if ((on != 0) != ctx->ktime) destroy_graphs(ctx);
+  ctx->ktime = on != 0;
+  ctx->kt_sum_ms = 0.0;
+  ctx->kt_count = 0;
+  return TLS_OK;
+}
+
+int32_t tls_kernel_timing(const tls_ctx* ctx, double* avg_ms, int64_t* count) {
+  if (!ctx) return TLS_ERR_ARG;
+  if (avg_ms) *avg_ms = ctx->kt_count ? ctx->kt_sum_ms / (double)ctx->kt_count : 0.0;
+  if (count) *count = ctx->kt_count;
   return TLS_OK;
 }
 

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NTHR) k_reduce_tiles(const BlkDesc* __restrict
 //   DOT: partial sum rdot[g] * z[g]
 // ---------------------------------------------------------------------------------------
 template <int MODE, int DOT>
-__global__ void __launch_bounds__(NTHR) k_prolong(int n, const int* __restrict__ pull_ptr,
+__global__ void __launch_bounds__(NTHR, 8) k_prolong(int n, const int* __restrict__ pull_ptr,
                                                   const int* __restrict__ pull_pos,
                                                   const double* __restrict__ yloc,
                                                   const long long* __restrict__ zrow,
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(NTHR) k_pcg_pupdate(int n, const PcgState* st,
 // ---------------------------------------------------------------------------------------
 constexpr int GCH = 8;  // columns per gemv_t pass
 // part[i*G + block] = partial V[:, i] . w for i < ncols
-__global__ void __launch_bounds__(NTHR) k_gm_gemvt(int n, const double* __restrict__ V, long long ldv,
+__global__ void __launch_bounds__(NTHR, 8) k_gm_gemvt(int n, const double* __restrict__ V, long long ldv,
                                                    int ncols, const double* __restrict__ w,
                                                    double* __restrict__ part, const int* stop) {
   if (*stop) return;
@@ -577,7 +577,7 @@ __global__ void k_gm_hreduce(const double* __restrict__ part, int G, double* __r
 }
 // w -= V[:, :ncols] h  (ncols < 0: read the count from st->k); optional partial w.w
 template <int NORM>
-__global__ void __launch_bounds__(NTHR) k_gm_gemvn(int n, const double* __restrict__ V, long long ldv,
+__global__ void __launch_bounds__(NTHR, 8) k_gm_gemvn(int n, const double* __restrict__ V, long long ldv,
                                                    int ncols, const GmState* st,
                                                    const double* __restrict__ h,
                                                    double* __restrict__ w, double* __restrict__ part,
@@ -872,8 +872,7 @@ __device__ __forceinline__ void prefetch_u_item(const BandDesc& b, int I, int j)
 // inverted diagonal tile, upper triangular: warp w's strip keeps rows 0 .. 8w+7
 __device__ __forceinline__ int udiag_strip_off(int w) { return 32 * w * w + 32 * w; }
 
-// pf: L2 prefetch distance in items (2 when >= 3 CTAs share an SM; deeper when few subdomains
-// leave SMs with 1-2 CTAs and so fewer bytes in flight)
+// pf: L2 prefetch distance in items (2 measured best; TLS_BAND_PF overrides for sweeps)
 __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restrict__ bands,
                                                         const double* __restrict__ x,
                                                         double* __restrict__ y, const int* done,
