@@ -119,6 +119,8 @@ struct tls_ctx {
   // ---- banded Cholesky local operators (local_kind == 1)
   int local_kind = 0;                 // 0: packed inverse tiles, 1: band factors
   size_t restrict_smem = 0;
+  int restrict_cw = 32;               // coarse columns (warps) per k_restrict CTA (measured:
+                                      // 8 per CTA loses 7% on configuration 3, tools/ab_env.sh)
   std::vector<BandDesc> h_band;
   BandDesc* d_band = nullptr;
   std::vector<void*> band_allocs;
@@ -313,7 +315,10 @@ static int enq_gather(tls_ctx* ctx, cudaStream_t s, const double* r, const int* 
 }
 
 static int enq_restrict(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
-  k_restrict<<<ctx->nsub, 32 * std::min(std::max(ctx->kmax, 8), 32), ctx->restrict_smem, s>>>(
+  // one warp per coarse column; all columns of a subdomain in one CTA (r_int gathered once)
+  const int cw = ctx->restrict_cw;
+  const dim3 grid(ctx->nsub, (ctx->kmax + cw - 1) / cw);
+  k_restrict<<<grid, 32 * std::min(ctx->kmax, cw), ctx->restrict_smem, s>>>(
       ctx->d_sub_idxoff, ctx->d_idx, ctx->d_nint, ctx->d_zoff,
                                         ctx->d_kcnt, ctx->d_cstart, ctx->d_Z, r,
                                         ctx->xloc + ctx->coarse_xoff, done);
@@ -700,6 +705,10 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     int mi = 1;
     for (int s = 0; s < n_sub; ++s) mi = std::max(mi, ctx->h_nint[s]);
     ctx->restrict_smem = sizeof(double) * (size_t)mi;
+    if (const char* e = getenv("TLS_RESTRICT_CW")) {  // tuning override (1..32)
+      const int v = atoi(e);
+      if (v >= 1 && v <= 32) ctx->restrict_cw = v;
+    }
     static size_t rsmem_set = 48 * 1024;
     CK(raise_smem((const void*)k_restrict, ctx->restrict_smem, rsmem_set));
   }

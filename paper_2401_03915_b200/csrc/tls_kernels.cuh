@@ -148,15 +148,16 @@ __global__ void __launch_bounds__(1024) k_restrict(const long long* __restrict__
                                                    double* __restrict__ c, const int* done) {
   if (done && *done) return;
   extern __shared__ __align__(16) double rs[];  // r on this subdomain's interior
+  // grid (subdomains, column groups): CTA (s, g) handles columns g*nw .. g*nw+nw-1 of Z_s
   const int s = blockIdx.x;
   const int ks = kcnt[s], ni = nint[s];
-  if (ks == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((int)blockIdx.y * nw >= ks) return;
   const int* id = idx + sub_idxoff[s];
   for (int p = threadIdx.x; p < ni; p += blockDim.x) rs[p] = __ldg(r + __ldg(id + p));
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* zs = Z + zoff[s];
-  for (int col = warp; col < ks; col += nw) {
+  for (int col = blockIdx.y * nw + warp; col < ks; col += nw * gridDim.y) {
     const double* zc = zs + (long long)col * ni;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int p = lane;

@@ -771,6 +771,14 @@ def _band_bytes(codes):
     return 8 * int((k * 4096 + 2304).sum()) + 12 * k.size
 
 
+def _release_cache(torch, dev, frac=0.25):
+    """End of setup: hand torch's cached setup workspace back to the driver only when it is a
+    large share of the device (every cudaFree synchronises and costs ms; SURVEY.md §8d TTS)."""
+    _, total = torch.cuda.mem_get_info(dev)
+    if torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev) > frac * total:
+        torch.cuda.empty_cache()
+
+
 def _make_room(torch, dev, nbytes, slack=1 << 29):
     """Return torch's cached blocks to the driver only when the library's next cudaMalloc of
     ``nbytes`` would not fit (emptying the cache every batch costs a re-map of the batch
@@ -981,7 +989,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         del A, Binv
     del a_buf
     if not want_coarse:
-        torch.cuda.empty_cache()
+        _release_cache(torch, dev)
         return None
     # rank filter (src/coarse.py:119-155): pivoted-QR magnitudes vs the GLOBAL largest pivot
     own = range(lo, hi)
@@ -1034,12 +1042,12 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     if counts.sum() == 0:
         if any_cols > 0:
             warnings.warn("rank filter removed every coarse column; coarse level disabled")
-        torch.cuda.empty_cache()
+        _release_cache(torch, dev)
         return CoarseData(csr.shape[0], maps, [np.zeros((int(n_int[s]), 0)) for s in range(N)],
                           [0] * N, 0) if any_cols > 0 else None
     nC = int(counts.sum())
     owner = np.asarray(owner, dtype=np.int64)
-    torch.cuda.empty_cache()
+    _make_room(torch, dev, 8 * nC * nC * 3)  # A0, its factor and inverse (torch allocations)
     if VERBOSE:
         _log(t0, "stage times: " + ", ".join(f"{k} {v:.2f}s" for k, v in _STAGE.items()))
     _log(t0, f"local operators done; assembling A0 ({nC} x {nC})")
@@ -1056,7 +1064,6 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         del A0
         if int(info) != 0:
             raise RuntimeError(f"coarse operator is not positive definite: {int(info)}-th leading minor")
-        torch.cuda.empty_cache()
         # the packed-tile store reads the lower triangle (and full diagonal tiles) only
         A0inv = torch.cholesky_inverse(L).contiguous()
         del L
@@ -1076,13 +1083,15 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     zcat = (torch.cat([z_dev[s].mT.contiguous().reshape(-1) for s in own]) if len(own) else
             torch.zeros(1, dtype=torch.float64, device=dev)).contiguous()
     k32 = np.asarray(counts, dtype=np.int32)
-    torch.cuda.empty_cache()  # the library cudaMalloc's the packed coarse operator (~4 nC^2 bytes)
+    # the library cudaMalloc's the packed coarse operator (~4 nC^2 bytes, 8 nC^2 if general):
+    # torch's cached blocks go back to the driver only when that would not fit
+    _make_room(torch, dev, 8 * nC * nC if not symmetric else 4 * nC * nC + 8 * nC * 64)
     handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
                                        _lib.ptr(A0inv), s_ptr))
     torch.cuda.current_stream().synchronize()
     z_list = [z_host[s] if s in z_host else z_all[s].cpu().numpy() for s in range(N)]
     del A0, A0inv, zcat, z_dev, z_all
-    torch.cuda.empty_cache()
+    _release_cache(torch, dev)
     cd = CoarseData(csr.shape[0], maps, z_list, [int(c) for c in counts], nnz)
     cd.cut_gaps = gaps  # owned subdomains only
     return cd
