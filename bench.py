@@ -328,10 +328,13 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     its = 0
     launches = 0
+    prof_range = os.environ.get("TLS_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     with ClockSampler(local) as clk:
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        if prof_range:
+            torch.cuda.profiler.start()
         e0.record(stream)
         for _ in range(args.steps):
             x, rep = solver(b_dev)
@@ -339,6 +342,8 @@ def main():
             launches += rep.gpu_launches
         e1.record(stream)
         torch.cuda.synchronize()
+        if prof_range:
+            torch.cuda.profiler.stop()
     ms = e0.elapsed_time(e1)
     ms = _max_over_ranks(ms, world, torch)
     value = its / (ms / 1e3)

@@ -43,6 +43,7 @@ import time
 import warnings
 
 import numpy as np
+import scipy.sparse as sp
 import scipy.linalg as sla
 
 from . import _lib
@@ -537,19 +538,72 @@ def _profile_bytes(adj, perm):
     return float(K.sum() * 64 * 64 * 8 + nb * 2304 * 8)
 
 
+class _LocalGraphs:
+    """Local sparsity graphs of subdomains from the global adjacency: one global->local position
+    map (reset after each use) instead of scipy's column fancy-indexing, and an RCM cache keyed
+    on the local pattern -- subdomains of a tiled grid share a handful of local patterns."""
+
+    def __init__(self, adj_csr):
+        self.adj = adj_csr
+        self.pos = np.full(adj_csr.shape[0], -1, dtype=np.int64)
+        self.cache = {}
+
+    def local(self, idx):
+        """(local row pointer, local columns): per row the diagonal first, then the neighbours
+        in DESCENDING global index -- the entry order scipy produces for the pattern of
+        ``adj[idx][:, idx] + I`` that RCM walks, so the orders equal the dense-path ones."""
+        a = self.adj
+        n = idx.size
+        self.pos[idx] = np.arange(n)
+        starts, ends = a.indptr[idx], a.indptr[idx + 1]
+        lens = ends - starts
+        tot = int(lens.sum())
+        # each row's global columns are ascending in the CSR: read them back to front
+        rev = np.repeat(ends - 1 + np.cumsum(np.concatenate([[0], lens[:-1]])), lens) - np.arange(tot)
+        lc = self.pos[a.indices[rev]]
+        self.pos[idx] = -1
+        rows = np.repeat(np.arange(n), lens)
+        keep = lc >= 0
+        rows, lc = rows[keep], lc[keep]
+        cnt = np.bincount(rows, minlength=n) + 1
+        ptr = np.concatenate([[0], np.cumsum(cnt)])
+        cols = np.empty(int(ptr[-1]), dtype=np.int64)
+        cols[ptr[:-1]] = np.arange(n)
+        off = np.arange(rows.size) - np.concatenate([[0], np.cumsum(cnt - 1)])[rows]
+        cols[ptr[rows] + 1 + off] = lc
+        return ptr, cols
+
+    def rcm(self, idx):
+        from scipy.sparse.csgraph import reverse_cuthill_mckee
+        ptr, cols = self.local(idx)
+        key = (idx.size, hash(ptr.tobytes()), hash(cols.tobytes()))
+        hit = self.cache.get(key)
+        if hit is not None and np.array_equal(hit[0], ptr) and np.array_equal(hit[1], cols):
+            return hit[2]
+        n = idx.size
+        sub = sp.csr_matrix((np.ones(cols.size, dtype=np.int8), cols.astype(np.int32), ptr.astype(np.int32)),
+                            shape=(n, n))
+        out = np.asarray(reverse_cuthill_mckee(sub, symmetric_mode=True), dtype=np.int64)
+        self.cache[key] = (ptr, cols, out)
+        return out
+
+
+_LG = {}
+
+
 def local_orders(adj_csr, maps, kind):
     """Factor row order of every subdomain: "lex" = ascending global index (a plane sweep for
-    grid operators), "rcm" = reverse Cuthill-McKee of the local graph."""
-    import scipy.sparse as sp
-    from scipy.sparse.csgraph import reverse_cuthill_mckee
+    grid operators), "rcm" = reverse Cuthill-McKee of the local graph (with the diagonal, as
+    scipy's RCM on A_ii's pattern)."""
     out = []
+    if kind == "lex":
+        return [np.argsort(m.indices, kind="stable").astype(np.int64) for m in maps]
+    lg = _LG.get(id(adj_csr))
+    if lg is None or lg.adj is not adj_csr:
+        _LG.clear()
+        lg = _LG[id(adj_csr)] = _LocalGraphs(adj_csr)
     for m in maps:
-        if kind == "lex":
-            out.append(np.argsort(m.indices, kind="stable").astype(np.int64))
-        else:
-            sub = adj_csr[m.indices][:, m.indices]
-            sub = (sub + sp.identity(sub.shape[0], dtype=sub.dtype, format="csr")).tocsr()
-            out.append(np.asarray(reverse_cuthill_mckee(sub, symmetric_mode=True), dtype=np.int64))
+        out.append(lg.rcm(np.asarray(m.indices, dtype=np.int64)))
     return out
 
 
