@@ -394,13 +394,6 @@ __global__ void __launch_bounds__(NTHR) k_xunpack(long long m, const int* __rest
     dst[__ldg(idx + p)] = buf[p];
 }
 
-// deflated combination after the sharded all-reduces: z = (q + w) - Qu  (src/precond.py:136)
-__global__ void __launch_bounds__(NTHR) k_defl_combine(int n, const double* __restrict__ q,
-                                                       const double* __restrict__ w,
-                                                       double* __restrict__ z, const int* done) {
-  if (done && *done) return;
-  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) z[i] = (q[i] + w[i]) - z[i];
-}
 
 // ---------------------------------------------------------------------------------------
 // K8  Krylov vector kernels and scalar steps (src/krylov.py:58-107)
