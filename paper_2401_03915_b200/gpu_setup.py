@@ -1109,7 +1109,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     del w_dev
     if sharded:
         shard.coll.allreduce(A0, op="sum")
-    nnz = int(torch.count_nonzero(A0))  # the pattern of Z^T A Z is symmetric
+    # count_nonzero (src/coarse.py:168) in row blocks: no n_C^2 temporary next to A0
+    nnz = sum(int(torch.count_nonzero(A0[i:i + 4096])) for i in range(0, nC, 4096))
     _log(t0, "A0 assembled; factorising")
     if symmetric:
         # symmetrise (src/coarse.py:169-170) the lower triangle Cholesky reads, in place

@@ -127,3 +127,57 @@ def test_sharded_callback_and_spmv(B):
         assert seen == list(range(1, rep.iterations + 1))
         np.testing.assert_allclose(x, d["x"], rtol=0, atol=1e-8 * np.abs(d["x"]).max())
         assert np.array_equal(y, a @ v) or np.abs(y - a @ v).max() <= 1e-12 * np.abs(a @ v).max()
+
+
+def _group_run(n, fn):
+    from paper_2401_03915_b200.distributed import LocalGroup
+    grp = LocalGroup(n)
+
+    def body(shard):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            out = fn(shard)
+            stream.synchronize()
+            return out
+
+    return grp.run(body)
+
+
+@pytest.mark.parametrize("combo", ["asm_additive_gevp", "asm_deflated_svd", "ras_additive_full",
+                                   "ras_deflated_gevp", "asm_none_gevp", "ras_none_svd"])
+def test_sharded_variants_match_reference(B, combo):
+    """The reference's apply variants (tests/test_precond.py:78-101 grid, tau threshold path,
+    partition_graph owners) on 3 ranks: every rank returns the reference's z."""
+    d = dict(golden("variants_p2d8"))
+    a = golden_csr(d)
+    one, comb, kind = combo.split("_")
+
+    def fn(shard):
+        mat = B.SparseMat(a, symmetric=True)
+        pre = B.setup(mat, 4, overlap=2, tau=0.05, coarse=kind, one_level=one, combine=comb, shard=shard)
+        return [pre.apply(r) for r in d["r"]]
+
+    for zs in _group_run(3, fn):
+        for z, zr in zip(zs, d["z_" + combo]):
+            np.testing.assert_allclose(z, zr, rtol=0, atol=1e-11 * np.abs(zr).max())
+
+
+def test_sharded_nonsymmetric_unrestarted_gmres_and_unpreconditioned(B):
+    """Nonsymmetric defaults (RAS + deflated + SVD, band LU) with the reference's unrestarted GMRES
+    on 2 ranks, and the unpreconditioned PCG / GMRES loops through a sharded handle."""
+    d = dict(golden("adv12"))
+    a = golden_csr(d)
+
+    def fn(shard):
+        mat = B.SparseMat(a)
+        pre = B.setup(mat, 4, overlap=2, tau=0.05, shard=shard, local="band")
+        z = pre.apply(d["r"][0])
+        x, rep = B.gmres(mat, pre, d["b"], tol=1e-10)
+        return z, x, rep
+
+    res = _group_run(2, fn)
+    for z, x, rep in res:
+        np.testing.assert_allclose(z, d["z"][0], rtol=0, atol=1e-10 * np.abs(d["z"][0]).max())
+        assert abs(rep.iterations - int(d["iterations"])) <= 1
+        np.testing.assert_allclose(x, d["x"], rtol=0, atol=1e-8 * np.abs(d["x"]).max())
+    assert np.array_equal(res[0][1], res[1][1])

@@ -23,6 +23,7 @@ t0 = time.perf_counter()
 B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes)
 torch.cuda.synchronize()
 print(f"setup wall (no profiler) {time.perf_counter() - t0:.3f} s")
+torch.cuda.empty_cache()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], with_stack=False) as prof:
     t0 = time.perf_counter()
     B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes)
