@@ -90,7 +90,8 @@ struct tls_ctx {
   // ---- work vectors
   double *t1 = nullptr, *t2 = nullptr, *t3 = nullptr, *t4 = nullptr, *t5 = nullptr, *t6 = nullptr,
          *t7 = nullptr, *vb = nullptr, *vx = nullptr, *vr = nullptr, *vp = nullptr, *vap = nullptr,
-         *vz = nullptr, *hist = nullptr, *ab = nullptr, *h_x = nullptr;
+         *vz = nullptr, *hist = nullptr, *ab = nullptr, *h_x = nullptr,
+         *cz = nullptr;  // coarse prolongation Z yc of the additive band schedule
   int hist_cap = 0;
   double* part = nullptr;
   int64_t part_cap = 0;
@@ -421,17 +422,20 @@ static int enq_apply(tls_ctx* ctx, cudaStream_t s, double* r, double* z, bool do
     // the coarse chain (restrict -> [sum over ranks] -> A0^{-1} tiles -> reduce) reads r and
     // writes only the coarse segments, the band solve reads/writes only the local segments: run
     // them side by side (a fork/join that CUDA-graph capture turns into parallel branches)
+    // (the coarse prolongation Z yc is computed on that branch too, into cz; the prolongation
+    // after the join only adds the local-solve contributions to it)
     CK(cudaEventRecord(ctx->ev_fork, s));
     CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
     TRY(enq_restrict_all(ctx, ctx->aux, r, done));
     TRY(enq_solve(ctx, ctx->aux, L_COARSE, done));
+    TRY((enq_prolong<2, 0>(ctx, ctx->aux, nullptr, nullptr, nullptr, ctx->cz, done)));
     CK(cudaEventRecord(ctx->ev_join, ctx->aux));
     TRY(enq_gather(ctx, s, r, done));
     TRY(enq_solve(ctx, s, L_LOCAL, done));
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     TRY(enq_rev(ctx, s, done));
-    TRY(dot ? enq_prolong<1, 1>(ctx, s, nullptr, nullptr, r, z, done)
-            : enq_prolong<1, 0>(ctx, s, nullptr, nullptr, r, z, done));
+    TRY(dot ? enq_prolong<4, 1>(ctx, s, ctx->cz, nullptr, r, z, done)
+            : enq_prolong<4, 0>(ctx, s, ctx->cz, nullptr, r, z, done));
   } else if (ctx->combine == TLS_ADDITIVE) {
     if (!r_full) TRY(enq_halo(ctx, s, r, done));
     TRY(enq_gather(ctx, s, r, done));
@@ -543,7 +547,7 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   double** vecs[] = {&ctx->t1, &ctx->t2, &ctx->t3, &ctx->t4, &ctx->t5, &ctx->t6, &ctx->t7, &ctx->vb,
                      &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz, &ctx->hist, &ctx->part,
                      &ctx->V, &ctx->H, &ctx->cs, &ctx->sn, &ctx->gv, &ctx->yv, &ctx->h1, &ctx->h2,
-                     &ctx->pin, &ctx->pout, &ctx->halo.sbuf, &ctx->halo.rbuf, &ctx->rev.sbuf,
+                     &ctx->pin, &ctx->pout, &ctx->cz, &ctx->halo.sbuf, &ctx->halo.rbuf, &ctx->rev.sbuf,
                      &ctx->rev.rbuf};
   for (double** v : vecs) dfree(*v);
   dfree(ctx->d_nofo); dfree(ctx->halo.d_sidx); dfree(ctx->halo.d_ridx); dfree(ctx->rev.d_sidx);
@@ -626,7 +630,8 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
     ctx->part_cap = need;
   }
   double** vecs[] = {&ctx->t1, &ctx->t2, &ctx->t3, &ctx->t4, &ctx->t5, &ctx->t6, &ctx->t7,
-                     &ctx->vb, &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz, &ctx->pin, &ctx->pout};
+                     &ctx->vb, &ctx->vx, &ctx->vr, &ctx->vp, &ctx->vap, &ctx->vz, &ctx->pin, &ctx->pout,
+                     &ctx->cz};
   for (double** v : vecs) {
     TRY(dalloc(ctx, *v, nrows));
     CK(cudaMemset(*v, 0, sizeof(double) * nrows));  // ghost rows are read (x 0) before any halo

@@ -313,6 +313,8 @@ __global__ void __launch_bounds__(NTHR) k_reduce_tiles(const BlkDesc* __restrict
 // src/coarse.py:43-44).
 //   MODE 0: z = one-level          1: z = one-level + coarse  (additive, src/precond.py:132)
 //   MODE 2: z = coarse             3: z = (q + w) - coarse    (deflated, src/precond.py:134-136)
+//   MODE 4: z = one-level + qv     (additive with the coarse part Z yc precomputed into qv by a
+//           MODE 2 launch on the side branch that overlaps the local solves)
 //   DOT: partial sum rdot[g] * z[g]
 // ---------------------------------------------------------------------------------------
 template <int MODE, int DOT>
@@ -335,11 +337,11 @@ __global__ void __launch_bounds__(NTHR, 8) k_prolong(int n, const int* __restric
   double dacc = 0.0;
   for (int g = blockIdx.x * NTHR + threadIdx.x; g < n; g += gridDim.x * NTHR) {
     double one = 0.0, cz = 0.0;
-    if (MODE == 0 || MODE == 1) {
+    if (MODE == 0 || MODE == 1 || MODE == 4) {
       const int beg = __ldg(pull_ptr + g), end = __ldg(pull_ptr + g + 1);
       for (int q = beg; q < end; ++q) one += __ldg(yloc + __ldg(pull_pos + q));
     }
-    if (MODE >= 1) {
+    if (MODE >= 1 && MODE <= 3) {
       const long long zo = __ldg(zrow + g);
       if (zo >= 0) {
         const int k = __ldg(zk + g), c0 = __ldg(zc + g), st = __ldg(zst + g);
@@ -351,7 +353,8 @@ __global__ void __launch_bounds__(NTHR, 8) k_prolong(int n, const int* __restric
     if (MODE == 0) out = one;
     else if (MODE == 1) out = one + cz;
     else if (MODE == 2) out = cz;
-    else out = (qv[g] + wv[g]) - cz;
+    else if (MODE == 3) out = (qv[g] + wv[g]) - cz;
+    else out = one + qv[g];
     z[g] = out;
     if (DOT) dacc += rdot[g] * out;
   }
