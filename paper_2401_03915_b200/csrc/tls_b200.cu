@@ -274,7 +274,9 @@ static int spmv_lpr(tls_ctx* ctx, cudaStream_t s, const double* x, double* y, co
 // which unit/out lists a solve stage uses
 enum { L_LOCAL = 0, L_COARSE = 1, L_ALL = 2 };
 
-static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done) {
+// r_src (band local operators only): gather R_i r inside the band kernel instead of from xloc
+static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
+                     const double* r_src = nullptr) {
   if (ctx->local_kind >= 1 && which != L_COARSE) {
     const bool timed = ctx->ktime && ctx->capturing;
     if (timed) {
@@ -287,7 +289,8 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done) {
       }
       CK(cudaEventRecordWithFlags(ctx->kt_a[ctx->kt_n], s, cudaEventRecordExternal));
     }
-    k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf);
+    k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
+                                                         r_src ? ctx->d_gidx : nullptr, r_src);
     CKL();
     if (timed) CK(cudaEventRecordWithFlags(ctx->kt_b[ctx->kt_n++], s, cudaEventRecordExternal));
     if (which == L_LOCAL) return TLS_OK;
@@ -405,6 +408,13 @@ static int enq_dot(tls_ctx* ctx, cudaStream_t s, const double* a, const double* 
   return enq_allreduce_part(ctx, s, ctx->G);
 }
 
+// one-level local solves of r: gather + tiles, or the band kernel gathering r itself
+static int enq_local(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
+  if (ctx->local_kind >= 1) return enq_solve(ctx, s, L_LOCAL, done, r);
+  TRY(enq_gather(ctx, s, r, done));
+  return enq_solve(ctx, s, L_LOCAL, done);
+}
+
 // z = M^{-1} r (src/precond.py:128-136) on the owned rows.  r must be valid on the owned rows;
 // r_full: its ghost rows are valid too (no halo needed).  dot: r.z partials (summed over the
 // ranks) in ctx->part (G of them).
@@ -412,8 +422,7 @@ static int enq_apply(tls_ctx* ctx, cudaStream_t s, double* r, double* z, bool do
                      bool r_full = false) {
   if (!has_coarse(ctx)) {
     if (!r_full) TRY(enq_halo(ctx, s, r, done));
-    TRY(enq_gather(ctx, s, r, done));
-    TRY(enq_solve(ctx, s, L_LOCAL, done));
+    TRY(enq_local(ctx, s, r, done));
     TRY(enq_rev(ctx, s, done));
     TRY(dot ? enq_prolong<0, 1>(ctx, s, nullptr, nullptr, r, z, done)
             : enq_prolong<0, 0>(ctx, s, nullptr, nullptr, r, z, done));
@@ -430,8 +439,7 @@ static int enq_apply(tls_ctx* ctx, cudaStream_t s, double* r, double* z, bool do
     TRY(enq_solve(ctx, ctx->aux, L_COARSE, done));
     TRY((enq_prolong<2, 0>(ctx, ctx->aux, nullptr, nullptr, nullptr, ctx->cz, done)));
     CK(cudaEventRecord(ctx->ev_join, ctx->aux));
-    TRY(enq_gather(ctx, s, r, done));
-    TRY(enq_solve(ctx, s, L_LOCAL, done));
+    TRY(enq_local(ctx, s, r, done));
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     TRY(enq_rev(ctx, s, done));
     TRY(dot ? enq_prolong<4, 1>(ctx, s, ctx->cz, nullptr, r, z, done)
@@ -453,8 +461,7 @@ static int enq_apply(tls_ctx* ctx, cudaStream_t s, double* r, double* z, bool do
     TRY(enq_halo(ctx, s, ctx->t1, done));
     TRY((spmv_lpr<1, 0>(ctx, s, ctx->t1, ctx->t2, r, nullptr, done)));
     TRY(enq_halo(ctx, s, ctx->t2, done));
-    TRY(enq_gather(ctx, s, ctx->t2, done));
-    TRY(enq_solve(ctx, s, L_LOCAL, done));
+    TRY(enq_local(ctx, s, ctx->t2, done));
     TRY(enq_rev(ctx, s, done));
     TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, ctx->t3, done)));
     TRY(enq_halo(ctx, s, ctx->t3, done));
@@ -1145,8 +1152,7 @@ int32_t tls_apply_one_level(tls_ctx* ctx, const double* r, double* z, void* stre
   double* ri;
   TRY(api_in(ctx, s, r, &ri));
   double* zi = api_out_buf(ctx, z);
-  TRY(enq_gather(ctx, s, ri, nullptr));
-  TRY(enq_solve(ctx, s, L_LOCAL, nullptr));
+  TRY(enq_local(ctx, s, ri, nullptr));
   TRY(enq_rev(ctx, s, nullptr));
   TRY((enq_prolong<0, 0>(ctx, s, nullptr, nullptr, nullptr, zi, nullptr)));
   return api_out(ctx, s, zi, z);
@@ -1576,7 +1582,8 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   for (int i = 0; i <= reps; ++i) {
     if (i == 1) CK(cudaEventRecord(e0, s));
     if (band)
-      k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr, ctx->band_pf);
+      k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr, ctx->band_pf,
+                                                           nullptr, nullptr);
     else
       k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
     CKL();

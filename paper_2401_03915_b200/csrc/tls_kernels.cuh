@@ -870,10 +870,13 @@ __device__ __forceinline__ void prefetch_u_item(const BandDesc& b, int I, int j)
 __device__ __forceinline__ int udiag_strip_off(int w) { return 32 * w * w + 32 * w; }
 
 // pf: L2 prefetch distance in items (2 measured best; TLS_BAND_PF overrides for sweeps)
+// gidx != nullptr: the restriction R_i r is fused into the load (v[p] = r[gidx[xoff + p]],
+// K2 without its own launch and without the xloc round trip); otherwise v = x[xoff ...]
 __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restrict__ bands,
                                                         const double* __restrict__ x,
                                                         double* __restrict__ y, const int* done,
-                                                        int pf) {
+                                                        int pf, const int* __restrict__ gidx,
+                                                        const double* __restrict__ r) {
   if (done && *done) return;
   extern __shared__ __align__(16) double sm[];
   const BandDesc b = bands[blockIdx.x];
@@ -887,7 +890,14 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   const int doff = diag_strip_off(warp) + (2 * lane - 8 * warp);
   if (threadIdx.x == 0)
     for (int j = 2; j < pf; ++j) prefetch_fwd_item(b, 0, j);  // items >= 2 of the stream head
-  for (int i = threadIdx.x; i < npad; i += NTHR) v[i] = x[b.xoff + i];
+  if (gidx) {
+    for (int i = threadIdx.x; i < npad; i += NTHR) {
+      const int g = __ldg(gidx + b.xoff + i);
+      v[i] = g >= 0 ? __ldg(r + g) : 0.0;
+    }
+  } else {
+    for (int i = threadIdx.x; i < npad; i += NTHR) v[i] = x[b.xoff + i];
+  }
   __syncthreads();
   // forward sweep: L u = x  (the factor is one contiguous stream in this order)
   for (int I = 0; I < b.nb; ++I) {
