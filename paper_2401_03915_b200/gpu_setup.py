@@ -651,9 +651,10 @@ def lu_growth(torch, csr, maps, perm_kind, adj_csr, device, sample=None):
 def _lex_perm(torch, A, perms, n_list, ld):
     cnt = A.shape[0]
     dev = A.device
-    P = torch.arange(ld, device=dev).repeat(cnt, 1)
+    Ph = np.tile(np.arange(ld, dtype=np.int64), (cnt, 1))  # built on the host, one upload
     for b in range(cnt):
-        P[b, : n_list[b]] = torch.as_tensor(perms[b], device=dev)
+        Ph[b, : n_list[b]] = perms[b]
+    P = torch.from_numpy(Ph).to(dev)
     AP = torch.gather(A, 1, P[:, :, None].expand(cnt, ld, ld))
     AP = torch.gather(AP, 2, P[:, None, :].expand(cnt, ld, ld)).contiguous()
     return AP, P, perms
@@ -1047,15 +1048,30 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         return None
     # rank filter (src/coarse.py:119-155): pivoted-QR magnitudes vs the GLOBAL largest pivot
     own = range(lo, hi)
-    z_host = {s: z_dev[s].cpu().numpy() for s in own}
-    pivots = []
+    # one device->host copy of every owned block, then the host pivoted QRs (LAPACK geqp3, the
+    # reference's rank test) on all host threads
+    flat = torch.cat([z_dev[s].reshape(-1) for s in own]).cpu().numpy() if len(own) else np.zeros(0)
+    z_host, off = {}, 0
     for s in own:
+        sh = tuple(z_dev[s].shape)
+        z_host[s] = flat[off:off + sh[0] * sh[1]].reshape(sh)
+        off += sh[0] * sh[1]
+
+    def _geqp3(s):
         z = z_host[s]
         if z.shape[1] == 0:
-            continue
+            return s, None, None
         r, perm = sla.qr(z, mode="r", pivoting=True)
-        rd = np.abs(np.diag(r))
-        for j in range(z.shape[1]):
+        return s, np.abs(np.diag(r)), perm
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+        qrs = list(ex.map(_geqp3, own))
+    pivots = []
+    for s, rd, perm in qrs:
+        if rd is None:
+            continue
+        for j in range(z_host[s].shape[1]):
             pivots.append((rd[j] if j < rd.size else 0.0, s, int(perm[j])))
     largest = max((p[0] for p in pivots), default=0.0)
     any_cols = float(len(pivots))
