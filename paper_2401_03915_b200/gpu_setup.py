@@ -258,23 +258,32 @@ def _subdomain_columns(torch, kind, A, Bring, n, ni, nin, tau, n_modes):
     return V.contiguous(), _cut_gap(sv, keep)
 
 
-def _orth(torch, X):
-    """Batched orthonormalisation: CholeskyQR2 (two GEMM + p x p Cholesky passes)."""
+def _orth(torch, X, check=True):
+    """Batched orthonormalisation: CholeskyQR2 (two GEMM + p x p Cholesky passes).
+
+    check=False skips the per-call host test of the Cholesky info (a device sync); the caller
+    then tests the result for non-finite values at its next sync point and falls back."""
+    X0 = X
+    bad = None
     for _ in range(2):
         G = X.mT @ X
         R, info = torch.linalg.cholesky_ex(G, upper=True)
-        if bool((info != 0).any()):  # numerically rank-deficient block: Householder fallback
-            return torch.linalg.qr(X).Q
+        if check and bool((info != 0).any()):  # numerically rank-deficient block: Householder
+            return torch.linalg.qr(X0).Q
+        bad = info != 0 if bad is None else bad | (info != 0)
         X = torch.linalg.solve_triangular(R, X, upper=True, left=False)
-    return X
+    return X if check else (X, bad)
 
 
-def _rayleigh_ritz(torch, M, X, k):
+def _rayleigh_ritz(torch, M, X, k, bad=None):
     MX = M @ X
     T = X.mT @ MX
     # the p x p projected problem is tiny: solve it on the host (batched GPU eigh loops one
     # cuSOLVER call per matrix once p > 32)
-    th_all, S = torch.linalg.eigh((0.5 * (T + T.mT)).cpu())
+    Th = (0.5 * (T + T.mT)).cpu()
+    if bad is not None and bool(bad.cpu().any()):  # (no extra stall: the copy above synced)
+        return None  # CholeskyQR2 broke down on X's block (caller falls back)
+    th_all, S = torch.linalg.eigh(Th)
     th_all = torch.flip(th_all, dims=[-1]).to(M.device)
     S = torch.flip(S, dims=[-1]).to(M.device)
     Xr = X @ S
@@ -343,16 +352,13 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
     gen.manual_seed(seed)
     X = _orth(torch, torch.randn((b, m, p), generator=gen, dtype=M.dtype, device=M.device))
     X = _orth(torch, M @ (M @ X))
-    th, X, MX = _rayleigh_ritz(torch, M, X, p)
+    th, X, MX = _rayleigh_ritz(torch, M, X, p)  # checked _orth: always orthonormal here
     scale = th[:, :1].abs().clamp(min=1e-300)
     res = float("inf")
     products = 3
     for it in range(1, maxit + 1):
         R = MX[:, :, :k] - X[:, :, :k] * th[:, None, :k]
         res_b = (R.norm(dim=1) / scale).amax(dim=1)                     # (b,)
-        res = float(res_b.max())
-        if res <= tol:
-            return th[:, :k], X[:, :, :k], products
         a = th[:, p - 1].clamp(min=0.0)
         e = (0.5 * a).clamp(min=1e-300)
         x1 = ((th[:, 0] - e) / e).clamp(min=1.0 + 1e-12)
@@ -360,7 +366,10 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
         per = (torch.acosh(x1) - torch.acosh(xk)).clamp(min=1e-12)
         d_b = torch.floor(np.log(rmax) / per).clamp(min=1, max=dmax)
         d_b = torch.where(res_b > tol, d_b, torch.zeros_like(d_b))       # converged: leave as is
-        d = int(d_b.max())
+        host = torch.stack([res_b.max(), d_b.max()]).cpu()               # ONE sync per step
+        res, d = float(host[0]), int(host[1])
+        if res <= tol:
+            return th[:, :k], X[:, :, :k], products
         if trace is not None:
             trace.append((d, res, int((res_b > tol).sum()), float(per.max())))
         c = e[:, None, None]
@@ -374,8 +383,11 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
             Y1 = torch.where(live, Y2, Y1)
         products += d
         Y1 = Y1 / Y1.norm(dim=1, keepdim=True).clamp(min=1e-300)
-        X = _orth(torch, Y1)
-        th, X, MX = _rayleigh_ritz(torch, M, X, p)
+        Xo, bad = _orth(torch, Y1, check=False)  # no sync in _orth: tested with the RR copy
+        rr = _rayleigh_ritz(torch, M, Xo, p, bad=bad)
+        if rr is None:  # CholeskyQR2 broke down: Householder QR of the same block
+            rr = _rayleigh_ritz(torch, M, torch.linalg.qr(Y1).Q, p)
+        th, X, MX = rr
         products += 1
     raise RuntimeError(f"Chebyshev subspace iteration did not converge: residual {res:.2e} after {maxit} steps")
 
@@ -1065,8 +1077,18 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         return s, np.abs(np.diag(r)), perm
 
     from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
-        qrs = list(ex.map(_geqp3, own))
+    try:  # one BLAS thread per pool worker (no oversubscription)
+        from threadpoolctl import threadpool_limits
+        limit = threadpool_limits(limits=1)
+    except Exception:  # threadpoolctl missing: run the QRs serially with BLAS threads
+        limit = None
+    try:
+        workers = min(16, os.cpu_count() or 1) if limit is not None else 1
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            qrs = list(ex.map(_geqp3, own))
+    finally:
+        if limit is not None:
+            limit.restore_original_limits()
     pivots = []
     for s, rd, perm in qrs:
         if rd is None:
