@@ -28,6 +28,7 @@ namespace {
 
 constexpr int PCG_GRAPH_ITERS = 25;  // replacement period of src/krylov.py:88
 constexpr int MAX_GRID = 148 * 8;    // 148 SMs x 8 resident 256-thread CTAs
+constexpr int GM_FUSED_MAXCOLS = 96; // fused CGS2 step while (nc + 1) x 256 doubles fit in smem
 
 template <class T>
 void dfree(T*& p) {
@@ -103,6 +104,7 @@ struct tls_ctx {
   double *V = nullptr, *H = nullptr, *cs = nullptr, *sn = nullptr, *gv = nullptr, *yv = nullptr,
          *h1 = nullptr, *h2 = nullptr;
   int gm_cols = 0;
+  bool gm_fused = true;               // CGS2 middle step as one kernel (TLS_GM_FUSED=0: two)
   // ---- graphs
   cudaGraphExec_t pcg_exec[2] = {nullptr, nullptr};
   int pcg_exec_launches[2] = {0, 0};
@@ -1362,19 +1364,28 @@ static int enq_gm_step(tls_ctx* ctx, cudaStream_t s, int j, bool prec) {
     TRY((spmv_lpr<0, 0>(ctx, s, vj, w, nullptr, nullptr, stop)));
   }
   const int nc = j + 1;
-  double* hs[2] = {ctx->h1, ctx->h2};
-  for (int pass = 0; pass < 2; ++pass) {
+  // CGS2 (src/krylov.py:157-165 to the same accuracy): h1 = V^T w; w -= V h1 fused with
+  // h2 = V^T w (one read of V); w -= V h2 with the norm partials -> 3 reads of V, not 4
+  k_gm_gemvt<<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, w + r0, ctx->part, stop);
+  CKL();
+  k_gm_hreduce<<<nc, NTHR, 0, s>>>(ctx->part, ctx->G, ctx->h1, stop);
+  CKL();
+  TRY(enq_allreduce(ctx, s, ctx->h1, nc));
+  if (ctx->gm_fused && nc <= GM_FUSED_MAXCOLS) {
+    k_gm_update_gemvt<<<ctx->G, NTHR, sizeof(double) * ((size_t)(nc + 1) * NTHR + nc), s>>>(
+        no, ctx->V + r0, ldv, nc, ctx->h1, w + r0, ctx->part, stop);
+    CKL();
+  } else {
+    k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, st, ctx->h1, w + r0, ctx->part, 1, stop);
+    CKL();
     k_gm_gemvt<<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, w + r0, ctx->part, stop);
     CKL();
-    k_gm_hreduce<<<nc, NTHR, 0, s>>>(ctx->part, ctx->G, hs[pass], stop);
-    CKL();
-    TRY(enq_allreduce(ctx, s, hs[pass], nc));
-    if (pass == 0)
-      k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, st, hs[pass], w + r0, ctx->part, 1, stop);
-    else
-      k_gm_gemvn<1><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, st, hs[pass], w + r0, ctx->part, 1, stop);
-    CKL();
   }
+  k_gm_hreduce<<<nc, NTHR, 0, s>>>(ctx->part, ctx->G, ctx->h2, stop);
+  CKL();
+  TRY(enq_allreduce(ctx, s, ctx->h2, nc));
+  k_gm_gemvn<1><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, st, ctx->h2, w + r0, ctx->part, 1, stop);
+  CKL();
   TRY(enq_allreduce_part(ctx, s, ctx->G));
   k_gm_givens<<<1, NTHR, 0, s>>>(st, j, ctx->gm_cols + 1, ctx->H, ctx->h1, ctx->h2, ctx->part, ctx->G,
                                  ctx->cs, ctx->sn, ctx->gv, ctx->hist);
@@ -1430,6 +1441,12 @@ static int ensure_gm(tls_ctx* ctx, int mcols) {
     destroy_graphs(ctx);
   }
   ctx->gm_cols = mcols;
+  if (const char* e = getenv("TLS_GM_FUSED")) ctx->gm_fused = atoi(e) != 0;
+  if (ctx->gm_fused) {  // (nc + 1) x NTHR + nc doubles of shared memory for the widest fused step
+    static size_t fsmem = 48 * 1024;
+    const int mc = std::min(mcols + 1, GM_FUSED_MAXCOLS);
+    CK(raise_smem((const void*)k_gm_update_gemvt, sizeof(double) * ((size_t)(mc + 1) * NTHR + mc), fsmem));
+  }
   for (int i = 0; i < 2; ++i) {
     if (ctx->gm_exec[i]) cudaGraphExecDestroy(ctx->gm_exec[i]);
     ctx->gm_exec[i] = nullptr;

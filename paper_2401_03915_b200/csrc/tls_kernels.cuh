@@ -564,6 +564,52 @@ __global__ void __launch_bounds__(NTHR, 8) k_gm_gemvt(int n, const double* __res
     __syncthreads();
   }
 }
+// CGS2 middle step, one read of V instead of two: w -= V[:, :ncols] h (pass-1 update) and the
+// pass-2 projections part[i*G + block] = partial V[:, i] . w_new.  Rows go through shared memory
+// in tiles of NTHR: the tile of V (ncols x NTHR, coalesced column loads) is used for the update
+// of its rows and, after a barrier, for the dot products (warp c reduces columns c, c+8, ...),
+// accumulated per CTA in a fixed tile order -> deterministic.  Dynamic smem: (ncols+1)*NTHR + ncols doubles.
+__global__ void __launch_bounds__(NTHR) k_gm_update_gemvt(int n, const double* __restrict__ V, long long ldv,
+                                                          int ncols, const double* __restrict__ h,
+                                                          double* __restrict__ w, double* __restrict__ part,
+                                                          const int* stop) {
+  if (*stop) return;
+  extern __shared__ __align__(16) double smv[];
+  double* vt = smv;                       // ncols x NTHR
+  double* wt = smv + (long long)ncols * NTHR;
+  double* acc = wt + NTHR;                // ncols
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = threadIdx.x; c < ncols; c += NTHR) acc[c] = 0.0;
+  for (long long row0 = (long long)blockIdx.x * NTHR; row0 < n; row0 += (long long)gridDim.x * NTHR) {
+    const long long i = row0 + threadIdx.x;
+    double s = 0.0;
+    if (i < n) {
+      for (int c = 0; c < ncols; ++c) {
+        const double v = V[(long long)c * ldv + i];
+        vt[c * NTHR + threadIdx.x] = v;
+        s += v * __ldg(h + c);
+      }
+      const double out = w[i] - s;
+      w[i] = out;
+      wt[threadIdx.x] = out;
+    } else {
+      for (int c = 0; c < ncols; ++c) vt[c * NTHR + threadIdx.x] = 0.0;
+      wt[threadIdx.x] = 0.0;
+    }
+    __syncthreads();
+    for (int c = warp; c < ncols; c += NTHR / 32) {
+      double d = 0.0;
+#pragma unroll
+      for (int r = lane; r < NTHR; r += 32) d += vt[c * NTHR + r] * wt[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
+      if (lane == 0) acc[c] += d;
+    }
+    __syncthreads();
+  }
+  for (int c = threadIdx.x; c < ncols; c += NTHR) part[(long long)c * gridDim.x + blockIdx.x] = acc[c];
+}
+
 // h[i] = sum_b part[i*G + b]; one block per column
 __global__ void k_gm_hreduce(const double* __restrict__ part, int G, double* __restrict__ h,
                              const int* stop) {
