@@ -391,6 +391,10 @@ def main():
     else:  # inverse tiles (the profiled launch also covers the coarse block): packed A_ii^{-1}
         ns = np.array([m.n_local for m in pre.maps], dtype=np.float64)
         local_algo = float((8.0 * ns * (ns + 1) / 2 if sym else 8.0 * ns * ns).sum() + 16.0 * ns.sum())
+    if world > 1:  # every rank streams its own slab's factors: the iteration moves the sum
+        t = torch.tensor([local_algo], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t)
+        local_algo = float(t.item())
     it_bytes, it_parts = iteration_bytes(cfg, a, pre, local_algo)
     loop_ach = it_bytes * value / 1e9
     # true residual of the final solve
