@@ -187,6 +187,10 @@ int32_t tls_comm_init_nccl(tls_ctx* ctx, const void* unique_id, int32_t nranks, 
 int32_t tls_group_create(int32_t nmembers, tls_group** out);
 void tls_group_destroy(tls_group* g);
 int32_t tls_comm_init_group(tls_ctx* ctx, tls_group* g, int32_t rank);
+/* test transport: capturable, moves no data, logs (kind, count, peers) of every collective the
+ * sharded schedule issues -- validates CUDA-graph capture of the NCCL schedule on one GPU */
+int32_t tls_comm_init_record(tls_ctx* ctx, int32_t nranks, int32_t rank);
+int64_t tls_comm_record_log(const tls_ctx* ctx, int64_t* out, int64_t cap);
 
 /* ---- measurement: average device time (ms) of the dominant kernel (batched local
  * solve) over the last solve, timed with CUDA events on the launching stream, and

@@ -86,6 +86,8 @@ SIGNATURES = {
     "tls_group_create": (_I32, [_I32, C.POINTER(_P)]),
     "tls_group_destroy": (None, [_P]),
     "tls_comm_init_group": (_I32, [_P, _P, _I32]),
+    "tls_comm_init_record": (_I32, [_P, _I32, _I32]),
+    "tls_comm_record_log": (_I64, [_P, _P, _I64]),
 }
 
 _lib = None

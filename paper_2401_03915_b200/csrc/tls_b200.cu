@@ -1941,6 +1941,26 @@ int32_t tls_comm_init_nccl(tls_ctx* ctx, const void* unique_id, int32_t nranks, 
   return TLS_OK;
 }
 
+// test transport: capturable, moves nothing, logs the collective sequence (RecordComm)
+int32_t tls_comm_init_record(tls_ctx* ctx, int32_t nranks, int32_t rank) {
+  if (!ctx || nranks < 2 || rank < 0 || rank >= nranks) return ctx ? fail(ctx, TLS_ERR_ARG, "bad record comm") : TLS_ERR_ARG;
+  auto* c = new RecordComm();
+  c->rank = rank;
+  c->nranks = nranks;
+  delete ctx->comm;
+  ctx->comm = c;
+  destroy_graphs(ctx);
+  return TLS_OK;
+}
+
+int64_t tls_comm_record_log(const tls_ctx* ctx, int64_t* out, int64_t cap) {
+  auto* rc = ctx ? dynamic_cast<RecordComm*>(ctx->comm) : nullptr;
+  if (!rc) return -1;
+  const int64_t n = (int64_t)rc->log.size();
+  for (int64_t i = 0; i < std::min(n, cap); ++i) out[i] = rc->log[i];
+  return n;
+}
+
 int32_t tls_group_create(int32_t nmembers, tls_group** out) {
   if (!out || nmembers < 1 || nmembers > MAX_GROUP) return TLS_ERR_ARG;
   auto* g = new tls_group(nmembers);

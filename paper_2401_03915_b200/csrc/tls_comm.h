@@ -121,6 +121,23 @@ struct NcclComm : Comm {
   bool capturable() const override { return true; }
 };
 
+// ---------------------------------------------------------------- recording (tests)
+// Capturable stand-in that moves no data and logs every collective the schedule issues
+// (kind, element count, peers): lets a single-GPU test capture the sharded PCG / GMRES graphs
+// exactly as the NCCL transport would and compare the per-rank collective sequences.
+struct RecordComm : Comm {
+  std::vector<long long> log;  // triples: kind (1 all-reduce, 2 exchange), count, peers
+  cudaError_t allreduce_sum(double*, long long count, cudaStream_t, std::string&) override {
+    log.insert(log.end(), {1LL, count, 0LL});
+    return cudaSuccess;
+  }
+  cudaError_t exchange(const XPlan& x, cudaStream_t, std::string&) override {
+    log.insert(log.end(), {2LL, x.stot + x.rtot, (long long)x.peers.size()});
+    return cudaSuccess;
+  }
+  bool capturable() const override { return true; }
+};
+
 // ---------------------------------------------------------------- in-process group
 struct GroupPtrs {
   const double* p[MAX_GROUP];

@@ -181,3 +181,44 @@ def test_sharded_nonsymmetric_unrestarted_gmres_and_unpreconditioned(B):
         assert abs(rep.iterations - int(d["iterations"])) <= 1
         np.testing.assert_allclose(x, d["x"], rtol=0, atol=1e-8 * np.abs(d["x"]).max())
     assert np.array_equal(res[0][1], res[1][1])
+
+
+@pytest.mark.parametrize("name,solver", [("cfg2_m24", "pcg"), ("cfg3_m64", "gmres")])
+def test_sharded_schedule_captures_into_graphs(B, name, solver):
+    """The NCCL transport runs the sharded schedule inside captured CUDA graphs; the in-process
+    group cannot be captured (host barriers).  Here each rank's handle gets a recording
+    transport (capturable, moves no data, logs every collective) and runs the solve through the
+    graph path: capture must succeed, and every rank must issue the same collective sequence
+    (kinds and all-reduce sizes) -- the condition for NCCL not to deadlock."""
+    import ctypes as C
+    d = dict(golden(name))
+    a = golden_csr(d)
+
+    def fn(shard):
+        mat = B.SparseMat(a, symmetric=bool(d["symmetric"]))
+        pre = B.setup(mat, int(d["n_sub"]), overlap=int(d["overlap"]), owner=d["owner"],
+                      coarse=str(d["coarse"]), n_modes=int(d["n_modes"]), shard=shard)
+        return mat, pre
+
+    res = _group_run(2, fn)
+    logs = []
+    for rank, (mat, pre) in enumerate(res):
+        h = pre.handle
+        h.check(h.lib.tls_comm_init_record(h.ctx, 2, rank))
+        try:  # the numbers are meaningless without data exchange; only the schedule matters
+            if solver == "pcg":
+                B.pcg(mat, pre, d["b"], tol=1e-30, maxit=30)
+            else:
+                B.gmres(mat, pre, d["b"], tol=1e-30, maxit=20, restart=10)
+        except Exception as e:  # noqa: BLE001  (breakdown on partial dot products is fine)
+            assert "curvature" in str(e) or "breakdown" in str(e).lower(), e
+        n = h.lib.tls_comm_record_log(h.ctx, None, 0)
+        buf = (C.c_int64 * n)()
+        h.lib.tls_comm_record_log(h.ctx, buf, n)
+        log = np.array(buf[:], dtype=np.int64).reshape(-1, 3)
+        logs.append(log)
+    assert len(logs[0]) > 25 and len(logs[0]) == len(logs[1])
+    assert np.array_equal(logs[0][:, 0], logs[1][:, 0])
+    ar = logs[0][:, 0] == 1
+    assert np.array_equal(logs[0][ar, 1], logs[1][ar, 1])
+    assert (logs[0][:, 0] == 2).any()  # halo exchanges are part of the captured schedule
