@@ -203,6 +203,13 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms,
 int32_t tls_set_kernel_timing(tls_ctx* ctx, int32_t on);
 int32_t tls_kernel_timing(const tls_ctx* ctx, double* avg_ms, int64_t* count);
 
+/* ---- setup: banded Cholesky of a batch of SPD blocks (factor order, dense ld x ld row-major,
+ * ld = 64 nbk) in place on the device, one CTA per block, DMMA tile products; reach[J] (host,
+ * multiple of 64) = end row of the band below panel J; dinv receives the inverted 64 x 64
+ * diagonal blocks (count x nbk x 64 x 64), info the 1-based first non-positive pivot row. */
+int32_t tls_band_cholesky(double* ap, int64_t ld, int32_t count, const int32_t* reach, int32_t nbk,
+                          double* dinv, int32_t* info, void* stream);
+
 /* ---- Matrix Market ingest / output (src/sparsemat.py:201-372).
  * Host-side, multithreaded.  tls_mm_parse / tls_mm_load parse text / a file (nthreads <= 0: all
  * host threads) with the reference's dialect, validation order and error texts; on

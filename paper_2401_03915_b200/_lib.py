@@ -72,6 +72,7 @@ SIGNATURES = {
     "tls_set_halo": (_I32, [_P, _I32, _P, _P, _P, _P, _P]),
     "tls_set_remote_contrib": (_I32, [_P, _I32, _P, _P, _P, _P]),
     "tls_set_local_kind": (_I32, [_P, _I32]),
+    "tls_band_cholesky": (_I32, [_P, _I64, _I32, _P, _I32, _P, _P, _P]),
     "tls_mm_parse": (_I32, [C.c_char_p, _I64, _I32, C.POINTER(_P)]),
     "tls_mm_load": (_I32, [C.c_char_p, _I32, C.POINTER(_P)]),
     "tls_mm_info": (_I32, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I32),

@@ -1823,6 +1823,26 @@ int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first_g, int32_t count, co
   return TLS_OK;
 }
 
+// ---- setup: banded Cholesky of a batch (K9, DMMA) ----------------------------------------------
+int32_t tls_band_cholesky(double* ap, int64_t ld, int32_t count, const int32_t* reach, int32_t nbk,
+                          double* dinv, int32_t* info, void* stream) {
+  if (!ap || !dinv || !info || !reach || count <= 0 || nbk <= 0 || ld != 64LL * nbk) return TLS_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int J = 0; J < nbk; ++J)
+    if (reach[J] < 64 * (J + 1) || reach[J] > ld || reach[J] % 64) return TLS_ERR_ARG;
+  const size_t smem = sizeof(double) * 5 * 64 * CP;
+  static size_t set = 48 * 1024;
+  if (raise_smem((const void*)k_band_chol, smem, set) != cudaSuccess) return TLS_ERR_CUDA;
+  int* d_reach = nullptr;
+  if (cudaMallocAsync((void**)&d_reach, sizeof(int) * nbk, s) != cudaSuccess) return TLS_ERR_OOM;
+  if (cudaMemcpyAsync(d_reach, reach, sizeof(int) * nbk, cudaMemcpyHostToDevice, s) != cudaSuccess) return TLS_ERR_CUDA;
+  k_band_chol<<<count, 256, smem, s>>>(ap, ld, d_reach, nbk, dinv, info);
+  if (cudaGetLastError() != cudaSuccess) return TLS_ERR_CUDA;
+  cudaFreeAsync(d_reach, s);
+  // the host array must outlive the async copy
+  return cudaStreamSynchronize(s) == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;
+}
+
 // ---- sharding -------------------------------------------------------------------------------
 int32_t tls_set_row_partition(tls_ctx* ctx, int64_t n, const int32_t* new_of_old, int32_t nranks,
                               const int32_t* row_starts, int32_t rank) {

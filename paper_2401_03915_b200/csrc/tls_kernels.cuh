@@ -1096,6 +1096,132 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
   for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
 }
 
+// ---------------------------------------------------------------------------------------
+// K9  Banded Cholesky of a batch of SPD blocks (setup; src/subdomain.py:80-82 in the factor
+//     order), one CTA per block, the whole right-looking blocked factorisation in ONE launch:
+//     per 64-column panel J, the 64 x 64 diagonal block is factored and inverted in shared
+//     memory, the panel below it (rows up to reach[J], the band's lowest reach) becomes
+//     P L_JJ^{-T}, and the trailing band square is updated T -= P P^T -- the two tile products
+//     on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64).  Rows/columns outside the envelope
+//     stay zero (no fill outside the profile).  Writes the factor in place (lower; the strict
+//     upper part of the diagonal blocks is left for the caller to clear), the inverted diagonal
+//     blocks to dinv (nbk x 64 x 64 row-major per block) and info = 1-based row of the first
+//     non-positive pivot (0: SPD).  Dynamic smem: 5 padded 64 x 65 tiles.
+// ---------------------------------------------------------------------------------------
+constexpr int CP = 65;  // padded smem tile row
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+// acc(64 x 64) = X (64 x 64, smem, padded) * Y^T (Y 64 x 64, smem, padded); warp w owns output
+// rows 8w..8w+7 (8 blocks of 8 x 8, 16 doubles per lane)
+__device__ __forceinline__ void tile_xyt(const double* X, const double* Y, double (&acc)[8][2]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gr = lane >> 2, gc = lane & 3;
+#pragma unroll
+  for (int bj = 0; bj < 8; ++bj) acc[bj][0] = acc[bj][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < 64; k0 += 4) {
+    const double a = X[(8 * w + gr) * CP + k0 + gc];
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj) dmma_8x8x4(acc[bj][0], acc[bj][1], a, Y[(8 * bj + gr) * CP + k0 + gc]);
+  }
+}
+__device__ __forceinline__ void load_tile(double* T, const double* G, long long ld) {
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) T[(e >> 6) * CP + (e & 63)] = G[(long long)(e >> 6) * ld + (e & 63)];
+}
+
+__global__ void __launch_bounds__(256, 1) k_band_chol(double* __restrict__ AP, long long ld, const int* __restrict__ reach,
+                                                      int nbk, double* __restrict__ dinv, int* __restrict__ info) {
+  extern __shared__ __align__(16) double cs[];
+  double* Ds = cs;                 // diagonal block -> L_JJ (lower)
+  double* Ls = Ds + 64 * CP;       // L_JJ^{-1}
+  double* Ta = Ls + 64 * CP;
+  double* Tb = Ta + 64 * CP;
+  double* Tc = Tb + 64 * CP;
+  __shared__ int bad;
+  double* A = AP + (long long)blockIdx.x * ld * ld;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, gr = lane >> 2, gc = lane & 3;
+  if (tid == 0) bad = 0;
+  for (int J = 0; J < nbk; ++J) {
+    const long long j0 = 64LL * J;
+    load_tile(Ds, A + j0 * ld + j0, ld);
+    __syncthreads();
+    // 64 x 64 Cholesky in shared memory (right-looking, lower triangle only)
+    for (int k = 0; k < 64; ++k) {
+      if (tid == 0) {
+        double d = Ds[k * CP + k];
+        if (!(d > 0.0)) {
+          if (bad == 0) bad = (int)(j0 + k + 1);
+          d = 1.0;  // keep going without NaNs; the caller raises on info
+        }
+        Ds[k * CP + k] = sqrt(d);
+      }
+      __syncthreads();
+      const double piv = Ds[k * CP + k];
+      for (int i = k + 1 + tid; i < 64; i += blockDim.x) Ds[i * CP + k] /= piv;
+      __syncthreads();
+      const int m = 63 - k;
+      for (int e = tid; e < m * m; e += blockDim.x) {
+        const int i = k + 1 + e / m, j = k + 1 + e % m;
+        if (j <= i) Ds[i * CP + j] -= Ds[i * CP + k] * Ds[j * CP + k];
+      }
+      __syncthreads();
+    }
+    // inverse of the lower-triangular L_JJ, one column per thread (forward substitution)
+    if (tid < 64) {
+      const int j = tid;
+      for (int i = 0; i < j; ++i) Ls[i * CP + j] = 0.0;
+      Ls[j * CP + j] = 1.0 / Ds[j * CP + j];
+      for (int i = j + 1; i < 64; ++i) {
+        double acc = 0.0;
+        for (int q = j; q < i; ++q) acc += Ds[i * CP + q] * Ls[q * CP + j];
+        Ls[i * CP + j] = -acc / Ds[i * CP + i];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < 64 * 64; e += blockDim.x) {
+      const int r = e >> 6, c = e & 63;
+      A[(j0 + r) * ld + j0 + c] = Ds[r * CP + c];
+      dinv[((long long)blockIdx.x * nbk + J) * 4096 + e] = Ls[r * CP + c];
+    }
+    const int mt = (int)((reach[J] - j0 - 64) / 64);
+    // panel: P_t <- P_t L_JJ^{-T}
+    for (int t = 0; t < mt; ++t) {
+      double* G = A + (j0 + 64 + 64LL * t) * ld + j0;
+      __syncthreads();
+      load_tile(Ta, G, ld);
+      __syncthreads();
+      double acc[8][2];
+      tile_xyt(Ta, Ls, acc);
+#pragma unroll
+      for (int bj = 0; bj < 8; ++bj) {
+        G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc] = acc[bj][0];
+        G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc + 1] = acc[bj][1];
+      }
+    }
+    __syncthreads();
+    // trailing band square: T(ti, tj) -= P_ti P_tj^T, tj <= ti
+    for (int ti = 0; ti < mt; ++ti) {
+      load_tile(Ta, A + (j0 + 64 + 64LL * ti) * ld + j0, ld);
+      for (int tj = 0; tj <= ti; ++tj) {
+        double* G = A + (j0 + 64 + 64LL * ti) * ld + j0 + 64 + 64LL * tj;
+        load_tile(Tb, A + (j0 + 64 + 64LL * tj) * ld + j0, ld);
+        __syncthreads();
+        double acc[8][2];
+        tile_xyt(Ta, Tb, acc);
+#pragma unroll
+        for (int bj = 0; bj < 8; ++bj) {
+          G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc] -= acc[bj][0];
+          G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc + 1] -= acc[bj][1];
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) info[blockIdx.x] = bad;
+}
+
 // pack band steps of one subdomain batch: L (row-major ld x ld, factor order, identity
 // padding) and the inverted diagonal tiles dinv (nbmax x 64 x 64 row-major per subdomain)
 __global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, const double* __restrict__ L,

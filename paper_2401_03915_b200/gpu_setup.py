@@ -759,6 +759,35 @@ def _band_cholesky_inplace(torch, AP, kmax):
     return AP, info
 
 
+BAND_CHOL = os.environ.get("TLS_BAND_CHOL", "kernel")
+
+
+def _band_reach(kmax, nbk):
+    """End row of the band below each panel J: rows I > J with I - kmax[I] <= J."""
+    rows = np.arange(nbk)
+    out = np.empty(nbk, dtype=np.int32)
+    for J in range(nbk):
+        r = rows[(rows > J) & (rows - kmax <= J)]
+        out[J] = (int(r.max()) + 1) * 64 if r.size else (J + 1) * 64
+    return out
+
+
+def band_cholesky_kernel(torch, AP, kmax):
+    """K9 (libtls_b200 ``tls_band_cholesky``): in-place banded Cholesky of the batch AP
+    (cnt, ld, ld) in factor order; returns (L, Dinv, info) like the library path."""
+    cnt, ld, _ = AP.shape
+    nbk = ld // 64
+    reach = _band_reach(np.asarray(kmax, dtype=np.int64), nbk)
+    Dinv = torch.empty((cnt, nbk, 64, 64), dtype=torch.float64, device=AP.device)
+    info = torch.empty(cnt, dtype=torch.int32, device=AP.device)
+    rc = _lib.load().tls_band_cholesky(_lib.ptr(AP), ld, cnt, _lib.ptr(reach), nbk, _lib.ptr(Dinv),
+                                       _lib.ptr(info), stream_ptr())
+    if rc != 0:
+        raise RuntimeError(f"tls_band_cholesky failed ({rc})")
+    AP.masked_fill_(torch.ones(ld, ld, dtype=torch.bool, device=AP.device).triu_(1), 0.0)
+    return AP, Dinv, info
+
+
 def _band_factor(torch, A, perm_list, n_list, ld):
     """Lexicographic factor order, band profile, Cholesky and diagonal-tile inverses of a batch.
 
@@ -779,10 +808,13 @@ def _band_factor(torch, A, perm_list, n_list, ld):
     # leading all-zero 8-column strips of each panel (the factor keeps the profile of A_P)
     fz = ((fmin % 64) // 8).cpu().numpy().astype(np.int32)
     fz = np.where(kc > 0, fz, 0)
-    L, info = _band_cholesky_inplace(torch, AP, kc.max(axis=0))
-    Ld = L.view(cnt, nbk, 64, nbk, 64).diagonal(dim1=1, dim2=3).permute(0, 3, 1, 2)
-    eye = torch.eye(64, dtype=torch.float64, device=dev).expand(cnt, nbk, 64, 64)
-    Dinv = torch.linalg.solve_triangular(Ld, eye, upper=False).contiguous()
+    if BAND_CHOL == "torch":  # library path (batched cuSOLVER potrf / trsm + bmm per panel)
+        L, info = _band_cholesky_inplace(torch, AP, kc.max(axis=0))
+        Ld = L.view(cnt, nbk, 64, nbk, 64).diagonal(dim1=1, dim2=3).permute(0, 3, 1, 2)
+        eye = torch.eye(64, dtype=torch.float64, device=dev).expand(cnt, nbk, 64, 64)
+        Dinv = torch.linalg.solve_triangular(Ld, eye, upper=False).contiguous()
+    else:  # in-tree K9: one launch for the batch, DMMA tile products
+        L, Dinv, info = band_cholesky_kernel(torch, AP, kc.max(axis=0))
     kcnts = [kc[b, : -(-n_list[b] // 64)] for b in range(cnt)]
     codes = [(kc[b] | (fz[b] << 16))[: -(-n_list[b] // 64)].astype(np.int32) for b in range(cnt)]
     return L, Dinv, perms, kcnts, info, P, codes
