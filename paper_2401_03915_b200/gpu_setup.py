@@ -808,7 +808,8 @@ def _band_factor(torch, A, perm_list, n_list, ld):
     # leading all-zero 8-column strips of each panel (the factor keeps the profile of A_P)
     fz = ((fmin % 64) // 8).cpu().numpy().astype(np.int32)
     fz = np.where(kc > 0, fz, 0)
-    if BAND_CHOL == "torch":  # library path (batched cuSOLVER potrf / trsm + bmm per panel)
+    if BAND_CHOL == "torch" or not AP.is_cuda:  # library path (batched potrf / trsm + bmm per
+        # panel); also the CPU-tensor path the host tests of the setup algebra use
         L, info = _band_cholesky_inplace(torch, AP, kc.max(axis=0))
         Ld = L.view(cnt, nbk, 64, nbk, 64).diagonal(dim1=1, dim2=3).permute(0, 3, 1, 2)
         eye = torch.eye(64, dtype=torch.float64, device=dev).expand(cnt, nbk, 64, 64)
