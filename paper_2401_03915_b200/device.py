@@ -12,7 +12,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .errors import BreakdownError, SubdomainSetupError
+from .errors import SubdomainSetupError
 
 
 def _torch():
@@ -98,6 +98,3 @@ def to_device(v, n, device):
     t = torch.from_numpy(np.ascontiguousarray(a)).to(torch.device("cuda", device))
     return t, (lambda out: out.cpu().numpy())
 
-
-def raise_breakdown(st):
-    raise BreakdownError(int(st.iteration), float(st.value))
