@@ -132,6 +132,7 @@ struct tls_ctx {
   double band_bytes = 0.0;            // stored factor bytes (read twice per apply)
   size_t band_smem = 0;
   int band_pf = 2;                    // L2 prefetch distance of k_band_solve (items)
+  int band_unr = 1;                   // tiles per load round (k_band_solve<UNR>)
   // ---- sharding: this handle owns global subdomains [own_lo, own_hi) and the
   // rows [r0, r1) of the internal numbering (rows renumbered rank by rank: nofo[g] = internal id
   // of caller row g; identity and [0, n) on one GPU)
@@ -291,8 +292,12 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
       }
       CK(cudaEventRecordWithFlags(ctx->kt_a[ctx->kt_n], s, cudaEventRecordExternal));
     }
-    k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
-                                                         r_src ? ctx->d_gidx : nullptr, r_src);
+    if (ctx->band_unr == 2)
+      k_band_solve<2><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
+                                                              r_src ? ctx->d_gidx : nullptr, r_src);
+    else
+      k_band_solve<1><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
+                                                              r_src ? ctx->d_gidx : nullptr, r_src);
     CKL();
     if (timed) CK(cudaEventRecordWithFlags(ctx->kt_b[ctx->kt_n++], s, cudaEventRecordExternal));
     if (which == L_LOCAL) return TLS_OK;
@@ -740,8 +745,17 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     }
     TRY(upload(ctx, ctx->d_band, ctx->h_band.data(), n_sub));
     ctx->band_smem = sizeof(double) * ((size_t)maxnb * TT + 8 * TT + TT);
-    static size_t smem_set = 0;
-    CK(raise_smem((const void*)k_band_solve, ctx->band_smem, smem_set));
+    static size_t smem_set = 0, smem_set2 = 0;
+    CK(raise_smem((const void*)k_band_solve<1>, ctx->band_smem, smem_set));
+    CK(raise_smem((const void*)k_band_solve<2>, ctx->band_smem, smem_set2));
+    // one tile per load round: two (UNR = 2, 128 registers, 2 CTAs/SM) measured slower on
+    // configuration 3 (1,249 vs 1,300 it/s) and mixed on 8-rank configuration 2 slabs
+    // (profiles/ab_band_unr_r01.txt); kept selectable for the few-subdomains-per-GPU regime
+    ctx->band_unr = 1;
+    if (const char* e = getenv("TLS_BAND_UNR")) {
+      const int v = atoi(e);
+      if (v == 1 || v == 2) ctx->band_unr = v;
+    }
     // prefetch distance 2 items (measured: 4 and 6 lose 1-15% on configurations 2 and 3 --
     // tools/sweep_pf.sh, profiles/pf_sweep_r01.txt)
     ctx->band_pf = 2;
@@ -1599,8 +1613,12 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   for (int i = 0; i <= reps; ++i) {
     if (i == 1) CK(cudaEventRecord(e0, s));
     if (band)
-      k_band_solve<<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr, ctx->band_pf,
-                                                           nullptr, nullptr);
+      if (ctx->band_unr == 2)
+        k_band_solve<2><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr,
+                                                                ctx->band_pf, nullptr, nullptr);
+      else
+        k_band_solve<1><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr,
+                                                                ctx->band_pf, nullptr, nullptr);
     else
       k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
     CKL();

@@ -918,7 +918,11 @@ __device__ __forceinline__ int udiag_strip_off(int w) { return 32 * w * w + 32 *
 // pf: L2 prefetch distance in items (2 measured best; TLS_BAND_PF overrides for sweeps)
 // gidx != nullptr: the restriction R_i r is fused into the load (v[p] = r[gidx[xoff + p]],
 // K2 without its own launch and without the xloc round trip); otherwise v = x[xoff ...]
-__global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restrict__ bands,
+// UNR = tiles loaded per round (1: 64 registers, 4 CTAs/SM -- many subdomains per GPU; 2: two
+// tiles in flight per warp, 2 CTAs/SM -- few subdomain CTAs per SM, where one CTA's sweep is the
+// critical path).  Both accumulate in the same order (bit-identical results).
+template <int UNR>
+__global__ void __launch_bounds__(NTHR, UNR == 1 ? 4 : 2) k_band_solve(const BandDesc* __restrict__ bands,
                                                         const double* __restrict__ x,
                                                         double* __restrict__ y, const int* done,
                                                         int pf, const int* __restrict__ gidx,
@@ -950,16 +954,29 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
     const double* blk = b.data + b.step_off[I];
     const int code = b.kcnt[I], K = code & 0xffff, fz = code >> 16;
     double ra0 = 0.0, ra1 = 0.0;
-    for (int k = 0; k < K; ++k) {
-      if (threadIdx.x == 0) prefetch_fwd_item(b, I, k + pf);  // pf items ahead, into L2
-      if (k * 8 + warp < fz) continue;               // strip left of the band profile: zeros
-      const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
-      double2 w[8];
+    for (int k = 0; k < K; k += UNR) {
+      if (threadIdx.x == 0) {                        // pf items ahead, into L2
+        prefetch_fwd_item(b, I, k + pf);
+        if (UNR == 2 && k + 1 < K) prefetch_fwd_item(b, I, k + 1 + pf);
+      }
+      double2 w[UNR][8];
+      bool act[UNR];
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) w[kk] = ldg_stream2(tp + kk * TT);
-      const double* uj = v + (I - K + k) * TT + c0;
+      for (int q = 0; q < UNR; ++q) {
+        act[q] = k + q < K && !((k + q) * 8 + warp < fz);  // strips left of the profile: zeros
+        if (act[q]) {
+          const double* tp = blk + (long long)(k + q) * TT * TT + c0 * TT + 2 * lane;
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) { ra0 += w[kk].x * uj[kk]; ra1 += w[kk].y * uj[kk]; }
+          for (int kk = 0; kk < 8; ++kk) w[q][kk] = ldg_stream2(tp + kk * TT);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        if (!act[q]) continue;
+        const double* uj = v + (I - K + k + q) * TT + c0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) { ra0 += w[q][kk].x * uj[kk]; ra1 += w[q][kk].y * uj[kk]; }
+      }
     }
     if (threadIdx.x == 0) prefetch_fwd_item(b, I, K + pf);
     red[warp * TT + 2 * lane] = ra0;
@@ -1004,16 +1021,29 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
       const double* blk = b.udata + b.ustep_off[I];
       const int code = b.ucnt[I], R = code & 0xffff, tz = code >> 16;
       double ra0 = 0.0, ra1 = 0.0;
-      for (int k = 0; k < R; ++k) {
-        if (threadIdx.x == 0) prefetch_u_item(b, I, k + pf);
-        if (k * 8 + warp >= 8 * R - tz) continue;    // strip right of the band profile: zeros
-        const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
-        double2 w[8];
+      for (int k = 0; k < R; k += UNR) {
+        if (threadIdx.x == 0) {
+          prefetch_u_item(b, I, k + pf);
+          if (UNR == 2 && k + 1 < R) prefetch_u_item(b, I, k + 1 + pf);
+        }
+        double2 w[UNR][8];
+        bool act[UNR];
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) w[kk] = ldg_stream2(tp + kk * TT);
-        const double* yj = v + (I + 1 + k) * TT + c0;
+        for (int q = 0; q < UNR; ++q) {
+          act[q] = k + q < R && !((k + q) * 8 + warp >= 8 * R - tz);  // right of the profile
+          if (act[q]) {
+            const double* tp = blk + (long long)(k + q) * TT * TT + c0 * TT + 2 * lane;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) { ra0 += w[kk].x * yj[kk]; ra1 += w[kk].y * yj[kk]; }
+            for (int kk = 0; kk < 8; ++kk) w[q][kk] = ldg_stream2(tp + kk * TT);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          if (!act[q]) continue;
+          const double* yj = v + (I + 1 + k + q) * TT + c0;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) { ra0 += w[q][kk].x * yj[kk]; ra1 += w[q][kk].y * yj[kk]; }
+        }
       }
       if (threadIdx.x == 0) prefetch_u_item(b, I, R + pf);
       red[warp * TT + 2 * lane] = ra0;
@@ -1078,18 +1108,31 @@ __global__ void __launch_bounds__(NTHR, 4) k_band_solve(const BandDesc* __restri
       __syncthreads();
     }
     const double y0 = v[J * TT + 2 * lane], y1 = v[J * TT + 2 * lane + 1];
-    for (int k = 0; k < K; ++k) {
-      if (threadIdx.x == 0) prefetch_bwd_item(b, J, k + 1 + pf);
-      if (k * 8 + warp < fz) continue;
-      const double* tp = blk + (long long)k * TT * TT + c0 * TT + 2 * lane;
-      double cp[8];
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const double2 w = ldg_stream2(tp + kk * TT);
-        cp[kk] = w.x * y0 + w.y * y1;
+    for (int k = 0; k < K; k += UNR) {
+      if (threadIdx.x == 0) {
+        prefetch_bwd_item(b, J, k + 1 + pf);
+        if (UNR == 2 && k + 1 < K) prefetch_bwd_item(b, J, k + 2 + pf);
       }
-      const double val = warp_reduce8(cp, lane);
-      if ((lane & 3) == 0) v[(J - K + k) * TT + c0 + colsel] -= val;
+      double2 w[UNR][8];
+      bool act[UNR];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        act[q] = k + q < K && !((k + q) * 8 + warp < fz);
+        if (act[q]) {
+          const double* tp = blk + (long long)(k + q) * TT * TT + c0 * TT + 2 * lane;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) w[q][kk] = ldg_stream2(tp + kk * TT);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        if (!act[q]) continue;
+        double cp[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) cp[kk] = w[q][kk].x * y0 + w[q][kk].y * y1;
+        const double val = warp_reduce8(cp, lane);
+        if ((lane & 3) == 0) v[(J - K + k + q) * TT + c0 + colsel] -= val;
+      }
     }
     __syncthreads();
   }
