@@ -295,7 +295,6 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_2401_03915_b200 as B
-    from paper_2401_03915_b200 import _lib
     from paper_2401_03915_b200 import build as BLD
     BLD.build()
 

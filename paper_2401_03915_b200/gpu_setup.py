@@ -37,7 +37,6 @@ a library call on the SETUP path; the per-iteration path is all in-tree CUDA.
 
 from __future__ import annotations
 
-import math
 import os
 import time
 import warnings

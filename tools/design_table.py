@@ -1,5 +1,4 @@
 """Markdown table of the measured bench lines (profiles/bench_cfg*_<round>.json) for DESIGN.md."""
-import glob
 import json
 import os
 import sys

@@ -13,7 +13,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np  # noqa: E402
+
 import torch  # noqa: E402
 
 import paper_2401_03915_b200 as B  # noqa: E402
