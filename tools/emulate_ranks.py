@@ -67,6 +67,10 @@ for N in Ns:
         for rank, (mat, pre) in enumerate(res):
             h = pre.handle
             h.check(h.lib.tls_comm_init_record(h.ctx, N, rank))
+            if os.environ.get("TLS_PROFILE_RANGE") == "1" and rank == 1:  # ncu on one rank's solve
+                torch.cuda.profiler.start()
+                timed(mat, pre, 25)
+                torch.cuda.profiler.stop()
             timed(mat, pre, 25)
             t25, _ = timed(mat, pre, 25)
             t75, its = timed(mat, pre, 75)
