@@ -29,6 +29,8 @@ namespace {
 constexpr int PCG_GRAPH_ITERS = 25;  // replacement period of src/krylov.py:88
 constexpr int MAX_GRID = 148 * 8;    // 148 SMs x 8 resident 256-thread CTAs
 constexpr int GM_FUSED_MAXCOLS = 96; // fused CGS2 step while (nc + 1) x 256 doubles fit in smem
+constexpr int RING_S = 4;            // tiles in flight per warp in k_band_solve_ring
+constexpr size_t RING_BYTES = sizeof(double) * 8 * RING_S * 512;
 
 template <class T>
 void dfree(T*& p) {
@@ -133,6 +135,7 @@ struct tls_ctx {
   size_t band_smem = 0;
   int band_pf = 2;                    // L2 prefetch distance of k_band_solve (items)
   int band_unr = 1;                   // tiles per load round (k_band_solve<UNR>)
+  int band_ring = 0;                  // k_band_solve_ring (per-warp cp.async rings)
   // ---- sharding: this handle owns global subdomains [own_lo, own_hi) and the
   // rows [r0, r1) of the internal numbering (rows renumbered rank by rank: nofo[g] = internal id
   // of caller row g; identity and [0, n) on one GPU)
@@ -292,7 +295,10 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
       }
       CK(cudaEventRecordWithFlags(ctx->kt_a[ctx->kt_n], s, cudaEventRecordExternal));
     }
-    if (ctx->band_unr == 2)
+    if (ctx->band_ring)
+      k_band_solve_ring<RING_S><<<ctx->nsub, NTHR, ctx->band_smem + RING_BYTES, s>>>(
+          ctx->d_band, ctx->xloc, ctx->yloc, done, r_src ? ctx->d_gidx : nullptr, r_src);
+    else if (ctx->band_unr == 2)
       k_band_solve<2><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
                                                               r_src ? ctx->d_gidx : nullptr, r_src);
     else
@@ -745,9 +751,15 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     }
     TRY(upload(ctx, ctx->d_band, ctx->h_band.data(), n_sub));
     ctx->band_smem = sizeof(double) * ((size_t)maxnb * TT + 8 * TT + TT);
-    static size_t smem_set = 0, smem_set2 = 0;
+    static size_t smem_set = 0, smem_set2 = 0, smem_set3 = 0;
     CK(raise_smem((const void*)k_band_solve<1>, ctx->band_smem, smem_set));
     CK(raise_smem((const void*)k_band_solve<2>, ctx->band_smem, smem_set2));
+    CK(raise_smem((const void*)k_band_solve_ring<RING_S>, ctx->band_smem + RING_BYTES, smem_set3));
+    // per-warp cp.async rings (1 CTA/SM) when all subdomains fit one wave of the SMs: measured
+    // 0.79 -> 0.57 ms per iteration on an 8-rank configuration-2 slab (64 subdomains); with more
+    // subdomains than SMs the 4-CTA/SM kernel wins (cfg3: 1,293 vs 1,045 it/s; ab_band_ring_r01)
+    ctx->band_ring = n_sub <= 148 ? 1 : 0;
+    if (const char* e = getenv("TLS_BAND_RING")) ctx->band_ring = atoi(e) != 0;
     // one tile per load round: two (UNR = 2, 128 registers, 2 CTAs/SM) measured slower on
     // configuration 3 (1,249 vs 1,300 it/s) and mixed on 8-rank configuration 2 slabs
     // (profiles/ab_band_unr_r01.txt); kept selectable for the few-subdomains-per-GPU regime
@@ -1613,7 +1625,10 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   for (int i = 0; i <= reps; ++i) {
     if (i == 1) CK(cudaEventRecord(e0, s));
     if (band)
-      if (ctx->band_unr == 2)
+      if (ctx->band_ring)
+        k_band_solve_ring<RING_S><<<ctx->nsub, NTHR, ctx->band_smem + RING_BYTES, s>>>(
+            ctx->d_band, ctx->xloc, ctx->yloc, nullptr, nullptr, nullptr);
+      else if (ctx->band_unr == 2)
         k_band_solve<2><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr,
                                                                 ctx->band_pf, nullptr, nullptr);
       else

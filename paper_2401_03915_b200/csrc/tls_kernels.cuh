@@ -1265,6 +1265,255 @@ __global__ void __launch_bounds__(256, 1) k_band_chol(double* __restrict__ AP, l
   if (tid == 0) info[blockIdx.x] = bad;
 }
 
+// ---------------------------------------------------------------------------------------
+// K3d  k_band_solve_ring<S>: the same sweeps as k_band_solve, but every warp streams ITS slice of
+//      the panel tiles (8 columns x 64 rows = 4 KB) through a private S-deep shared-memory ring
+//      with cp.async (16 B per lane, one commit group per tile): S tiles are always in flight per
+//      warp, across step boundaries (the tiles do not depend on the solve), so a sweep never
+//      waits on DRAM latency when one CTA holds an SM -- the regime of few subdomains per GPU
+//      (ncu on k_band_solve there: long-scoreboard + barrier stalls, 37% L2 hits).  One CTA per
+//      SM (ring + local vector); same arithmetic order as k_band_solve (bit-identical results).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// producer cursor over one stream of panel tiles (forward: L by ascending steps; bwd: L by
+// descending steps; U: U by descending steps); issues this warp's slice of the next tile
+struct RingProducer {
+  int I, k, slot;
+  __device__ __forceinline__ void issue(const BandDesc& b, int mode, double* ring, int warp, int lane, int S) {
+    const int c0 = warp * 8;
+    // advance to the next existing tile
+    while (I >= 0 && I < b.nb) {
+      const int code = mode == 2 ? b.ucnt[I] : b.kcnt[I];
+      const int K = code & 0xffff;
+      if (k < K) break;
+      I += mode == 0 ? 1 : -1;
+      k = 0;
+    }
+    if (I >= 0 && I < b.nb) {
+      const int code = mode == 2 ? b.ucnt[I] : b.kcnt[I];
+      const int K = code & 0xffff, z = code >> 16;
+      const bool zero = mode == 2 ? (k * 8 + warp >= 8 * K - z) : (k * 8 + warp < z);
+      if (!zero) {
+        const double* base = mode == 2 ? b.udata + b.ustep_off[I] : b.data + b.step_off[I];
+        const double* tp = base + (long long)k * TT * TT + c0 * TT + 2 * lane;
+        double* dst = ring + (long long)slot * 512 + 2 * lane;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) cp_async16(dst + kk * 64, tp + kk * TT);
+      }
+      ++k;
+    }
+    cp_async_commit();  // (possibly empty) group: one per consumed position
+    slot = slot + 1 == S ? 0 : slot + 1;
+  }
+};
+
+template <int S>
+__global__ void __launch_bounds__(NTHR, 1) k_band_solve_ring(const BandDesc* __restrict__ bands,
+                                                             const double* __restrict__ x,
+                                                             double* __restrict__ y, const int* done,
+                                                             const int* __restrict__ gidx,
+                                                             const double* __restrict__ r) {
+  if (done && *done) return;
+  extern __shared__ __align__(16) double sm[];
+  const BandDesc b = bands[blockIdx.x];
+  const int npad = b.nb * TT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c0 = warp * 8;
+  double* ringw = sm + (long long)warp * S * 512;  // this warp's ring (S x 512 doubles)
+  double* v = sm + 8 * S * 512;
+  double* red = v + npad;
+  double* t = red + 8 * TT;
+  const int dlen = TT - 8 * warp;
+  const bool drow = lane >= 4 * warp;
+  const int doff = diag_strip_off(warp) + (2 * lane - 8 * warp);
+  RingProducer prod{0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < S; ++q) prod.issue(b, 0, ringw, warp, lane, S);
+  if (gidx) {
+    for (int i = threadIdx.x; i < npad; i += NTHR) {
+      const int g = __ldg(gidx + b.xoff + i);
+      v[i] = g >= 0 ? __ldg(r + g) : 0.0;
+    }
+  } else {
+    for (int i = threadIdx.x; i < npad; i += NTHR) v[i] = x[b.xoff + i];
+  }
+  __syncthreads();
+  int cs = 0;
+  // forward sweep
+  for (int I = 0; I < b.nb; ++I) {
+    const double* blk = b.data + b.step_off[I];
+    const int code = b.kcnt[I], K = code & 0xffff, fz = code >> 16;
+    double ra0 = 0.0, ra1 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      cp_async_wait<S - 1>();
+      if (!(k * 8 + warp < fz)) {
+        const double* rs = ringw + (long long)cs * 512 + 2 * lane;
+        const double* uj = v + (I - K + k) * TT + c0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = *reinterpret_cast<const double2*>(rs + kk * 64);
+          ra0 += w.x * uj[kk];
+          ra1 += w.y * uj[kk];
+        }
+      }
+      cs = cs + 1 == S ? 0 : cs + 1;
+      prod.issue(b, 0, ringw, warp, lane, S);
+    }
+    red[warp * TT + 2 * lane] = ra0;
+    red[warp * TT + 2 * lane + 1] = ra1;
+    __syncthreads();
+    if (threadIdx.x < TT) {
+      double sacc = v[I * TT + threadIdx.x];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc -= red[w * TT + threadIdx.x];
+      t[threadIdx.x] = sacc;
+    }
+    __syncthreads();
+    {
+      double d0 = 0.0, d1 = 0.0;
+      if (drow) {
+        const double* dp = blk + (long long)K * TT * TT + doff;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = ldg_stream2(dp + kk * dlen);
+          d0 += w.x * t[c0 + kk];
+          d1 += w.y * t[c0 + kk];
+        }
+      }
+      red[warp * TT + 2 * lane] = d0;
+      red[warp * TT + 2 * lane + 1] = d1;
+    }
+    __syncthreads();
+    if (threadIdx.x < TT) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc += red[w * TT + threadIdx.x];
+      v[I * TT + threadIdx.x] = sacc;
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();  // drain the (empty) tail groups before the ring is reused
+  if (b.udata) {
+    const int ulen = 8 * warp + 8;
+    const bool urow = lane <= 4 * warp + 3;
+    const int uoff = udiag_strip_off(warp) + 2 * lane;
+    RingProducer up{b.nb - 1, 0, 0};
+#pragma unroll
+    for (int q = 0; q < S; ++q) up.issue(b, 2, ringw, warp, lane, S);
+    cs = 0;
+    for (int I = b.nb - 1; I >= 0; --I) {
+      const double* blk = b.udata + b.ustep_off[I];
+      const int code = b.ucnt[I], R = code & 0xffff, tz = code >> 16;
+      double ra0 = 0.0, ra1 = 0.0;
+      for (int k = 0; k < R; ++k) {
+        cp_async_wait<S - 1>();
+        if (!(k * 8 + warp >= 8 * R - tz)) {
+          const double* rs = ringw + (long long)cs * 512 + 2 * lane;
+          const double* yj = v + (I + 1 + k) * TT + c0;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const double2 w = *reinterpret_cast<const double2*>(rs + kk * 64);
+            ra0 += w.x * yj[kk];
+            ra1 += w.y * yj[kk];
+          }
+        }
+        cs = cs + 1 == S ? 0 : cs + 1;
+        up.issue(b, 2, ringw, warp, lane, S);
+      }
+      red[warp * TT + 2 * lane] = ra0;
+      red[warp * TT + 2 * lane + 1] = ra1;
+      __syncthreads();
+      if (threadIdx.x < TT) {
+        double sacc = v[I * TT + threadIdx.x];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sacc -= red[w * TT + threadIdx.x];
+        t[threadIdx.x] = sacc;
+      }
+      __syncthreads();
+      {
+        double d0 = 0.0, d1 = 0.0;
+        if (urow) {
+          const double* dp = blk + (long long)R * TT * TT + uoff;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const double2 w = ldg_stream2(dp + kk * ulen);
+            d0 += w.x * t[c0 + kk];
+            d1 += w.y * t[c0 + kk];
+          }
+        }
+        red[warp * TT + 2 * lane] = d0;
+        red[warp * TT + 2 * lane + 1] = d1;
+      }
+      __syncthreads();
+      if (threadIdx.x < TT) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sacc += red[w * TT + threadIdx.x];
+        v[I * TT + threadIdx.x] = sacc;
+      }
+      __syncthreads();
+    }
+    cp_async_wait<0>();
+    for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
+    return;
+  }
+  // Cholesky backward: L^T y = u
+  const int colsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  RingProducer bp{b.nb - 1, 0, 0};
+#pragma unroll
+  for (int q = 0; q < S; ++q) bp.issue(b, 1, ringw, warp, lane, S);
+  cs = 0;
+  for (int J = b.nb - 1; J >= 0; --J) {
+    const double* blk = b.data + b.step_off[J];
+    const int code = b.kcnt[J], K = code & 0xffff, fz = code >> 16;
+    {
+      const double u0 = v[J * TT + 2 * lane], u1 = v[J * TT + 2 * lane + 1];
+      double cp[8];
+      if (drow) {
+        const double* dp = blk + (long long)K * TT * TT + doff;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = ldg_stream2(dp + kk * dlen);
+          cp[kk] = w.x * u0 + w.y * u1;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) cp[kk] = 0.0;
+      }
+      const double yv = warp_reduce8(cp, lane);
+      __syncthreads();  // every warp has read v_J
+      if ((lane & 3) == 0) v[J * TT + c0 + colsel] = yv;
+      __syncthreads();
+    }
+    const double y0 = v[J * TT + 2 * lane], y1 = v[J * TT + 2 * lane + 1];
+    for (int k = 0; k < K; ++k) {
+      cp_async_wait<S - 1>();
+      if (!(k * 8 + warp < fz)) {
+        const double* rs = ringw + (long long)cs * 512 + 2 * lane;
+        double cp[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = *reinterpret_cast<const double2*>(rs + kk * 64);
+          cp[kk] = w.x * y0 + w.y * y1;
+        }
+        const double val = warp_reduce8(cp, lane);
+        if ((lane & 3) == 0) v[(J - K + k) * TT + c0 + colsel] -= val;
+      }
+      cs = cs + 1 == S ? 0 : cs + 1;
+      bp.issue(b, 1, ringw, warp, lane, S);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
+}
+
 // pack band steps of one subdomain batch: L (row-major ld x ld, factor order, identity
 // padding) and the inverted diagonal tiles dinv (nbmax x 64 x 64 row-major per subdomain)
 __global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, const double* __restrict__ L,
