@@ -29,8 +29,8 @@ namespace {
 constexpr int PCG_GRAPH_ITERS = 25;  // replacement period of src/krylov.py:88
 constexpr int MAX_GRID = 148 * 8;    // 148 SMs x 8 resident 256-thread CTAs
 constexpr int GM_FUSED_MAXCOLS = 96; // fused CGS2 step while (nc + 1) x 256 doubles fit in smem
-constexpr int RING_S = 4;            // tiles in flight per warp in k_band_solve_ring
-constexpr size_t RING_BYTES = sizeof(double) * 8 * RING_S * 512;
+// shared memory of the per-warp rings of k_band_solve_ring<S> (8 warps x S tiles x 4 KB)
+constexpr size_t ring_bytes(int S) { return sizeof(double) * 8 * (size_t)S * 512; }
 
 template <class T>
 void dfree(T*& p) {
@@ -295,8 +295,11 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
       }
       CK(cudaEventRecordWithFlags(ctx->kt_a[ctx->kt_n], s, cudaEventRecordExternal));
     }
-    if (ctx->band_ring)
-      k_band_solve_ring<RING_S><<<ctx->nsub, NTHR, ctx->band_smem + RING_BYTES, s>>>(
+    if (ctx->band_ring == 4)
+      k_band_solve_ring<4><<<ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4), s>>>(
+          ctx->d_band, ctx->xloc, ctx->yloc, done, r_src ? ctx->d_gidx : nullptr, r_src);
+    else if (ctx->band_ring == 2)
+      k_band_solve_ring<2><<<ctx->nsub, NTHR, ctx->band_smem + ring_bytes(2), s>>>(
           ctx->d_band, ctx->xloc, ctx->yloc, done, r_src ? ctx->d_gidx : nullptr, r_src);
     else if (ctx->band_unr == 2)
       k_band_solve<2><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
@@ -751,15 +754,21 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     }
     TRY(upload(ctx, ctx->d_band, ctx->h_band.data(), n_sub));
     ctx->band_smem = sizeof(double) * ((size_t)maxnb * TT + 8 * TT + TT);
-    static size_t smem_set = 0, smem_set2 = 0, smem_set3 = 0;
+    static size_t smem_set = 0, smem_set2 = 0, smem_set3 = 0, smem_set4 = 0;
     CK(raise_smem((const void*)k_band_solve<1>, ctx->band_smem, smem_set));
     CK(raise_smem((const void*)k_band_solve<2>, ctx->band_smem, smem_set2));
-    CK(raise_smem((const void*)k_band_solve_ring<RING_S>, ctx->band_smem + RING_BYTES, smem_set3));
-    // per-warp cp.async rings (1 CTA/SM) when all subdomains fit one wave of the SMs: measured
-    // 0.79 -> 0.57 ms per iteration on an 8-rank configuration-2 slab (64 subdomains); with more
-    // subdomains than SMs the 4-CTA/SM kernel wins (cfg3: 1,293 vs 1,045 it/s; ab_band_ring_r01)
-    ctx->band_ring = n_sub <= 148 ? 1 : 0;
-    if (const char* e = getenv("TLS_BAND_RING")) ctx->band_ring = atoi(e) != 0;
+    CK(raise_smem((const void*)k_band_solve_ring<4>, ctx->band_smem + ring_bytes(4), smem_set3));
+    CK(raise_smem((const void*)k_band_solve_ring<2>, ctx->band_smem + ring_bytes(2), smem_set4));
+    // per-warp cp.async rings, 4 deep at 1 CTA/SM, when the subdomains fit one wave (<= 148;
+    // an 8-rank configuration-2 slab: 0.79 -> 0.57 ms per iteration); otherwise the 4-CTA/SM
+    // kernel (the 2-deep ring at 2 CTAs/SM for <= 296 subdomains measured cfg3 -4.5%, cfg4 +4.9%,
+    // 2-rank slab +2%: selectable with TLS_BAND_RING=2; profiles/ab_band_ring_r01.txt)
+    ctx->band_ring = n_sub <= 148 ? 4 : 0;
+    if (ctx->band_smem + ring_bytes(ctx->band_ring) > 227 * 1024) ctx->band_ring = 0;
+    if (const char* e = getenv("TLS_BAND_RING")) {
+      const int v = atoi(e);
+      if (v == 0 || v == 2 || v == 4) ctx->band_ring = v;
+    }
     // one tile per load round: two (UNR = 2, 128 registers, 2 CTAs/SM) measured slower on
     // configuration 3 (1,249 vs 1,300 it/s) and mixed on 8-rank configuration 2 slabs
     // (profiles/ab_band_unr_r01.txt); kept selectable for the few-subdomains-per-GPU regime
@@ -1625,8 +1634,11 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   for (int i = 0; i <= reps; ++i) {
     if (i == 1) CK(cudaEventRecord(e0, s));
     if (band)
-      if (ctx->band_ring)
-        k_band_solve_ring<RING_S><<<ctx->nsub, NTHR, ctx->band_smem + RING_BYTES, s>>>(
+      if (ctx->band_ring == 4)
+        k_band_solve_ring<4><<<ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4), s>>>(
+            ctx->d_band, ctx->xloc, ctx->yloc, nullptr, nullptr, nullptr);
+      else if (ctx->band_ring == 2)
+        k_band_solve_ring<2><<<ctx->nsub, NTHR, ctx->band_smem + ring_bytes(2), s>>>(
             ctx->d_band, ctx->xloc, ctx->yloc, nullptr, nullptr, nullptr);
       else if (ctx->band_unr == 2)
         k_band_solve<2><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr,

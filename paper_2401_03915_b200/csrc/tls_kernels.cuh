@@ -1315,7 +1315,7 @@ struct RingProducer {
 };
 
 template <int S>
-__global__ void __launch_bounds__(NTHR, 1) k_band_solve_ring(const BandDesc* __restrict__ bands,
+__global__ void __launch_bounds__(NTHR, S <= 2 ? 2 : 1) k_band_solve_ring(const BandDesc* __restrict__ bands,
                                                              const double* __restrict__ x,
                                                              double* __restrict__ y, const int* done,
                                                              const int* __restrict__ gidx,
