@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "tls_b200.h"
@@ -114,6 +115,7 @@ struct tls_ctx {
   int gm_exec_cols[2] = {0, 0};
   int gm_exec_launches[2] = {0, 0};
   int launches = 0;  // kernels enqueued since the counter was reset
+  int pdl = 1;       // programmatic dependent launch on every kernel (TLS_PDL=0: off)
   // ---- in-graph timing of the local-solve kernel (bench roofline over real solves)
   bool ktime = false, capturing = false;
   std::vector<cudaEvent_t> kt_a, kt_b;  // one pair per band-solve node of the captured graph
@@ -151,6 +153,24 @@ struct tls_ctx {
   long long Xrecv = 0;                // tail of yloc holding the received contributions
   double *pin = nullptr, *pout = nullptr;  // caller-numbering staging vectors
 };
+
+template <typename... KArgs, typename... Args>
+static void launch_k(const tls_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (ctx && ctx->pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 struct tls_group {
   GroupShared shared;
@@ -219,6 +239,12 @@ static cudaError_t raise_smem(const void* fn, size_t bytes, size_t& current) {
   return e;
 }
 
+// every kernel launch of the library: cudaLaunchKernelEx with programmatic stream serialization
+// (PDL) when ctx->pdl; errors surface through cudaGetLastError (CKL / the callers' checks)
+template <typename... KArgs, typename... Args>
+static void launch_k(const tls_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t s, Args&&... args);
+
 static int grid_for(int64_t work, int per_block) {
   int64_t g = (work + per_block - 1) / per_block;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, MAX_GRID));
@@ -260,7 +286,7 @@ static int spmv_lpr(tls_ctx* ctx, cudaStream_t s, const double* x, double* y, co
   const int grid = ctx->Gs;
 #define SPMV_CASE(L)                                                                                 \
   case L:                                                                                            \
-    k_spmv<L, MODE, DOT><<<grid, NTHR, 0, s>>>(ctx->r0, ctx->r1, ctx->rowptr, ctx->col, ctx->val, x, y, \
+    launch_k(ctx, k_spmv<L, MODE, DOT>, grid, NTHR, 0, s, ctx->r0, ctx->r1, ctx->rowptr, ctx->col, ctx->val, x, y, \
                                                b, part, done);                                       \
     break;
   switch (ctx->lpr) {
@@ -296,16 +322,16 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
       CK(cudaEventRecordWithFlags(ctx->kt_a[ctx->kt_n], s, cudaEventRecordExternal));
     }
     if (ctx->band_ring == 4)
-      k_band_solve_ring<4><<<ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4), s>>>(
+      launch_k(ctx, k_band_solve_ring<4>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4), s, 
           ctx->d_band, ctx->xloc, ctx->yloc, done, r_src ? ctx->d_gidx : nullptr, r_src);
     else if (ctx->band_ring == 2)
-      k_band_solve_ring<2><<<ctx->nsub, NTHR, ctx->band_smem + ring_bytes(2), s>>>(
+      launch_k(ctx, k_band_solve_ring<2>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(2), s, 
           ctx->d_band, ctx->xloc, ctx->yloc, done, r_src ? ctx->d_gidx : nullptr, r_src);
     else if (ctx->band_unr == 2)
-      k_band_solve<2><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
+      launch_k(ctx, k_band_solve<2>, ctx->nsub, NTHR, ctx->band_smem, s, ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
                                                               r_src ? ctx->d_gidx : nullptr, r_src);
     else
-      k_band_solve<1><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
+      launch_k(ctx, k_band_solve<1>, ctx->nsub, NTHR, ctx->band_smem, s, ctx->d_band, ctx->xloc, ctx->yloc, done, ctx->band_pf,
                                                               r_src ? ctx->d_gidx : nullptr, r_src);
     CKL();
     if (timed) CK(cudaEventRecordWithFlags(ctx->kt_b[ctx->kt_n++], s, cudaEventRecordExternal));
@@ -317,11 +343,11 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
   if (which == L_COARSE) { u0 = ctx->nu_local; nu = ctx->nu_coarse; o0 = ctx->no_local; no = ctx->no_coarse; }
   if (which == L_ALL) { nu = ctx->nu_local + ctx->nu_coarse; no = ctx->no_local + ctx->no_coarse; }
   if (nu > 0) {
-    k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, done);
+    launch_k(ctx, k_symv_tiles, nu, NTHR, 0, s, ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, done);
     CKL();
   }
   if (no > 0) {
-    k_reduce_tiles<<<(no + 7) / 8, NTHR, 0, s>>>(ctx->d_blk, ctx->d_outs + o0, no, ctx->d_red,
+    launch_k(ctx, k_reduce_tiles, (no + 7) / 8, NTHR, 0, s, ctx->d_blk, ctx->d_outs + o0, no, ctx->d_red,
                                                  ctx->slots, ctx->yloc, done);
     CKL();
   }
@@ -329,7 +355,7 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
 }
 
 static int enq_gather(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
-  k_gather<<<grid_for(ctx->Xloc, NTHR), NTHR, 0, s>>>(ctx->Xloc, ctx->d_gidx, r, ctx->xloc, done);
+  launch_k(ctx, k_gather, grid_for(ctx->Xloc, NTHR), NTHR, 0, s, ctx->Xloc, ctx->d_gidx, r, ctx->xloc, done);
   CKL();
   return TLS_OK;
 }
@@ -338,7 +364,7 @@ static int enq_restrict(tls_ctx* ctx, cudaStream_t s, const double* r, const int
   // one warp per coarse column; all columns of a subdomain in one CTA (r_int gathered once)
   const int cw = ctx->restrict_cw;
   const dim3 grid(ctx->nsub, (ctx->kmax + cw - 1) / cw);
-  k_restrict<<<grid, 32 * std::min(ctx->kmax, cw), ctx->restrict_smem, s>>>(
+  launch_k(ctx, k_restrict, grid, 32 * std::min(ctx->kmax, cw), ctx->restrict_smem, s, 
       ctx->d_sub_idxoff, ctx->d_idx, ctx->d_nint, ctx->d_zoff,
                                         ctx->d_kcnt, ctx->d_cstart, ctx->d_Z, r,
                                         ctx->xloc + ctx->coarse_xoff, done);
@@ -351,7 +377,7 @@ template <int MODE, int DOT>
 static int enq_prolong(tls_ctx* ctx, cudaStream_t s, const double* qv, const double* wv,
                        const double* rdot, double* z, const int* done) {
   const int r0 = ctx->r0;
-  k_prolong<MODE, DOT><<<ctx->G, NTHR, 0, s>>>(
+  launch_k(ctx, k_prolong<MODE, DOT>, ctx->G, NTHR, 0, s, 
       ctx->r1 - r0, ctx->d_pull_ptr + r0, ctx->d_pull_pos, ctx->yloc, ctx->d_zrow + r0, ctx->d_zst + r0,
       ctx->d_zk + r0, ctx->d_zc + r0, ctx->d_Z, ctx->yloc + ctx->coarse_xoff, qv ? qv + r0 : nullptr,
       wv ? wv + r0 : nullptr, rdot ? rdot + r0 : nullptr, z + r0, ctx->part, done);
@@ -385,14 +411,14 @@ static int enq_exchange(tls_ctx* ctx, cudaStream_t s, XPlan& x, const double* sr
                         const int* done) {
   if (!sharded(ctx)) return TLS_OK;
   if (x.stot > 0) {
-    k_xpack<<<grid_for(x.stot, NTHR), NTHR, 0, s>>>(x.stot, x.d_sidx, src, x.sbuf, done);
+    launch_k(ctx, k_xpack, grid_for(x.stot, NTHR), NTHR, 0, s, x.stot, x.d_sidx, src, x.sbuf, done);
     CKL();
   }
   std::string err;
   cudaError_t e = ctx->comm->exchange(x, s, err);
   if (e != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
   if (x.rtot > 0) {
-    k_xunpack<<<grid_for(x.rtot, NTHR), NTHR, 0, s>>>(x.rtot, x.d_ridx, x.rbuf, dst, done);
+    launch_k(ctx, k_xunpack, grid_for(x.rtot, NTHR), NTHR, 0, s, x.rtot, x.d_ridx, x.rbuf, dst, done);
     CKL();
   }
   return TLS_OK;
@@ -419,7 +445,7 @@ static int enq_restrict_all(tls_ctx* ctx, cudaStream_t s, const double* r, const
 }
 
 static int enq_dot(tls_ctx* ctx, cudaStream_t s, const double* a, const double* b, const int* done) {
-  k_dot<<<ctx->G, NTHR, 0, s>>>(nown(ctx), a + ctx->r0, b + ctx->r0, ctx->part, done);
+  launch_k(ctx, k_dot, ctx->G, NTHR, 0, s, nown(ctx), a + ctx->r0, b + ctx->r0, ctx->part, done);
   CKL();
   return enq_allreduce_part(ctx, s, ctx->G);
 }
@@ -494,9 +520,9 @@ static int enq_identity(tls_ctx* ctx, cudaStream_t s, const double* r, double* z
                         const int* done) {
   const int r0 = ctx->r0;
   if (dot)
-    k_copy_dot<1><<<ctx->G, NTHR, 0, s>>>(nown(ctx), r + r0, z + r0, ctx->part, done);
+    launch_k(ctx, k_copy_dot<1>, ctx->G, NTHR, 0, s, nown(ctx), r + r0, z + r0, ctx->part, done);
   else
-    k_copy_dot<0><<<ctx->G, NTHR, 0, s>>>(nown(ctx), r + r0, z + r0, ctx->part, done);
+    launch_k(ctx, k_copy_dot<0>, ctx->G, NTHR, 0, s, nown(ctx), r + r0, z + r0, ctx->part, done);
   CKL();
   return dot ? enq_allreduce_part(ctx, s, ctx->G) : TLS_OK;
 }
@@ -509,7 +535,7 @@ static int api_in(tls_ctx* ctx, cudaStream_t s, const double* v_in, double** v_i
     *v_int = const_cast<double*>(v_in);
     return TLS_OK;
   }
-  k_perm_in<<<grid_for(ctx->n, NTHR), NTHR, 0, s>>>(ctx->n, ctx->d_nofo, v_in, ctx->pin);
+  launch_k(ctx, k_perm_in, grid_for(ctx->n, NTHR), NTHR, 0, s, ctx->n, ctx->d_nofo, v_in, ctx->pin);
   CKL();
   *v_int = ctx->pin;
   return TLS_OK;
@@ -520,7 +546,7 @@ static int api_out(tls_ctx* ctx, cudaStream_t s, const double* v_int, double* ou
     if (v_int != out) CK(cudaMemcpyAsync(out, v_int, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, s));
     return TLS_OK;
   }
-  k_perm_out<<<grid_for(ctx->n, NTHR), NTHR, 0, s>>>(ctx->n, ctx->d_nofo, ctx->r0, ctx->r1, v_int, out);
+  launch_k(ctx, k_perm_out, grid_for(ctx->n, NTHR), NTHR, 0, s, ctx->n, ctx->d_nofo, ctx->r0, ctx->r1, v_int, out);
   CKL();
   return enq_allreduce(ctx, s, out, ctx->n);
 }
@@ -552,6 +578,7 @@ int32_t tls_ctx_create(int32_t device, tls_ctx** out) {
     delete ctx;
     return TLS_ERR_OOM;
   }
+  if (const char* e = getenv("TLS_PDL")) ctx->pdl = atoi(e) != 0;
   *out = ctx;
   return TLS_OK;
 }
@@ -823,12 +850,12 @@ int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first_g, int32_t count, double*
   sval = pos + 2 * (size_t)items;
   CK(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)count * ld * ld, s));
   dim3 g1(grid_for(ctx->max_n, NTHR) / 4 + 1, count);
-  k_seg_prep<<<g1, NTHR, 0, s>>>(count, ctx->d_sub_idxoff, ctx->d_sub_n, first, beg, beg + count, pos);
+  launch_k(ctx, k_seg_prep, g1, NTHR, 0, s, count, ctx->d_sub_idxoff, ctx->d_sub_n, first, beg, beg + count, pos);
   CKL();
   CK(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, ctx->d_idx + base, skey, pos, sval, items, count, beg,
                                          beg + count, s));
   dim3 g2(std::max<int>(1, (int)std::min<int64_t>((ld + 7) / 8, 4096)), count);
-  k_extract<<<g2, NTHR, 0, s>>>(count, ctx->d_sub_idxoff, ctx->d_sub_n, ctx->d_idx, first, skey, sval,
+  launch_k(ctx, k_extract, g2, NTHR, 0, s, count, ctx->d_sub_idxoff, ctx->d_sub_n, ctx->d_idx, first, skey, sval,
                                 ctx->rowptr, ctx->col, ctx->val, out, ld);
   CKL();
   CK(cudaFreeAsync(tmp, s));
@@ -847,7 +874,7 @@ int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first_g, int32_t count, co
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
   dim3 g(512, count);
-  k_pack_tiles<<<g, NTHR, 0, s>>>(ctx->d_blk, first, inv, ld, ld * ld);
+  launch_k(ctx, k_pack_tiles, g, NTHR, 0, s, ctx->d_blk, first, inv, ld, ld * ld);
   CKL();
   for (int i = first; i < first + count; ++i) ctx->stored[i] = 1;
   ctx->finalized = false;
@@ -900,7 +927,7 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
   ctx->h_blk[ctx->nsub] = cb;
   CK(cudaMemcpy(ctx->d_blk, ctx->h_blk.data(), sizeof(BlkDesc) * (ctx->nsub + 1), cudaMemcpyHostToDevice));
   dim3 g((unsigned)std::min<int64_t>(ntiles, 8192), 1);
-  k_pack_tiles<<<g, NTHR, 0, s>>>(ctx->d_blk, ctx->nsub, a0inv, n_coarse, 0);
+  launch_k(ctx, k_pack_tiles, g, NTHR, 0, s, ctx->d_blk, ctx->nsub, a0inv, n_coarse, 0);
   CKL();
   return TLS_OK;
 }
@@ -1219,32 +1246,32 @@ static int enq_pcg_iter(tls_ctx* ctx, cudaStream_t s, bool replace, bool prec) {
   TRY(enq_halo(ctx, s, ctx->vp, done));
   TRY((spmv_lpr<0, 1>(ctx, s, ctx->vp, ctx->vap, nullptr, ctx->part, done)));
   TRY(enq_allreduce_part(ctx, s, ctx->Gs));
-  k_pcg_alpha<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->ab);
+  launch_k(ctx, k_pcg_alpha, 1, NTHR, 0, s, st, ctx->part, ctx->Gs, ctx->ab);
   CKL();
   if (!replace) {
-    k_pcg_update<<<ctx->G, NTHR, 0, s>>>(no, st, ctx->vx + r0, ctx->vr + r0, ctx->vp + r0, ctx->vap + r0,
+    launch_k(ctx, k_pcg_update, ctx->G, NTHR, 0, s, no, st, ctx->vx + r0, ctx->vr + r0, ctx->vp + r0, ctx->vap + r0,
                                          ctx->part, 1);
     CKL();
     TRY(enq_allreduce_part(ctx, s, ctx->G));
-    k_pcg_hist<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->G, ctx->hist);
+    launch_k(ctx, k_pcg_hist, 1, NTHR, 0, s, st, ctx->part, ctx->G, ctx->hist);
     CKL();
   } else {
-    k_pcg_update<<<ctx->G, NTHR, 0, s>>>(no, st, ctx->vx + r0, ctx->vr + r0, ctx->vp + r0, ctx->vap + r0,
+    launch_k(ctx, k_pcg_update, ctx->G, NTHR, 0, s, no, st, ctx->vx + r0, ctx->vr + r0, ctx->vp + r0, ctx->vap + r0,
                                          ctx->part, 0);
     CKL();
     TRY(enq_halo(ctx, s, ctx->vx, done));
     TRY((spmv_lpr<1, 2>(ctx, s, ctx->vx, ctx->vr, ctx->vb, ctx->part, done)));
     TRY(enq_allreduce_part(ctx, s, ctx->Gs));
-    k_pcg_hist<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->hist);
+    launch_k(ctx, k_pcg_hist, 1, NTHR, 0, s, st, ctx->part, ctx->Gs, ctx->hist);
     CKL();
   }
   if (prec)
     TRY(enq_apply(ctx, s, ctx->vr, ctx->vz, true, done));
   else
     TRY(enq_identity(ctx, s, ctx->vr, ctx->vz, true, done));
-  k_pcg_beta<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->G, ctx->ab);
+  launch_k(ctx, k_pcg_beta, 1, NTHR, 0, s, st, ctx->part, ctx->G, ctx->ab);
   CKL();
-  k_pcg_pupdate<<<ctx->G, NTHR, 0, s>>>(no, st, ctx->vp + r0, ctx->vz + r0);
+  launch_k(ctx, k_pcg_pupdate, ctx->G, NTHR, 0, s, no, st, ctx->vp + r0, ctx->vz + r0);
   CKL();
   return TLS_OK;
 }
@@ -1276,7 +1303,7 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
   if (ctx->h_nofo.empty()) {
     CK(cudaMemcpyAsync(ctx->vb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   } else {
-    k_perm_in<<<grid_for(n, NTHR), NTHR, 0, s>>>(n, ctx->d_nofo, b, ctx->vb);
+    launch_k(ctx, k_perm_in, grid_for(n, NTHR), NTHR, 0, s, n, ctx->d_nofo, b, ctx->vb);
     CKL();
   }
   CK(cudaMemcpyAsync(ctx->vr, ctx->vb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -1286,7 +1313,7 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
   h.maxit = maxit;
   CK(cudaMemcpyAsync(ctx->pcg, &h, sizeof(PcgState), cudaMemcpyHostToDevice, s));
   TRY(enq_dot(ctx, s, ctx->vb, ctx->vb, nullptr));
-  k_pcg_init<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
+  launch_k(ctx, k_pcg_init, 1, NTHR, 0, s, ctx->pcg, ctx->part, ctx->G);
   CKL();
   CK(cudaMemcpyAsync(&h, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -1306,7 +1333,7 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
     TRY(enq_apply(ctx, s, ctx->vr, ctx->vz, true, nullptr, true));
   else
     TRY(enq_identity(ctx, s, ctx->vr, ctx->vz, true, nullptr));
-  k_pcg_rz0<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
+  launch_k(ctx, k_pcg_rz0, 1, NTHR, 0, s, ctx->pcg, ctx->part, ctx->G);
   CKL();
   CK(cudaMemcpyAsync(ctx->vp, ctx->vz, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   const bool host_loop = cb || (sharded(ctx) && !ctx->comm->capturable());
@@ -1401,31 +1428,31 @@ static int enq_gm_step(tls_ctx* ctx, cudaStream_t s, int j, bool prec) {
   const int nc = j + 1;
   // CGS2 (src/krylov.py:157-165 to the same accuracy): h1 = V^T w; w -= V h1 fused with
   // h2 = V^T w (one read of V); w -= V h2 with the norm partials -> 3 reads of V, not 4
-  k_gm_gemvt<<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, w + r0, ctx->part, stop);
+  launch_k(ctx, k_gm_gemvt, ctx->G, NTHR, 0, s, no, ctx->V + r0, ldv, nc, w + r0, ctx->part, stop);
   CKL();
-  k_gm_hreduce<<<nc, NTHR, 0, s>>>(ctx->part, ctx->G, ctx->h1, stop);
+  launch_k(ctx, k_gm_hreduce, nc, NTHR, 0, s, ctx->part, ctx->G, ctx->h1, stop);
   CKL();
   TRY(enq_allreduce(ctx, s, ctx->h1, nc));
   if (ctx->gm_fused && nc <= GM_FUSED_MAXCOLS) {
-    k_gm_update_gemvt<<<ctx->G, NTHR, sizeof(double) * ((size_t)(nc + 1) * NTHR + nc), s>>>(
+    launch_k(ctx, k_gm_update_gemvt, ctx->G, NTHR, sizeof(double) * ((size_t)(nc + 1) * NTHR + nc), s, 
         no, ctx->V + r0, ldv, nc, ctx->h1, w + r0, ctx->part, stop);
     CKL();
   } else {
-    k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, st, ctx->h1, w + r0, ctx->part, 1, stop);
+    launch_k(ctx, k_gm_gemvn<0>, ctx->G, NTHR, 0, s, no, ctx->V + r0, ldv, nc, st, ctx->h1, w + r0, ctx->part, 1, stop);
     CKL();
-    k_gm_gemvt<<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, w + r0, ctx->part, stop);
+    launch_k(ctx, k_gm_gemvt, ctx->G, NTHR, 0, s, no, ctx->V + r0, ldv, nc, w + r0, ctx->part, stop);
     CKL();
   }
-  k_gm_hreduce<<<nc, NTHR, 0, s>>>(ctx->part, ctx->G, ctx->h2, stop);
+  launch_k(ctx, k_gm_hreduce, nc, NTHR, 0, s, ctx->part, ctx->G, ctx->h2, stop);
   CKL();
   TRY(enq_allreduce(ctx, s, ctx->h2, nc));
-  k_gm_gemvn<1><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ldv, nc, st, ctx->h2, w + r0, ctx->part, 1, stop);
+  launch_k(ctx, k_gm_gemvn<1>, ctx->G, NTHR, 0, s, no, ctx->V + r0, ldv, nc, st, ctx->h2, w + r0, ctx->part, 1, stop);
   CKL();
   TRY(enq_allreduce_part(ctx, s, ctx->G));
-  k_gm_givens<<<1, NTHR, 0, s>>>(st, j, ctx->gm_cols + 1, ctx->H, ctx->h1, ctx->h2, ctx->part, ctx->G,
+  launch_k(ctx, k_gm_givens, 1, NTHR, 0, s, st, j, ctx->gm_cols + 1, ctx->H, ctx->h1, ctx->h2, ctx->part, ctx->G,
                                  ctx->cs, ctx->sn, ctx->gv, ctx->hist);
   CKL();
-  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(no, st, w + r0, ctx->V + (long long)(j + 1) * ldv + r0, 0);
+  launch_k(ctx, k_gm_scale, ctx->G, NTHR, 0, s, no, st, w + r0, ctx->V + (long long)(j + 1) * ldv + r0, 0);
   CKL();
   return TLS_OK;
 }
@@ -1433,26 +1460,26 @@ static int enq_gm_step(tls_ctx* ctx, cudaStream_t s, int j, bool prec) {
 static int enq_gm_cycle_end(tls_ctx* ctx, cudaStream_t s, bool prec) {
   GmState* st = ctx->gm;
   const int r0 = ctx->r0, no = nown(ctx);
-  k_gm_trisolve<<<1, 32, 0, s>>>(st, ctx->gm_cols + 1, ctx->H, ctx->gv, ctx->yv);
+  launch_k(ctx, k_gm_trisolve, 1, 32, 0, s, st, ctx->gm_cols + 1, ctx->H, ctx->gv, ctx->yv);
   CKL();
-  k_gm_gemvn<0><<<ctx->G, NTHR, 0, s>>>(no, ctx->V + r0, ctx->n, -1, st, ctx->yv, ctx->t7 + r0, nullptr, 0,
+  launch_k(ctx, k_gm_gemvn<0>, ctx->G, NTHR, 0, s, no, ctx->V + r0, ctx->n, -1, st, ctx->yv, ctx->t7 + r0, nullptr, 0,
                                         nullptr);
   CKL();
   if (prec) {
     TRY(enq_apply(ctx, s, ctx->t7, ctx->t5, false, nullptr));
-    k_axpy1<<<ctx->G, NTHR, 0, s>>>(no, ctx->vx + r0, ctx->t5 + r0, nullptr);
+    launch_k(ctx, k_axpy1, ctx->G, NTHR, 0, s, no, ctx->vx + r0, ctx->t5 + r0, nullptr);
   } else {
-    k_axpy1<<<ctx->G, NTHR, 0, s>>>(no, ctx->vx + r0, ctx->t7 + r0, nullptr);
+    launch_k(ctx, k_axpy1, ctx->G, NTHR, 0, s, no, ctx->vx + r0, ctx->t7 + r0, nullptr);
   }
   CKL();
-  k_gm_cycle_end<<<1, 32, 0, s>>>(st);
+  launch_k(ctx, k_gm_cycle_end, 1, 32, 0, s, st);
   CKL();
   TRY(enq_halo(ctx, s, ctx->vx, &st->done));
   TRY((spmv_lpr<1, 2>(ctx, s, ctx->vx, ctx->vr, ctx->vb, ctx->part, &st->done)));
   TRY(enq_allreduce_part(ctx, s, ctx->Gs));
-  k_gm_cycle_begin<<<1, NTHR, 0, s>>>(st, ctx->part, ctx->Gs, ctx->gv, ctx->gm_cols);
+  launch_k(ctx, k_gm_cycle_begin, 1, NTHR, 0, s, st, ctx->part, ctx->Gs, ctx->gv, ctx->gm_cols);
   CKL();
-  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(no, st, ctx->vr + r0, ctx->V + r0, 1);
+  launch_k(ctx, k_gm_scale, ctx->G, NTHR, 0, s, no, st, ctx->vr + r0, ctx->V + r0, 1);
   CKL();
   return TLS_OK;
 }
@@ -1520,7 +1547,7 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
   if (ctx->h_nofo.empty()) {
     CK(cudaMemcpyAsync(ctx->vb, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   } else {
-    k_perm_in<<<grid_for(n, NTHR), NTHR, 0, s>>>(n, ctx->d_nofo, b, ctx->vb);
+    launch_k(ctx, k_perm_in, grid_for(n, NTHR), NTHR, 0, s, n, ctx->d_nofo, b, ctx->vb);
     CKL();
   }
   CK(cudaMemcpyAsync(ctx->vr, ctx->vb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -1528,7 +1555,7 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
   CK(cudaMemsetAsync(ctx->H, 0, sizeof(double) * (size_t)(mcols + 1) * (mcols + 1), s));
   TRY(enq_dot(ctx, s, ctx->vb, ctx->vb, nullptr));
   // reuse pcg init to get ||b|| then seed the first cycle
-  k_pcg_init<<<1, NTHR, 0, s>>>(ctx->pcg, ctx->part, ctx->G);
+  launch_k(ctx, k_pcg_init, 1, NTHR, 0, s, ctx->pcg, ctx->part, ctx->G);
   CKL();
   PcgState hp{};
   CK(cudaMemcpyAsync(&hp, ctx->pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
@@ -1544,9 +1571,9 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
   }
   h.bnorm = hp.bnorm;
   CK(cudaMemcpyAsync(ctx->gm, &h, sizeof(GmState), cudaMemcpyHostToDevice, s));
-  k_gm_cycle_begin<<<1, NTHR, 0, s>>>(ctx->gm, ctx->part, ctx->G, ctx->gv, mcols);
+  launch_k(ctx, k_gm_cycle_begin, 1, NTHR, 0, s, ctx->gm, ctx->part, ctx->G, ctx->gv, mcols);
   CKL();
-  k_gm_scale<<<ctx->G, NTHR, 0, s>>>(nown(ctx), ctx->gm, ctx->vr + ctx->r0, ctx->V + ctx->r0, 1);
+  launch_k(ctx, k_gm_scale, ctx->G, NTHR, 0, s, nown(ctx), ctx->gm, ctx->vr + ctx->r0, ctx->V + ctx->r0, 1);
   CKL();
   const double one = 1.0;
   CK(cudaMemcpyAsync(ctx->hist, &one, sizeof(double), cudaMemcpyHostToDevice, s));
@@ -1635,19 +1662,19 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
     if (i == 1) CK(cudaEventRecord(e0, s));
     if (band)
       if (ctx->band_ring == 4)
-        k_band_solve_ring<4><<<ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4), s>>>(
+        launch_k(ctx, k_band_solve_ring<4>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4), s, 
             ctx->d_band, ctx->xloc, ctx->yloc, nullptr, nullptr, nullptr);
       else if (ctx->band_ring == 2)
-        k_band_solve_ring<2><<<ctx->nsub, NTHR, ctx->band_smem + ring_bytes(2), s>>>(
+        launch_k(ctx, k_band_solve_ring<2>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(2), s, 
             ctx->d_band, ctx->xloc, ctx->yloc, nullptr, nullptr, nullptr);
       else if (ctx->band_unr == 2)
-        k_band_solve<2><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr,
+        launch_k(ctx, k_band_solve<2>, ctx->nsub, NTHR, ctx->band_smem, s, ctx->d_band, ctx->xloc, ctx->yloc, nullptr,
                                                                 ctx->band_pf, nullptr, nullptr);
       else
-        k_band_solve<1><<<ctx->nsub, NTHR, ctx->band_smem, s>>>(ctx->d_band, ctx->xloc, ctx->yloc, nullptr,
+        launch_k(ctx, k_band_solve<1>, ctx->nsub, NTHR, ctx->band_smem, s, ctx->d_band, ctx->xloc, ctx->yloc, nullptr,
                                                                 ctx->band_pf, nullptr, nullptr);
     else
-      k_symv_tiles<<<nu, NTHR, 0, s>>>(ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
+      launch_k(ctx, k_symv_tiles, nu, NTHR, 0, s, ctx->d_blk, ctx->d_units + u0, ctx->xloc, ctx->slots, nullptr);
     CKL();
   }
   CK(cudaEventRecord(e1, s));
@@ -1756,7 +1783,7 @@ int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const
   ctx->band_bytes += 2.0 * 8.0 * need;  // forward with L, backward with L^T
   CK(cudaMemcpy(ctx->d_band + first, ctx->h_band.data() + first, sizeof(BandDesc) * count, cudaMemcpyHostToDevice));
   dim3 g(std::min(nbmax, 256), count);
-  k_pack_band<<<g, NTHR, 0, s>>>(ctx->d_band, first, L, ld, dinv, nbmax);
+  launch_k(ctx, k_pack_band, g, NTHR, 0, s, ctx->d_band, first, L, ld, dinv, nbmax);
   CKL();
   for (int i = first; i < first + count; ++i) ctx->stored[i] = 1;
   ctx->finalized = false;
@@ -1859,9 +1886,9 @@ int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first_g, int32_t count, co
   ctx->band_bytes += 8.0 * (needL + needU);  // forward with L, backward with U
   CK(cudaMemcpy(ctx->d_band + first, ctx->h_band.data() + first, sizeof(BandDesc) * count, cudaMemcpyHostToDevice));
   dim3 g(std::min(nbmax, 256), count);
-  k_pack_band<<<g, NTHR, 0, s>>>(ctx->d_band, first, LU, ld, ldinv, nbmax);
+  launch_k(ctx, k_pack_band, g, NTHR, 0, s, ctx->d_band, first, LU, ld, ldinv, nbmax);
   CKL();
-  k_pack_band_u<<<g, NTHR, 0, s>>>(ctx->d_band, first, LU, ld, udinv, nbmax);
+  launch_k(ctx, k_pack_band_u, g, NTHR, 0, s, ctx->d_band, first, LU, ld, udinv, nbmax);
   CKL();
   for (int i = first; i < first + count; ++i) ctx->stored[i] = 1;
   ctx->finalized = false;
@@ -1881,7 +1908,7 @@ int32_t tls_band_cholesky(double* ap, int64_t ld, int32_t count, const int32_t* 
   int* d_reach = nullptr;
   if (cudaMallocAsync((void**)&d_reach, sizeof(int) * nbk, s) != cudaSuccess) return TLS_ERR_OOM;
   if (cudaMemcpyAsync(d_reach, reach, sizeof(int) * nbk, cudaMemcpyHostToDevice, s) != cudaSuccess) return TLS_ERR_CUDA;
-  k_band_chol<<<count, 256, smem, s>>>(ap, ld, d_reach, nbk, dinv, info);
+  launch_k(nullptr, k_band_chol, count, 256, smem, s, ap, ld, d_reach, nbk, dinv, info);
   if (cudaGetLastError() != cudaSuccess) return TLS_ERR_CUDA;
   cudaFreeAsync(d_reach, s);
   // the host array must outlive the async copy

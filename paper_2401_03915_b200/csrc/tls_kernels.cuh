@@ -10,6 +10,22 @@
 
 namespace tls {
 
+// Programmatic dependent launch (sm_90+): every kernel waits for its predecessors' completion
+// before touching memory; with the launch attribute set (tls_b200.cu launch_k) its launch is
+// processed while the predecessor still runs (implicit trigger at the predecessor's end).  An
+// explicit early trigger (TLS_PDL_EARLY_TRIGGER) let dependents occupy SM slots during
+// multi-wave predecessors: measured -16% on GMRES configurations.  Without the attribute the
+// wait is a no-op.
+#ifndef TLS_PDL_EARLY_TRIGGER
+#define PDL_ENTRY() asm volatile("griddepcontrol.wait;" ::: "memory")
+#else
+#define PDL_ENTRY()                                                          \
+  do {                                                                       \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");          \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                       \
+  } while (0)
+#endif
+
 constexpr int TT = 64;          // tile edge (64x64 fp64 = 32 KiB, column-major inside)
 constexpr int UR = 8;           // tile-rows per work unit
 constexpr int UW = 8;           // tile-cols per work unit
@@ -85,6 +101,7 @@ __global__ void __launch_bounds__(NTHR) k_spmv(int r0, int n, const int* __restr
                                                const double* __restrict__ x, double* __restrict__ y,
                                                const double* __restrict__ b,
                                                double* __restrict__ part, const int* done) {
+  PDL_ENTRY();
   // rows [r0, n): the whole matrix, or this rank's owned row range on the sharded path
   if (done && *done) return;
   __shared__ double sh[32];
@@ -121,6 +138,7 @@ __global__ void __launch_bounds__(NTHR) k_spmv(int r0, int n, const int* __restr
 __global__ void __launch_bounds__(NTHR) k_gather(long long m, const int* __restrict__ gidx,
                                                  const double* __restrict__ r,
                                                  double* __restrict__ xloc, const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   for (long long p = blockIdx.x * (long long)NTHR + threadIdx.x; p < m;
        p += (long long)gridDim.x * NTHR) {
@@ -146,6 +164,7 @@ __global__ void __launch_bounds__(1024) k_restrict(const long long* __restrict__
                                                    const double* __restrict__ Z,
                                                    const double* __restrict__ r,
                                                    double* __restrict__ c, const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   extern __shared__ __align__(16) double rs[];  // r on this subdomain's interior
   // grid (subdomains, column groups): CTA (s, g) handles columns g*nw .. g*nw+nw-1 of Z_s
@@ -217,6 +236,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_symv_tiles(const BlkDesc* __restric
                                                         const double* __restrict__ x,
                                                         double* __restrict__ slots,
                                                         const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   __shared__ __align__(16) double xr[UR * TT];
   __shared__ __align__(16) double xc[UW * TT];
@@ -290,6 +310,7 @@ __global__ void __launch_bounds__(NTHR) k_reduce_tiles(const BlkDesc* __restrict
                                                        const int* __restrict__ red,
                                                        const double* __restrict__ slots,
                                                        double* __restrict__ y, const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   const int o = blockIdx.x * (NTHR / 32) + (threadIdx.x >> 5);
   if (o >= nout) return;
@@ -332,6 +353,7 @@ __global__ void __launch_bounds__(NTHR, 8) k_prolong(int n, const int* __restric
                                                   const double* __restrict__ rdot,
                                                   double* __restrict__ z, double* __restrict__ part,
                                                   const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   __shared__ double sh[32];
   double dacc = 0.0;
@@ -372,11 +394,13 @@ __global__ void __launch_bounds__(NTHR, 8) k_prolong(int n, const int* __restric
 // dst[nofo[g]] = src[g]  (caller numbering -> internal numbering, all rows)
 __global__ void __launch_bounds__(NTHR) k_perm_in(int n, const int* __restrict__ nofo,
                                                   const double* __restrict__ src, double* __restrict__ dst) {
+  PDL_ENTRY();
   for (int g = blockIdx.x * NTHR + threadIdx.x; g < n; g += gridDim.x * NTHR) dst[__ldg(nofo + g)] = src[g];
 }
 // dst[g] = src[nofo[g]] for owned rows, 0 elsewhere (completed by a sum all-reduce)
 __global__ void __launch_bounds__(NTHR) k_perm_out(int n, const int* __restrict__ nofo, int r0, int r1,
                                                    const double* __restrict__ src, double* __restrict__ dst) {
+  PDL_ENTRY();
   for (int g = blockIdx.x * NTHR + threadIdx.x; g < n; g += gridDim.x * NTHR) {
     const int i = __ldg(nofo + g);
     dst[g] = (i >= r0 && i < r1) ? src[i] : 0.0;
@@ -385,6 +409,7 @@ __global__ void __launch_bounds__(NTHR) k_perm_out(int n, const int* __restrict_
 __global__ void __launch_bounds__(NTHR) k_xpack(long long m, const int* __restrict__ idx,
                                                 const double* __restrict__ src, double* __restrict__ buf,
                                                 const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   for (long long p = blockIdx.x * (long long)NTHR + threadIdx.x; p < m; p += (long long)gridDim.x * NTHR)
     buf[p] = src[__ldg(idx + p)];
@@ -392,6 +417,7 @@ __global__ void __launch_bounds__(NTHR) k_xpack(long long m, const int* __restri
 __global__ void __launch_bounds__(NTHR) k_xunpack(long long m, const int* __restrict__ idx,
                                                   const double* __restrict__ buf, double* __restrict__ dst,
                                                   const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   for (long long p = blockIdx.x * (long long)NTHR + threadIdx.x; p < m; p += (long long)gridDim.x * NTHR)
     dst[__ldg(idx + p)] = buf[p];
@@ -405,6 +431,7 @@ template <int DOT>  // z = r (precond None, src/krylov.py:52-55); DOT: partial r
 __global__ void __launch_bounds__(NTHR) k_copy_dot(int n, const double* __restrict__ r,
                                                    double* __restrict__ z, double* __restrict__ part,
                                                    const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   __shared__ double sh[32];
   double acc = 0.0;
@@ -422,6 +449,7 @@ __global__ void __launch_bounds__(NTHR) k_copy_dot(int n, const double* __restri
 __global__ void __launch_bounds__(NTHR) k_dot(int n, const double* __restrict__ a,
                                               const double* __restrict__ b,
                                               double* __restrict__ part, const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   __shared__ double sh[32];
   double acc = 0.0;
@@ -432,6 +460,7 @@ __global__ void __launch_bounds__(NTHR) k_dot(int n, const double* __restrict__ 
 
 // PCG scalars ------------------------------------------------------------------------------
 __global__ void k_pcg_init(PcgState* st, const double* part, int np) {
+  PDL_ENTRY();
   __shared__ double sh[32];
   const double s = sum_partials(part, np, sh);
   if (threadIdx.x == 0) {
@@ -443,12 +472,14 @@ __global__ void k_pcg_init(PcgState* st, const double* part, int np) {
   }
 }
 __global__ void k_pcg_rz0(PcgState* st, const double* part, int np) {
+  PDL_ENTRY();
   __shared__ double sh[32];
   const double s = sum_partials(part, np, sh);
   if (threadIdx.x == 0) st->rz = s;
 }
 // curvature p.Ap -> alpha; BreakdownError when <= 0 (src/krylov.py:81-85)
 __global__ void k_pcg_alpha(PcgState* st, const double* part, int np, double* ab) {
+  PDL_ENTRY();
   if (st->done) return;
   __shared__ double sh[32];
   const double s = sum_partials(part, np, sh);
@@ -472,6 +503,7 @@ __global__ void __launch_bounds__(NTHR) k_pcg_update(int n, const PcgState* st, 
                                                      const double* __restrict__ p,
                                                      const double* __restrict__ ap,
                                                      double* __restrict__ part, int update_r) {
+  PDL_ENTRY();
   if (st->done) return;
   __shared__ double sh[32];
   const double alpha = st->alpha;
@@ -491,6 +523,7 @@ __global__ void __launch_bounds__(NTHR) k_pcg_update(int n, const PcgState* st, 
 }
 // history entry and stopping test (src/krylov.py:90-96)
 __global__ void k_pcg_hist(PcgState* st, const double* part, int np, double* hist) {
+  PDL_ENTRY();
   if (st->done) return;
   __shared__ double sh[32];
   const double s = sum_partials(part, np, sh);
@@ -507,6 +540,7 @@ __global__ void k_pcg_hist(PcgState* st, const double* part, int np, double* his
   }
 }
 __global__ void k_pcg_beta(PcgState* st, const double* part, int np, double* ab) {
+  PDL_ENTRY();
   if (st->done) return;
   __shared__ double sh[32];
   const double s = sum_partials(part, np, sh);
@@ -519,6 +553,7 @@ __global__ void k_pcg_beta(PcgState* st, const double* part, int np, double* ab)
 // p = z + beta p (src/krylov.py:101)
 __global__ void __launch_bounds__(NTHR) k_pcg_pupdate(int n, const PcgState* st, double* __restrict__ p,
                                                       const double* __restrict__ z) {
+  PDL_ENTRY();
   if (st->done) return;
   const double beta = st->beta;
   for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) p[i] = z[i] + beta * p[i];
@@ -534,6 +569,7 @@ constexpr int GCH = 8;  // columns per gemv_t pass
 __global__ void __launch_bounds__(NTHR, 8) k_gm_gemvt(int n, const double* __restrict__ V, long long ldv,
                                                    int ncols, const double* __restrict__ w,
                                                    double* __restrict__ part, const int* stop) {
+  PDL_ENTRY();
   if (*stop) return;
   __shared__ double sh[NTHR / 32][GCH];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -573,6 +609,7 @@ __global__ void __launch_bounds__(NTHR) k_gm_update_gemvt(int n, const double* _
                                                           int ncols, const double* __restrict__ h,
                                                           double* __restrict__ w, double* __restrict__ part,
                                                           const int* stop) {
+  PDL_ENTRY();
   if (*stop) return;
   extern __shared__ __align__(16) double smv[];
   double* vt = smv;                       // ncols x NTHR
@@ -613,6 +650,7 @@ __global__ void __launch_bounds__(NTHR) k_gm_update_gemvt(int n, const double* _
 // h[i] = sum_b part[i*G + b]; one block per column
 __global__ void k_gm_hreduce(const double* __restrict__ part, int G, double* __restrict__ h,
                              const int* stop) {
+  PDL_ENTRY();
   if (*stop) return;
   __shared__ double sh[32];
   const double s = sum_partials(part + (long long)blockIdx.x * G, G, sh);
@@ -625,6 +663,7 @@ __global__ void __launch_bounds__(NTHR, 8) k_gm_gemvn(int n, const double* __res
                                                    const double* __restrict__ h,
                                                    double* __restrict__ w, double* __restrict__ part,
                                                    int subtract, const int* stop) {
+  PDL_ENTRY();
   if (stop && *stop) return;
   __shared__ double sh[32];
   const int nc = ncols >= 0 ? ncols : st->k;
@@ -646,6 +685,7 @@ __global__ void k_gm_givens(GmState* st, int j, int ldh, double* __restrict__ H,
                             const double* __restrict__ h1, const double* __restrict__ h2,
                             const double* __restrict__ part, int np, double* __restrict__ cs,
                             double* __restrict__ sn, double* __restrict__ g, double* __restrict__ hist) {
+  PDL_ENTRY();
   if (st->cycle_stop) return;
   __shared__ double sh[32];
   const double s = sum_partials(part, np, sh);
@@ -683,6 +723,7 @@ __global__ void k_gm_givens(GmState* st, int j, int ldh, double* __restrict__ H,
 // v_{j+1} = w / hn
 __global__ void __launch_bounds__(NTHR) k_gm_scale(int n, const GmState* st, const double* __restrict__ w,
                                                    double* __restrict__ v, int use_rn) {
+  PDL_ENTRY();
   if (!use_rn && st->cycle_stop) return;
   const double d = use_rn ? st->rn : st->hn;
   for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) v[i] = w[i] / d;
@@ -690,6 +731,7 @@ __global__ void __launch_bounds__(NTHR) k_gm_scale(int n, const GmState* st, con
 // y = H[:k,:k]^{-1} g[:k] (solve_triangular, src/krylov.py:191)
 __global__ void k_gm_trisolve(const GmState* st, int ldh, const double* __restrict__ H,
                               const double* __restrict__ g, double* __restrict__ y) {
+  PDL_ENTRY();
   if (threadIdx.x != 0) return;
   const int k = st->k;
   for (int i = k - 1; i >= 0; --i) {
@@ -700,17 +742,20 @@ __global__ void k_gm_trisolve(const GmState* st, int ldh, const double* __restri
 }
 __global__ void __launch_bounds__(NTHR) k_axpy1(int n, double* __restrict__ x, const double* __restrict__ t,
                                                 const int* done) {
+  PDL_ENTRY();
   if (done && *done) return;
   for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) x[i] += t[i];
 }
 // end of a cycle: account iterations, decide whether to restart
 __global__ void k_gm_cycle_end(GmState* st) {
+  PDL_ENTRY();
   if (threadIdx.x != 0) return;
   st->total += st->k;
   if (st->converged || st->total >= st->maxit || !st->restarted) st->done = 1;
 }
 // new cycle on r = b - A x: rn, tolerance rescale, V_0 = r / rn, g = rn e1
 __global__ void k_gm_cycle_begin(GmState* st, const double* part, int np, double* g, int mcols) {
+  PDL_ENTRY();
   if (st->done) return;
   __shared__ double sh[32];
   const double s = sum_partials(part, np, sh);
@@ -741,6 +786,7 @@ __global__ void k_gm_cycle_begin(GmState* st, const double* part, int np, double
 // binary search in its subdomain's sorted list -- no n-sized map per subdomain.
 __global__ void k_seg_prep(int count, const long long* __restrict__ sub_idxoff, const int* __restrict__ sub_n,
                            int first, int* __restrict__ beg, int* __restrict__ end, int* __restrict__ pos) {
+  PDL_ENTRY();
   const int b = blockIdx.y;
   const int s = first + b;
   const long long base = sub_idxoff[first];
@@ -765,6 +811,7 @@ __global__ void k_extract(int count, const long long* __restrict__ sub_idxoff,
                           const int* __restrict__ skey, const int* __restrict__ sval,
                           const int* __restrict__ rowptr, const int* __restrict__ col,
                           const double* __restrict__ val, double* __restrict__ out, long long ld) {
+  PDL_ENTRY();
   const int b = blockIdx.y;
   const int s = first + b;
   const int ns = sub_n[s];
@@ -791,6 +838,7 @@ __global__ void k_extract(int count, const long long* __restrict__ sub_idxoff,
 // coalesced row reads into shared memory, column-major (tile layout) coalesced writes.
 __global__ void k_pack_tiles(const BlkDesc* __restrict__ blks, int first_blk, const double* __restrict__ inv,
                              long long ld, long long batch_stride) {
+  PDL_ENTRY();
   __shared__ double tile[TT][TT + 1];
   const int b = blockIdx.y;
   const BlkDesc bd = blks[first_blk + b];
@@ -927,6 +975,7 @@ __global__ void __launch_bounds__(NTHR, UNR == 1 ? 4 : 2) k_band_solve(const Ban
                                                         double* __restrict__ y, const int* done,
                                                         int pf, const int* __restrict__ gidx,
                                                         const double* __restrict__ r) {
+  PDL_ENTRY();
   if (done && *done) return;
   extern __shared__ __align__(16) double sm[];
   const BandDesc b = bands[blockIdx.x];
@@ -1175,6 +1224,7 @@ __device__ __forceinline__ void load_tile(double* T, const double* G, long long 
 
 __global__ void __launch_bounds__(256, 1) k_band_chol(double* __restrict__ AP, long long ld, const int* __restrict__ reach,
                                                       int nbk, double* __restrict__ dinv, int* __restrict__ info) {
+  PDL_ENTRY();
   extern __shared__ __align__(16) double cs[];
   double* Ds = cs;                 // diagonal block -> L_JJ (lower)
   double* Ls = Ds + 64 * CP;       // L_JJ^{-1}
@@ -1320,6 +1370,7 @@ __global__ void __launch_bounds__(NTHR, S <= 2 ? 2 : 1) k_band_solve_ring(const 
                                                              double* __restrict__ y, const int* done,
                                                              const int* __restrict__ gidx,
                                                              const double* __restrict__ r) {
+  PDL_ENTRY();
   if (done && *done) return;
   extern __shared__ __align__(16) double sm[];
   const BandDesc b = bands[blockIdx.x];
@@ -1518,6 +1569,7 @@ __global__ void __launch_bounds__(NTHR, S <= 2 ? 2 : 1) k_band_solve_ring(const 
 // padding) and the inverted diagonal tiles dinv (nbmax x 64 x 64 row-major per subdomain)
 __global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, const double* __restrict__ L,
                             long long ld, const double* __restrict__ dinv, int nbmax) {
+  PDL_ENTRY();
   const int bi = blockIdx.y;
   const BandDesc bd = bands[first_band + bi];
   const double* Lb = L + (long long)bi * ld * ld;
@@ -1548,6 +1600,7 @@ __global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, 
 // the inverted upper diagonal tiles udinv (nbmax x 64 x 64 row-major per subdomain)
 __global__ void k_pack_band_u(const BandDesc* __restrict__ bands, int first_band, const double* __restrict__ LU,
                               long long ld, const double* __restrict__ udinv, int nbmax) {
+  PDL_ENTRY();
   const int bi = blockIdx.y;
   const BandDesc bd = bands[first_band + bi];
   const double* Ub = LU + (long long)bi * ld * ld;
