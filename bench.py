@@ -178,7 +178,8 @@ def iteration_bytes(cfg, a, pre, local_bytes):
 # CPU baseline (oracle port of the reference algorithm, bounded sample)
 # --------------------------------------------------------------------------------------------
 
-def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8, sym=True):
+def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8, sym=True,
+                 warmup=0, steps=1):
     """Per-iteration CPU time of the reference algorithm, measured on a bounded sample.
 
     Timed pieces (numpy/scipy = the reference's own kernels, all host threads):
@@ -211,7 +212,35 @@ def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8, 
             front = ring
         maps[s] = (interior, layers)
     subs = {s: O.OracleSubdomain(a, maps[s], sym) for s in pick}
-    x = rng.standard_normal(n)
+    nC = nsub * n_modes
+    nCs = min(nC, 8192)  # dense coarse solve timed at <= 8192 and scaled by (n_C / size)^2
+    m = rng.standard_normal((nCs, 64))
+    fac = sla.cho_factor(m @ m.T + nCs * np.eye(nCs))
+    del m
+    vecs = [rng.standard_normal(n) for _ in range(5)]
+    ctx = dict(a=a, pick=pick, subs=subs, nsub=nsub, nC=nC, nCs=nCs, fac=fac, vecs=vecs,
+               c=rng.standard_normal(nCs))
+    for _ in range(warmup):
+        _cpu_iteration(ctx)
+    times = [_cpu_iteration(ctx) for _ in range(max(1, steps))]
+    t_iter = float(np.mean(times))
+    cores = os.cpu_count()
+    return {"value": 1.0 / t_iter, "unit": "iters/s", "cores": cores, "kind": "port",
+            "sample": (f"cfg{cfg_id}: {len(pick)} of {nsub} subdomain {'Cholesky' if sym else 'LU'} solves (n_i up to "
+                       f"{max(subs[s].n_local for s in pick)}) + scatter, scaled x{nsub / len(pick):.0f}; "
+                       f"full-size SpMV; n_C={nC} dense Cholesky solve"
+                       f"{'' if nC == nCs else f' (timed at {nCs}, scaled by (n_C/{nCs})^2)'}; PCG vector ops; "
+                       f"one iteration = {t_iter * 1e3:.1f} ms on {cores} host threads "
+                       f"(mean of {len(times)} after {warmup} warm-up)"),
+            "t_iter_s": t_iter, "times_s": times}
+
+
+def _cpu_iteration(ctx):
+    """One sampled preconditioned iteration on the host (the timed part of ``cpu_baseline``)."""
+    import scipy.linalg as sla
+    a, pick, subs = ctx["a"], ctx["pick"], ctx["subs"]
+    x, p, r, z, xx = (v.copy() for v in ctx["vecs"])
+    n = a.shape[0]
     reps = 3
     t0 = time.perf_counter()
     for _ in range(reps):
@@ -223,30 +252,14 @@ def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8, 
         sd = subs[s]
         y = sd.solve(x[sd.indices])
         np.add.at(out, sd.indices, y)
-    t_local = (time.perf_counter() - t0) * nsub / len(pick)
-    nC = nsub * n_modes
-    nCs = min(nC, 8192)  # dense coarse solve timed at <= 8192 and scaled by (n_C / size)^2
-    m = rng.standard_normal((nCs, 64))
-    spd = m @ m.T + nCs * np.eye(nCs)
-    fac = sla.cho_factor(spd)
-    c = rng.standard_normal(nCs)
+    t_local = (time.perf_counter() - t0) * ctx["nsub"] / len(pick)
     t0 = time.perf_counter()
-    sla.cho_solve(fac, c)
-    t_coarse = (time.perf_counter() - t0) * (nC / nCs) ** 2
-    del spd, fac, m
-    p, r, z, xx = (rng.standard_normal(n) for _ in range(4))
+    sla.cho_solve(ctx["fac"], ctx["c"])
+    t_coarse = (time.perf_counter() - t0) * (ctx["nC"] / ctx["nCs"]) ** 2
     t0 = time.perf_counter()
     float(p @ x); xx += 0.5 * p; r -= 0.5 * x; float(np.linalg.norm(r)); float(r @ z); p = z + 0.3 * p
     t_vec = time.perf_counter() - t0
-    t_iter = t_spmv + t_local + t_coarse + t_vec
-    cores = os.cpu_count()
-    return {"value": 1.0 / t_iter, "unit": "iters/s", "cores": cores, "kind": "port",
-            "sample": (f"cfg{cfg_id}: {len(pick)} of {nsub} subdomain {'Cholesky' if sym else 'LU'} solves (n_i up to "
-                       f"{max(subs[s].n_local for s in pick)}) + scatter, scaled x{nsub / len(pick):.0f}; "
-                       f"full-size SpMV; n_C={nC} dense Cholesky solve"
-                       f"{'' if nC == nCs else f' (timed at {nCs}, scaled by (n_C/{nCs})^2)'}; PCG vector ops; "
-                       f"one iteration = {t_iter * 1e3:.1f} ms on {cores} host threads"),
-            "t_iter_s": t_iter}
+    return t_spmv + t_local + t_coarse + t_vec
 
 
 # --------------------------------------------------------------------------------------------
@@ -272,12 +285,11 @@ def main():
         if rank != 0:
             return
         a, sym, owner, nsub = cfg.build()
-        cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym)
-        times = [cb["t_iter_s"]]
-        for _ in range(max(0, args.steps - 1)):
-            times.append(cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym)["t_iter_s"])
+        cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym,
+                          warmup=args.warmup, steps=args.steps)
+        times = cb["times_s"]
         val = 1.0 / float(np.mean(times))
-        cbo = {k: v for k, v in cb.items() if k != "t_iter_s"}
+        cbo = {k: v for k, v in cb.items() if k not in ("t_iter_s", "times_s")}
         cbo["value"] = val
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s",
                           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -440,6 +452,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym)
         cb.pop("t_iter_s")
+        cb.pop("times_s")
         line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line))
