@@ -76,7 +76,9 @@ const char* tls_ctx_last_error(const tls_ctx* ctx);
 int64_t tls_ctx_device_bytes(const tls_ctx* ctx);
 
 /* ---- SparseMat: replaces SparseMat(csr) canonical storage (src/sparsemat.py:36-52)
- * indptr/indices/data are HOST arrays of a canonical CSR (sorted, unique columns). */
+ * indptr/indices/data are HOST arrays of a canonical CSR (sorted, unique columns).
+ * The structure is bounds-checked on the host (indptr[0] = 0, non-decreasing, indptr[n] = nnz,
+ * 0 <= indices < n): TLS_ERR_DIM with the offending row / entry in tls_ctx_last_error. */
 int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_t* indptr,
                           const int32_t* indices, const double* data, int32_t symmetric);
 /* y = A x : replaces SparseMat.matvec (src/sparsemat.py:125-129) */

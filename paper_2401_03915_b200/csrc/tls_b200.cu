@@ -626,6 +626,18 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
                           const int32_t* indices, const double* data, int32_t symmetric) {
   if (!ctx || nrows <= 0 || nrows > INT32_MAX || nnz < 0 || nnz >= INT32_MAX)
     return ctx ? fail(ctx, TLS_ERR_ARG, "matrix size out of the supported int32 range") : TLS_ERR_ARG;
+  // host-side bounds check of the CSR structure: every device kernel indexes through indptr and
+  // indices without checks, so a malformed matrix is refused here, before anything is uploaded
+  if (!indptr || (nnz > 0 && (!indices || !data)))
+    return fail(ctx, TLS_ERR_ARG, "null CSR array");
+  if (indptr[0] != 0 || indptr[nrows] != nnz)
+    return fail(ctx, TLS_ERR_DIM, "indptr must start at 0 and end at nnz");
+  for (int64_t i = 0; i < nrows; ++i)
+    if (indptr[i + 1] < indptr[i])
+      return fail(ctx, TLS_ERR_DIM, "indptr decreases at row " + std::to_string(i));
+  for (int64_t k = 0; k < nnz; ++k)
+    if ((uint32_t)indices[k] >= (uint32_t)nrows)
+      return fail(ctx, TLS_ERR_DIM, "column index out of range at entry " + std::to_string(k));
   CK(cudaSetDevice(ctx->device));
   const bool renum = !ctx->h_nofo.empty();
   if (renum && (int64_t)ctx->h_nofo.size() != nrows)

@@ -320,3 +320,28 @@ def test_band_lu_and_inverse_agree(B, name):
         np.testing.assert_allclose(pb.apply(r), z, rtol=0, atol=tol * np.abs(z).max())
     x, rep = B.gmres(mat, pb, d["b"], tol=float(d["tol"]), restart=int(d["restart"]))
     assert abs(rep.iterations - int(d["iterations"])) <= 1
+
+
+def test_matrix_upload_refuses_malformed_csr(B):
+    """Host bounds check in tls_matrix_upload: the device kernels index through indptr/indices
+    unchecked, so malformed structure must be refused before upload (TLS_ERR_DIM -> ValueError)."""
+    from types import SimpleNamespace
+
+    from paper_2401_03915_b200 import device as D
+
+    def csr(indptr, indices, n=3):
+        indices = np.asarray(indices, dtype=np.int32)
+        return SimpleNamespace(indptr=np.asarray(indptr), indices=indices,
+                               data=np.ones(indices.size), shape=(n, n))
+
+    h = D.Handle(0)
+    cases = [(csr([0, 1, 2, 3], [0, 3, 2]), "column index out of range at entry 1"),
+             (csr([0, 1, 2, 3], [0, -1, 2]), "column index out of range at entry 1"),
+             (csr([0, 2, 1, 3], [0, 1, 2]), "indptr decreases at row 1"),
+             (csr([1, 1, 2, 3], [0, 1, 2]), "indptr must start at 0"),
+             (csr([0, 1, 2, 2], [0, 1, 2]), "indptr must start at 0")]
+    for bad, msg in cases:
+        with pytest.raises(ValueError, match=msg):
+            h.upload_matrix(bad, True)
+    h.upload_matrix(csr([0, 1, 2, 3], [0, 1, 2]), True)  # the handle stays usable
+    assert h.n == 3
