@@ -39,6 +39,7 @@ from __future__ import annotations
 
 import os
 import time
+from concurrent.futures import ThreadPoolExecutor
 import warnings
 
 import numpy as np
@@ -956,15 +957,26 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     t0 = time.perf_counter()
     _log(t0, f"subdomains [{lo},{hi}) of {N}, local={local}, ld={ld}, batch={batch}")
     a_buf = torch.empty((min(batch, hi - lo), ld, ld), dtype=torch.float64, device=dev)
+    # the host factor orders of batch b+1 are computed on one worker thread while batch b's device
+    # work runs (the main thread mostly waits in stream syncs); a single worker, so the shared
+    # _LocalGraphs scratch is never used by two threads at once
+    order_pool = ThreadPoolExecutor(max_workers=1) if band else None
+
+    def _orders_of(f):
+        return local_orders(adj, [maps[f + b] for b in range(min(batch, hi - f))], order_kind)
+
+    next_orders = order_pool.submit(_orders_of, lo) if band else None
     for first in range(lo, hi, batch):
         cnt = min(batch, hi - first)
+        if band:
+            perm_list = next_orders.result()
+            next_orders = order_pool.submit(_orders_of, first + batch) if first + batch < hi else None
         if first > lo:
             _log(t0, f"batch at {first}")
         tb0 = time.perf_counter() if VERBOSE else 0.0
         A = a_buf[:cnt]
         handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
         if band_lu:
-            perm_list = local_orders(adj, [maps[first + b] for b in range(cnt)], order_kind)
             n_list = [int(n_loc[first + b]) for b in range(cnt)]
             LU, piv, Ldinv, Udinv, pin, pout, lcodes, ucodes, info, P = _band_lu_factor(
                 torch, A, perm_list, n_list, ld)
@@ -1008,8 +1020,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             continue
         if band:
             tb = _stage("extract", tb0)
-            perm_list = local_orders(adj, [maps[first + b] for b in range(cnt)], order_kind)
-            tb = _stage("orders (host)", tb)
+            tb = _stage("orders (host, wait)", tb)
             n_list = [int(n_loc[first + b]) for b in range(cnt)]
             L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld)
             tb = _stage("band factor", tb)
@@ -1087,6 +1098,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                 w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
         del A, Binv
     del a_buf
+    if order_pool is not None:
+        order_pool.shutdown()
     if not want_coarse:
         _release_cache(torch, dev)
         return None
@@ -1108,7 +1121,6 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         r, perm = sla.qr(z, mode="r", pivoting=True)
         return s, np.abs(np.diag(r)), perm
 
-    from concurrent.futures import ThreadPoolExecutor
     try:  # one BLAS thread per pool worker (no oversubscription)
         from threadpoolctl import threadpool_limits
         limit = threadpool_limits(limits=1)
