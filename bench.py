@@ -70,8 +70,8 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _run_nvml(self):
-        """In-process NVML queries (~0.1 ms each): dense sampling even over a 1-2 s timed region."""
+    def _nvml_sampler(self):
+        """In-process NVML query (~0.1 ms): dense sampling even over a millisecond timed region."""
         import pynvml as N
         N.nvmlInit()
         h = N.nvmlDeviceGetHandleByIndex(self.index)
@@ -79,18 +79,21 @@ class ClockSampler:
         get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             N.nvmlDeviceGetCurrentClocksThrottleReasons
         bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
-        while not self._stop.is_set():
+
+        def sample():
             r = get_reasons(h)
             self.samples.append([str(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), str(mx)] +
                                 ["Active" if r & b else "Not Active" for b in bits])
-            self._stop.wait(0.02)
+        return sample
 
     def _run(self):
-        try:
-            self._run_nvml()
-            return
-        except Exception:
-            pass
+        if self._sample is not None:
+            try:
+                while not self._stop.wait(0.02):
+                    self._sample()
+                return
+            except Exception:
+                pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -103,6 +106,11 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        try:  # NVML is initialised and sampled once here, so even a very short region has a sample
+            self._sample = self._nvml_sampler()
+            self._sample()
+        except Exception:
+            self._sample = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -111,6 +119,11 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if self._sample is not None:
+            try:  # and once at the end of the region
+                self._sample()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
