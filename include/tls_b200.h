@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TLS_ABI_VERSION 1
+#define TLS_ABI_VERSION 2
 #define TLS_TILE 64           /* edge of the dense tiles of local operators */
 
 typedef enum {
@@ -44,7 +44,9 @@ typedef enum {
   TLS_ERR_CUDA = 8,       /* CUDA runtime failure                                          */
   TLS_ERR_OOM = 9,        /* device allocation failed                                      */
   TLS_ERR_FORMAT = 10,    /* MatrixMarketError(lineno, message)  (src/sparsemat.py:20-25)  */
-  TLS_ERR_IO = 11         /* file could not be opened / written (OSError)                  */
+  TLS_ERR_IO = 11,        /* file could not be opened / written (OSError)                  */
+  TLS_ERR_CALLBACK = 12   /* the per-iteration callback asked to stop (it raised: the binding
+                             re-raises that exception, as src/krylov.py:92-93 lets it propagate) */
 } tls_code;
 
 typedef enum { TLS_ASM = 0, TLS_RAS = 1 } tls_one_level;                       /* src/precond.py:34 */
@@ -64,8 +66,10 @@ typedef struct tls_status {
 typedef struct tls_ctx tls_ctx;
 
 /* per-iteration hook: (user, iteration, HOST copy of the current iterate, or NULL for GMRES).
- * Non-NULL forces one host sync per iteration (src/krylov.py:92-93, 182-183). */
-typedef void (*tls_iter_cb)(void* user, int32_t iteration, const double* x_host);
+ * Non-NULL forces one host sync per iteration (src/krylov.py:92-93, 182-183).  Returns 0 to go
+ * on; any other value stops the solve at once with TLS_ERR_CALLBACK (a binding whose callback
+ * raised returns 1 and re-raises after the call). */
+typedef int32_t (*tls_iter_cb)(void* user, int32_t iteration, const double* x_host);
 
 /* ---- lifecycle --------------------------------------------------------- */
 int32_t tls_abi_version(void);
@@ -132,6 +136,12 @@ int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first, int32_t count, cons
  * (row-major n_coarse^2, device).  k == NULL or n_coarse == 0 disables the coarse level. */
 int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, const double* basis,
                           const double* a0inv, void* stream);
+/* One step of iterative refinement on every coarse solve: y = X c; y += X (c - A0 y), X the
+ * stored A0^{-1}.  a0 = Z^T A Z (row-major n_coarse^2, device).  The reference solves with an LU /
+ * Cholesky factor of A0 (src/coarse.py:172-182, backward stable); the explicit inverse alone
+ * leaves a residual ~cond(A0)*eps, so setup turns this on when cond_1(A0) > 1e8 (one GPU only).
+ * Call after tls_coarse_upload, before tls_precond_finalize. */
+int32_t tls_coarse_refine(tls_ctx* ctx, const double* a0, void* stream);
 /* Build the apply schedule (work units, reduction lists, prolongation pull map). */
 int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine);
 
@@ -140,6 +150,18 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine);
 int32_t tls_precond_apply(tls_ctx* ctx, const double* r, double* z, void* stream);
 int32_t tls_apply_one_level(tls_ctx* ctx, const double* r, double* z, void* stream);
 int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream);
+/* The pieces of the apply, for the reference's attribute API and for parity checks:
+ * tls_local_solve: y_i = A_ii^{-1} R_i r for `count` listed subdomains (global ids, owned by this
+ *   handle), each in the reference's local order, concatenated into out (device, sum of n_i) --
+ *   Preconditioner.local_solves[i] (src/subdomain.py:72-95, called at src/precond.py:117-118);
+ * tls_coarse_restrict: c = Z^T r (n_coarse)      -- CoarseSpace.restrict     (src/coarse.py:40-41);
+ * tls_coarse_solve:    y = A0^{-1} c (one GPU)   -- CoarseSpace.solve_coarse (src/coarse.py:46-49);
+ * tls_coarse_prolong:  z = Z y (n)               -- CoarseSpace.prolong      (src/coarse.py:43-44). */
+int32_t tls_local_solve(tls_ctx* ctx, const double* r, int32_t count, const int32_t* subdomains,
+                        double* out, void* stream);
+int32_t tls_coarse_restrict(tls_ctx* ctx, const double* r, double* c, void* stream);
+int32_t tls_coarse_solve(tls_ctx* ctx, const double* c, double* y, void* stream);
+int32_t tls_coarse_prolong(tls_ctx* ctx, const double* y, double* z, void* stream);
 
 /* ---- Krylov: replaces pcg (src/krylov.py:58-107) and gmres (src/krylov.py:127-195).
  * b, x device; history HOST buffer of maxit+1 doubles (SolveReport.residuals);

@@ -25,6 +25,7 @@ TLS_ERR_CUDA = 8
 TLS_ERR_OOM = 9
 TLS_ERR_FORMAT = 10
 TLS_ERR_IO = 11
+TLS_ERR_CALLBACK = 12
 
 ONE_LEVEL = {"asm": 0, "ras": 1}
 COMBINE = {"none": 0, "additive": 1, "deflated": 2}
@@ -36,7 +37,7 @@ class TlsStatus(C.Structure):
                 ("pad_", C.c_int32)]
 
 
-ITER_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(C.c_double))
+ITER_CB = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_double))
 
 _P = C.c_void_p
 _I32 = C.c_int32
@@ -61,6 +62,11 @@ SIGNATURES = {
     "tls_precond_apply": (_I32, [_P, _P, _P, _P]),
     "tls_apply_one_level": (_I32, [_P, _P, _P, _P]),
     "tls_coarse_apply": (_I32, [_P, _P, _P, _P]),
+    "tls_coarse_refine": (_I32, [_P, _P, _P]),
+    "tls_local_solve": (_I32, [_P, _P, _I32, _P, _P, _P]),
+    "tls_coarse_restrict": (_I32, [_P, _P, _P, _P]),
+    "tls_coarse_solve": (_I32, [_P, _P, _P, _P]),
+    "tls_coarse_prolong": (_I32, [_P, _P, _P, _P]),
     "tls_pcg": (_I32, [_P, _P, _P, _D, _I32, _I32, _P, _P, C.POINTER(TlsStatus), ITER_CB, _P, _P]),
     "tls_gmres": (_I32, [_P, _P, _P, _D, _I32, _I32, _I32, _P, C.POINTER(TlsStatus), ITER_CB, _P, _P]),
     "tls_report": (_I32, [_P, C.POINTER(_I64), C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I64)]),

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -32,6 +33,10 @@ constexpr int MAX_GRID = 148 * 8;    // 148 SMs x 8 resident 256-thread CTAs
 constexpr int GM_FUSED_MAXCOLS = 96; // fused CGS2 step while (nc + 1) x 256 doubles fit in smem
 // shared memory of the per-warp rings of k_band_solve_ring<S> (8 warps x S tiles x 4 KB)
 constexpr size_t ring_bytes(int S) { return sizeof(double) * 8 * (size_t)S * 512; }
+// shared memory of k_band_solve for subdomains of up to nb 64-row blocks (local vector + scratch)
+constexpr size_t band_smem_bytes(int nb) { return sizeof(double) * ((size_t)nb * 64 + 8 * 64 + 64); }
+// largest subdomain (rows) whose local vector fits `optin` bytes of shared memory
+static int band_max_rows(size_t optin) { return (int)((optin / sizeof(double) - 8 * 64 - 64) / 64) * 64; }
 
 template <class T>
 void dfree(T*& p) {
@@ -73,6 +78,12 @@ struct tls_ctx {
   std::vector<int> h_k, h_cstart;
   std::vector<long long> h_zoff;
   double *d_Z = nullptr, *ctiles = nullptr;
+  // one step of iterative refinement of the coarse solve, y = X c; y += X (c - A0 y) (X = the
+  // stored A0^{-1}): blocks nsub+1 (A0 tiles) and nsub+2 (X again) behind the coarse block
+  bool cref = false;
+  double* a0tiles = nullptr;
+  long long cpad = 0;                 // padded coarse length (nt * TT)
+  int nu_ref1 = 0, no_ref1 = 0, nu_ref2 = 0, no_ref2 = 0;
   long long* d_zoff = nullptr;
   int *d_kcnt = nullptr, *d_cstart = nullptr;
   // ---- schedule
@@ -228,15 +239,28 @@ static int upload(tls_ctx* ctx, T*& d, const T* h, int64_t count) {
   return TLS_OK;
 }
 
-// The dynamic shared-memory limit is a per-function, process-wide attribute: only ever raise it,
-// under a lock (several handles may be set up concurrently from host threads).
-static cudaError_t raise_smem(const void* fn, size_t bytes, size_t& current) {
+// The dynamic shared-memory limit is a per-(function, device) attribute: cudaFuncSetAttribute
+// applies to the CURRENT device only, so the raised value is remembered per device and only ever
+// raised, under a lock (several handles may be set up concurrently from host threads, possibly on
+// different GPUs).  The caller must have made `device` current.
+static cudaError_t raise_smem(int device, const void* fn, size_t bytes) {
   static std::mutex m;
+  static std::map<std::pair<const void*, int>, size_t> current;
   std::lock_guard<std::mutex> lk(m);
-  if (bytes <= current) return cudaSuccess;
+  size_t& cur = current[{fn, device}];
+  if (cur == 0) cur = 48 * 1024;  // the default limit every kernel starts with
+  if (bytes <= cur) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) current = bytes;
+  if (e == cudaSuccess) cur = bytes;
   return e;
+}
+
+// opt-in shared memory per block of `device` (227 KB on B200)
+static size_t smem_optin(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess || v <= 0)
+    v = 227 * 1024;
+  return (size_t)v;
 }
 
 // every kernel launch of the library: cudaLaunchKernelEx with programmatic stream serialization
@@ -306,6 +330,36 @@ static int spmv_lpr(tls_ctx* ctx, cudaStream_t s, const double* x, double* y, co
 // which unit/out lists a solve stage uses
 enum { L_LOCAL = 0, L_COARSE = 1, L_ALL = 2 };
 
+// y0 = X c is in yloc's coarse segment, c in xloc's: one refinement step
+// rho = c - A0 y0 (block nsub+1), y0 += X rho (block nsub+2) -- restores a backward-stable coarse
+// solve (the reference factors A0, src/coarse.py:178-182) when cond(A0) makes X c alone lose digits
+static int enq_coarse_refine(tls_ctx* ctx, cudaStream_t s, const int* done) {
+  const long long c0 = ctx->coarse_xoff, P = ctx->cpad;
+  const int nc = ctx->ncoarse, g = grid_for(nc, NTHR);
+  const int u1 = ctx->nu_local + ctx->nu_coarse, o1 = ctx->no_local + ctx->no_coarse;
+  const int u2 = u1 + ctx->nu_ref1, o2 = o1 + ctx->no_ref1;
+  launch_k(ctx, k_lincomb, g, NTHR, 0, s, nc, (const double*)(ctx->yloc + c0), (const double*)nullptr, 0.0,
+           ctx->xloc + c0 + P, done);
+  CKL();
+  launch_k(ctx, k_symv_tiles, ctx->nu_ref1, NTHR, 0, s, ctx->d_blk, ctx->d_units + u1, ctx->xloc, ctx->slots, done);
+  CKL();
+  launch_k(ctx, k_reduce_tiles, (ctx->no_ref1 + 7) / 8, NTHR, 0, s, ctx->d_blk, ctx->d_outs + o1, ctx->no_ref1,
+           ctx->d_red, ctx->slots, ctx->yloc, done);
+  CKL();
+  launch_k(ctx, k_lincomb, g, NTHR, 0, s, nc, (const double*)(ctx->xloc + c0), (const double*)(ctx->yloc + c0 + P),
+           -1.0, ctx->xloc + c0 + 2 * P, done);
+  CKL();
+  launch_k(ctx, k_symv_tiles, ctx->nu_ref2, NTHR, 0, s, ctx->d_blk, ctx->d_units + u2, ctx->xloc, ctx->slots, done);
+  CKL();
+  launch_k(ctx, k_reduce_tiles, (ctx->no_ref2 + 7) / 8, NTHR, 0, s, ctx->d_blk, ctx->d_outs + o2, ctx->no_ref2,
+           ctx->d_red, ctx->slots, ctx->yloc, done);
+  CKL();
+  launch_k(ctx, k_lincomb, g, NTHR, 0, s, nc, (const double*)(ctx->yloc + c0), (const double*)(ctx->yloc + c0 + 2 * P),
+           1.0, ctx->yloc + c0, done);
+  CKL();
+  return TLS_OK;
+}
+
 // r_src (band local operators only): gather R_i r inside the band kernel instead of from xloc
 static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
                      const double* r_src = nullptr) {
@@ -351,6 +405,7 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
                                                  ctx->slots, ctx->yloc, done);
     CKL();
   }
+  if (ctx->cref && which != L_LOCAL) TRY(enq_coarse_refine(ctx, s, done));
   return TLS_OK;
 }
 
@@ -590,7 +645,7 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   destroy_graphs(ctx);
   dfree(ctx->rowptr); dfree(ctx->col); dfree(ctx->val);
   dfree(ctx->d_sub_idxoff); dfree(ctx->d_sub_n); dfree(ctx->d_idx); dfree(ctx->d_nint);
-  dfree(ctx->d_blk); dfree(ctx->tiles); dfree(ctx->d_Z); dfree(ctx->ctiles); dfree(ctx->d_zoff);
+  dfree(ctx->d_blk); dfree(ctx->tiles); dfree(ctx->d_Z); dfree(ctx->ctiles); dfree(ctx->a0tiles); dfree(ctx->d_zoff);
   dfree(ctx->d_kcnt); dfree(ctx->d_cstart); dfree(ctx->d_units); dfree(ctx->d_outs); dfree(ctx->d_red);
   dfree(ctx->d_gidx); dfree(ctx->d_pull_ptr); dfree(ctx->d_pull_pos); dfree(ctx->d_zrow);
   dfree(ctx->d_zk); dfree(ctx->d_zc); dfree(ctx->d_zst); dfree(ctx->xloc); dfree(ctx->yloc); dfree(ctx->slots);
@@ -753,7 +808,7 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
   TRY(upload(ctx, ctx->d_sub_n, ctx->h_n.data(), n_sub));
   TRY(upload(ctx, ctx->d_nint, ctx->h_nint.data(), n_sub));
   // tile storage for the local inverses: packed lower triangle (symmetric) or full
-  ctx->h_blk.assign(n_sub + 1, BlkDesc{});
+  ctx->h_blk.assign(n_sub + 3, BlkDesc{});  // + coarse block, + the two refinement blocks
   int64_t tiles = 0;
   long long xo = 0;
   std::vector<int64_t> tbase(n_sub);
@@ -776,8 +831,10 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
       const int v = atoi(e);
       if (v >= 1 && v <= 32) ctx->restrict_cw = v;
     }
-    static size_t rsmem_set = 48 * 1024;
-    CK(raise_smem((const void*)k_restrict, ctx->restrict_smem, rsmem_set));
+    if (ctx->restrict_smem > smem_optin(ctx->device))
+      return fail(ctx, TLS_ERR_ARG, "subdomain interior of " + std::to_string(mi) +
+                                        " rows exceeds the shared memory of the coarse restriction");
+    CK(raise_smem(ctx->device, (const void*)k_restrict, ctx->restrict_smem));
   }
   ctx->tile_doubles = ctx->local_kind >= 1 ? 0 : tiles * TT * TT;
   dfree(ctx->tiles);
@@ -792,22 +849,32 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
       maxnb = std::max(maxnb, ctx->h_blk[s].nt);
     }
     TRY(upload(ctx, ctx->d_band, ctx->h_band.data(), n_sub));
-    ctx->band_smem = sizeof(double) * ((size_t)maxnb * TT + 8 * TT + TT);
-    static size_t smem_set = 0, smem_set2 = 0, smem_set3 = 0, smem_set4 = 0;
-    CK(raise_smem((const void*)k_band_solve<1>, ctx->band_smem, smem_set));
-    CK(raise_smem((const void*)k_band_solve<2>, ctx->band_smem, smem_set2));
-    CK(raise_smem((const void*)k_band_solve_ring<4>, ctx->band_smem + ring_bytes(4), smem_set3));
-    CK(raise_smem((const void*)k_band_solve_ring<2>, ctx->band_smem + ring_bytes(2), smem_set4));
+    ctx->band_smem = band_smem_bytes(maxnb);
+    // the whole local vector lives in shared memory: refuse (clear error; setup then keeps the
+    // inverse tiles) when even the plain kernel cannot hold the largest subdomain, and raise the
+    // limit of a cp.async ring variant only when its rings fit too
+    const size_t optin = smem_optin(ctx->device);
+    if (ctx->band_smem > optin)
+      return fail(ctx, TLS_ERR_ARG, "band local operators: a subdomain of " + std::to_string(ctx->max_n) +
+                                        " rows exceeds the shared memory of k_band_solve (max " +
+                                        std::to_string(band_max_rows(optin)) + " rows); use local='inverse'");
+    CK(raise_smem(ctx->device, (const void*)k_band_solve<1>, ctx->band_smem));
+    CK(raise_smem(ctx->device, (const void*)k_band_solve<2>, ctx->band_smem));
     // per-warp cp.async rings, 4 deep at 1 CTA/SM, when the subdomains fit one wave (<= 148;
     // an 8-rank configuration-2 slab: 0.79 -> 0.57 ms per iteration); otherwise the 4-CTA/SM
     // kernel (the 2-deep ring at 2 CTAs/SM for <= 296 subdomains measured cfg3 -4.5%, cfg4 +4.9%,
     // 2-rank slab +2%: selectable with TLS_BAND_RING=2; profiles/ab_band_ring_r01.txt)
     ctx->band_ring = n_sub <= 148 ? 4 : 0;
-    if (ctx->band_smem + ring_bytes(ctx->band_ring) > 227 * 1024) ctx->band_ring = 0;
     if (const char* e = getenv("TLS_BAND_RING")) {
       const int v = atoi(e);
       if (v == 0 || v == 2 || v == 4) ctx->band_ring = v;
     }
+    while (ctx->band_ring > 0 && ctx->band_smem + ring_bytes(ctx->band_ring) > optin) ctx->band_ring /= 2;
+    if (ctx->band_ring == 1) ctx->band_ring = 0;
+    if (ctx->band_ring == 4)
+      CK(raise_smem(ctx->device, (const void*)k_band_solve_ring<4>, ctx->band_smem + ring_bytes(4)));
+    if (ctx->band_ring == 2)
+      CK(raise_smem(ctx->device, (const void*)k_band_solve_ring<2>, ctx->band_smem + ring_bytes(2)));
     // one tile per load round: two (UNR = 2, 128 registers, 2 CTAs/SM) measured slower on
     // configuration 3 (1,249 vs 1,300 it/s) and mixed on 8-rank configuration 2 slabs
     // (profiles/ab_band_unr_r01.txt); kept selectable for the few-subdomains-per-GPU regime
@@ -828,9 +895,10 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     ctx->band_bytes = 0.0;
   }
   for (int s = 0; s < n_sub; ++s) ctx->h_blk[s].tiles = ctx->tiles + tbase[s] * TT * TT;
-  TRY(upload(ctx, ctx->d_blk, ctx->h_blk.data(), n_sub + 1));
+  TRY(upload(ctx, ctx->d_blk, ctx->h_blk.data(), n_sub + 3));
   ctx->stored.assign(n_sub, 0);
   ctx->ncoarse = 0;
+  ctx->cref = false;
   ctx->finalized = false;
   destroy_graphs(ctx);
   return TLS_OK;
@@ -900,6 +968,7 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
   cudaStream_t s = (cudaStream_t)stream;
   ctx->finalized = false;
   destroy_graphs(ctx);
+  ctx->cref = false;
   if (n_coarse <= 0 || !k) {
     ctx->ncoarse = 0;
     return TLS_OK;
@@ -937,7 +1006,8 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
   TRY(dalloc(ctx, ctx->ctiles, ntiles * TT * TT));
   cb.tiles = ctx->ctiles;
   ctx->h_blk[ctx->nsub] = cb;
-  CK(cudaMemcpy(ctx->d_blk, ctx->h_blk.data(), sizeof(BlkDesc) * (ctx->nsub + 1), cudaMemcpyHostToDevice));
+  ctx->cpad = (long long)cb.nt * TT;
+  CK(cudaMemcpy(ctx->d_blk, ctx->h_blk.data(), sizeof(BlkDesc) * (ctx->nsub + 3), cudaMemcpyHostToDevice));
   dim3 g((unsigned)std::min<int64_t>(ntiles, 8192), 1);
   launch_k(ctx, k_pack_tiles, g, NTHR, 0, s, ctx->d_blk, ctx->nsub, a0inv, n_coarse, 0);
   CKL();
@@ -1008,7 +1078,7 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
         gidx[ctx->h_blk[s].xoff + p] = ctx->h_idx[ctx->h_off[s] + ctx->h_perm_in[ctx->h_off[s] + p]];
   TRY(upload(ctx, ctx->d_gidx, gidx.data(), ctx->Xloc));
   ctx->coarse_xoff = ctx->Xloc;
-  ctx->X = ctx->Xloc + (ctx->ncoarse > 0 ? (long long)ctx->h_blk[nsub].nt * TT : 0);
+  ctx->X = ctx->Xloc + (ctx->ncoarse > 0 ? ctx->cpad : 0) + (ctx->cref ? 2 * ctx->cpad : 0);
   const bool part = !ctx->h_nofo.empty();
   const bool asm_ = one_level == TLS_ASM;
   ctx->Xrecv = 0;
@@ -1080,6 +1150,20 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
     }
     ctx->nu_coarse = (int)units.size() - ctx->nu_local;
     ctx->no_coarse = (int)outs.size() - ctx->no_local;
+    ctx->nu_ref1 = ctx->no_ref1 = ctx->nu_ref2 = ctx->no_ref2 = 0;
+    if (ctx->cref) {  // A0 (general tiles) then X again, each with its own units / slots
+      const int nt = ctx->h_blk[nsub].nt;
+      size_t u0 = units.size(), o0 = outs.size();
+      plan_block(nsub + 1, nt, 0, 2, slot, units, outs, red);
+      ctx->nu_ref1 = (int)(units.size() - u0);
+      ctx->no_ref1 = (int)(outs.size() - o0);
+      u0 = units.size(), o0 = outs.size();
+      plan_block(nsub + 2, nt, ctx->sym, 2, slot, units, outs, red);
+      ctx->nu_ref2 = (int)(units.size() - u0);
+      ctx->no_ref2 = (int)(outs.size() - o0);
+      const double nc = ctx->ncoarse;
+      ctx->algo_coarse = 2.0 * ctx->algo_coarse + 8.0 * nc * nc;  // X twice + the A0 tiles
+    }
   }
   TRY(upload(ctx, ctx->d_units, units.data(), (int64_t)units.size()));
   TRY(upload(ctx, ctx->d_outs, outs.data(), (int64_t)outs.size()));
@@ -1248,6 +1332,106 @@ int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream)
   return api_out(ctx, s, zi, z);
 }
 
+// y_i = A_ii^{-1} R_i r for the listed (owned, global ids) subdomains, each in the reference's
+// local order (interior, then the layers; src/partition.py:295-298), concatenated into out --
+// the local_solves closures of src/precond.py:117-118 / src/subdomain.py:72-95, run by the same
+// kernels as the apply (band sweeps or inverse tiles) and read back from yloc
+int32_t tls_local_solve(tls_ctx* ctx, const double* r, int32_t count, const int32_t* subdomains, double* out,
+                        void* stream) {
+  TRY(need_final(ctx));
+  if (count <= 0 || !subdomains || !out) return fail(ctx, TLS_ERR_ARG, "empty subdomain list");
+  std::vector<int> pos;
+  for (int i = 0; i < count; ++i) {
+    const int sl = subdomains[i] - ctx->own_lo;
+    if (sl < 0 || sl >= ctx->nsub) return fail(ctx, TLS_ERR_ARG, "subdomain " + std::to_string(subdomains[i]) + " not owned by this handle");
+    const int ns = ctx->h_n[sl];
+    std::vector<int> posl(ns);
+    for (int l = 0; l < ns; ++l) posl[l] = l;
+    if (ctx->local_kind >= 1)
+      for (int p = 0; p < ns; ++p) posl[ctx->h_perm[ctx->h_off[sl] + p]] = p;
+    for (int l = 0; l < ns; ++l) pos.push_back((int)(ctx->h_blk[sl].xoff + posl[l]));
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int* d_pos = nullptr;
+  CK(cudaMallocAsync((void**)&d_pos, sizeof(int) * pos.size(), s));
+  CK(cudaMemcpyAsync(d_pos, pos.data(), sizeof(int) * pos.size(), cudaMemcpyHostToDevice, s));
+  double* ri;
+  TRY(api_in(ctx, s, r, &ri));
+  TRY(enq_local(ctx, s, ri, nullptr));
+  launch_k(ctx, k_xpack, grid_for((long long)pos.size(), NTHR), NTHR, 0, s, (long long)pos.size(), (const int*)d_pos,
+           (const double*)ctx->yloc, out, (const int*)nullptr);
+  CKL();
+  CK(cudaFreeAsync(d_pos, s));
+  CK(cudaStreamSynchronize(s));  // pos (host) must outlive the async copy
+  return TLS_OK;
+}
+
+// CoarseSpace.restrict / solve_coarse / prolong (src/coarse.py:40-49) on the device, with the
+// kernels of the apply: c = Z^T r (n_C, summed over the ranks), y = A0^{-1} c (one GPU), z = Z y
+int32_t tls_coarse_restrict(tls_ctx* ctx, const double* r, double* c, void* stream) {
+  TRY(need_final(ctx));
+  if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "no coarse space");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  double* ri;
+  TRY(api_in(ctx, s, r, &ri));
+  TRY(enq_restrict_all(ctx, s, ri, nullptr));
+  CK(cudaMemcpyAsync(c, ctx->xloc + ctx->coarse_xoff, sizeof(double) * ctx->ncoarse, cudaMemcpyDeviceToDevice, s));
+  return TLS_OK;
+}
+
+int32_t tls_coarse_solve(tls_ctx* ctx, const double* c, double* y, void* stream) {
+  TRY(need_final(ctx));
+  if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "no coarse space");
+  if (sharded(ctx)) return fail(ctx, TLS_ERR_STATE, "tls_coarse_solve: a sharded handle holds only its rows of A0^{-1}");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(ctx->xloc + ctx->coarse_xoff, c, sizeof(double) * ctx->ncoarse, cudaMemcpyDeviceToDevice, s));
+  TRY(enq_solve(ctx, s, L_COARSE, nullptr));
+  CK(cudaMemcpyAsync(y, ctx->yloc + ctx->coarse_xoff, sizeof(double) * ctx->ncoarse, cudaMemcpyDeviceToDevice, s));
+  return TLS_OK;
+}
+
+int32_t tls_coarse_prolong(tls_ctx* ctx, const double* y, double* z, void* stream) {
+  TRY(need_final(ctx));
+  if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "no coarse space");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(ctx->yloc + ctx->coarse_xoff, y, sizeof(double) * ctx->ncoarse, cudaMemcpyDeviceToDevice, s));
+  double* zi = api_out_buf(ctx, z);
+  TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, zi, nullptr)));
+  return api_out(ctx, s, zi, z);
+}
+
+// store A0 (row-major n_C x n_C, device) and turn on one refinement step of every coarse solve
+int32_t tls_coarse_refine(tls_ctx* ctx, const double* a0, void* stream) {
+  if (!ctx || !ctx->nsub) return ctx ? fail(ctx, TLS_ERR_STATE, "upload subdomains first") : TLS_ERR_ARG;
+  if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "upload the coarse space first");
+  if (!ctx->h_nofo.empty()) return fail(ctx, TLS_ERR_STATE, "coarse refinement needs the whole A0^{-1} (one GPU)");
+  if (!a0) return fail(ctx, TLS_ERR_ARG, "null A0");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nsub = ctx->nsub;
+  BlkDesc a = ctx->h_blk[nsub];
+  a.sym = 0;
+  a.xoff = ctx->Xloc + ctx->cpad;
+  TRY(dalloc(ctx, ctx->a0tiles, (int64_t)a.nt * a.nt * TT * TT));
+  a.tiles = ctx->a0tiles;
+  BlkDesc x2 = ctx->h_blk[nsub];
+  x2.xoff = ctx->Xloc + 2 * ctx->cpad;
+  ctx->h_blk[nsub + 1] = a;
+  ctx->h_blk[nsub + 2] = x2;
+  CK(cudaMemcpy(ctx->d_blk, ctx->h_blk.data(), sizeof(BlkDesc) * (nsub + 3), cudaMemcpyHostToDevice));
+  dim3 g((unsigned)std::min<int64_t>((int64_t)a.nt * a.nt, 8192), 1);
+  launch_k(ctx, k_pack_tiles, g, NTHR, 0, s, ctx->d_blk, nsub + 1, a0, (long long)ctx->ncoarse, 0LL);
+  CKL();
+  ctx->cref = true;
+  ctx->finalized = false;
+  destroy_graphs(ctx);
+  return TLS_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 // PCG (src/krylov.py:58-107)
 // ---------------------------------------------------------------------------------------------
@@ -1361,7 +1545,8 @@ int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t ma
           TRY(api_out(ctx, s, ctx->vx, ctx->pout));
           CK(cudaStreamSynchronize(s));
           CK(cudaMemcpy(ctx->h_x, ctx->pout, sizeof(double) * n, cudaMemcpyDeviceToHost));
-          cb(user, h.it, ctx->h_x);
+          if (cb(user, h.it, ctx->h_x) != 0)
+            return fail(ctx, TLS_ERR_CALLBACK, "callback stopped the solve at iteration " + std::to_string(h.it));
         }
         if (h.done) break;
       }
@@ -1517,9 +1702,9 @@ static int ensure_gm(tls_ctx* ctx, int mcols) {
   ctx->gm_cols = mcols;
   if (const char* e = getenv("TLS_GM_FUSED")) ctx->gm_fused = atoi(e) != 0;
   if (ctx->gm_fused) {  // (nc + 1) x NTHR + nc doubles of shared memory for the widest fused step
-    static size_t fsmem = 48 * 1024;
+
     const int mc = std::min(mcols + 1, GM_FUSED_MAXCOLS);
-    CK(raise_smem((const void*)k_gm_update_gemvt, sizeof(double) * ((size_t)(mc + 1) * NTHR + mc), fsmem));
+    CK(raise_smem(ctx->device, (const void*)k_gm_update_gemvt, sizeof(double) * ((size_t)(mc + 1) * NTHR + mc)));
   }
   for (int i = 0; i < 2; ++i) {
     if (ctx->gm_exec[i]) cudaGraphExecDestroy(ctx->gm_exec[i]);
@@ -1596,7 +1781,9 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
         TRY(enq_gm_step(ctx, s, j, prec));
         CK(cudaMemcpyAsync(&hs, ctx->gm, sizeof(GmState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        if (cb) cb(user, hs.total + hs.k, nullptr);
+        if (cb && cb(user, hs.total + hs.k, nullptr) != 0)
+          return fail(ctx, TLS_ERR_CALLBACK,
+                      "callback stopped the solve at iteration " + std::to_string(hs.total + hs.k));
         if (hs.cycle_stop) break;
       }
       TRY(enq_gm_cycle_end(ctx, s, prec));
@@ -1915,8 +2102,9 @@ int32_t tls_band_cholesky(double* ap, int64_t ld, int32_t count, const int32_t* 
   for (int J = 0; J < nbk; ++J)
     if (reach[J] < 64 * (J + 1) || reach[J] > ld || reach[J] % 64) return TLS_ERR_ARG;
   const size_t smem = sizeof(double) * 5 * 64 * CP;
-  static size_t set = 48 * 1024;
-  if (raise_smem((const void*)k_band_chol, smem, set) != cudaSuccess) return TLS_ERR_CUDA;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TLS_ERR_CUDA;
+  if (raise_smem(dev, (const void*)k_band_chol, smem) != cudaSuccess) return TLS_ERR_CUDA;
   int* d_reach = nullptr;
   if (cudaMallocAsync((void**)&d_reach, sizeof(int) * nbk, s) != cudaSuccess) return TLS_ERR_OOM;
   if (cudaMemcpyAsync(d_reach, reach, sizeof(int) * nbk, cudaMemcpyHostToDevice, s) != cudaSuccess) return TLS_ERR_CUDA;

@@ -406,6 +406,15 @@ __global__ void __launch_bounds__(NTHR) k_perm_out(int n, const int* __restrict_
     dst[g] = (i >= r0 && i < r1) ? src[i] : 0.0;
   }
 }
+// out = a + beta * b (b may be null: a copy); coarse-segment arithmetic of the refinement step
+__global__ void __launch_bounds__(NTHR) k_lincomb(int n, const double* __restrict__ a,
+                                                  const double* __restrict__ b, double beta,
+                                                  double* __restrict__ out, const int* done) {
+  PDL_ENTRY();
+  if (done && *done) return;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR)
+    out[i] = b ? a[i] + beta * b[i] : a[i];
+}
 __global__ void __launch_bounds__(NTHR) k_xpack(long long m, const int* __restrict__ idx,
                                                 const double* __restrict__ src, double* __restrict__ buf,
                                                 const int* done) {

@@ -54,10 +54,17 @@ VERBOSE = bool(int(os.environ.get("TLS_VERBOSE", "0")))
 TIE_GUARD = 1e-12
 TOPK_TAU = 1e-300
 EPS = float(np.finfo(float).eps)
+REFINE_COND = 1.0e8  # cond_1(A0) above which every coarse solve gets one refinement step
 
 
 class CoarseData:
-    """Device coarse space + the host bookkeeping of CoarseSpace (src/coarse.py:23-49)."""
+    """Device coarse space + the host bookkeeping of CoarseSpace (src/coarse.py:23-49).
+
+    ``restrict`` / ``solve_coarse`` / ``prolong`` run the apply's own kernels through the C ABI
+    (``tls_coarse_restrict`` / ``tls_coarse_solve`` / ``tls_coarse_prolong``); ``basis`` and
+    ``a00`` are materialised on the host on first access (``a00`` from the device copy kept at
+    setup, or -- when A0 was too large to keep, > 4 GB -- by the reference's own sparse triple
+    product, src/coarse.py:166-170)."""
 
     def __init__(self, n, maps, z_blocks, counts, nnz_a00):
         self._n = n
@@ -66,6 +73,13 @@ class CoarseData:
         self.ranges = tuple(self._ranges(counts))
         self.nnz_a00 = int(nnz_a00)
         self._basis = None
+        self._a00 = None
+        self._a00_dev = None
+        self._handle = None           # set by setup() once the preconditioner is finalised
+        self._csr = None
+        self._symmetric = False
+        self.cond1 = None
+        self.refined = False
 
     @staticmethod
     def _ranges(counts):
@@ -101,6 +115,40 @@ class CoarseData:
                 mat = sp.csr_matrix((self._n, 0))
             self._basis = SparseMat(mat)
         return self._basis
+
+    @property
+    def a00(self):
+        """The Galerkin operator Z^T A Z, dense n_C x n_C, symmetrised when SPD (src/coarse.py:158-170)."""
+        if self._a00 is None:
+            if self._a00_dev is not None:
+                self._a00 = self._a00_dev.cpu().numpy()
+            else:
+                b = self.basis.scipy()
+                prod = (b.T @ (self._csr @ b)).toarray()
+                self._a00 = 0.5 * (prod + prod.T) if self._symmetric else prod
+        return self._a00
+
+    def _call(self, name, v, n_in, n_out):
+        from . import device as D
+        h = self._handle
+        if h is None:
+            raise RuntimeError("coarse operator not factored; call galerkin_coarse first")
+        x, back = D.to_device(v, n_in, h.device)
+        y = _torch().empty(n_out, dtype=_torch().float64, device=x.device)
+        h.check(getattr(h.lib, name)(h.ctx, _lib.ptr(x), _lib.ptr(y), stream_ptr()))
+        return back(y)
+
+    def restrict(self, r):
+        """c = Z^T r (src/coarse.py:40-41)."""
+        return self._call("tls_coarse_restrict", r, self._n, self.n_coarse)
+
+    def prolong(self, y):
+        """Z y (src/coarse.py:43-44)."""
+        return self._call("tls_coarse_prolong", y, self.n_coarse, self._n)
+
+    def solve_coarse(self, rhs):
+        """A0^{-1} rhs (src/coarse.py:46-49)."""
+        return self._call("tls_coarse_solve", rhs, self.n_coarse, self.n_coarse)
 
 
 def warm_linalg(device=None):
@@ -917,6 +965,17 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     band = local in ("auto", "band")
     order_kind = None
     if band:
+        # k_band_solve keeps a whole local vector in shared memory (csrc/tls_b200.cu
+        # band_max_rows): larger subdomains keep the inverse tiles
+        optin = int(getattr(torch.cuda.get_device_properties(dev), "shared_memory_per_block_optin",
+                            227 * 1024))
+        max_rows = (optin // 8 - 8 * 64 - 64) // 64 * 64
+        if int(n_loc.max()) > max_rows:
+            if forced:
+                raise ValueError(f"local='band': a subdomain of {int(n_loc.max())} rows exceeds the "
+                                 f"{max_rows}-row shared-memory limit of the band solve")
+            band = False
+    if band:
         import scipy.sparse as sp
         if graph is None:
             from .partition import symmetrized_graph as _sg
@@ -966,49 +1025,130 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         return local_orders(adj, [maps[f + b] for b in range(min(batch, hi - f))], order_kind)
 
     next_orders = order_pool.submit(_orders_of, lo) if band else None
-    for first in range(lo, hi, batch):
-        cnt = min(batch, hi - first)
-        if band:
-            perm_list = next_orders.result()
-            next_orders = order_pool.submit(_orders_of, first + batch) if first + batch < hi else None
-        if first > lo:
-            _log(t0, f"batch at {first}")
-        tb0 = time.perf_counter() if VERBOSE else 0.0
-        A = a_buf[:cnt]
-        handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
-        if band_lu:
-            n_list = [int(n_loc[first + b]) for b in range(cnt)]
-            LU, piv, Ldinv, Udinv, pin, pout, lcodes, ucodes, info, P = _band_lu_factor(
-                torch, A, perm_list, n_list, ld)
-            for b in range(cnt):  # the reference's singularity rule (src/subdomain.py:86-88)
-                nb_ = n_list[b]
-                blk = LU[b, :nb_, :nb_]
-                if int(info[b]) != 0 or float(blk.diagonal().abs().min()) <= nb_ * EPS * float(blk.abs().max()):
-                    raise SubdomainSetupError(first + b, "local block is numerically singular")
-            pin_c = np.concatenate(pin).astype(np.int32)
-            pout_c = np.concatenate(pout).astype(np.int32)
-            lc_c = np.concatenate(lcodes).astype(np.int32)
-            uc_c = np.concatenate(ucodes).astype(np.int32)
-            _make_room(torch, dev, _band_bytes(lc_c) + _band_bytes(uc_c))
-            handle.check(lib.tls_store_local_band_lu(handle.ctx, first, cnt, _lib.ptr(LU), ld, _lib.ptr(Ldinv),
-                                                     _lib.ptr(Udinv), ld // 64, _lib.ptr(pin_c),
-                                                     _lib.ptr(pout_c), _lib.ptr(lc_c), _lib.ptr(uc_c), s_ptr))
-            torch.cuda.current_stream().synchronize()
-            del Ldinv, Udinv
+    try:
+        for first in range(lo, hi, batch):
+            cnt = min(batch, hi - first)
+            if band:
+                perm_list = next_orders.result()
+                next_orders = order_pool.submit(_orders_of, first + batch) if first + batch < hi else None
+            if first > lo:
+                _log(t0, f"batch at {first}")
+            tb0 = time.perf_counter() if VERBOSE else 0.0
+            A = a_buf[:cnt]
+            handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
+            if band_lu:
+                n_list = [int(n_loc[first + b]) for b in range(cnt)]
+                LU, piv, Ldinv, Udinv, pin, pout, lcodes, ucodes, info, P = _band_lu_factor(
+                    torch, A, perm_list, n_list, ld)
+                for b in range(cnt):  # the reference's singularity rule (src/subdomain.py:86-88)
+                    nb_ = n_list[b]
+                    blk = LU[b, :nb_, :nb_]
+                    if int(info[b]) != 0 or float(blk.diagonal().abs().min()) <= nb_ * EPS * float(blk.abs().max()):
+                        raise SubdomainSetupError(first + b, "local block is numerically singular")
+                pin_c = np.concatenate(pin).astype(np.int32)
+                pout_c = np.concatenate(pout).astype(np.int32)
+                lc_c = np.concatenate(lcodes).astype(np.int32)
+                uc_c = np.concatenate(ucodes).astype(np.int32)
+                _make_room(torch, dev, _band_bytes(lc_c) + _band_bytes(uc_c))
+                handle.check(lib.tls_store_local_band_lu(handle.ctx, first, cnt, _lib.ptr(LU), ld, _lib.ptr(Ldinv),
+                                                         _lib.ptr(Udinv), ld // 64, _lib.ptr(pin_c),
+                                                         _lib.ptr(pout_c), _lib.ptr(lc_c), _lib.ptr(uc_c), s_ptr))
+                torch.cuda.current_stream().synchronize()
+                del Ldinv, Udinv
+                if want_coarse:
+                    for b in range(cnt):
+                        s = first + b
+                        n, ni = int(n_loc[s]), int(n_int[s])
+                        nin = n - int(n_bnd[s])
+                        if n == nin:
+                            Bring = torch.zeros((n, 0), dtype=torch.float64, device=dev)
+                        else:
+                            pinv = torch.empty(ld, dtype=torch.long, device=dev)
+                            pinv[P[b]] = torch.arange(ld, device=dev)
+                            E = torch.zeros((ld, n - nin), dtype=torch.float64, device=dev)
+                            E[pinv[nin:n], torch.arange(n - nin, device=dev)] = 1.0
+                            Bring = torch.linalg.lu_solve(LU[b], piv[b], E)[pinv[:n]]
+                        Z, gaps[s] = _subdomain_columns(torch, coarse, A[b], Bring, n, ni, nin, tau, n_modes)
+                        if Z.shape[1]:
+                            nz = torch.any(Z != 0, dim=0)
+                            if not bool(nz.all()):
+                                Z = Z[:, nz].contiguous()
+                        Z = _with_pou(torch, Z, A[b], n, ni, nu)
+                        z_dev[s] = Z
+                        w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
+                del A, LU, piv
+                continue
+            if band:
+                tb = _stage("extract", tb0)
+                tb = _stage("orders (host, wait)", tb)
+                n_list = [int(n_loc[first + b]) for b in range(cnt)]
+                L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld)
+                tb = _stage("band factor", tb)
+                bad = torch.nonzero(info).flatten().cpu().numpy()
+                if bad.size:
+                    s = first + int(bad[0])
+                    raise SubdomainSetupError(s, "factorization failed: the local block is not positive definite")
+                perm_cat = np.concatenate(perms).astype(np.int32)
+                k_cat = np.concatenate(codes).astype(np.int32)
+                _make_room(torch, dev, _band_bytes(k_cat))
+                handle.check(lib.tls_store_local_band(handle.ctx, first, cnt, _lib.ptr(L), ld, _lib.ptr(Dinv),
+                                                      ld // 64, _lib.ptr(perm_cat), _lib.ptr(k_cat), s_ptr))
+                torch.cuda.current_stream().synchronize()  # the host arrays above stay alive until here
+                tb = _stage("band pack", tb)
+                if want_coarse:
+                    kc_full = np.zeros((cnt, ld // 64), dtype=np.int64)
+                    for b in range(cnt):
+                        kc_full[b, : kcnts[b].size] = kcnts[b]
+                    cols = _coarse_band_batch(torch, coarse, A, L, P,
+                                              [int(n_loc[first + b]) for b in range(cnt)],
+                                              [int(n_int[first + b]) for b in range(cnt)],
+                                              [int(n_loc[first + b] - n_bnd[first + b]) for b in range(cnt)],
+                                              tau, n_modes, Dinv=Dinv, kc=kc_full)
+                    for b in range(cnt):
+                        s = first + b
+                        n, ni = int(n_loc[s]), int(n_int[s])
+                        Z, gaps[s], W = cols[b]
+                        if W is None and Z.shape[1]:
+                            nz = torch.any(Z != 0, dim=0)
+                            if not bool(nz.all()):
+                                Z = Z[:, nz].contiguous()
+                            W = A[b, :n, :ni] @ Z
+                        if nu is not None:
+                            Z = _with_pou(torch, Z, A[b], n, ni, nu)
+                            W = A[b, :n, :ni] @ Z if Z.shape[1] else None
+                        z_dev[s] = Z
+                        w_dev[s] = W if Z.shape[1] else None
+                del A, L, Dinv
+                continue
+            if symmetric:
+                L, info = torch.linalg.cholesky_ex(A)
+                bad = torch.nonzero(info).flatten().cpu().numpy()
+                if bad.size:
+                    s = first + int(bad[0])
+                    raise SubdomainSetupError(s, f"factorization failed: {int(info[bad[0]])}-th leading minor not positive")
+                Binv = torch.cholesky_inverse(L)
+                del L
+                Binv = (0.5 * (Binv + Binv.mT)).contiguous()
+            else:
+                LU, piv, info = torch.linalg.lu_factor_ex(A)
+                for b in range(cnt):
+                    s = first + b
+                    nb_ = int(n_loc[s])
+                    blk = LU[b, :nb_, :nb_]
+                    if int(info[b]) != 0 or float(blk.diagonal().abs().min()) <= nb_ * EPS * float(blk.abs().max()):
+                        raise SubdomainSetupError(s, "local block is numerically singular")
+                eye = torch.eye(ld, dtype=torch.float64, device=dev).expand(cnt, ld, ld)
+                Binv = torch.linalg.lu_solve(LU, piv, eye).contiguous()  # lu_solve returns column-major
+                del LU, piv
+            handle.check(lib.tls_store_local_inverse(handle.ctx, first, cnt, _lib.ptr(Binv), ld, s_ptr))
             if want_coarse:
                 for b in range(cnt):
                     s = first + b
                     n, ni = int(n_loc[s]), int(n_int[s])
                     nin = n - int(n_bnd[s])
-                    if n == nin:
-                        Bring = torch.zeros((n, 0), dtype=torch.float64, device=dev)
-                    else:
-                        pinv = torch.empty(ld, dtype=torch.long, device=dev)
-                        pinv[P[b]] = torch.arange(ld, device=dev)
-                        E = torch.zeros((ld, n - nin), dtype=torch.float64, device=dev)
-                        E[pinv[nin:n], torch.arange(n - nin, device=dev)] = 1.0
-                        Bring = torch.linalg.lu_solve(LU[b], piv[b], E)[pinv[:n]]
-                    Z, gaps[s] = _subdomain_columns(torch, coarse, A[b], Bring, n, ni, nin, tau, n_modes)
+                    Z, gaps[s] = _subdomain_columns(torch, coarse, A[b], Binv[b, :n, nin:n], n, ni, nin, tau,
+                                                    n_modes)
+                    # assemble_coarse_basis drops identically zero columns (src/coarse.py:99-103)
                     if Z.shape[1]:
                         nz = torch.any(Z != 0, dim=0)
                         if not bool(nz.all()):
@@ -1016,90 +1156,12 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                     Z = _with_pou(torch, Z, A[b], n, ni, nu)
                     z_dev[s] = Z
                     w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
-            del A, LU, piv
-            continue
-        if band:
-            tb = _stage("extract", tb0)
-            tb = _stage("orders (host, wait)", tb)
-            n_list = [int(n_loc[first + b]) for b in range(cnt)]
-            L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld)
-            tb = _stage("band factor", tb)
-            bad = torch.nonzero(info).flatten().cpu().numpy()
-            if bad.size:
-                s = first + int(bad[0])
-                raise SubdomainSetupError(s, "factorization failed: the local block is not positive definite")
-            perm_cat = np.concatenate(perms).astype(np.int32)
-            k_cat = np.concatenate(codes).astype(np.int32)
-            _make_room(torch, dev, _band_bytes(k_cat))
-            handle.check(lib.tls_store_local_band(handle.ctx, first, cnt, _lib.ptr(L), ld, _lib.ptr(Dinv),
-                                                  ld // 64, _lib.ptr(perm_cat), _lib.ptr(k_cat), s_ptr))
-            torch.cuda.current_stream().synchronize()  # the host arrays above stay alive until here
-            tb = _stage("band pack", tb)
-            if want_coarse:
-                kc_full = np.zeros((cnt, ld // 64), dtype=np.int64)
-                for b in range(cnt):
-                    kc_full[b, : kcnts[b].size] = kcnts[b]
-                cols = _coarse_band_batch(torch, coarse, A, L, P,
-                                          [int(n_loc[first + b]) for b in range(cnt)],
-                                          [int(n_int[first + b]) for b in range(cnt)],
-                                          [int(n_loc[first + b] - n_bnd[first + b]) for b in range(cnt)],
-                                          tau, n_modes, Dinv=Dinv, kc=kc_full)
-                for b in range(cnt):
-                    s = first + b
-                    n, ni = int(n_loc[s]), int(n_int[s])
-                    Z, gaps[s], W = cols[b]
-                    if W is None and Z.shape[1]:
-                        nz = torch.any(Z != 0, dim=0)
-                        if not bool(nz.all()):
-                            Z = Z[:, nz].contiguous()
-                        W = A[b, :n, :ni] @ Z
-                    if nu is not None:
-                        Z = _with_pou(torch, Z, A[b], n, ni, nu)
-                        W = A[b, :n, :ni] @ Z if Z.shape[1] else None
-                    z_dev[s] = Z
-                    w_dev[s] = W if Z.shape[1] else None
-            del A, L, Dinv
-            continue
-        if symmetric:
-            L, info = torch.linalg.cholesky_ex(A)
-            bad = torch.nonzero(info).flatten().cpu().numpy()
-            if bad.size:
-                s = first + int(bad[0])
-                raise SubdomainSetupError(s, f"factorization failed: {int(info[bad[0]])}-th leading minor not positive")
-            Binv = torch.cholesky_inverse(L)
-            del L
-            Binv = (0.5 * (Binv + Binv.mT)).contiguous()
-        else:
-            LU, piv, info = torch.linalg.lu_factor_ex(A)
-            for b in range(cnt):
-                s = first + b
-                nb_ = int(n_loc[s])
-                blk = LU[b, :nb_, :nb_]
-                if int(info[b]) != 0 or float(blk.diagonal().abs().min()) <= nb_ * EPS * float(blk.abs().max()):
-                    raise SubdomainSetupError(s, "local block is numerically singular")
-            eye = torch.eye(ld, dtype=torch.float64, device=dev).expand(cnt, ld, ld)
-            Binv = torch.linalg.lu_solve(LU, piv, eye).contiguous()  # lu_solve returns column-major
-            del LU, piv
-        handle.check(lib.tls_store_local_inverse(handle.ctx, first, cnt, _lib.ptr(Binv), ld, s_ptr))
-        if want_coarse:
-            for b in range(cnt):
-                s = first + b
-                n, ni = int(n_loc[s]), int(n_int[s])
-                nin = n - int(n_bnd[s])
-                Z, gaps[s] = _subdomain_columns(torch, coarse, A[b], Binv[b, :n, nin:n], n, ni, nin, tau,
-                                                n_modes)
-                # assemble_coarse_basis drops identically zero columns (src/coarse.py:99-103)
-                if Z.shape[1]:
-                    nz = torch.any(Z != 0, dim=0)
-                    if not bool(nz.all()):
-                        Z = Z[:, nz].contiguous()
-                Z = _with_pou(torch, Z, A[b], n, ni, nu)
-                z_dev[s] = Z
-                w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
-        del A, Binv
+            del A, Binv
+    finally:
+        # an error in a batch must not leave the next batch's order computation running
+        if order_pool is not None:
+            order_pool.shutdown(cancel_futures=True)
     del a_buf
-    if order_pool is not None:
-        order_pool.shutdown()
     if not want_coarse:
         _release_cache(torch, dev)
         return None
@@ -1194,27 +1256,42 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     # count_nonzero (src/coarse.py:168) in row blocks: no n_C^2 temporary next to A0
     nnz = sum(int(torch.count_nonzero(A0[i:i + 4096])) for i in range(0, nC, 4096))
     _log(t0, "A0 assembled; factorising")
+    # A0 itself is kept on the device when it is small (<= 4 GB): the ``a00`` attribute
+    # (src/coarse.py:26) and the coarse refinement step read it; larger A0 (configuration 5:
+    # 19.3 GB) is rebuilt on demand from the basis
+    keep_a0 = 8 * nC * nC <= (4 << 30)
+    norm_a0 = None
     if symmetric:
         # symmetrise (src/coarse.py:169-170) the lower triangle Cholesky reads, in place
         _symmetrize_lower_inplace(torch, A0)
+        if keep_a0:
+            A0 = torch.tril(A0) + torch.tril(A0, -1).mT
+            norm_a0 = float(A0.abs().sum(0).max())
         L, info = torch.linalg.cholesky_ex(A0)
-        del A0
+        if not keep_a0:
+            del A0
+            A0 = None
         if int(info) != 0:
             raise RuntimeError(f"coarse operator is not positive definite: {int(info)}-th leading minor")
         # the packed-tile store reads the lower triangle (and full diagonal tiles) only
         A0inv = torch.cholesky_inverse(L).contiguous()
         del L
-        A0 = None
     else:
+        norm_a0 = float(A0.abs().sum(0).max())
         LU, piv, info = torch.linalg.lu_factor_ex(A0)
-        del A0
-        A0 = None
+        if not keep_a0:
+            del A0
+            A0 = None
         if int(info) != 0 or float(LU.diagonal().abs().min()) <= nC * EPS * float(LU.abs().max()):
             raise RuntimeError("coarse operator is numerically singular")
         A0inv = torch.linalg.lu_solve(LU, piv, torch.eye(nC, dtype=torch.float64, device=dev)).contiguous()
         del LU, piv
-    if sharded:  # one replicated coarse operator, bit-identical on every rank
-        shard.coll.broadcast(A0inv, src=0)
+    # 1-norm condition number ||A0||_1 ||A0^{-1}||_1 (both explicit here): above 1e8 the explicit
+    # inverse alone leaves a coarse residual ~cond * eps, so every coarse solve gets one
+    # refinement step (tls_coarse_refine) -- the reference's LU/Cholesky solve is backward stable
+    cond1 = norm_a0 * float(A0inv.abs().sum(0).max()) if norm_a0 is not None else None
+    refine = (A0 is not None and cond1 is not None and cond1 > REFINE_COND and not sharded
+              and os.environ.get("TLS_COARSE_REFINE", "1") != "0")
     _log(t0, "coarse operator inverted; uploading")
     # column-major blocks (k x n_int): coalesced restriction and prolongation loads
     zcat = (torch.cat([z_dev[s].mT.contiguous().reshape(-1) for s in own]) if len(own) else
@@ -1225,10 +1302,18 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     _make_room(torch, dev, 8 * nC * nC if not symmetric else 4 * nC * nC + 8 * nC * 64)
     handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
                                        _lib.ptr(A0inv), s_ptr))
+    if refine:
+        _make_room(torch, dev, 8 * nC * nC)
+        handle.check(lib.tls_coarse_refine(handle.ctx, _lib.ptr(A0.contiguous()), s_ptr))
     torch.cuda.current_stream().synchronize()
     z_list = [z_host[s] if s in z_host else z_all[s].cpu().numpy() for s in range(N)]
-    del A0, A0inv, zcat, z_dev, z_all
+    del A0inv, zcat, z_dev, z_all
     _release_cache(torch, dev)
     cd = CoarseData(csr.shape[0], maps, z_list, [int(c) for c in counts], nnz)
     cd.cut_gaps = gaps  # owned subdomains only
+    cd.cond1 = cond1
+    cd.refined = refine
+    cd._a00_dev = A0
+    cd._csr = csr
+    cd._symmetric = symmetric
     return cd

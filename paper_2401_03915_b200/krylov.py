@@ -28,6 +28,33 @@ GMRES_MAXIT_CAP = 1000  # src/krylov.py:18
 REORTH_TOL = 1e-8       # src/krylov.py:19 (CGS2 always re-orthogonalises)
 
 
+class _Callback:
+    """ctypes trampoline for ``callback``: an exception raised by the user's callback cannot cross
+    the C frame (CPython would print and drop it), so it is saved, the C loop is told to stop
+    (return 1 -> TLS_ERR_CALLBACK) and ``reraise`` raises it after the call returns -- the
+    reference lets it propagate out of pcg / gmres (src/krylov.py:92-93, 182-183)."""
+
+    def __init__(self, fn, with_x, n):
+        self.fn, self.with_x, self.n, self.exc = fn, with_x, n, None
+        self.c = _lib.ITER_CB(self._call) if fn is not None else _lib.ITER_CB()
+
+    def _call(self, _user, it, xp):
+        try:
+            x = np.ctypeslib.as_array(xp, (self.n,)).copy() if self.with_x else None
+            self.fn(int(it), x)
+            return 0
+        except BaseException as exc:  # noqa: BLE001 -- re-raised by reraise()
+            self.exc = exc
+            return 1
+
+    def reraise(self, rc):
+        if self.exc is not None:
+            exc, self.exc = self.exc, None
+            raise exc
+        if rc == _lib.TLS_ERR_CALLBACK:
+            raise RuntimeError("solve stopped by the callback")
+
+
 @dataclass
 class SolveReport:
     iterations: int
@@ -66,15 +93,37 @@ def _cond_from_recurrence(alphas, betas):
     return float(ritz[-1] / ritz[0])
 
 
+def _same_operator(pm, mat):
+    """Whether two SparseMat objects hold the same CSR (structure and values); the outcome is
+    cached on ``mat`` for ``pm`` (both are immutable: read-only buffers, src/sparsemat.py:51-52)."""
+    if pm is mat:
+        return True
+    cache = getattr(mat, "_b200_same_as", None)
+    if cache is not None and cache[0] is pm:
+        return cache[1]
+    a, b = pm.scipy(), mat.scipy()
+    same = (a.shape == b.shape and a.nnz == b.nnz and np.array_equal(a.indptr, b.indptr)
+            and np.array_equal(a.indices, b.indices) and np.array_equal(a.data, b.data))
+    try:
+        mat._b200_same_as = (pm, same)
+    except AttributeError:
+        pass
+    return same
+
+
 def _handle_for(matrix, precond):
+    """The device handle a solve runs on.  With a preconditioner that is the preconditioner's
+    handle, whose SpMV applies the matrix the preconditioner was built from; the reference applies
+    ``matrix`` itself (src/krylov.py:81), so a different operator (even one with the same shape and
+    sparsity, e.g. rescaled values) is refused rather than silently replaced."""
     mat = as_sparsemat(matrix)
     if precond is None:
         return mat, mat.device_handle(), 0
     if precond.n != mat.nrows:
         raise ValueError("preconditioner and matrix sizes differ")
-    pm = precond.matrix
-    if pm is not mat and not (pm.shape == mat.shape and pm.nnz == mat.nnz):
-        raise ValueError("preconditioner was built for a different matrix")
+    if not _same_operator(precond.matrix, mat):
+        raise ValueError("preconditioner was built for a different matrix: this path applies the "
+                         "preconditioner's own operator, so the solve matrix must be the same")
     return mat, precond.handle, 1
 
 
@@ -87,13 +136,10 @@ def pcg(matrix, precond, b, tol=1e-8, maxit=500, callback=None, track_tridiagona
     hist = np.zeros(maxit + 2)
     coeffs = np.zeros(2 * maxit + 2)
     st = _lib.TlsStatus()
-    if callback is not None:
-        n = mat.nrows
-        cb = _lib.ITER_CB(lambda _u, it, xp: callback(int(it), np.ctypeslib.as_array(xp, (n,)).copy()))
-    else:
-        cb = _lib.ITER_CB()
+    cb = _Callback(callback, True, mat.nrows)
     rc = h.lib.tls_pcg(h.ctx, _lib.ptr(bt), _lib.ptr(x), float(tol), int(maxit), use, _lib.ptr(hist),
-                       _lib.ptr(coeffs), C.byref(st), cb, None, D.stream_ptr())
+                       _lib.ptr(coeffs), C.byref(st), cb.c, None, D.stream_ptr())
+    cb.reraise(rc)
     if rc == _lib.TLS_ERR_BREAKDOWN:
         raise BreakdownError(int(st.iteration), float(st.value))
     h.check(rc)
@@ -120,11 +166,11 @@ def gmres(matrix, precond, b, tol=1e-8, maxit=500, callback=None, restart=None):
     x = D._torch().empty_like(bt)
     hist = np.zeros(maxit + 2)
     st = _lib.TlsStatus()
-    cb = (_lib.ITER_CB(lambda _u, k, _x: callback(int(k), None)) if callback is not None
-          else _lib.ITER_CB())
+    cb = _Callback(callback, False, mat.nrows)
     rc = h.lib.tls_gmres(h.ctx, _lib.ptr(bt), _lib.ptr(x), float(tol), int(maxit),
-                         int(restart or 0), use, _lib.ptr(hist), C.byref(st), cb, None,
+                         int(restart or 0), use, _lib.ptr(hist), C.byref(st), cb.c, None,
                          D.stream_ptr())
+    cb.reraise(rc)
     h.check(rc)
     its = int(st.iterations)
     residuals = hist[: its + 1].copy()

@@ -1,18 +1,35 @@
-"""BASELINE.json configurations 2 and 3 at FULL size (n = 2.1 M / 1.05 M) through size-independent
-properties (the dense reference cannot run them: DENSE_GUARD):
-* overlap index sets and colours bit-exact against the oracle's restatement of extend_overlap /
-  color_subdomains (src/partition.py:278-334);
-* the apply is linear (to rounding) and, for ASM + additive, symmetric: <M x, y> = <x, M y>;
-* the banded and the dense-inverse local operators agree on sampled subdomains' solves (through
-  the one-level apply on vectors supported in one subdomain's interior);
-* the solves reach the tolerance on the TRUE residual ||b - A x|| / ||b||, with the iteration
-  counts this build measures (pinned: a change in them flags a change in the algorithm)."""
+"""All five BASELINE.json configurations at FULL size against the reference itself.
+
+The fixtures ``tests/golden/full_cfg{2,3,4,5}.npz`` were written by ``oracle/make_golden_fullsize.py``
+running the reference package (``tlschwarz``) in the build container:
+
+* configurations 3 and 4 (n = 1.05 M / 785 k, GMRES(50), RAS + deflated + top-k SVD coarse space):
+  the reference's whole pipeline -- every index set (SHA-256), mode counts, coarse size, the
+  apply / one-level / coarse outputs on a seeded vector (8,192 sampled entries + 3 full inner
+  products + norms), the GMRES(50) residual history, the iterate and its true residual;
+* configurations 2 and 5 (n = 2.1 M / 16.8 M, PCG, ASM + additive + top-k harmonic-pencil
+  modes; the reference cannot set them up: DENSE_GUARD and ~0.24 / 2 TB of dense blocks,
+  SURVEY.md §0.3): every index set and the colouring (SHA-256 of the reference's own
+  extend_overlap / color_subdomains on the whole problem) and, on 8 sampled subdomains (corner,
+  edge, face, interior), the reference's dense local solve y_i = A_ii^{-1} R_i r and the span of
+  its top-k coarse columns (orthogonal projection of 4 seeded vectors).
+
+Size-independent properties on every configuration: the coarse correction is the A-orthogonal
+projection onto span(Z) (Z A0^{-1} Z^T A v = v for v = Z y: checks A0 = Z^T A Z and its solve at
+full size), the sampled Galerkin blocks equal Z_s^T A Z_t, and the true residual of every solve
+reaches the tolerance.  Tolerances are written next to each check.
+"""
+
+import hashlib
+import os
 
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
 @pytest.fixture(scope="module")
@@ -25,28 +42,132 @@ def B():
     return mod
 
 
-@pytest.fixture(scope="module")
-def cfg2(B):
-    cfg = B.problems.CONFIGS[2]
+def maps_digest(maps, colors, k_c):
+    """Same byte layout as oracle/make_golden_fullsize.py::maps_digest."""
+    h = hashlib.sha256()
+    for s in maps:
+        h.update(np.int64(s.interior.size).tobytes())
+        h.update(np.asarray([l.size for l in s.layers], np.int64).tobytes())
+        h.update(np.asarray(s.indices, np.int64).tobytes())
+    h.update(np.asarray(colors, np.int64).tobytes())
+    h.update(np.int64(k_c).tobytes())
+    return h.hexdigest()
+
+
+def check_vec(v, g, prefix, rel):
+    """Sampled entries, norms and inner products of v against the fixture, relative to max|v|."""
+    n = v.size
+    scale = float(g[prefix + "_maxabs"])
+    idx = g[prefix + "_idx"]
+    err = np.abs(v[idx] - g[prefix + "_vals"]).max() / scale
+    assert err <= rel, (prefix, err)
+    w = np.random.default_rng(77 + 1).standard_normal((3, n))
+    dots = w @ v
+    derr = np.abs(dots - g[prefix + "_dots"]).max() / (np.sqrt(n) * scale)
+    assert derr <= rel, (prefix, "dots", derr)
+    assert abs(np.linalg.norm(v) - float(g[prefix + "_norm"])) <= rel * np.sqrt(n) * scale
+    return err
+
+
+def galerkin_projection(B, pre, a, rel):
+    """Z A0^{-1} Z^T A (Z y) = Z y: A0 is Z^T A Z and the coarse solve inverts it (full size)."""
+    cs = pre.coarse
+    y = np.random.default_rng(31).standard_normal(cs.n_coarse)
+    v = cs.prolong(y)
+    u = pre.coarse_apply(a @ v)
+    err = np.abs(u - v).max() / np.abs(v).max()
+    assert err <= rel, err
+    return err
+
+
+def galerkin_blocks(pre, a, subs, rel):
+    """Sampled blocks (s, t) of A0 against Z_s^T A[int_s, int_t] Z_t from the device basis."""
+    cs = pre.coarse
+    a00 = cs.a00
+    a = a.tocsr()
+    for s in subs:
+        cols = a[pre.maps[s].interior]
+        nb = np.unique(pre.coarse_owner[cols.indices])
+        for t in nb[:3]:
+            zs, zt = cs._z[s], cs._z[int(t)]
+            blk = zs.T @ (cols[:, pre.maps[int(t)].interior] @ zt)
+            (s0, s1), (t0, t1) = cs.ranges[s], cs.ranges[int(t)]
+            got = a00[s0:s1, t0:t1]
+            assert np.abs(got - blk).max() <= rel * max(np.abs(blk).max(), 1e-300), (s, int(t))
+
+
+# ------------------------------------------------------------------------------------------------
+# configurations 2 and 5: whole-problem index sets + sampled subdomains vs the reference
+# ------------------------------------------------------------------------------------------------
+
+def _sampled_setup(B, cid):
+    g = np.load(os.path.join(GOLD, f"full_cfg{cid}.npz"))
+    cfg = B.problems.CONFIGS[cid]
     a, sym, owner, nsub = cfg.build()
+    assert a.shape[0] == int(g["n"]) and a.nnz == int(g["nnz"]) and nsub == int(g["n_sub"])
     mat = B.SparseMat(a, symmetric=sym)
     pre = B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes)
-    return cfg, a, owner, nsub, mat, pre
+    pre.coarse_owner = np.asarray(owner)
+    return cfg, g, a, mat, pre
 
 
-def test_full_cfg2_index_sets_bit_exact(B, cfg2):
-    from oracle import tls_oracle as O
-    cfg, a, owner, nsub, mat, pre = cfg2
-    gptr, gadj = O.symmetrized_graph(a)
-    maps = O.extend_overlap(gptr, gadj, owner, nsub, cfg.overlap)
-    for s in range(0, nsub, 7):
-        assert np.array_equal(pre.maps[s].indices, O.indices_of(maps[s]))
-    k_c, colors = O.color_subdomains(maps, a.shape[0])
-    assert pre.k_c == k_c and np.array_equal(np.asarray(pre.colors), np.asarray(colors))
+@pytest.fixture(scope="module")
+def cfg2(B):
+    return _sampled_setup(B, 2)
+
+
+@pytest.fixture(scope="module")
+def cfg5(B):
+    return _sampled_setup(B, 5)
+
+
+def _check_sampled(B, data, iterations):
+    cfg, g, a, mat, pre = data
+    # every index set and the colouring, bit for bit (reference extend_overlap / color_subdomains)
+    assert pre.k_c == int(g["k_c"])
+    assert maps_digest(pre.maps, pre.colors, pre.k_c) == str(g["digest"])
+    subs = [int(s) for s in g["sampled"]]
+    # local solves: the reference's dense Cholesky solve (cho_solve, src/subdomain.py:80-82) vs the
+    # banded factor sweeps, relative to max|y| -- within 1e-10 (north star)
+    r = np.random.default_rng(321).standard_normal(a.shape[0])
+    ys = pre.solve_local(r, subs)
+    for s, y in zip(subs, ys):
+        want = g[f"s{s}_y"]
+        assert y.shape == want.shape
+        err = np.abs(y - want).max() / np.abs(want).max()
+        assert err <= 1e-10, (s, err)
+    # coarse spans: the reference's top-k harmonic-pencil columns (m x m generalized eigh,
+    # src/spectral.py:111-132) vs the device subspace iteration on the reduced pencil: the
+    # projections onto the two spans agree to 1e-8 (principal-angle sine bound)
+    for s in subs:
+        z = pre.coarse._z[s]
+        assert z.shape[1] == int(g[f"s{s}_k"]) == cfg.n_modes
+        q, _ = np.linalg.qr(z)
+        w = np.random.default_rng(1000 + s).standard_normal((z.shape[0], 4))
+        err = np.abs(q @ (q.T @ w) - g[f"s{s}_proj"]).max() / np.abs(w).max()
+        assert err <= 1e-8, (s, err)
+    # Galerkin operator: projection property (relative 1e-9) on the whole coarse space
+    galerkin_projection(B, pre, a, 1e-9)
+    # solve: true residual reaches the tolerance; iteration count as measured on this build (the
+    # reference cannot run these sizes; the 216-subdomain same-generator analog matches it exactly)
+    b = cfg.rhs(a.shape[0])
+    x, rep = B.pcg(mat, pre, b, tol=cfg.tol, maxit=cfg.maxit)
+    assert rep.converged and abs(rep.iterations - iterations) <= 1, rep.iterations
+    true = np.linalg.norm(b - a @ x) / np.linalg.norm(b)
+    assert true <= 1.01 * cfg.tol and abs(true - rep.residuals[-1]) <= 1e-3 * cfg.tol
+
+
+def test_full_cfg2_against_reference(B, cfg2):
+    _check_sampled(B, cfg2, 166)
+
+
+def test_full_cfg2_galerkin_blocks(B, cfg2):
+    cfg, g, a, mat, pre = cfg2
+    galerkin_blocks(pre, a, [int(s) for s in g["sampled"]], 1e-11)
 
 
 def test_full_cfg2_apply_linear_and_symmetric(B, cfg2):
-    cfg, a, owner, nsub, mat, pre = cfg2
+    cfg, g, a, mat, pre = cfg2
     rng = np.random.default_rng(11)
     x, y = rng.standard_normal(a.shape[0]), rng.standard_normal(a.shape[0])
     mx, my, mxy = pre.apply(x), pre.apply(y), pre.apply(2.0 * x - 3.0 * y)
@@ -56,26 +177,56 @@ def test_full_cfg2_apply_linear_and_symmetric(B, cfg2):
     assert abs(lhs - rhs) <= 1e-11 * (abs(lhs) + abs(rhs))
 
 
-def test_full_cfg2_true_residual(B, cfg2):
-    cfg, a, owner, nsub, mat, pre = cfg2
-    b = cfg.rhs(a.shape[0])
-    x, rep = B.pcg(mat, pre, b, tol=cfg.tol, maxit=cfg.maxit)
-    assert rep.converged and rep.iterations == 166, rep.iterations
-    true = np.linalg.norm(b - a @ x) / np.linalg.norm(b)
-    assert true <= 1.01 * cfg.tol and abs(true - rep.residuals[-1]) <= 1e-3 * cfg.tol
+def test_full_cfg5_against_reference(B, cfg5):
+    _check_sampled(B, cfg5, 534)
 
 
-def test_full_cfg3_gmres_true_residual(B):
-    cfg = B.problems.CONFIGS[3]
+# ------------------------------------------------------------------------------------------------
+# configurations 3 and 4: the reference's whole pipeline at full size
+# ------------------------------------------------------------------------------------------------
+
+def _full(B, cid, apply_rel, hist_abs):
+    g = np.load(os.path.join(GOLD, f"full_cfg{cid}.npz"))
+    cfg = B.problems.CONFIGS[cid]
     a, sym, owner, nsub = cfg.build()
+    n = a.shape[0]
+    assert n == int(g["n"]) and a.nnz == int(g["nnz"])
     mat = B.SparseMat(a, symmetric=sym)
     pre = B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes)
-    b = cfg.rhs(a.shape[0])
-    x, rep = B.gmres(mat, pre, b, tol=cfg.tol, maxit=cfg.maxit, restart=cfg.restart)
-    assert rep.converged and rep.iterations == 37, rep.iterations
+    assert pre.local_kind == "band-lu"  # the default path the bench measures
+    assert pre.k_c == int(g["k_c"])
+    assert maps_digest(pre.maps, pre.colors, pre.k_c) == str(g["digest"])
+    assert tuple(pre.report.mode_counts) == tuple(int(c) for c in g["mode_counts"])
+    assert pre.report.n_coarse == int(g["n_coarse"])
+    assert abs(pre.report.nnz_coarse - int(g["nnz_coarse"])) <= 1e-3 * int(g["nnz_coarse"])
+    r = np.random.default_rng(123).standard_normal(n)
+    errs = {"z": check_vec(pre.apply(r), g, "z", apply_rel),
+            "z_one": check_vec(pre.apply_one_level(r), g, "z_one", 1e-10),
+            "z_coarse": check_vec(pre.coarse_apply(r), g, "z_coarse", apply_rel)}
+    b = cfg.rhs(n)
+    maxit = int(g["maxit"])
+    x, rep = B.gmres(mat, pre, b, tol=cfg.tol, maxit=maxit, restart=cfg.restart)
+    hist = np.asarray(g["history"])
+    assert abs(rep.iterations - int(g["iterations"])) <= 1, (rep.iterations, int(g["iterations"]))
+    assert bool(rep.converged) == bool(g["converged"])
+    k = min(len(hist), len(rep.residuals))
+    herr = np.abs(rep.residuals[:k] - hist[:k]).max()
+    assert herr <= hist_abs, herr
     true = np.linalg.norm(b - a @ x) / np.linalg.norm(b)
-    assert true <= 1.01 * cfg.tol
-    rng = np.random.default_rng(12)
-    u, v = rng.standard_normal(a.shape[0]), rng.standard_normal(a.shape[0])
-    mu, mv, muv = pre.apply(u), pre.apply(v), pre.apply(u + 0.5 * v)
-    assert np.abs(muv - (mu + 0.5 * mv)).max() <= 1e-11 * np.abs(muv).max()
+    if bool(g["converged"]):
+        assert true <= 1.01 * cfg.tol
+    assert abs(true - float(g["true_residual"])) <= max(1e-3 * float(g["true_residual"]), 1e-2 * cfg.tol)
+    return pre, a, errs, herr
+
+
+def test_full_cfg3_against_reference(B):
+    pre, a, errs, herr = _full(B, 3, 1e-10, 1e-10)
+    galerkin_projection(B, pre, a, 1e-9)
+
+
+def test_full_cfg4_against_reference(B):
+    # saddle point: cond(A0) ~ 1e9; the coarse solve is refined once, and the
+    # apply agrees with the reference's LU solve to 1e-8 of max|z|
+    pre, a, errs, herr = _full(B, 4, 1e-8, 1e-8)
+    assert pre.coarse.refined
+    galerkin_projection(B, pre, a, 1e-6)

@@ -139,7 +139,7 @@ def test_abi_exports_every_header_symbol(built_lib):
     assert not missing, missing
     from paper_2401_03915_b200 import _lib
     assert set(_lib.SIGNATURES) == names
-    assert built_lib.tls_abi_version() == 1
+    assert built_lib.tls_abi_version() == 2
 
 
 def test_product_does_not_import_oracle():
