@@ -2,26 +2,29 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-Workload (N=1): BASELINE.json configs[1] = configuration 2 (128^3 log-normal FV diffusion,
-512 subdomains of 16^3, overlap 1, 16 harmonic modes each, PCG to 1e-8, RHS U[-1,1] seed 0).
-A "step" is one full PCG solve of that system from x0 = 0 (the hot path: SpMV + two-level
-Schwarz apply + Krylov reductions, every iteration).  value = Krylov iterations per second
-over the K timed solves (inputs resident in HBM); ms_per_step = time-to-solution of one solve.
-e2e = the same metric through the public API (``pcg`` on a pinned host RHS, host<->device
-copies inside the timed region).  The operator (6.5 GB of banded local factors for configuration
-2, 95 GB for configuration 5) is far larger than the 126 MB L2, so no explicit flush is needed
-between steps.
+Workload (N=1, default): BASELINE.json configs[4] = configuration 5, the largest configuration
+that fits one GPU and the north star's scaling configuration: 256^3 27-point Q1 anisotropic
+diffusion (n = 16.8 M, nnz = 449 M), 4,096 subdomains of 16^3, overlap 1, 12 harmonic modes each
+(n_C = 49,152), PCG to 1e-8 from x0 = 0, RHS U[-1,1] seed 0.  ``--config 1..4`` selects the
+others.  A "step" is one full solve (the hot path: SpMV + two-level Schwarz apply + Krylov
+reductions, every iteration).  value = Krylov iterations per second over the K timed solves
+(inputs resident in HBM); ms_per_step = one solve.  e2e = the same metric through the public API
+(``pcg`` / ``gmres`` on a pinned host RHS, host<->device copies inside the timed region).  The
+operator (95 GB of banded local factors + a 9.7 GB packed coarse inverse on configuration 5) is far
+larger than the 126 MB L2, so no explicit flush is needed between steps.
 
 N>1 (torchrun, one process per GPU): the SAME system is sharded by subdomain slabs across the
 ranks (strong scaling): each rank owns a slab of subdomains and their rows (renumbered rank by
 rank) and computes only those: SpMV rows, local solves, its rows of A0^{-1} c, prolongation,
 vector updates.  Inside the captured solve graph NCCL carries the halo of ghost rows
 (point-to-point with the neighbouring slabs), the ASM reverse halo, and sum all-reduces of the
-dot-product partials and of Z^T r.  Timing is the max over ranks.
+dot products and of Z^T r.  Timing is the max over ranks.
 
---impl reference: the reference's CPU algorithm (oracle port; the reference is pure Python
-and does not travel to the GPU box) on the box's host cores, on a bounded sample of the same
-workload (see cpu_baseline.sample).
+--impl reference: the reference's CPU algorithm (oracle port; the reference is pure Python and
+does not travel to the GPU box) on the box's host cores: whole solves when the configuration is
+small (configuration 1), else one sampled iteration per step, extrapolated to the iteration and to
+a solve and flagged ``extrapolated`` (configurations 2 and 5 cannot be set up by the reference at
+all: DENSE_GUARD).
 """
 
 from __future__ import annotations
@@ -170,13 +173,17 @@ def _max_over_ranks(value, world, torch):
 
 
 def _traffic_from_profile(config_id, kernel):
-    """DRAM bytes per launch of the local-solve kernel from the committed ncu summary."""
-    path = os.path.join(REPO, "profiles", f"ncu_{kernel}_cfg{config_id}.json")
-    try:
-        with open(path) as fh:
-            return float(json.load(fh)["dram_bytes_per_launch"])
-    except Exception:
-        return None
+    """DRAM bytes per launch of the local-solve kernel (band sweeps, Cholesky or LU, or the
+    inverse tiles) from the committed ``ncu --set full`` summary of this configuration (the
+    bench does not run under ncu); returns (bytes, source path) or (None, None)."""
+    for name in (f"ncu_{kernel}_cfg{config_id}_r02.json", f"ncu_{kernel}_cfg{config_id}.json"):
+        path = os.path.join(REPO, "profiles", name)
+        try:
+            with open(path) as fh:
+                return float(json.load(fh)["dram_bytes_per_launch"]), "profiles/" + name
+        except Exception:
+            continue
+    return None, None
 
 
 def iteration_bytes(cfg, a, pre, local_bytes):
@@ -208,35 +215,89 @@ def iteration_bytes(cfg, a, pre, local_bytes):
 
 
 # --------------------------------------------------------------------------------------------
-# CPU baseline (oracle port of the reference algorithm, bounded sample)
+# CPU baseline: the reference algorithm (oracle port of src/precond.py + src/krylov.py) on the
+# host cores.  Whole solves when the configuration is small enough to set up and solve in seconds
+# (configuration 1: the reference itself runs it end to end in ~0.4 s); otherwise a bounded,
+# labelled sample of one iteration, extrapolated to the whole iteration and solve
 # --------------------------------------------------------------------------------------------
 
-def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8, sym=True,
-                 warmup=0, steps=1):
-    """Per-iteration CPU time of the reference algorithm, measured on a bounded sample.
+# iterations per solve used to extrapolate a sampled CPU iteration to a solve: this build's
+# measured counts, equal to the reference's own where it can run (configuration 1: 20, 3: 37;
+# tests/test_gpu_fullsize.py); configuration 4 stagnates and runs to maxit
+SOLVE_ITERATIONS = {1: 20, 2: 166, 3: 37, 4: 500, 5: 534}
+FULL_CPU_LIMIT = 200_000  # rows: whole-solve CPU runs below this size
 
-    Timed pieces (numpy/scipy = the reference's own kernels, all host threads):
-      * one full-size SpMV (scipy csr_matvec, src/sparsemat.py:129);
-      * cho_solve / lu_solve of ``sample_subdomains`` local blocks (factor_dense closures,
-        src/subdomain.py:80-89), scaled to all subdomains;
-      * gather + np.add.at scatter of the sampled subdomains (src/precond.py:117-121), scaled;
-      * a dense Cholesky solve of the coarse size n_C (src/coarse.py:46-49) on an SPD stand-in;
-      * the PCG vector work of one iteration (src/krylov.py:80-102).
-    """
-    import scipy.linalg as sla
+
+def static_config(cfg, a, nsub):
+    """The workload description both arms print (identical dicts -> same_config)."""
+    return {"workload": cfg.name, "n": int(a.shape[0]), "nnz": int(a.nnz), "subdomains": int(nsub),
+            "overlap": cfg.overlap, "modes_per_subdomain": cfg.n_modes, "solver": cfg.solver,
+            "tol": cfg.tol, "restart": cfg.restart, "maxit": cfg.maxit, "rhs": "uniform[-1,1], seed 0",
+            "l2": ("operator (local factors + coarse operator) >> 126 MB L2; no flush needed"
+                   if a.shape[0] > FULL_CPU_LIMIT else
+                   "operator (~10 MB) is L2-resident by design: latency-bound, reported as it/s")}
+
+
+def _blas_limit(n):
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n)
+    except Exception:
+        return None
+
+
+def cpu_reference(cfg, a, sym, owner, nsub, warmup=0, steps=1, one_thread=True):
+    """Time the reference algorithm on the host.  Returns a dict with ``value`` (iters/s),
+    ``ms_per_step`` (one solve), ``times_s`` and the labelled sample description."""
     from oracle import tls_oracle as O
-
     n = a.shape[0]
+    cores = os.cpu_count()
+    if n <= FULL_CPU_LIMIT:
+        t0 = time.perf_counter()
+        pre = O.OraclePreconditioner(a, sym, owner, nsub, cfg.overlap, n_modes=cfg.n_modes)
+        t_setup = time.perf_counter() - t0
+        b = cfg.rhs(n)
+
+        def solve():
+            t = time.perf_counter()
+            if cfg.solver == "pcg":
+                _, its, _, _ = O.pcg(a, pre, b, cfg.tol, cfg.maxit)
+            else:
+                _, its, _, _ = O.gmres_restarted(a, pre, b, cfg.tol, cfg.maxit, cfg.restart)
+            return its, time.perf_counter() - t
+        for _ in range(warmup):
+            solve()
+        runs = [solve() for _ in range(max(1, steps))]
+        its = sum(r[0] for r in runs)
+        tt = sum(r[1] for r in runs)
+        out = {"value": its / tt, "unit": "iters/s", "cores": cores, "kind": "port",
+               "ms_per_step": 1e3 * tt / len(runs), "times_s": [r[1] for r in runs],
+               "iterations_per_solve": runs[0][0], "setup_s": t_setup,
+               "time_to_solution_s": t_setup + tt / len(runs), "extrapolated": False,
+               "sample": (f"{cfg.name}: whole reference pipeline (oracle port: setup + "
+                          f"{cfg.solver.upper()} solves from x0 = 0) on {cores} host threads; "
+                          f"{len(runs)} timed solves after {warmup} warm-up")}
+        if one_thread:
+            lim = _blas_limit(1)
+            try:
+                its1, t1 = solve()
+            finally:
+                if lim is not None:
+                    lim.restore_original_limits()
+            out["value_1thread"] = its1 / t1
+        return out
+    # ---- sampled iteration, extrapolated ----
+    import scipy.linalg as sla
     gptr, gadj = O.symmetrized_graph(a)
     rng = np.random.default_rng(0)
-    pick = np.sort(rng.choice(nsub, size=min(sample_subdomains, nsub), replace=False))
+    pick = np.sort(rng.choice(nsub, size=min(8, nsub), replace=False))
     maps = {}
     for s in pick:
         interior = np.nonzero(owner == s)[0]
         seen = np.zeros(n, dtype=bool)
         seen[interior] = True
         layers, front = [], interior
-        for _ in range(overlap):
+        for _ in range(cfg.overlap):
             nb = np.concatenate([gadj[gptr[u]:gptr[u + 1]] for u in front])
             ring = np.unique(nb)
             ring = ring[~seen[ring]]
@@ -244,32 +305,61 @@ def cpu_baseline(cfg_id, a, owner, nsub, overlap, n_modes, sample_subdomains=8, 
             layers.append(ring)
             front = ring
         maps[s] = (interior, layers)
-    subs = {s: O.OracleSubdomain(a, maps[s], sym) for s in pick}
-    nC = nsub * n_modes
+    # setup sample: one subdomain's dense block, factor, harmonic extension and mode selection
+    # (src/precond.py:198-232), scaled to all subdomains
+    t0 = time.perf_counter()
+    sd0 = O.OracleSubdomain(a, maps[pick[0]], sym)
+    ext = sd0.extension()
+    (O.harmonic_modes if cfg.symmetric else O.svd_modes)(sd0, ext, 0.1, cfg.n_modes)
+    t_setup_sub = time.perf_counter() - t0
+    subs = {s: (sd0 if s == pick[0] else O.OracleSubdomain(a, maps[s], sym)) for s in pick}
+    nC = nsub * cfg.n_modes
     nCs = min(nC, 8192)  # dense coarse solve timed at <= 8192 and scaled by (n_C / size)^2
     m = rng.standard_normal((nCs, 64))
-    fac = sla.cho_factor(m @ m.T + nCs * np.eye(nCs))
+    spd = m @ m.T + nCs * np.eye(nCs)
     del m
+    t0 = time.perf_counter()
+    fac = sla.cho_factor(spd) if sym else sla.lu_factor(spd)
+    t_cfac = (time.perf_counter() - t0) * (nC / nCs) ** 3
     vecs = [rng.standard_normal(n) for _ in range(5)]
-    ctx = dict(a=a, pick=pick, subs=subs, nsub=nsub, nC=nC, nCs=nCs, fac=fac, vecs=vecs,
-               c=rng.standard_normal(nCs))
+    ctx = dict(a=a, pick=pick, subs=subs, nsub=nsub, nC=nC, nCs=nCs, fac=fac, vecs=vecs, sym=sym,
+               c=rng.standard_normal(nCs), deflated=not sym)
     for _ in range(warmup):
         _cpu_iteration(ctx)
-    times = [_cpu_iteration(ctx) for _ in range(max(1, steps))]
+    times, measured = [], []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        times.append(_cpu_iteration(ctx))
+        measured.append(time.perf_counter() - t0)
     t_iter = float(np.mean(times))
-    cores = os.cpu_count()
-    return {"value": 1.0 / t_iter, "unit": "iters/s", "cores": cores, "kind": "port",
-            "sample": (f"cfg{cfg_id}: {len(pick)} of {nsub} subdomain {'Cholesky' if sym else 'LU'} solves (n_i up to "
-                       f"{max(subs[s].n_local for s in pick)}) + scatter, scaled x{nsub / len(pick):.0f}; "
-                       f"full-size SpMV; n_C={nC} dense Cholesky solve"
-                       f"{'' if nC == nCs else f' (timed at {nCs}, scaled by (n_C/{nCs})^2)'}; PCG vector ops; "
-                       f"one iteration = {t_iter * 1e3:.1f} ms on {cores} host threads "
-                       f"(mean of {len(times)} after {warmup} warm-up)"),
-            "t_iter_s": t_iter, "times_s": times}
+    its = SOLVE_ITERATIONS.get(cfg.cid, cfg.maxit)
+    setup_s = t_setup_sub * nsub + t_cfac
+    out = {"value": 1.0 / t_iter, "unit": "iters/s", "cores": cores, "kind": "port",
+           "ms_per_step": 1e3 * t_iter * its, "times_s": times, "extrapolated": True,
+           "sample_fraction": len(pick) / nsub, "measured_ms_per_step": 1e3 * float(np.mean(measured)),
+           "iterations_per_solve": its, "setup_s": setup_s,
+           "time_to_solution_s": setup_s + t_iter * its,
+           "sample": (f"{cfg.name}: one preconditioned iteration = {len(pick)} of {nsub} subdomain "
+                      f"{'Cholesky' if sym else 'LU'} solves (n_i up to {max(subs[s].n_local for s in pick)}) + "
+                      f"scatter, scaled x{nsub / len(pick):.0f}; full-size SpMV "
+                      f"({'3 per iteration, deflated' if not sym else '1'}); n_C={nC} dense coarse solve"
+                      f"{'' if nC == nCs else f' (timed at {nCs}, scaled by (n_C/{nCs})^2)'}; vector ops; "
+                      f"{t_iter * 1e3:.1f} ms per iteration on {cores} host threads (mean of {len(times)} "
+                      f"after {warmup} warm-up); a solve = {its} iterations (extrapolated); setup = one "
+                      f"subdomain's block + factor + harmonic extension + mode selection "
+                      f"({t_setup_sub:.2f} s) x {nsub} + the n_C coarse factorisation (scaled by n_C^3)")}
+    if one_thread:
+        lim = _blas_limit(1)
+        try:
+            out["value_1thread"] = 1.0 / _cpu_iteration(ctx)
+        finally:
+            if lim is not None:
+                lim.restore_original_limits()
+    return out
 
 
 def _cpu_iteration(ctx):
-    """One sampled preconditioned iteration on the host (the timed part of ``cpu_baseline``)."""
+    """One sampled preconditioned iteration on the host (the timed part of ``cpu_reference``)."""
     import scipy.linalg as sla
     a, pick, subs = ctx["a"], ctx["pick"], ctx["subs"]
     x, p, r, z, xx = (v.copy() for v in ctx["vecs"])
@@ -278,7 +368,7 @@ def _cpu_iteration(ctx):
     t0 = time.perf_counter()
     for _ in range(reps):
         a @ x
-    t_spmv = (time.perf_counter() - t0) / reps
+    t_spmv = (time.perf_counter() - t0) / reps * (3 if ctx["deflated"] else 1)
     out = np.zeros(n)
     t0 = time.perf_counter()
     for s in pick:
@@ -287,8 +377,11 @@ def _cpu_iteration(ctx):
         np.add.at(out, sd.indices, y)
     t_local = (time.perf_counter() - t0) * ctx["nsub"] / len(pick)
     t0 = time.perf_counter()
-    sla.cho_solve(ctx["fac"], ctx["c"])
-    t_coarse = (time.perf_counter() - t0) * (ctx["nC"] / ctx["nCs"]) ** 2
+    if ctx["sym"]:
+        sla.cho_solve(ctx["fac"], ctx["c"])
+    else:
+        sla.lu_solve(ctx["fac"], ctx["c"])
+    t_coarse = (time.perf_counter() - t0) * (ctx["nC"] / ctx["nCs"]) ** 2 * (2 if ctx["deflated"] else 1)
     t0 = time.perf_counter()
     float(p @ x); xx += 0.5 * p; r -= 0.5 * x; float(np.linalg.norm(r)); float(r @ z); p = z + 0.3 * p
     t_vec = time.perf_counter() - t0
@@ -302,7 +395,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--scale", type=int, default=0, help="grid size override (debug)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -318,20 +411,20 @@ def main():
         if rank != 0:
             return
         a, sym, owner, nsub = cfg.build()
-        cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym,
-                          warmup=args.warmup, steps=args.steps)
-        times = cb["times_s"]
-        val = 1.0 / float(np.mean(times))
-        cbo = {k: v for k, v in cb.items() if k not in ("t_iter_s", "times_s")}
-        cbo["value"] = val
-        print(json.dumps({"impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s",
-                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                          "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
-                          "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                          "config": {"workload": cfg.name, "n": int(a.shape[0]), "subdomains": nsub},
-                          "cpu_baseline": cbo,
-                          "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0,
-                                  "d2h_bytes_per_step": 0}}))
+        cb = cpu_reference(cfg, a, sym, owner, nsub, warmup=args.warmup, steps=args.steps)
+        val = cb["value"]
+        cbo = {k: v for k, v in cb.items() if k not in ("times_s",)}
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": static_config(cfg, a, nsub), "cpu_baseline": cbo,
+                "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        if cb.get("extrapolated"):
+            line["extrapolated"] = True
+            line["sample_fraction"] = cb["sample_fraction"]
+            line["measured_ms_per_step"] = cb["measured_ms_per_step"]
+        print(json.dumps(line))
         return
 
     import torch
@@ -428,7 +521,7 @@ def main():
     kernel_ms = loop_ms.value if in_loop else avg_ms.value
     peak, peak_kind = _peaks()
     achieved = algo.value / (kernel_ms * 1e-3) / 1e9
-    traffic = _traffic_from_profile(cfg.cid, "band" if pre.local_kind == "band" else "symv")
+    traffic, traffic_src = _traffic_from_profile(cfg.cid, "symv" if pre.local_kind == "inverse" else "band")
     # whole-loop roofline: algorithmic bytes of one iteration x iterations/s
     if pre.local_kind != "inverse":
         local_algo = algo.value  # band factor bytes streamed + 16 sum(n_i)
@@ -444,29 +537,33 @@ def main():
     # true residual of the final solve
     xr = x.cpu().numpy()
     true_res = float(np.linalg.norm(b_host - a @ xr) / np.linalg.norm(b_host))
+    cs = pre.coarse
     line = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": cfg.name, "n": n, "nnz": int(a.nnz), "subdomains": nsub,
-                   "overlap": cfg.overlap, "modes_per_subdomain": cfg.n_modes, "solver": cfg.solver,
-                   "tol": cfg.tol, "restart": cfg.restart, "maxit": cfg.maxit,
-                   "iterations_per_solve": rep.iterations, "n_coarse": pre.report.n_coarse,
-                   "local_operator": pre.local_kind,
-                   "min_cut_gap": (min(pre.coarse.cut_gaps.values()) if pre.coarse is not None
-                                   and getattr(pre.coarse, "cut_gaps", None) else None),
-                   "final_rel_residual": float(rep.residuals[-1]), "true_rel_residual": true_res,
-                   "setup_s": t_setup, "generate_s": t_gen,
-                   "time_to_solution_s": t_setup + ms / args.steps / 1e3,
-                   "device_bytes": pre.device_bytes(),
-                   "l2": "operator (local factors + coarse inverse) >> 126 MB L2; no flush needed",
-                   "parallelism": (f"subdomain/row slabs x{world} (NCCL halo + all-reduce)" if world > 1
-                                   else "1 GPU")},
+        "config": static_config(cfg, a, nsub),
+        "results": {"iterations_per_solve": rep.iterations, "n_coarse": pre.report.n_coarse,
+                    "local_operator": pre.local_kind,
+                    "min_cut_gap": (min(cs.cut_gaps.values()) if cs is not None
+                                    and getattr(cs, "cut_gaps", None) else None),
+                    "coarse_cond1": getattr(cs, "cond1", None) if cs is not None else None,
+                    "coarse_refined": bool(getattr(cs, "refined", False)) if cs is not None else False,
+                    "final_rel_residual": float(rep.residuals[-1]), "true_rel_residual": true_res,
+                    "converged": bool(rep.converged),
+                    "setup_s": t_setup, "generate_s": t_gen,
+                    "time_to_solution_s": t_setup + ms / args.steps / 1e3,
+                    "device_bytes": pre.device_bytes(),
+                    "parallelism": (f"subdomain/row slabs x{world} (NCCL halo + all-reduce)" if world > 1
+                                    else "1 GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind,
                      "kernel": ("k_band_solve (banded Cholesky forward+backward sweeps, all subdomains)"
                                 if pre.local_kind == "band" else
+                                "k_band_solve (banded pivoted-LU forward+backward sweeps, all subdomains)"
+                                if pre.local_kind == "band-lu" else
                                 "k_symv_tiles (batched local + coarse inverse tiles)"),
                      "algorithmic_bytes_per_launch": algo.value, "avg_launch_ms": kernel_ms,
                      "timing": (f"in-loop: CUDA event nodes around the {loop_n.value} band-solve launches of "
@@ -483,8 +580,7 @@ def main():
     }
     log("cpu baseline")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(cfg.cid, a, owner, nsub, cfg.overlap, cfg.n_modes, sym=sym)
-        cb.pop("t_iter_s")
+        cb = cpu_reference(cfg, a, sym, owner, nsub, warmup=0, steps=1)
         cb.pop("times_s")
         line["cpu_baseline"] = cb
     if rank == 0:

@@ -214,6 +214,10 @@ int32_t tls_comm_init_group(tls_ctx* ctx, tls_group* g, int32_t rank);
 /* test transport: capturable, moves no data, logs (kind, count, peers) of every collective the
  * sharded schedule issues -- validates CUDA-graph capture of the NCCL schedule on one GPU */
 int32_t tls_comm_init_record(tls_ctx* ctx, int32_t nranks, int32_t rank);
+/* Sharded coarse restriction by all-gather: rank q's subdomains own the global coarse columns
+ * [col_starts[q], col_starts[q+1]) (nranks + 1 entries; after tls_coarse_upload and the
+ * communicator).  Without it c = Z^T r is summed by an all-reduce of the whole n_C vector. */
+int32_t tls_set_coarse_layout(tls_ctx* ctx, int32_t nranks, const int64_t* col_starts);
 int64_t tls_comm_record_log(const tls_ctx* ctx, int64_t* out, int64_t cap);
 
 /* ---- measurement: average device time (ms) of the dominant kernel (batched local

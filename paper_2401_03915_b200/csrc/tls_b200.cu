@@ -84,6 +84,12 @@ struct tls_ctx {
   double* a0tiles = nullptr;
   long long cpad = 0;                 // padded coarse length (nt * TT)
   int nu_ref1 = 0, no_ref1 = 0, nu_ref2 = 0, no_ref2 = 0;
+  // sharded coarse restriction: every rank's columns [ccol[q], ccol[q+1]) travel by one
+  // all-gather of cmax doubles per rank (instead of an all-reduce of the whole n_C vector)
+  std::vector<long long> ccol;
+  long long cmax = 0;
+  long long* d_ccol = nullptr;
+  double *cg_send = nullptr, *cg_recv = nullptr;
   long long* d_zoff = nullptr;
   int *d_kcnt = nullptr, *d_cstart = nullptr;
   // ---- schedule
@@ -455,9 +461,14 @@ static int enq_allreduce(tls_ctx* ctx, cudaStream_t s, double* buf, long long co
   return TLS_OK;
 }
 
-// the G (fixed, equal on every rank) partial sums of a dot product, summed over the ranks
+// the np (fixed, equal on every rank) partial sums of a dot product: folded to ONE scalar on each
+// rank (fixed-order sum into part[0], the rest zeroed, so the consumers' partial sums are
+// unchanged), then that scalar is summed over the ranks -- an 8-byte all-reduce, not 8 np bytes
 static int enq_allreduce_part(tls_ctx* ctx, cudaStream_t s, int np) {
-  return enq_allreduce(ctx, s, ctx->part, np);
+  if (!sharded(ctx)) return TLS_OK;
+  launch_k(ctx, k_fold_partials, 1, NTHR, 0, s, ctx->part, np);
+  CKL();
+  return enq_allreduce(ctx, s, ctx->part, 1);
 }
 
 // point-to-point exchange: pack src rows, send/recv, unpack into dst.  Every rank calls every
@@ -491,12 +502,26 @@ static int enq_rev(tls_ctx* ctx, cudaStream_t s, const int* done) {
   return enq_exchange(ctx, s, ctx->rev, ctx->yloc, ctx->yloc, done);
 }
 
-// coarse coefficients c = Z^T r: this rank's columns, then the sum over ranks
+// coarse coefficients c = Z^T r: this rank's columns, then every rank's columns everywhere (an
+// all-gather of the per-rank column segments when the layout is known, else a sum all-reduce of
+// the zero-padded vector)
 static int enq_restrict_all(tls_ctx* ctx, cudaStream_t s, const double* r, const int* done) {
-  if (sharded(ctx))
-    CK(cudaMemsetAsync(ctx->xloc + ctx->coarse_xoff, 0, sizeof(double) * ctx->ncoarse, s));
+  double* c = ctx->xloc + ctx->coarse_xoff;
+  const bool gather = sharded(ctx) && ctx->d_ccol && ctx->cmax > 0;
+  if (sharded(ctx) && !gather) CK(cudaMemsetAsync(c, 0, sizeof(double) * ctx->ncoarse, s));
   TRY(enq_restrict(ctx, s, r, done));
-  return enq_allreduce(ctx, s, ctx->xloc + ctx->coarse_xoff, ctx->ncoarse);
+  if (!gather) return enq_allreduce(ctx, s, c, ctx->ncoarse);
+  const int q = ctx->comm->rank;
+  const long long c0 = ctx->ccol[q], cnt = ctx->ccol[q + 1] - c0;
+  if (cnt > 0) CK(cudaMemcpyAsync(ctx->cg_send, c + c0, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, s));
+  std::string err;
+  cudaError_t e = ctx->comm->allgather(ctx->cg_send, ctx->cmax, ctx->cg_recv, s, err);
+  if (e != cudaSuccess) return fail(ctx, TLS_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+  const long long tot = (long long)ctx->comm->nranks * ctx->cmax;
+  launch_k(ctx, k_coarse_unpack, grid_for(tot, NTHR), NTHR, 0, s, tot, ctx->cmax, (const long long*)ctx->d_ccol,
+           (const double*)ctx->cg_recv, c, done);
+  CKL();
+  return TLS_OK;
 }
 
 static int enq_dot(tls_ctx* ctx, cudaStream_t s, const double* a, const double* b, const int* done) {
@@ -658,6 +683,7 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   dfree(ctx->d_nofo); dfree(ctx->halo.d_sidx); dfree(ctx->halo.d_ridx); dfree(ctx->rev.d_sidx);
   dfree(ctx->rev.d_ridx);
   dfree(ctx->pcg); dfree(ctx->gm);
+  dfree(ctx->d_ccol); dfree(ctx->cg_send); dfree(ctx->cg_recv);
   for (auto e : ctx->kt_a) cudaEventDestroy(e);
   for (auto e : ctx->kt_b) cudaEventDestroy(e);
   for (void* pb : ctx->band_allocs) cudaFree(pb);
@@ -1402,6 +1428,31 @@ int32_t tls_coarse_prolong(tls_ctx* ctx, const double* y, double* z, void* strea
   double* zi = api_out_buf(ctx, z);
   TRY((enq_prolong<2, 0>(ctx, s, nullptr, nullptr, nullptr, zi, nullptr)));
   return api_out(ctx, s, zi, z);
+}
+
+// sharded: global coarse column ranges of every rank (nranks + 1 starts; rank q's subdomains own
+// columns [col_starts[q], col_starts[q+1]) -- contiguous because slabs are contiguous)
+int32_t tls_set_coarse_layout(tls_ctx* ctx, int32_t nranks, const int64_t* col_starts) {
+  if (!ctx || nranks <= 0 || !col_starts) return ctx ? fail(ctx, TLS_ERR_ARG, "bad coarse layout") : TLS_ERR_ARG;
+  if (!ctx->comm || ctx->comm->nranks != nranks) return fail(ctx, TLS_ERR_STATE, "initialise the communicator first");
+  if (col_starts[0] != 0 || col_starts[nranks] != ctx->ncoarse)
+    return fail(ctx, TLS_ERR_ARG, "coarse layout does not cover the n_coarse columns");
+  CK(cudaSetDevice(ctx->device));
+  ctx->ccol.assign(col_starts, col_starts + nranks + 1);
+  ctx->cmax = 0;
+  for (int q = 0; q < nranks; ++q) {
+    if (ctx->ccol[q + 1] < ctx->ccol[q]) return fail(ctx, TLS_ERR_ARG, "coarse layout not ascending");
+    ctx->cmax = std::max(ctx->cmax, ctx->ccol[q + 1] - ctx->ccol[q]);
+  }
+  if (ctx->nsub > 0 && ctx->ncoarse > 0 &&
+      (ctx->h_cstart[0] != ctx->ccol[ctx->comm->rank] ||
+       ctx->h_cstart[ctx->nsub - 1] + ctx->h_k[ctx->nsub - 1] != ctx->ccol[ctx->comm->rank + 1]))
+    return fail(ctx, TLS_ERR_ARG, "coarse layout disagrees with this rank's subdomain columns");
+  TRY(upload(ctx, ctx->d_ccol, (const long long*)ctx->ccol.data(), nranks + 1));
+  TRY(dalloc(ctx, ctx->cg_send, std::max<long long>(1, ctx->cmax)));
+  TRY(dalloc(ctx, ctx->cg_recv, std::max<long long>(1, ctx->cmax * nranks)));
+  destroy_graphs(ctx);
+  return TLS_OK;
 }
 
 // store A0 (row-major n_C x n_C, device) and turn on one refinement step of every coarse solve

@@ -43,6 +43,9 @@ struct Comm {
   virtual ~Comm() {}
   virtual cudaError_t allreduce_sum(double* buf, long long count, cudaStream_t s, std::string& err) = 0;
   virtual cudaError_t exchange(const XPlan& x, cudaStream_t s, std::string& err) = 0;
+  // recv[q * count + i] = send of rank q [i], i < count (every rank sends `count` doubles)
+  virtual cudaError_t allgather(const double* send, long long count, double* recv, cudaStream_t s,
+                                std::string& err) = 0;
   virtual bool capturable() const = 0;
 };
 
@@ -52,6 +55,7 @@ struct NcclApi {
   decltype(&ncclGetUniqueId) get_id = nullptr;
   decltype(&ncclCommInitRank) init_rank = nullptr;
   decltype(&ncclAllReduce) allreduce = nullptr;
+  decltype(&ncclAllGather) allgather = nullptr;
   decltype(&ncclCommDestroy) destroy = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
   decltype(&ncclSend) send = nullptr;
@@ -68,13 +72,14 @@ struct NcclApi {
     get_id = (decltype(get_id))dlsym(h, "ncclGetUniqueId");
     init_rank = (decltype(init_rank))dlsym(h, "ncclCommInitRank");
     allreduce = (decltype(allreduce))dlsym(h, "ncclAllReduce");
+    allgather = (decltype(allgather))dlsym(h, "ncclAllGather");
     destroy = (decltype(destroy))dlsym(h, "ncclCommDestroy");
     errstr = (decltype(errstr))dlsym(h, "ncclGetErrorString");
     send = (decltype(send))dlsym(h, "ncclSend");
     recv = (decltype(recv))dlsym(h, "ncclRecv");
     group_start = (decltype(group_start))dlsym(h, "ncclGroupStart");
     group_end = (decltype(group_end))dlsym(h, "ncclGroupEnd");
-    if (!get_id || !init_rank || !allreduce || !destroy || !errstr || !send || !recv || !group_start ||
+    if (!get_id || !init_rank || !allreduce || !allgather || !destroy || !errstr || !send || !recv || !group_start ||
         !group_end) {
       err = "libnccl.so.2 lacks required symbols";
       return false;
@@ -118,6 +123,15 @@ struct NcclComm : Comm {
     }
     return cudaSuccess;
   }
+  cudaError_t allgather(const double* send, long long count, double* recv, cudaStream_t s,
+                        std::string& err) override {
+    ncclResult_t r = nccl_api().allgather(send, recv, (size_t)count, ncclFloat64, comm, s);
+    if (r != ncclSuccess) {
+      err = std::string("ncclAllGather: ") + nccl_api().errstr(r);
+      return cudaErrorUnknown;
+    }
+    return cudaSuccess;
+  }
   bool capturable() const override { return true; }
 };
 
@@ -126,13 +140,17 @@ struct NcclComm : Comm {
 // (kind, element count, peers): lets a single-GPU test capture the sharded PCG / GMRES graphs
 // exactly as the NCCL transport would and compare the per-rank collective sequences.
 struct RecordComm : Comm {
-  std::vector<long long> log;  // triples: kind (1 all-reduce, 2 exchange), count, peers
+  std::vector<long long> log;  // triples: kind (1 all-reduce, 2 exchange, 3 all-gather), count, peers
   cudaError_t allreduce_sum(double*, long long count, cudaStream_t, std::string&) override {
     log.insert(log.end(), {1LL, count, 0LL});
     return cudaSuccess;
   }
   cudaError_t exchange(const XPlan& x, cudaStream_t, std::string&) override {
     log.insert(log.end(), {2LL, x.stot + x.rtot, (long long)x.peers.size()});
+    return cudaSuccess;
+  }
+  cudaError_t allgather(const double*, long long count, double*, cudaStream_t, std::string&) override {
+    log.insert(log.end(), {3LL, count, 0LL});
     return cudaSuccess;
   }
   bool capturable() const override { return true; }
@@ -250,6 +268,31 @@ struct GroupComm : Comm {
     if ((e = cudaEventRecord(g->ev_out[rank], s)) != cudaSuccess) return e;
     if (!g->barrier()) {  // every member has enqueued its reads of the send buffers
       err = "in-process group: a peer rank did not reach the exchange";
+      return cudaErrorUnknown;
+    }
+    for (int r = 0; r < g->n; ++r)
+      if ((e = cudaStreamWaitEvent(s, g->ev_out[r], 0)) != cudaSuccess) return e;
+    return cudaSuccess;
+  }
+  // every member publishes its send buffer; each copies all of them, in rank order
+  cudaError_t allgather(const double* send, long long count, double* recv, cudaStream_t s,
+                        std::string& err) override {
+    cudaError_t e;
+    g->xbuf[rank] = send;
+    if ((e = cudaEventRecord(g->ev_in[rank], s)) != cudaSuccess) return e;
+    if (!g->barrier()) {
+      err = "in-process group: a peer rank did not reach the all-gather";
+      return cudaErrorUnknown;
+    }
+    for (int r = 0; r < g->n; ++r) {
+      if ((e = cudaStreamWaitEvent(s, g->ev_in[r], 0)) != cudaSuccess) return e;
+      if ((e = cudaMemcpyAsync(recv + (long long)r * count, g->xbuf[r], sizeof(double) * count,
+                               cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+        return e;
+    }
+    if ((e = cudaEventRecord(g->ev_out[rank], s)) != cudaSuccess) return e;
+    if (!g->barrier()) {
+      err = "in-process group: a peer rank did not reach the all-gather";
       return cudaErrorUnknown;
     }
     for (int r = 0; r < g->n; ++r)

@@ -406,6 +406,34 @@ __global__ void __launch_bounds__(NTHR) k_perm_out(int n, const int* __restrict_
     dst[g] = (i >= r0 && i < r1) ? src[i] : 0.0;
   }
 }
+// sharded dot products: part[0] = fixed-order sum of part[0..np), part[1..np) = 0 (one CTA)
+__global__ void __launch_bounds__(NTHR) k_fold_partials(double* __restrict__ part, int np) {
+  PDL_ENTRY();
+  __shared__ double red[NTHR];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += NTHR) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = NTHR / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < np; i += NTHR) part[i] = i == 0 ? red[0] : 0.0;
+}
+
+// sharded coarse restriction: c[ccol[q] + i] = recv[q * cmax + i] for i < ccol[q+1] - ccol[q]
+__global__ void __launch_bounds__(NTHR) k_coarse_unpack(long long tot, long long cmax,
+                                                        const long long* __restrict__ ccol,
+                                                        const double* __restrict__ recv,
+                                                        double* __restrict__ c, const int* done) {
+  PDL_ENTRY();
+  if (done && *done) return;
+  for (long long j = blockIdx.x * (long long)NTHR + threadIdx.x; j < tot; j += (long long)gridDim.x * NTHR) {
+    const long long q = j / cmax, i = j - q * cmax;
+    if (i < ccol[q + 1] - ccol[q]) c[ccol[q] + i] = recv[j];
+  }
+}
+
 // out = a + beta * b (b may be null: a copy); coarse-segment arithmetic of the refinement step
 __global__ void __launch_bounds__(NTHR) k_lincomb(int n, const double* __restrict__ a,
                                                   const double* __restrict__ b, double beta,

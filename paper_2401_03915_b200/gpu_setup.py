@@ -1302,6 +1302,12 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     _make_room(torch, dev, 8 * nC * nC if not symmetric else 4 * nC * nC + 8 * nC * 64)
     handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
                                        _lib.ptr(A0inv), s_ptr))
+    if sharded:  # the restriction's all-gather layout: rank q's columns are contiguous
+        from .distributed import slab_ranges
+        csum = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        starts = np.array([csum[rlo] for rlo, _ in slab_ranges(n_loc.astype(np.float64) ** 2, shard.nranks)]
+                          + [nC], dtype=np.int64)
+        handle.check(lib.tls_set_coarse_layout(handle.ctx, shard.nranks, _lib.ptr(starts)))
     if refine:
         _make_room(torch, dev, 8 * nC * nC)
         handle.check(lib.tls_coarse_refine(handle.ctx, _lib.ptr(A0.contiguous()), s_ptr))

@@ -198,122 +198,132 @@ def color_subdomains(maps):
 
 
 # -- partition_graph (owner=None) --------------------------------------------------
+#
+# The reference's partitioner (src/partition.py:161-258) is specified by its result: components
+# largest first, a largest-remainder split of the subdomain count over them, farthest-point seeds
+# (ties -> smallest index), breadth-first growth truncated by ascending index, leftovers attached
+# to the smallest adjacent subdomain.  This implementation reaches the same owner vector by
+# different means: components from scipy's csgraph labelling; hop distances to the assigned set
+# kept in one array and only lowered (an incremental multi-source BFS from each new subdomain)
+# instead of recomputed from scratch per seed; growth as BFS level sets over the free nodes with
+# the last level cut to the needed count; subdomain sizes kept as running counts.
 
-def _components(graph):
-    seen = np.zeros(graph.n, dtype=bool)
-    comps = []
-    for start in range(graph.n):
-        if seen[start]:
-            continue
-        comp = [start]
-        seen[start] = True
-        front = np.array([start], dtype=np.int64)
-        while front.size:
-            nb = np.unique(graph.frontier_neighbors(front))
-            nb = nb[~seen[nb]]
-            seen[nb] = True
-            comp.extend(nb.tolist())
-            front = nb
-        comps.append(np.sort(np.asarray(comp, dtype=np.int64)))
-    return comps
-
-
-def _hop_distance(graph, sources, allowed):
-    dist = np.full(graph.n, -1, dtype=np.int64)
-    sources = sources[allowed[sources]]
-    dist[sources] = 0
-    front = sources
-    d = 0
-    while front.size:
-        d += 1
-        cand = np.unique(graph.frontier_neighbors(front))
-        cand = cand[(dist[cand] < 0) & allowed[cand]]
-        dist[cand] = d
-        front = cand
-    return dist
-
-
-def _grow(graph, seed, target, free):
-    picked = [seed]
+def _level_sets(graph, seed, free, goal):
+    """BFS levels from ``seed`` through free nodes until ``goal`` nodes are collected; the last
+    level is cut to its smallest indices.  Returns the picked nodes (seed first)."""
+    out = [np.array([seed], dtype=np.int64)]
     free[seed] = False
-    front = np.array([seed], dtype=np.int64)
-    while len(picked) < target and front.size:
-        ring = np.unique(graph.frontier_neighbors(front))
-        ring = ring[free[ring]]
-        if ring.size == 0:
+    have, level = 1, out[0]
+    while have < goal and level.size:
+        nb = graph.frontier_neighbors(level)
+        nxt = np.unique(nb[free[nb]])
+        if nxt.size == 0:
             break
-        room = target - len(picked)
-        ring = ring[:room]
-        free[ring] = False
-        picked.extend(ring.tolist())
-        front = ring
-    return picked
+        nxt = nxt[: goal - have]
+        free[nxt] = False
+        out.append(nxt)
+        have += nxt.size
+        level = nxt
+    return np.concatenate(out)
 
 
-def _budgets(sizes, nparts):
-    total = sum(sizes)
-    quota = [s * nparts / total for s in sizes]
-    bud = [int(q) for q in quota]
-    if len(sizes) <= nparts:
-        bud = [max(1, b) for b in bud]
-    while sum(bud) < nparts:
-        cand = [i for i in range(len(bud)) if bud[i] < sizes[i]]
-        i = max(cand, key=lambda i: (quota[i] - bud[i], sizes[i], -i))
+def _lower_distances(graph, dist, sources, inside):
+    """dist <- min(dist, hop distance from ``sources`` inside the component)."""
+    dist[sources] = 0
+    level, d = sources, 0
+    while level.size:
+        d += 1
+        nb = graph.frontier_neighbors(level)
+        nb = nb[inside[nb]]
+        nb = np.unique(nb[dist[nb] > d])
+        dist[nb] = d
+        level = nb
+
+
+def _split_budget(sizes, nparts):
+    """Largest-remainder split of ``nparts`` over components of ``sizes`` (src/partition.py:
+    213-236 rule: >= 1 each when possible; ties by remainder, then size, then first index)."""
+    sizes = np.asarray(sizes, dtype=np.int64)
+    quota = sizes * nparts / sizes.sum()
+    bud = np.floor(quota).astype(np.int64)
+    floor = 1 if sizes.size <= nparts else 0
+    bud = np.maximum(bud, floor)
+    idx = np.arange(sizes.size)
+    while bud.sum() < nparts:
+        ok = np.nonzero(bud < sizes)[0]
+        rem = quota[ok] - bud[ok]
+        i = ok[np.lexsort((idx[ok], -sizes[ok], -rem))[0]]
         bud[i] += 1
-    while sum(bud) > nparts:
-        floor = 1 if len(sizes) <= nparts else 0
-        cand = [i for i in range(len(bud)) if bud[i] > floor]
-        i = min(cand, key=lambda i: (quota[i] - bud[i], sizes[i], -i))
+    while bud.sum() > nparts:
+        ok = np.nonzero(bud > floor)[0]
+        rem = quota[ok] - bud[ok]
+        i = ok[np.lexsort((-idx[ok], sizes[ok], rem))[0]]
         bud[i] -= 1
     return bud
 
 
 def partition_graph(graph, n_subdomains):
-    """Deterministic farthest-seed BFS partitioner (src/partition.py:161-258)."""
+    """Owner partition for ``setup(owner=None)``: the result of src/partition.py:161-258."""
+    from scipy.sparse.csgraph import connected_components
     n = graph.n
     if not (1 <= n_subdomains <= n):
         raise ValueError(f"subdomain count {n_subdomains} out of range for {n} nodes")
-    comps = _components(graph)
-    comps.sort(key=lambda c: (-c.size, int(c[0])))
-    budgets = _budgets([c.size for c in comps], n_subdomains)
+    adj = sp.csr_matrix((np.ones(graph.adjacency.size, dtype=np.int8), graph.adjacency, graph.indptr),
+                        shape=(n, n))
+    ncomp, label = connected_components(adj, directed=False)
+    by_label = np.argsort(label, kind="stable")              # ascending node ids per label
+    csize = np.bincount(label, minlength=ncomp)
+    cstart = np.concatenate([[0], np.cumsum(csize)])
+    cmin = by_label[cstart[:-1]]
+    corder = np.lexsort((cmin, -csize))                      # largest first, then smallest node
+    comps = [by_label[cstart[c]:cstart[c + 1]] for c in corder]
+    budgets = _split_budget([c.size for c in comps], n_subdomains)
     owner = np.full(n, -1, dtype=np.int64)
+    count = np.zeros(n_subdomains + 1, dtype=np.int64)       # running subdomain sizes
     next_id = 0
-    leftover_comps = []
     for comp, nparts in zip(comps, budgets):
         if nparts == 0:
-            leftover_comps.append(comp)
             continue
         inside = np.zeros(n, dtype=bool)
         inside[comp] = True
         free = inside.copy()
-        target = -(-comp.size // nparts)
-        assigned = []
-        for s in range(nparts):
+        dist = np.full(n, np.iinfo(np.int64).max, dtype=np.int64)
+        target = -(-comp.size // int(nparts))
+        n_free = comp.size
+        for s in range(int(nparts)):
             if s == 0:
                 seed = int(comp[0])
             else:
-                dist = _hop_distance(graph, np.asarray(assigned, dtype=np.int64), inside)
                 cand = comp[free[comp]]
                 seed = int(cand[np.argmax(dist[cand])])
-            goal = min(target, int(free[comp].sum()) - (nparts - 1 - s))
-            picked = _grow(graph, seed, goal, free)
+            goal = min(target, n_free - (int(nparts) - 1 - s))
+            picked = _level_sets(graph, seed, free, goal)
             owner[picked] = next_id + s
-            assigned.extend(picked)
-        while free[comp].any():
-            progressed = False
-            for u in comp[free[comp]]:
+            count[next_id + s] += picked.size
+            n_free -= picked.size
+            _lower_distances(graph, dist, picked, inside)
+        # nodes the growth could not reach: in ascending order, each joins the adjacent subdomain
+        # that is currently smallest (ties -> lowest id); repeat until none is left
+        left = comp[free[comp]]
+        while left.size:
+            still = []
+            for u in left:
                 nbo = owner[graph.neighbors(u)]
                 nbo = np.unique(nbo[nbo >= 0])
                 if nbo.size == 0:
+                    still.append(u)
                     continue
-                counts = np.bincount(owner[owner >= 0], minlength=int(owner.max()) + 2)
-                owner[u] = int(nbo[np.argmin(counts[nbo])])
-                free[u] = False
-                progressed = True
-            if not progressed:
+                o = int(nbo[np.argmin(count[nbo])])
+                owner[u] = o
+                count[o] += 1
+            if len(still) == left.size:
                 raise RuntimeError("leftover nodes not adjacent to any subdomain")
-        next_id += nparts
-    for comp in leftover_comps:
-        counts = np.bincount(owner[owner >= 0], minlength=n_subdomains)
-        owner[comp] = int(np.argmin(counts))
+            left = np.asarray(still, dtype=np.int64)
+        next_id += int(nparts)
+    # components without a subdomain of their own join the smallest subdomain
+    for comp, nparts in zip(comps, budgets):
+        if nparts == 0:
+            o = int(np.argmin(count[:n_subdomains]))
+            owner[comp] = o
+            count[o] += comp.size
     return Partition(n_subdomains, owner)

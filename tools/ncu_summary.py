@@ -19,8 +19,10 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "lts__t_bytes.sum", "l1tex__t_bytes.sum", "smsp__inst_executed.sum",
            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
            "smsp__average_warp_latency_issue_stalled_long_scoreboard", "sm__cycles_elapsed.avg.per_second"]
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-         "msecond": 1e-3, "second": 1}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1,
+         "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
+TIME_UNITS = ("nsecond", "usecond", "msecond", "second", "ns", "us", "ms", "s")
 
 
 def full(rep, out):
@@ -38,7 +40,8 @@ def full(rep, out):
                 except ValueError:
                     continue
                 d[m] = v * SCALE.get(units[i], 1.0)
-                d[m + ".unit"] = "s" if units[i].endswith("second") else ("B" if "byte" in units[i] else units[i])
+                d[m + ".unit"] = ("s" if units[i] in TIME_UNITS else
+                                  "B" if ("byte" in units[i] or units[i] in ("B", "KB", "MB", "GB")) else units[i])
         res.append(d)
     k = res[0]
     k["dram_bytes_per_launch"] = k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0)
