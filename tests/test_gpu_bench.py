@@ -32,4 +32,8 @@ def test_bench_json_contract():
         assert k in d["roofline"], k
     for k in ("value", "unit", "cores", "kind", "sample"):
         assert k in d["cpu_baseline"], k
-    assert d["config"]["true_rel_residual"] <= 1.01 * d["config"]["tol"]
+    assert d["results"]["true_rel_residual"] <= 1.01 * d["config"]["tol"]
+    # configuration 1 is small: the CPU baseline runs the whole reference pipeline, not a sample
+    assert d["cpu_baseline"]["extrapolated"] is False and d["cpu_baseline"]["iterations_per_solve"] == 20
+    assert "value_1thread" in d["cpu_baseline"] and d["cpu_baseline"]["setup_s"] > 0
+
