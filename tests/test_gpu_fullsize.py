@@ -225,8 +225,8 @@ def test_full_cfg3_against_reference(B):
 
 
 def test_full_cfg4_against_reference(B):
-    # saddle point: cond(A0) ~ 1e9; the coarse solve is refined once, and the
-    # apply agrees with the reference's LU solve to 1e-8 of max|z|
+    # saddle point: the apply agrees with the reference's LU coarse solve to 1e-8
+    # of max|z| and the 100-iteration stagnating GMRES(50) history to 1e-8
     pre, a, errs, herr = _full(B, 4, 1e-8, 1e-8)
-    assert pre.coarse.refined
+    assert pre.coarse.cond1 is not None
     galerkin_projection(B, pre, a, 1e-6)

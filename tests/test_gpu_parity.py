@@ -2,7 +2,7 @@
 the CPU oracle on the same seeded inputs.
 
 Tolerances (fp64): index sets bit-exact; preconditioner apply <= 1e-10 relative to max|z|
-(config-4 saddle point: 1e-6, its coarse operator has cond ~1e10, SURVEY.md §0.4);
+(config-4 saddle point: 1e-8, its coarse operator has cond_1 ~1.5e7, SURVEY.md §0.4);
 iteration counts +-1; residual histories agree to 1e-10 absolute on the relative scale
 (1e-7 for config 4); the solution agrees to 1e-8 relative (1e-4 for config 4, whose
 reported residual is not its true residual)."""
@@ -30,7 +30,9 @@ def B():
 
 
 def _tols(name):
-    return (1e-6, 1e-7, 1e-4) if name.startswith("cfg4") else (1e-10, 1e-10, 1e-8)
+    # config-4 saddle point: cond_1(A0) ~ 1.5e7 -> both the reference's LU coarse solve and this
+    # one carry ~cond * eps forward error; measured apply difference 2.6e-10 (band-LU default)
+    return (1e-8, 1e-7, 1e-4) if name.startswith("cfg4") else (1e-10, 1e-10, 1e-8)
 
 
 _cache = {}
@@ -41,14 +43,12 @@ def _setup(B, name):
         d = golden(name)
         a = golden_csr(d)
         mat = B.SparseMat(a, symmetric=bool(d["symmetric"]))
-        # small batches so that multi-batch setup is exercised on every case.  The saddle-point
-        # analog (cfg4) is compared with the dense local operator the reference factors: its
-        # deflated operator amplifies O(eps) differences of the one-level solve by ~cond(A0), so
-        # its TRUE residual is rounding-sensitive; the band-LU path is checked
-        # by test_band_lu_and_inverse_agree (apply, reported history, iterations).
-        local = "inverse" if name.startswith("cfg4") else "auto"
+        # small batches so that multi-batch setup is exercised on every case; the default local
+        # operator (band Cholesky / band pivoted LU, as the bench runs it).  The saddle-point
+        # analog's (cfg4) deflated operator amplifies O(eps) differences by ~cond(A0), so its TRUE
+        # residual is rounding-sensitive
         pre = B.setup(mat, int(d["n_sub"]), overlap=int(d["overlap"]), owner=d["owner"],
-                      coarse=str(d["coarse"]), n_modes=int(d["n_modes"]), batch=5, local=local)
+                      coarse=str(d["coarse"]), n_modes=int(d["n_modes"]), batch=5)
         _cache[name] = (d, a, mat, pre)
     return _cache[name]
 
@@ -278,10 +278,41 @@ def test_config4_family_stall_history(B):
     a = golden_csr(d)
     mat = B.SparseMat(a)
     pre = B.setup(mat, int(d["n_sub"]), overlap=1, owner=d["owner"], coarse="svd", n_modes=20)
-    np.testing.assert_allclose(pre.apply(d["r"][0]), d["z"][0], rtol=0, atol=1e-6 * np.abs(d["z"][0]).max())
+    assert pre.local_kind == "band-lu"
+    # measured: apply 1.8e-9, history 4e-9 (cond_1(A0) = 3.8e7)
+    np.testing.assert_allclose(pre.apply(d["r"][0]), d["z"][0], rtol=0, atol=1e-8 * np.abs(d["z"][0]).max())
     x, rep = B.gmres(mat, pre, d["b"], tol=1e-7, maxit=100, restart=50)
     assert rep.iterations == 100 and not rep.converged
-    np.testing.assert_allclose(rep.residuals, d["history"], rtol=0, atol=1e-6)
+    np.testing.assert_allclose(rep.residuals, d["history"], rtol=0, atol=1e-8)
+
+
+def test_coarse_refinement_restores_backward_stability(B):
+    """One refinement step on the coarse solve (tls_coarse_refine; on automatically when
+    cond_1(A0) > 1e8): the coarse residual ||A0 y - c|| drops to the backward-stable level of the
+    reference's LU solve (src/coarse.py:178-182) and the apply is unchanged within cond * eps."""
+    from paper_2401_03915_b200 import gpu_setup as G
+    d = golden("cfg4_m32")
+    a = golden_csr(d)
+    mat = B.SparseMat(a)
+    kw = dict(overlap=1, owner=d["owner"], coarse="svd", n_modes=20)
+    plain = B.setup(mat, int(d["n_sub"]), **kw)
+    old = G.REFINE_COND
+    G.REFINE_COND = 0.0
+    try:
+        ref = B.setup(mat, int(d["n_sub"]), **kw)
+    finally:
+        G.REFINE_COND = old
+    assert ref.coarse.refined and not plain.coarse.refined and plain.coarse.cond1 > 1e6
+    a00 = ref.coarse.a00
+    c = np.random.default_rng(2).standard_normal(a00.shape[0])
+    res = []
+    for pre in (plain, ref):
+        y = pre.coarse.solve_coarse(c)
+        res.append(np.abs(a00 @ y - c).max() / (np.abs(a00).sum(1).max() * np.abs(y).max()))
+    assert res[1] <= 1e-14 and res[1] <= res[0], res
+    r = d["r"][0]
+    zp, zr = plain.apply(r), ref.apply(r)
+    assert np.abs(zp - zr).max() <= 1e-8 * np.abs(zr).max()
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2_m24", "cfg5_m16"])
@@ -314,7 +345,7 @@ def test_band_lu_and_inverse_agree(B, name):
     pb = B.setup(mat, int(d["n_sub"]), local="band", **kw)
     pi = B.setup(mat, int(d["n_sub"]), local="inverse", **kw)
     assert pi.local_kind == "inverse"
-    tol = 1e-6 if name.startswith("cfg4") else 1e-10
+    tol = 1e-8 if name.startswith("cfg4") else 1e-10
     for r, z1, z in zip(d["r"], d["z_one"], d["z"]):
         np.testing.assert_allclose(pb.apply_one_level(r), z1, rtol=0, atol=1e-10 * np.abs(z1).max())
         np.testing.assert_allclose(pb.apply(r), z, rtol=0, atol=tol * np.abs(z).max())
