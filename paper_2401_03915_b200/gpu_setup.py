@@ -1261,6 +1261,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     # 19.3 GB) is rebuilt on demand from the basis
     keep_a0 = 8 * nC * nC <= (4 << 30)
     norm_a0 = None
+    if not keep_a0:  # the factor and the inverse are two more n_C^2 buffers: defragment first
+        torch.cuda.empty_cache()
     if symmetric:
         # symmetrise (src/coarse.py:169-170) the lower triangle Cholesky reads, in place
         _symmetrize_lower_inplace(torch, A0)

@@ -116,11 +116,6 @@ def cfg2(B):
     return _sampled_setup(B, 2)
 
 
-@pytest.fixture(scope="module")
-def cfg5(B):
-    return _sampled_setup(B, 5)
-
-
 def _check_sampled(B, data, iterations):
     cfg, g, a, mat, pre = data
     # every index set and the colouring, bit for bit (reference extend_overlap / color_subdomains)
@@ -175,10 +170,6 @@ def test_full_cfg2_apply_linear_and_symmetric(B, cfg2):
     assert np.abs(mxy - (2.0 * mx - 3.0 * my)).max() <= 1e-12 * scale
     lhs, rhs = float(mx @ y), float(x @ my)
     assert abs(lhs - rhs) <= 1e-11 * (abs(lhs) + abs(rhs))
-
-
-def test_full_cfg5_against_reference(B, cfg5):
-    _check_sampled(B, cfg5, 534)
 
 
 # ------------------------------------------------------------------------------------------------
