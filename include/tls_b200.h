@@ -177,6 +177,45 @@ int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t 
                   int32_t restart, int32_t use_precond, double* history, tls_status* st,
                   tls_iter_cb cb, void* user, void* stream);
 
+/* ---- decomposition on the device, bit-exact with symmetrized_graph
+ * (src/sparsemat.py:180-195), extend_overlap (src/partition.py:278-301) and color_subdomains
+ * (src/partition.py:304-334).  Works on the uploaded matrix in the caller's numbering (not on a
+ * sharded handle).
+ * tls_graph_build: edges {i,j}, i != j, with |a_ij| > 0 or |a_ji| > 0 -> *nedges (directed count);
+ * tls_graph_fetch: host copies, gptr (n+1), gadj (nedges), rows in ascending column order;
+ * tls_overlap_build: overlap rings of every subdomain (owner: host, n entries in [0, n_sub)) and
+ *   the greedy colouring -> *total = sum of the index-set sizes, *k_c = colours used;
+ * tls_overlap_fetch: offsets (n_sub+1), layer_sizes (n_sub x overlap), indices (total: interior
+ *   ascending, then each layer ascending), colors (n_sub); host buffers;
+ * tls_graph_release: frees the device graph and the host results. */
+int32_t tls_graph_build(tls_ctx* ctx, int64_t* nedges);
+int32_t tls_graph_fetch(tls_ctx* ctx, int64_t* gptr, int32_t* gadj);
+int32_t tls_overlap_build(tls_ctx* ctx, int32_t n_sub, const int64_t* owner, int32_t overlap, int64_t* total,
+                          int32_t* k_c);
+int32_t tls_overlap_fetch(tls_ctx* ctx, int64_t* offsets, int64_t* layer_sizes, int64_t* indices, int64_t* colors);
+int32_t tls_graph_release(tls_ctx* ctx);
+
+/* ---- setup kernel K10: X <- (L L^T)^{-1} X for `count` banded Cholesky factors (L: count x ld x ld
+ * row-major, lower, factor order, ld = 64 nb; dinv: count x nb x 64 x 64 inverted diagonal tiles;
+ * kc: HOST count x nb panel-tile counts; X: count x ld x nrhs row-major, in place) on the FP64
+ * tensor cores -- the harmonic extension's multi-RHS solve (src/subdomain.py:108-120). */
+int32_t tls_band_solve_multi(const double* L, int64_t ld, int32_t count, const double* dinv, const int32_t* kc,
+                             int32_t nb, double* X, int64_t nrhs, void* stream);
+
+/* ---- setup kernel K12a: rank-filter pivots (src/coarse.py:119-155): column-pivoted Householder
+ * QR of `count` coarse blocks (block s: nrows[s] x ncols[s] column-major at W + woff[s], device,
+ * overwritten; ncols <= 64) -> HOST rdiag / perm (concatenated, sum(ncols) entries): |R_jj| and
+ * the original column at pivot position j. */
+int32_t tls_rank_filter_pivots(double* W, const int64_t* woff, const int32_t* nrows, const int32_t* ncols,
+                               int32_t count, double* rdiag, int32_t* perm, void* stream);
+
+/* ---- setup helper: batched symmetric eigensolver (parallel cyclic Jacobi, one CTA per matrix)
+ * for the p x p Rayleigh-Ritz matrices of the setup's subspace iteration (p <= 64): T (batch x p x
+ * p, device, symmetrised on load) -> w (batch x p, descending), V (batch x p x p, row-major, the
+ * eigenvectors as columns).  Stream-ordered; replaces the LAPACK eigh of src/spectral.py:80 on the
+ * projected problem. */
+int32_t tls_syevj_batched(const double* T, int64_t batch, int32_t p, double* w, double* V, void* stream);
+
 /* ---- SetupReport getters (src/precond.py:39-83) */
 int32_t tls_report(const tls_ctx* ctx, int64_t* n, int32_t* n_sub, int32_t* n_coarse,
                    int64_t* tile_bytes);

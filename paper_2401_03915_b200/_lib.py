@@ -96,6 +96,14 @@ SIGNATURES = {
     "tls_comm_init_record": (_I32, [_P, _I32, _I32]),
     "tls_comm_record_log": (_I64, [_P, _P, _I64]),
     "tls_set_coarse_layout": (_I32, [_P, _I32, _P]),
+    "tls_graph_build": (_I32, [_P, C.POINTER(_I64)]),
+    "tls_graph_fetch": (_I32, [_P, _P, _P]),
+    "tls_overlap_build": (_I32, [_P, _I32, _P, _I32, C.POINTER(_I64), C.POINTER(_I32)]),
+    "tls_overlap_fetch": (_I32, [_P, _P, _P, _P, _P]),
+    "tls_graph_release": (_I32, [_P]),
+    "tls_syevj_batched": (_I32, [_P, _I64, _I32, _P, _P, _P]),
+    "tls_band_solve_multi": (_I32, [_P, _I64, _I32, _P, _P, _I32, _P, _I64, _P]),
+    "tls_rank_filter_pivots": (_I32, [_P, _P, _P, _P, _I32, _P, _P, _P]),
 }
 
 _lib = None

@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "tls_b200.cu"), os.path.join(HERE, "csrc", "tls_mm.cpp")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("tls_kernels.cuh", "tls_comm.h")] + [os.path.join(REPO, "include", "tls_b200.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("tls_kernels.cuh", "tls_comm.h", "tls_graph.cuh")] + [os.path.join(REPO, "include", "tls_b200.h")]
 OUT = os.path.join(HERE, "libtls_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

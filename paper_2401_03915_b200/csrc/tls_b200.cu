@@ -23,6 +23,7 @@
 #include "tls_b200.h"
 #include "tls_comm.h"
 #include "tls_kernels.cuh"
+#include "tls_graph.cuh"
 
 using namespace tls;
 
@@ -169,6 +170,12 @@ struct tls_ctx {
   std::vector<int> rc_peer, rc_cnt, rc_sub, rc_row;  // remote contributions received (in order)
   long long Xrecv = 0;                // tail of yloc holding the received contributions
   double *pin = nullptr, *pout = nullptr;  // caller-numbering staging vectors
+  // ---- decomposition on the device (tls_graph_build / tls_overlap_build)
+  long long* g_ptr = nullptr;
+  int* g_adj = nullptr;
+  long long g_m = -1;
+  std::vector<long long> ov_off, ov_ls, ov_idx, ov_col;
+  int ov_nsub = 0, ov_delta = 0, ov_kc = 0;
 };
 
 template <typename... KArgs, typename... Args>
@@ -684,6 +691,7 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   dfree(ctx->rev.d_ridx);
   dfree(ctx->pcg); dfree(ctx->gm);
   dfree(ctx->d_ccol); dfree(ctx->cg_send); dfree(ctx->cg_recv);
+  dfree(ctx->g_ptr); dfree(ctx->g_adj);
   for (auto e : ctx->kt_a) cudaEventDestroy(e);
   for (auto e : ctx->kt_b) cudaEventDestroy(e);
   for (void* pb : ctx->band_allocs) cudaFree(pb);
@@ -1452,6 +1460,164 @@ int32_t tls_set_coarse_layout(tls_ctx* ctx, int32_t nranks, const int64_t* col_s
   TRY(dalloc(ctx, ctx->cg_send, std::max<long long>(1, ctx->cmax)));
   TRY(dalloc(ctx, ctx->cg_recv, std::max<long long>(1, ctx->cmax * nranks)));
   destroy_graphs(ctx);
+  return TLS_OK;
+}
+
+// K10: X <- (L L^T)^{-1} X for a batch of band Cholesky factors, many right-hand sides (DMMA)
+int32_t tls_band_solve_multi(const double* L, int64_t ld, int32_t count, const double* dinv, const int32_t* kc,
+                             int32_t nb, double* X, int64_t nrhs, void* stream) {
+  if (!L || !dinv || !kc || !X || count <= 0 || nb <= 0 || ld != 64LL * nb || nrhs <= 0) return TLS_ERR_ARG;
+  for (int64_t i = 0; i < (int64_t)count * nb; ++i)
+    if (kc[i] < 0 || kc[i] > i % nb) return TLS_ERR_ARG;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TLS_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem = sizeof(double) * 2 * 64 * CP;
+  if (raise_smem(dev, (const void*)k_band_trsm_multi, smem) != cudaSuccess) return TLS_ERR_CUDA;
+  int* d_kc = nullptr;
+  if (cudaMallocAsync((void**)&d_kc, sizeof(int) * (size_t)count * nb, s) != cudaSuccess) return TLS_ERR_OOM;
+  if (cudaMemcpyAsync(d_kc, kc, sizeof(int) * (size_t)count * nb, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return TLS_ERR_CUDA;
+  dim3 grid((unsigned)((nrhs + 63) / 64), (unsigned)count);
+  launch_k(nullptr, k_band_trsm_multi, grid, 256, smem, s, L, (long long)ld, dinv, (const int*)d_kc, (int)nb, X,
+           (long long)nrhs);
+  if (cudaGetLastError() != cudaSuccess) return TLS_ERR_CUDA;
+  cudaFreeAsync(d_kc, s);
+  return cudaStreamSynchronize(s) == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;  // kc (host) lifetime
+}
+
+// K12a: pivoted-QR pivot magnitudes of every subdomain's coarse block (rank filter)
+int32_t tls_rank_filter_pivots(double* W, const int64_t* woff, const int32_t* nrows, const int32_t* ncols,
+                               int32_t count, double* rdiag, int32_t* perm, void* stream) {
+  if (!W || !woff || !nrows || !ncols || !rdiag || !perm || count <= 0) return TLS_ERR_ARG;
+  std::vector<long long> roff(count + 1, 0);
+  for (int s = 0; s < count; ++s) {
+    if (ncols[s] < 0 || ncols[s] > 64 || nrows[s] < 0) return TLS_ERR_ARG;
+    roff[s + 1] = roff[s] + ncols[s];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  long long* d_woff = nullptr;
+  long long* d_roff = nullptr;
+  int *d_n = nullptr, *d_k = nullptr;
+  if (cudaMallocAsync((void**)&d_woff, sizeof(long long) * count, st) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_roff, sizeof(long long) * (count + 1), st) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_n, sizeof(int) * count, st) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_k, sizeof(int) * count, st) != cudaSuccess)
+    return TLS_ERR_OOM;
+  cudaMemcpyAsync(d_woff, woff, sizeof(long long) * count, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_roff, roff.data(), sizeof(long long) * (count + 1), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_n, nrows, sizeof(int) * count, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_k, ncols, sizeof(int) * count, cudaMemcpyHostToDevice, st);
+  double* d_rd = nullptr;
+  int* d_pm = nullptr;
+  if (cudaMallocAsync((void**)&d_rd, sizeof(double) * std::max<long long>(1, roff[count]), st) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_pm, sizeof(int) * std::max<long long>(1, roff[count]), st) != cudaSuccess)
+    return TLS_ERR_OOM;
+  launch_k(nullptr, k_pivoted_qr, count, 256, 0, st, W, (const long long*)d_woff, (const int*)d_n, (const int*)d_k,
+           (const long long*)d_roff, d_rd, d_pm);
+  if (cudaGetLastError() != cudaSuccess) return TLS_ERR_CUDA;
+  cudaMemcpyAsync(rdiag, d_rd, sizeof(double) * roff[count], cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(perm, d_pm, sizeof(int) * roff[count], cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_woff, st);
+  cudaFreeAsync(d_roff, st);
+  cudaFreeAsync(d_n, st);
+  cudaFreeAsync(d_k, st);
+  cudaFreeAsync(d_rd, st);
+  cudaFreeAsync(d_pm, st);
+  return cudaStreamSynchronize(st) == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;
+}
+
+// batched symmetric eigensolver (k_syevj_batched) for the setup's Rayleigh-Ritz matrices
+int32_t tls_syevj_batched(const double* T, int64_t batch, int32_t p, double* w, double* V, void* stream) {
+  if (!T || !w || !V || batch <= 0 || p <= 0 || p > EJ_MAX) return TLS_ERR_ARG;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TLS_ERR_CUDA;
+  const size_t smem = sizeof(double) * 2 * EJ_MAX * EJ_LD;
+  if (raise_smem(dev, (const void*)k_syevj_batched, smem) != cudaSuccess) return TLS_ERR_CUDA;
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int nb = (int)std::min<int64_t>(65535, batch - b0);
+    launch_k(nullptr, k_syevj_batched, nb, 256, smem, (cudaStream_t)stream, T + b0 * p * p, (int)p, w + b0 * p,
+             V + b0 * p * p, 30);
+  }
+  return cudaGetLastError() == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;
+}
+
+// ---- decomposition on the device (tls_graph.cuh; src/sparsemat.py:180-195, src/partition.py:278-334)
+int32_t tls_graph_build(tls_ctx* ctx, int64_t* nedges) {
+  if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "upload the matrix first") : TLS_ERR_ARG;
+  if (!ctx->h_nofo.empty()) return fail(ctx, TLS_ERR_STATE, "tls_graph_build needs the caller's row numbering");
+  CK(cudaSetDevice(ctx->device));
+  dfree(ctx->g_ptr);
+  dfree(ctx->g_adj);
+  long long m = 0;
+  std::string err;
+  cudaError_t e = graph::build_graph(ctx->n, ctx->rowptr, ctx->col, ctx->val, ctx->sym != 0, ctx->g_ptr, ctx->g_adj, m,
+                                     ctx->cap, err);
+  if (e != cudaSuccess)
+    return fail(ctx, e == cudaErrorMemoryAllocation ? TLS_ERR_OOM : TLS_ERR_CUDA,
+                "symmetrised graph: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+  CK(cudaStreamSynchronize(ctx->cap));
+  ctx->g_m = m;
+  if (nedges) *nedges = m;
+  return TLS_OK;
+}
+
+int32_t tls_graph_fetch(tls_ctx* ctx, int64_t* gptr, int32_t* gadj) {
+  if (!ctx || ctx->g_m < 0) return ctx ? fail(ctx, TLS_ERR_STATE, "build the graph first") : TLS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if (gptr) CK(cudaMemcpy(gptr, ctx->g_ptr, sizeof(long long) * (ctx->n + 1), cudaMemcpyDeviceToHost));
+  if (gadj && ctx->g_m > 0) CK(cudaMemcpy(gadj, ctx->g_adj, sizeof(int) * ctx->g_m, cudaMemcpyDeviceToHost));
+  return TLS_OK;
+}
+
+int32_t tls_overlap_build(tls_ctx* ctx, int32_t n_sub, const int64_t* owner, int32_t overlap, int64_t* total,
+                          int32_t* k_c) {
+  if (!ctx || ctx->g_m < 0) return ctx ? fail(ctx, TLS_ERR_STATE, "build the graph first") : TLS_ERR_ARG;
+  if (n_sub <= 0 || !owner) return fail(ctx, TLS_ERR_ARG, "bad subdomain count or owner vector");
+  if (overlap < 1) return fail(ctx, TLS_ERR_ARG, "overlap must be at least 1");
+  std::vector<int> own(ctx->n);
+  for (int i = 0; i < ctx->n; ++i) {
+    if (owner[i] < 0 || owner[i] >= n_sub) return fail(ctx, TLS_ERR_ARG, "owner ids out of range");
+    own[i] = (int)owner[i];
+  }
+  CK(cudaSetDevice(ctx->device));
+  int* d_owner = nullptr;
+  TRY(upload(ctx, d_owner, own.data(), ctx->n));
+  std::string err;
+  cudaError_t e = graph::overlap_and_colour(ctx->n, ctx->g_ptr, ctx->g_adj, d_owner, n_sub, overlap, ctx->ov_off,
+                                            ctx->ov_ls, ctx->ov_idx, ctx->ov_col, ctx->ov_kc, ctx->cap, err);
+  ctx->dev_bytes -= (int64_t)sizeof(int) * ctx->n;
+  dfree(d_owner);
+  if (e != cudaSuccess)
+    return fail(ctx, e == cudaErrorMemoryAllocation ? TLS_ERR_OOM : (e == cudaErrorInvalidValue ? TLS_ERR_ARG : TLS_ERR_CUDA),
+                "overlap: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+  ctx->ov_nsub = n_sub;
+  ctx->ov_delta = overlap;
+  if (total) *total = ctx->ov_idx.size();
+  if (k_c) *k_c = ctx->ov_kc;
+  return TLS_OK;
+}
+
+int32_t tls_overlap_fetch(tls_ctx* ctx, int64_t* offsets, int64_t* layer_sizes, int64_t* indices, int64_t* colors) {
+  if (!ctx || ctx->ov_nsub == 0) return ctx ? fail(ctx, TLS_ERR_STATE, "run tls_overlap_build first") : TLS_ERR_ARG;
+  if (offsets) std::copy(ctx->ov_off.begin(), ctx->ov_off.end(), offsets);
+  if (layer_sizes) std::copy(ctx->ov_ls.begin(), ctx->ov_ls.end(), layer_sizes);
+  if (indices) std::copy(ctx->ov_idx.begin(), ctx->ov_idx.end(), indices);
+  if (colors) std::copy(ctx->ov_col.begin(), ctx->ov_col.end(), colors);
+  return TLS_OK;
+}
+
+int32_t tls_graph_release(tls_ctx* ctx) {
+  if (!ctx) return TLS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  dfree(ctx->g_ptr);
+  dfree(ctx->g_adj);
+  ctx->g_m = -1;
+  std::vector<long long>().swap(ctx->ov_idx);
+  std::vector<long long>().swap(ctx->ov_off);
+  std::vector<long long>().swap(ctx->ov_ls);
+  std::vector<long long>().swap(ctx->ov_col);
+  ctx->ov_nsub = 0;
   return TLS_OK;
 }
 

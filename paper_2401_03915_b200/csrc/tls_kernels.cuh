@@ -406,6 +406,127 @@ __global__ void __launch_bounds__(NTHR) k_perm_out(int n, const int* __restrict_
     dst[g] = (i >= r0 && i < r1) ? src[i] : 0.0;
   }
 }
+// ---------------------------------------------------------------------------------------
+// K11 helper: batched symmetric eigensolver for the small Rayleigh-Ritz matrices of the setup's
+// subspace iteration (p x p, p <= 64; src/spectral.py:69-85 solves the full pencil with LAPACK
+// instead).  One CTA per matrix, matrix + eigenvectors in shared memory; parallel cyclic Jacobi
+// (round-robin pairing: p/2 disjoint rotations per round, p-1 rounds per sweep, the symmetric
+// 2x2 Schur rotation of Golub & Van Loan 8.5.1), until the off-diagonal Frobenius norm is below
+// 1e-15 of the whole; eigenvalues returned in descending order with their eigenvectors as
+// columns of V (row-major p x p).  Replaces a host round trip per Ritz step.
+// ---------------------------------------------------------------------------------------
+constexpr int EJ_MAX = 64;
+constexpr int EJ_LD = EJ_MAX + 1;
+
+__global__ void __launch_bounds__(256) k_syevj_batched(const double* __restrict__ T, int p,
+                                                       double* __restrict__ w, double* __restrict__ V,
+                                                       int max_sweeps) {
+  PDL_ENTRY();
+  extern __shared__ __align__(16) double ej_smem[];
+  double* A = ej_smem;                       // p x EJ_LD
+  double* Q = ej_smem + EJ_MAX * EJ_LD;      // p x EJ_LD
+  __shared__ double cs[EJ_MAX / 2], sn[EJ_MAX / 2], red[256];
+  __shared__ int pi_[EJ_MAX / 2], qi_[EJ_MAX / 2];
+  __shared__ int stop;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const double* Tb = T + (long long)b * p * p;
+  for (int e = tid; e < p * p; e += 256) {
+    const int i = e / p, j = e % p;
+    A[i * EJ_LD + j] = 0.5 * (Tb[i * p + j] + Tb[j * p + i]);
+    Q[i * EJ_LD + j] = i == j ? 1.0 : 0.0;
+  }
+  const int P = (p + 1) & ~1, np_ = P / 2;
+  __syncthreads();
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    // convergence: off-diagonal vs total Frobenius norm
+    double off = 0.0, tot = 0.0;
+    for (int e = tid; e < p * p; e += 256) {
+      const int i = e / p, j = e % p;
+      const double a = A[i * EJ_LD + j];
+      tot += a * a;
+      if (i != j) off += a * a;
+    }
+    red[tid] = off;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+      if (tid < h) red[tid] += red[tid + h];
+      __syncthreads();
+    }
+    const double offs = red[0];
+    __syncthreads();
+    red[tid] = tot;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+      if (tid < h) red[tid] += red[tid + h];
+      __syncthreads();
+    }
+    if (tid == 0) stop = !(offs > 1e-30 * red[0]) ? 1 : 0;
+    __syncthreads();
+    if (stop) break;
+    for (int r = 0; r < P - 1; ++r) {
+      if (tid < np_) {  // round-robin pair tid of round r (player 0 fixed, the others rotate)
+        const int m = tid;
+        const int pa = m == 0 ? 0 : ((m - 1 + r) % (P - 1)) + 1;
+        const int pb = ((P - 1 - m - 1 + r) % (P - 1)) + 1;
+        int i = min(pa, pb), j = max(pa, pb);
+        double c = 1.0, s = 0.0;
+        if (j < p) {
+          const double apq = A[i * EJ_LD + j];
+          if (apq != 0.0) {
+            const double tau = (A[j * EJ_LD + j] - A[i * EJ_LD + i]) / (2.0 * apq);
+            const double t = tau >= 0.0 ? 1.0 / (tau + sqrt(1.0 + tau * tau)) : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+          }
+        } else {
+          j = i;  // dummy partner (odd p): identity
+        }
+        pi_[m] = i;
+        qi_[m] = j;
+        cs[m] = c;
+        sn[m] = s;
+      }
+      __syncthreads();
+      // A <- A J and Q <- Q J (columns i, j of every pair)
+      for (int t = tid; t < p * np_; t += 256) {
+        const int k = t / np_, m = t % np_;
+        const int i = pi_[m], j = qi_[m];
+        if (i == j) continue;
+        const double c = cs[m], s = sn[m];
+        const double aki = A[k * EJ_LD + i], akj = A[k * EJ_LD + j];
+        A[k * EJ_LD + i] = c * aki - s * akj;
+        A[k * EJ_LD + j] = s * aki + c * akj;
+        const double qki = Q[k * EJ_LD + i], qkj = Q[k * EJ_LD + j];
+        Q[k * EJ_LD + i] = c * qki - s * qkj;
+        Q[k * EJ_LD + j] = s * qki + c * qkj;
+      }
+      __syncthreads();
+      // A <- J^T A (rows i, j of every pair)
+      for (int t = tid; t < p * np_; t += 256) {
+        const int k = t / np_, m = t % np_;
+        const int i = pi_[m], j = qi_[m];
+        if (i == j) continue;
+        const double c = cs[m], s = sn[m];
+        const double aik = A[i * EJ_LD + k], ajk = A[j * EJ_LD + k];
+        A[i * EJ_LD + k] = c * aik - s * ajk;
+        A[j * EJ_LD + k] = s * aik + c * ajk;
+      }
+      __syncthreads();
+    }
+  }
+  // descending order: rank of each eigenvalue (ties by index)
+  for (int j = tid; j < p; j += 256) {
+    const double d = A[j * EJ_LD + j];
+    int rk = 0;
+    for (int i = 0; i < p; ++i) {
+      const double e = A[i * EJ_LD + i];
+      rk += (e > d) || (e == d && i < j);
+    }
+    w[(long long)b * p + rk] = d;
+    for (int k = 0; k < p; ++k) V[(long long)b * p * p + (long long)k * p + rk] = Q[k * EJ_LD + j];
+  }
+}
+
 // sharded dot products: part[0] = fixed-order sum of part[0..np), part[1..np) = 0 (one CTA)
 __global__ void __launch_bounds__(NTHR) k_fold_partials(double* __restrict__ part, int np) {
   PDL_ENTRY();
@@ -1661,6 +1782,222 @@ __global__ void k_pack_band_u(const BandDesc* __restrict__ bands, int first_band
         dd[off + e] = Db[(long long)I * TT * TT + r * TT + (8 * w + kk)];
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K10  Banded triangular solves with many right-hand sides (setup: the harmonic extension,
+//      src/subdomain.py:108-120, as B[:, ring] = A_ii^{-1} E_ring on the band factor):
+//      X = (L L^T)^{-1} X for a batch of banded Cholesky factors (factor order, lower, 64-row
+//      blocks; kc[b][I] panel tiles left of the diagonal in block row I; dinv = inverted diagonal
+//      tiles, row-major).  Grid (RHS chunks of 64 columns, subdomains): every CTA sweeps its own
+//      64 columns forward (X_I = D_I^{-1} (X_I - sum_J L_IJ X_J)) and backward
+//      (X_I = D_I^{-T} X_I; X_J -= L_IJ^T X_I), every 64 x 64 x 64 tile product on the FP64
+//      tensor cores (mma.sync.m8n8k4.f64, tile_xyt: warp w owns output rows 8w..8w+7).
+//      Dynamic smem: 2 padded 64 x 65 tiles.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void tile_xyt_acc(const double* X, const double* Y, double (&acc)[8][2]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gr = lane >> 2, gc = lane & 3;
+#pragma unroll 4
+  for (int k0 = 0; k0 < 64; k0 += 4) {
+    const double a = X[(8 * w + gr) * CP + k0 + gc];
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj) dmma_8x8x4(acc[bj][0], acc[bj][1], a, Y[(8 * bj + gr) * CP + k0 + gc]);
+  }
+}
+
+// T[n][k] = G[k][n] for the valid columns n < nv (64 x 64 block of a row-major matrix, ld)
+__device__ __forceinline__ void load_tile_t(double* T, const double* G, long long ld, int nv) {
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    const int k = e >> 6, n = e & 63;
+    T[n * CP + k] = n < nv ? G[(long long)k * ld + n] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_band_trsm_multi(const double* __restrict__ L, long long ld,
+                                                         const double* __restrict__ dinv, const int* __restrict__ kc,
+                                                         int nb, double* __restrict__ Xall, long long nrhs) {
+  PDL_ENTRY();
+  extern __shared__ __align__(16) double ts[];
+  double* Xs = ts;             // X operand (rows m, cols k)
+  double* Ys = ts + 64 * CP;   // Y operand (rows n, cols k)
+  const int b = blockIdx.y;
+  const long long c0 = 64LL * blockIdx.x;
+  const int nv = (int)min(64LL, nrhs - c0);
+  const double* Lb = L + (long long)b * ld * ld;
+  const double* Db = dinv + (long long)b * nb * 64 * 64;
+  const int* kb = kc + (long long)b * nb;
+  double* X = Xall + (long long)b * ld * nrhs + c0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gr = lane >> 2, gc = lane & 3;
+  const int row = 8 * w + gr;
+  double acc[8][2];
+  // forward: X_I = D_I^{-1} (X_I - sum_J L_IJ X_J)
+  for (int I = 0; I < nb; ++I) {
+    const long long r0 = 64LL * I;
+    const int K = kb[I];
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj) acc[bj][0] = acc[bj][1] = 0.0;
+    for (int t = 0; t < K; ++t) {
+      const long long j0 = r0 - 64LL * (K - t);
+      load_tile(Xs, Lb + r0 * ld + j0, ld);
+      load_tile_t(Ys, X + j0 * nrhs, nrhs, nv);
+      __syncthreads();
+      tile_xyt_acc(Xs, Ys, acc);
+      __syncthreads();
+    }
+    // Ys[n][m] = X_I[m][n] - acc[m][n]
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 8 * bj + 2 * gc + e;
+        Ys[n * CP + row] = n < nv ? X[(r0 + row) * nrhs + n] - acc[bj][e] : 0.0;
+      }
+    load_tile(Xs, Db + (long long)I * 64 * 64, 64);
+    __syncthreads();
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj) acc[bj][0] = acc[bj][1] = 0.0;
+    tile_xyt_acc(Xs, Ys, acc);
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 8 * bj + 2 * gc + e;
+        if (n < nv) X[(r0 + row) * nrhs + n] = acc[bj][e];
+      }
+    __syncthreads();
+  }
+  // backward: X_I = D_I^{-T} X_I; X_J -= L_IJ^T X_I
+  for (int I = nb - 1; I >= 0; --I) {
+    const long long r0 = 64LL * I;
+    const int K = kb[I];
+    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {  // Xs[m][k] = D_I[k][m]
+      const int k = e >> 6, m = e & 63;
+      Xs[m * CP + k] = Db[(long long)I * 64 * 64 + e];
+    }
+    load_tile_t(Ys, X + r0 * nrhs, nrhs, nv);
+    __syncthreads();
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj) acc[bj][0] = acc[bj][1] = 0.0;
+    tile_xyt_acc(Xs, Ys, acc);
+    __syncthreads();
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 8 * bj + 2 * gc + e;
+        Ys[n * CP + row] = n < nv ? acc[bj][e] : 0.0;
+        if (n < nv) X[(r0 + row) * nrhs + n] = acc[bj][e];
+      }
+    for (int t = 0; t < K; ++t) {
+      const long long j0 = r0 - 64LL * (K - t);
+      __syncthreads();
+      for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {  // Xs[m][k] = L[r0 + k][j0 + m]
+        const int k = e >> 6, m = e & 63;
+        Xs[m * CP + k] = Lb[(r0 + k) * ld + j0 + m];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int bj = 0; bj < 8; ++bj) acc[bj][0] = acc[bj][1] = 0.0;
+      tile_xyt_acc(Xs, Ys, acc);
+#pragma unroll
+      for (int bj = 0; bj < 8; ++bj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = 8 * bj + 2 * gc + e;
+          if (n < nv) X[(j0 + row) * nrhs + n] -= acc[bj][e];
+        }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K12a  Rank filter pivots (setup; src/coarse.py:119-155 runs LAPACK geqp3 per subdomain block):
+//       column-pivoted Householder QR of each subdomain's coarse block W (n x k, column-major,
+//       overwritten), one CTA per subdomain.  Step j recomputes the remaining columns' norms over
+//       rows j.. (no downdating), takes the first largest as pivot, swaps it to j, and applies the
+//       Householder reflector that zeroes W[j+1:, j] to the columns right of it.  Outputs |R_jj|
+//       (rdiag, k per block) and the pivot order (perm: original column at position j).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum256(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) k_pivoted_qr(double* __restrict__ Wall, const long long* __restrict__ woff,
+                                                    const int* __restrict__ nrows, const int* __restrict__ ncols,
+                                                    const long long* __restrict__ roff, double* __restrict__ rdiag,
+                                                    int* __restrict__ perm) {
+  PDL_ENTRY();
+  __shared__ double red[256];
+  __shared__ double nrm[64];
+  __shared__ int pv[64];
+  const int s = blockIdx.x;
+  const int n = nrows[s], k = ncols[s];
+  double* W = Wall + woff[s];
+  double* rd = rdiag + roff[s];
+  int* pm = perm + roff[s];
+  if (threadIdx.x < k) pv[threadIdx.x] = threadIdx.x;
+  __syncthreads();
+  for (int j = 0; j < k && j < n; ++j) {
+    for (int c = j; c < k; ++c) {
+      double a = 0.0;
+      for (int i = j + threadIdx.x; i < n; i += 256) {
+        const double x = W[(long long)c * n + i];
+        a += x * x;
+      }
+      const double t = block_sum256(a, red);
+      if (threadIdx.x == 0) nrm[c] = t;
+    }
+    __syncthreads();
+    int p = j;
+    for (int c = j + 1; c < k; ++c)
+      if (nrm[c] > nrm[p]) p = c;
+    if (p != j) {  // swap columns j and p
+      for (int i = threadIdx.x; i < n; i += 256) {
+        const double t = W[(long long)j * n + i];
+        W[(long long)j * n + i] = W[(long long)p * n + i];
+        W[(long long)p * n + i] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = pv[j];
+        pv[j] = pv[p];
+        pv[p] = t;
+      }
+    }
+    __syncthreads();
+    // Householder: v = x - alpha e_1, alpha = -sign(x_0) ||x||; R_jj = alpha
+    const double xn = sqrt(nrm[p]);
+    const double x0 = W[(long long)j * n + j];
+    const double alpha = x0 >= 0.0 ? -xn : xn;
+    if (threadIdx.x == 0) rd[j] = fabs(alpha);
+    const double v0 = x0 - alpha;
+    const double vtv = xn * xn - x0 * x0 + v0 * v0;
+    __syncthreads();
+    if (vtv > 0.0) {
+      for (int c = j + 1; c < k; ++c) {
+        double a = threadIdx.x == 0 ? v0 * W[(long long)c * n + j] : 0.0;
+        for (int i = j + 1 + threadIdx.x; i < n; i += 256) a += W[(long long)j * n + i] * W[(long long)c * n + i];
+        const double f = 2.0 * block_sum256(a, red) / vtv;
+        if (threadIdx.x == 0) W[(long long)c * n + j] -= f * v0;
+        for (int i = j + 1 + threadIdx.x; i < n; i += 256) W[(long long)c * n + i] -= f * W[(long long)j * n + i];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) W[(long long)j * n + j] = alpha;
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < k; j += 256) {
+    pm[j] = pv[j];
+    if (j >= n) rd[j] = 0.0;
   }
 }
 

@@ -84,6 +84,51 @@ class Handle:
             self.ctx = None
 
 
+def device_graph(handle):
+    """Symmetrised sparsity graph of the handle's matrix, built on the device (tls_graph_build;
+    src/sparsemat.py:180-195) and returned as a host ``Graph`` (int64 row pointers, int32 columns)."""
+    from .partition import Graph
+    m = C.c_int64()
+    handle.check(handle.lib.tls_graph_build(handle.ctx, C.byref(m)))
+    gptr = np.empty(handle.n + 1, dtype=np.int64)
+    gadj = np.empty(max(1, m.value), dtype=np.int32)
+    handle.check(handle.lib.tls_graph_fetch(handle.ctx, _lib.ptr(gptr), _lib.ptr(gadj)))
+    return Graph(gptr, gadj[: m.value])
+
+
+def device_overlap(handle, part, overlap):
+    """Overlap rings + colouring of every subdomain on the device (tls_overlap_build; bit-exact
+    with src/partition.py:278-334) from the graph of the last ``device_graph`` call.
+    Returns (maps, k_c, colors); frees the device graph."""
+    from .partition import SubdomainMap
+    if overlap < 1:
+        raise ValueError("overlap must be at least 1")
+    nsub = part.n_subdomains
+    owner = np.ascontiguousarray(part.owner, dtype=np.int64)
+    tot, kc = C.c_int64(), C.c_int32()
+    try:
+        handle.check(handle.lib.tls_overlap_build(handle.ctx, nsub, _lib.ptr(owner), int(overlap), C.byref(tot),
+                                                  C.byref(kc)))
+        off = np.empty(nsub + 1, dtype=np.int64)
+        ls = np.empty(nsub * overlap, dtype=np.int64)
+        idx = np.empty(max(1, tot.value), dtype=np.int64)
+        colors = np.empty(nsub, dtype=np.int64)
+        handle.check(handle.lib.tls_overlap_fetch(handle.ctx, _lib.ptr(off), _lib.ptr(ls), _lib.ptr(idx),
+                                                  _lib.ptr(colors)))
+    finally:
+        handle.lib.tls_graph_release(handle.ctx)
+    ls = ls.reshape(nsub, overlap)
+    maps = []
+    n = part.owner.size
+    for s in range(nsub):
+        seg = idx[off[s]:off[s + 1]]
+        cut = np.cumsum(ls[s])
+        ni = seg.size - int(cut[-1])
+        layers = tuple(seg[ni + (cut[k] - ls[s, k]):ni + cut[k]] for k in range(overlap))
+        maps.append(SubdomainMap(s, n, seg[:ni], layers))
+    return maps, int(kc.value), colors
+
+
 def to_device(v, n, device):
     """(device fp64 tensor, converter back to the caller's type)."""
     torch = _torch()

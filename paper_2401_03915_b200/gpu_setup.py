@@ -374,7 +374,7 @@ def topk_subspace(torch, M, k, tol=1e-14, maxit=2000, seed=20240103, p=None):
     raise RuntimeError(f"subspace iteration did not converge: residual {res:.2e} after {maxit} sweeps")
 
 
-def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rmax=1e8, dmax=16,
+def _topk_chebyshev_host(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rmax=1e8, dmax=16,
                    trace=None):
     """Top-k eigenpairs (descending) of a batch of symmetric PSD matrices M (b, m, m).
 
@@ -440,7 +440,119 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
     raise RuntimeError(f"Chebyshev subspace iteration did not converge: residual {res:.2e} after {maxit} steps")
 
 
+def _eigh_desc(torch, T):
+    """Eigenpairs of a batch of small symmetric matrices, descending: the in-tree batched Jacobi
+    kernel (tls_syevj_batched, stream-ordered, no host round trip) for p <= 64."""
+    b, p, _ = T.shape
+    if p > 64 or not T.is_cuda:
+        w, S = torch.linalg.eigh(0.5 * (T + T.mT))
+        return torch.flip(w, dims=[-1]), torch.flip(S, dims=[-1])
+    Tc = T.contiguous()
+    w = torch.empty((b, p), dtype=T.dtype, device=T.device)
+    S = torch.empty((b, p, p), dtype=T.dtype, device=T.device)
+    rc = _lib.load().tls_syevj_batched(_lib.ptr(Tc), b, p, _lib.ptr(w), _lib.ptr(S), stream_ptr())
+    if rc != 0:
+        raise RuntimeError(f"tls_syevj_batched failed ({rc})")
+    return w, S
+
+
+def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rmax=1e8, dmax=16,
+                   trace=None, check_every=2):
+    """Top-k eigenpairs (descending) of a batch of symmetric PSD matrices M (b, m, m).
+
+    Chebyshev-filtered subspace iteration: each outer step applies T_d((M - c) / e) to the Ritz
+    block (columns = current Ritz vectors), with [0, a] (a = the block's smallest Ritz value, per
+    matrix) mapped onto [-1, 1]; the filtered columns are normalised, re-orthonormalised
+    (CholeskyQR2) and Rayleigh-Ritz'ed (p x p, on the device: tls_syevj_batched).  Every matrix
+    gets its own degree d_b (a matrix whose degree is reached stops updating), capped so the
+    filter's spread over its wanted Ritz values, R = T_d(x_1) / T_d(x_k), stays below ``rmax``.
+    Because each column starts as a Ritz vector, column i's pull toward the top modes is (its
+    residual) x R, not R: the columns stay far from collinear and the k-th keeps
+    ~eps * (1 + residual * R) relative precision.  Stops when every wanted Ritz pair has
+    ||M x - theta x|| <= tol * theta_1.  The whole iteration is stream-ordered: the host looks at
+    the residuals (one small copy) only every ``check_every`` steps, and the Chebyshev loop runs
+    the degree of that check (per-matrix degrees are masks), so batches pipeline on the device.
+    A CholeskyQR2 breakdown (non-finite block) falls back to ``_topk_chebyshev_host`` (Householder
+    QR, host checks every step).  Returns (theta, X, block products).
+    """
+    b, m, _ = M.shape
+    p = min(m, p or max(3 * k, k + 16))
+    if m <= max(96, 2 * p) or p > 64:
+        return _topk_chebyshev_host(torch, M, k, tol=tol, p=p, maxit=maxit, seed=seed, rmax=rmax,
+                                    dmax=dmax, trace=trace)
+    gen = torch.Generator(device=M.device)
+    gen.manual_seed(seed)
+    X = _orth(torch, torch.randn((b, m, p), generator=gen, dtype=M.dtype, device=M.device))
+    X = _orth(torch, M @ (M @ X))
+    MX = M @ X
+    th, S = _eigh_desc(torch, X.mT @ MX)
+    X, MX = X @ S, MX @ S
+    scale = th[:, :1].abs().clamp(min=1e-300)
+    products = 3
+    d = dmax
+    bad = torch.zeros(b, dtype=torch.bool, device=M.device)
+    res = float("inf")
+    for it in range(1, maxit + 1):
+        R = MX[:, :, :k] - X[:, :, :k] * th[:, None, :k]
+        res_b = (R.norm(dim=1) / scale).amax(dim=1)                     # (b,)
+        a = th[:, p - 1].clamp(min=0.0)
+        e = (0.5 * a).clamp(min=1e-300)
+        x1 = ((th[:, 0] - e) / e).clamp(min=1.0 + 1e-12)
+        xk = ((th[:, k - 1] - e) / e).clamp(min=1.0 + 1e-12)
+        per = (torch.acosh(x1) - torch.acosh(xk)).clamp(min=1e-12)
+        d_b = torch.floor(np.log(rmax) / per).clamp(min=1, max=dmax)
+        d_b = torch.where(res_b > tol, d_b, torch.zeros_like(d_b))       # converged: leave as is
+        if (it - 1) % check_every == 0:
+            host = torch.stack([torch.nan_to_num(res_b, nan=np.inf).max(), d_b.max(),
+                                bad.any().to(res_b.dtype)]).cpu()       # one small copy
+            res, d = float(host[0]), int(host[1])
+            if float(host[2]) != 0.0 or not np.isfinite(res):
+                return _topk_chebyshev_host(torch, M, k, tol=tol, p=p, maxit=maxit, seed=seed, rmax=rmax,
+                                            dmax=dmax, trace=trace)
+            if res <= tol:
+                return th[:, :k], X[:, :, :k], products
+            if trace is not None:
+                trace.append((d, res, int((res_b > tol).sum()), float(per.max())))
+        c = e[:, None, None]
+        inv_e = (1.0 / e)[:, None, None]
+        Y0 = X
+        Y1 = torch.where((d_b >= 1)[:, None, None], (MX - c * X) * inv_e, X)
+        for j in range(2, d + 1):
+            Y2 = 2.0 * (M @ Y1 - c * Y1) * inv_e - Y0
+            live = (d_b >= j)[:, None, None]
+            Y0 = torch.where(live, Y1, Y0)
+            Y1 = torch.where(live, Y2, Y1)
+        products += d
+        Y1 = Y1 / Y1.norm(dim=1, keepdim=True).clamp(min=1e-300)
+        Xo, bad_o = _orth(torch, Y1, check=False)   # breakdowns surface at the next check
+        bad = bad | bad_o
+        MX = M @ Xo
+        th, S = _eigh_desc(torch, Xo.mT @ MX)
+        X, MX = Xo @ S, MX @ S
+        products += 1
+    raise RuntimeError(f"Chebyshev subspace iteration did not converge: residual {res:.2e} after {maxit} steps")
+
+
 def band_solve_multi(torch, L, Dinv, kc, E):
+    """X = (L L^T)^{-1} E for a batch of banded Cholesky factors and many right-hand sides.
+
+    On the device: the in-tree K10 kernel (``tls_band_solve_multi``: one CTA per (subdomain,
+    64 right-hand sides), both sweeps on the FP64 tensor cores).  On CPU tensors (the host tests of
+    the setup algebra): the blocked torch restatement ``_band_solve_multi_torch``.
+    """
+    if E.is_cuda:
+        b, ld, nrhs = E.shape
+        X = E.contiguous().clone()
+        kci = np.ascontiguousarray(np.asarray(kc, dtype=np.int32).reshape(b, ld // 64))
+        rc = _lib.load().tls_band_solve_multi(_lib.ptr(L.contiguous()), ld, b, _lib.ptr(Dinv.contiguous()),
+                                              _lib.ptr(kci), ld // 64, _lib.ptr(X), nrhs, stream_ptr())
+        if rc != 0:
+            raise RuntimeError(f"tls_band_solve_multi failed ({rc})")
+        return X
+    return _band_solve_multi_torch(torch, L, Dinv, kc, E)
+
+
+def _band_solve_multi_torch(torch, L, Dinv, kc, E):
     """X = (L L^T)^{-1} E for a batch of banded Cholesky factors and many right-hand sides.
 
     Blocked banded forward/backward substitution over 64-row blocks with batched GEMMs: block
@@ -578,6 +690,36 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
             for j, b in enumerate(bs):
                 out[b] = _subdomain_columns(torch, kind, A[b], Bring[j], n, ni, nin, tau, n_modes) + (None,)
         del Bring
+    return out
+
+
+def _rank_pivots(torch, z_dev, own, dev):
+    """(|R_jj|, subdomain, original column) of the column-pivoted QR of every block z_dev[s]
+    (n_int x k), the pivots of src/coarse.py:133-141, computed on the device (K12a)."""
+    blocks = [s for s in own if z_dev[s].shape[1] > 0]
+    if not blocks:
+        return []
+    if any(z_dev[s].shape[1] > 64 for s in blocks):  # wide blocks (coarse="full"): host geqp3
+        out = []
+        for s in blocks:
+            r, perm = sla.qr(z_dev[s].cpu().numpy(), mode="r", pivoting=True)
+            rd = np.abs(np.diag(r))
+            out += [(rd[j] if j < rd.size else 0.0, s, int(perm[j])) for j in range(z_dev[s].shape[1])]
+        return out
+    W = torch.cat([z_dev[s].mT.contiguous().reshape(-1) for s in blocks])   # column-major blocks
+    nr = np.array([z_dev[s].shape[0] for s in blocks], dtype=np.int32)
+    nc = np.array([z_dev[s].shape[1] for s in blocks], dtype=np.int32)
+    woff = np.concatenate([[0], np.cumsum(nr.astype(np.int64) * nc)[:-1]]).astype(np.int64)
+    rd = np.empty(int(nc.sum()), dtype=np.float64)
+    pm = np.empty(int(nc.sum()), dtype=np.int32)
+    rc = _lib.load().tls_rank_filter_pivots(_lib.ptr(W), _lib.ptr(woff), _lib.ptr(nr), _lib.ptr(nc), len(blocks),
+                                            _lib.ptr(rd), _lib.ptr(pm), stream_ptr())
+    if rc != 0:
+        raise RuntimeError(f"tls_rank_filter_pivots failed ({rc})")
+    out, o = [], 0
+    for s, k in zip(blocks, nc):
+        out += [(float(rd[o + j]), s, int(pm[o + j])) for j in range(int(k))]
+        o += int(k)
     return out
 
 
@@ -1167,40 +1309,16 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         return None
     # rank filter (src/coarse.py:119-155): pivoted-QR magnitudes vs the GLOBAL largest pivot
     own = range(lo, hi)
-    # one device->host copy of every owned block, then the host pivoted QRs (LAPACK geqp3, the
-    # reference's rank test) on all host threads
+    # one device->host copy of every owned block (the host keeps the basis for CoarseData), and
+    # the column-pivoted QR of every block on the device (K12a, tls_rank_filter_pivots; the
+    # reference runs LAPACK geqp3 per block)
     flat = torch.cat([z_dev[s].reshape(-1) for s in own]).cpu().numpy() if len(own) else np.zeros(0)
     z_host, off = {}, 0
     for s in own:
         sh = tuple(z_dev[s].shape)
         z_host[s] = flat[off:off + sh[0] * sh[1]].reshape(sh)
         off += sh[0] * sh[1]
-
-    def _geqp3(s):
-        z = z_host[s]
-        if z.shape[1] == 0:
-            return s, None, None
-        r, perm = sla.qr(z, mode="r", pivoting=True)
-        return s, np.abs(np.diag(r)), perm
-
-    try:  # one BLAS thread per pool worker (no oversubscription)
-        from threadpoolctl import threadpool_limits
-        limit = threadpool_limits(limits=1)
-    except Exception:  # threadpoolctl missing: run the QRs serially with BLAS threads
-        limit = None
-    try:
-        workers = min(16, os.cpu_count() or 1) if limit is not None else 1
-        with ThreadPoolExecutor(max_workers=workers) as ex:
-            qrs = list(ex.map(_geqp3, own))
-    finally:
-        if limit is not None:
-            limit.restore_original_limits()
-    pivots = []
-    for s, rd, perm in qrs:
-        if rd is None:
-            continue
-        for j in range(z_host[s].shape[1]):
-            pivots.append((rd[j] if j < rd.size else 0.0, s, int(perm[j])))
+    pivots = _rank_pivots(torch, z_dev, own, dev) if len(own) else []
     largest = max((p[0] for p in pivots), default=0.0)
     any_cols = float(len(pivots))
     if sharded:

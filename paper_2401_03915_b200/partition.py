@@ -92,7 +92,9 @@ class Graph:
 
     def __init__(self, indptr, adjacency):
         self.indptr = np.asarray(indptr, dtype=np.int64)
-        self.adjacency = np.asarray(adjacency, dtype=np.int64)
+        adjacency = np.asarray(adjacency)
+        # int32 adjacency (the device-built graph) is kept as is: half the memory, same values
+        self.adjacency = adjacency if adjacency.dtype in (np.int32, np.int64) else adjacency.astype(np.int64)
         self.n = self.indptr.size - 1
 
     def neighbors(self, i):

@@ -1,0 +1,122 @@
+"""In-tree setup kernels against numpy/LAPACK on the same inputs: the batched Jacobi eigensolver
+of the Rayleigh-Ritz step (tls_syevj_batched; the dense eigh of src/spectral.py:69-85 on the
+projected problem) and the sync-light Chebyshev subspace iteration built on it."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2401_03915_b200 import build
+    build.build()
+    from paper_2401_03915_b200 import gpu_setup
+    return gpu_setup
+
+
+@pytest.mark.parametrize("p", [1, 2, 7, 8, 33, 39, 64])
+def test_syevj_batched_matches_lapack(G, p):
+    rng = np.random.default_rng(p)
+    b = 5
+    T = rng.standard_normal((b, p, p))
+    T = T + T.transpose(0, 2, 1)
+    T[1] = np.diag(np.arange(p, dtype=float))          # already diagonal
+    T[2] = np.eye(p) * 3.0                              # fully degenerate
+    q, _ = np.linalg.qr(rng.standard_normal((p, p)))
+    T[3] = q @ np.diag(np.repeat([5.0, 1.0, -2.0], -(-p // 3))[:p]) @ q.T   # clustered
+    Td = torch.as_tensor(T, device="cuda")
+    w, V = G._eigh_desc(torch, Td)
+    w, V = w.cpu().numpy(), V.cpu().numpy()
+    for j in range(b):
+        ref = np.sort(np.linalg.eigvalsh(T[j]))[::-1]
+        nrm = max(np.abs(T[j]).max(), 1.0)
+        assert np.abs(w[j] - ref).max() <= 1e-13 * nrm * p, j
+        assert np.abs(T[j] @ V[j] - V[j] * w[j][None, :]).max() <= 1e-12 * nrm, j
+        assert np.abs(V[j].T @ V[j] - np.eye(p)).max() <= 1e-12, j
+        assert np.all(np.diff(w[j]) <= 0)
+
+
+@pytest.mark.parametrize("decay", [0.5, 0.97])
+def test_chebyshev_on_device_matches_dense_eigh(G, decay):
+    rng = np.random.default_rng(3)
+    b, m, k = 6, 300, 12
+    Ms = []
+    for j in range(b):
+        q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+        ev = decay ** np.arange(m) * (1 + 0.1 * j)
+        Ms.append((q * ev) @ q.T)
+    M = torch.as_tensor(np.array(Ms), device="cuda")
+    th, X, _ = G.topk_chebyshev(torch, M, k)
+    for j in range(b):
+        w, Q = np.linalg.eigh(Ms[j])
+        w, Q = w[::-1][:k], Q[:, ::-1][:, :k]
+        assert np.abs(th[j].cpu().numpy() - w).max() <= 1e-12 * w[0]
+        Xj = X[j].cpu().numpy()
+        # same span: projector difference
+        assert np.abs(Xj @ Xj.T - Q @ Q.T).max() <= 1e-9
+
+
+def test_band_solve_multi_kernel_matches_torch_and_dense(G):
+    """K10 (tls_band_solve_multi, DMMA) = the blocked torch restatement = a dense Cholesky solve,
+    on banded SPD blocks with varying per-block panel counts and a ragged RHS count."""
+    rng = np.random.default_rng(11)
+    b, nb, nrhs = 3, 5, 70
+    ld = 64 * nb
+    A = np.zeros((b, ld, ld))
+    kc = np.zeros((b, nb), dtype=np.int64)
+    for j in range(b):
+        bw = [40, 100, 150][j]
+        M = np.zeros((ld, ld))
+        for d in range(bw + 1):
+            v = rng.standard_normal(ld - d) * 0.1
+            M += np.diag(v, -d)
+        M = M @ M.T + ld * np.eye(ld)
+        band = np.abs(np.subtract.outer(np.arange(ld), np.arange(ld))) <= bw
+        A[j] = np.where(band, M, 0.0) + 2 * bw * np.eye(ld)
+        for I in range(nb):
+            kc[j, I] = min(I, -(-bw // 64))
+    At = torch.as_tensor(A, device="cuda")
+    L = torch.linalg.cholesky(At)
+    Ld = L.view(b, nb, 64, nb, 64).diagonal(dim1=1, dim2=3).permute(0, 3, 1, 2)
+    eye = torch.eye(64, dtype=torch.float64, device="cuda").expand(b, nb, 64, 64)
+    Dinv = torch.linalg.solve_triangular(Ld, eye, upper=False).contiguous()
+    E = torch.as_tensor(rng.standard_normal((b, ld, nrhs)), device="cuda")
+    Xk = G.band_solve_multi(torch, L.contiguous(), Dinv, kc, E)
+    Xt = G._band_solve_multi_torch(torch, L, Dinv, kc, E)
+    Xd = torch.cholesky_solve(E, L)
+    scale = Xd.abs().max().item()
+    assert (Xk - Xd).abs().max().item() <= 1e-12 * scale
+    assert (Xk - Xt).abs().max().item() <= 1e-12 * scale
+
+
+def test_rank_filter_pivots_match_lapack_geqp3(G):
+    """K12a (device column-pivoted Householder QR) = LAPACK geqp3 (src/coarse.py:136): pivot order
+    and |R_jj| on well-separated blocks, incl. an exactly dependent column and a zero column."""
+    import scipy.linalg as sla
+    rng = np.random.default_rng(2)
+    blocks = {}
+    for s, (n, k) in enumerate([(300, 12), (64, 20), (1000, 3), (50, 1)]):
+        z = rng.standard_normal((n, k)) * np.logspace(0, -6, k)[None, :]
+        if k >= 3:
+            z[:, 2] = z[:, 0] - 2.0 * z[:, 1]      # dependent
+        if k >= 5:
+            z[:, 4] = 0.0                          # zero column
+        blocks[s] = torch.as_tensor(z, device="cuda")
+    piv = G._rank_pivots(torch, blocks, range(len(blocks)), torch.device("cuda"))
+    o = 0
+    for s in range(len(blocks)):
+        z = blocks[s].cpu().numpy()
+        r, perm = sla.qr(z, mode="r", pivoting=True)
+        rd = np.abs(np.diag(r))
+        mine = [p for p in piv if p[1] == s]
+        got = np.array([p[0] for p in mine])
+        want = np.array([rd[j] if j < rd.size else 0.0 for j in range(z.shape[1])])
+        big = want > 1e-10 * want.max()            # the filter's decision range (drop_tol 1e-10)
+        assert [p[2] for p, b in zip(mine, big) if b] == [int(q) for q, b in zip(perm, big) if b], s
+        assert np.abs(got[big] - want[big]).max() <= 1e-12 * want.max(), s
+        assert np.all(got[~big] <= 1e-10 * want.max()), s
