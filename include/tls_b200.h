@@ -195,6 +195,23 @@ int32_t tls_overlap_build(tls_ctx* ctx, int32_t n_sub, const int64_t* owner, int
 int32_t tls_overlap_fetch(tls_ctx* ctx, int64_t* offsets, int64_t* layer_sizes, int64_t* indices, int64_t* colors);
 int32_t tls_graph_release(tls_ctx* ctx);
 
+/* ---- setup kernel K12b: Galerkin assembly (src/coarse.py:158-168): for each plan entry p =
+ * (s, j) = plan_sj[2p..2p+1] and rows [plan_off[p], plan_off[p+1]) of rows / grp (HOST arrays):
+ * A0[cstart[j] + a, cstart[s] + b] = sum_r Z_j[rows[r], a] W_s[grp[r], b], with Z_j / W_s device
+ * row-major (n x kcnt) blocks at zptr[j] / wptr[s] (HOST pointer tables); A0 device n_C x n_C. */
+int32_t tls_galerkin_assemble(const int32_t* plan_sj, const int64_t* plan_off, int64_t nplan, const int64_t* zptr,
+                              const int64_t* wptr, const int32_t* kcnt, const int64_t* cstart, int32_t nsub,
+                              const int64_t* rows, const int64_t* grp, int64_t nrows, double* A0, int64_t nC,
+                              void* stream);
+
+/* ---- setup kernel K9b: banded LU with partial pivoting (src/subdomain.py:83-89) of `count` blocks
+ * (ap: count x ld x ld row-major, device, in place; ld = 64 nbk) in LAPACK's getrf format: packed
+ * unit-lower L and U, piv (device, count x ld, 1-based, interchanges applied across the whole row
+ * width), info (device, count: first zero pivot, 1-based, or 0).  lreach[J] / ureach[J] (HOST,
+ * multiples of 64): rows / columns the band can touch in panel J. */
+int32_t tls_band_lu(double* ap, int64_t ld, int32_t count, const int32_t* lreach, const int32_t* ureach, int32_t nbk,
+                    int32_t* piv, int32_t* info, void* stream);
+
 /* ---- setup kernel K10: X <- (L L^T)^{-1} X for `count` banded Cholesky factors (L: count x ld x ld
  * row-major, lower, factor order, ld = 64 nb; dinv: count x nb x 64 x 64 inverted diagonal tiles;
  * kc: HOST count x nb panel-tile counts; X: count x ld x nrhs row-major, in place) on the FP64

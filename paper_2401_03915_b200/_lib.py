@@ -103,6 +103,8 @@ SIGNATURES = {
     "tls_graph_release": (_I32, [_P]),
     "tls_syevj_batched": (_I32, [_P, _I64, _I32, _P, _P, _P]),
     "tls_band_solve_multi": (_I32, [_P, _I64, _I32, _P, _P, _I32, _P, _I64, _P]),
+    "tls_band_lu": (_I32, [_P, _I64, _I32, _P, _P, _I32, _P, _P, _P]),
+    "tls_galerkin_assemble": (_I32, [_P, _P, _I64, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _I64, _P]),
     "tls_rank_filter_pivots": (_I32, [_P, _P, _P, _P, _I32, _P, _P, _P]),
 }
 

@@ -1463,6 +1463,78 @@ int32_t tls_set_coarse_layout(tls_ctx* ctx, int32_t nranks, const int64_t* col_s
   return TLS_OK;
 }
 
+// K12b: Galerkin blocks of A0 = Z^T (A Z) from the per-subdomain Z_j and W_s = A_ii[:, :n_int] Z_s
+int32_t tls_galerkin_assemble(const int32_t* plan_sj, const int64_t* plan_off, int64_t nplan, const int64_t* zptr,
+                              const int64_t* wptr, const int32_t* kcnt, const int64_t* cstart, int32_t nsub,
+                              const int64_t* rows, const int64_t* grp, int64_t nrows, double* A0, int64_t nC,
+                              void* stream) {
+  if (!plan_sj || !plan_off || nplan <= 0 || !zptr || !wptr || !kcnt || !cstart || !rows || !grp || !A0)
+    return TLS_ERR_ARG;
+  for (int s = 0; s < nsub; ++s)
+    if (kcnt[s] < 0 || kcnt[s] > 64) return TLS_ERR_ARG;
+  std::vector<GalPlan> plan(nplan);
+  for (int64_t p = 0; p < nplan; ++p) {
+    plan[p] = GalPlan{plan_sj[2 * p], plan_sj[2 * p + 1], plan_off[p], plan_off[p + 1]};
+    if (plan[p].s < 0 || plan[p].s >= nsub || plan[p].j < 0 || plan[p].j >= nsub || plan[p].o0 < 0 ||
+        plan[p].o1 > nrows || plan[p].o1 < plan[p].o0)
+      return TLS_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  GalPlan* d_plan = nullptr;
+  long long *d_z = nullptr, *d_w = nullptr, *d_c = nullptr, *d_rows = nullptr, *d_grp = nullptr;
+  int* d_k = nullptr;
+  if (cudaMallocAsync((void**)&d_plan, sizeof(GalPlan) * nplan, s) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_z, sizeof(long long) * nsub, s) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_w, sizeof(long long) * nsub, s) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_c, sizeof(long long) * (nsub + 1), s) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_k, sizeof(int) * nsub, s) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_rows, sizeof(long long) * std::max<int64_t>(1, nrows), s) != cudaSuccess ||
+      cudaMallocAsync((void**)&d_grp, sizeof(long long) * std::max<int64_t>(1, nrows), s) != cudaSuccess)
+    return TLS_ERR_OOM;
+  cudaMemcpyAsync(d_plan, plan.data(), sizeof(GalPlan) * nplan, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_z, zptr, sizeof(long long) * nsub, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_w, wptr, sizeof(long long) * nsub, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_c, cstart, sizeof(long long) * (nsub + 1), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_k, kcnt, sizeof(int) * nsub, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_rows, rows, sizeof(long long) * nrows, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_grp, grp, sizeof(long long) * nrows, cudaMemcpyHostToDevice, s);
+  for (int64_t p0 = 0; p0 < nplan; p0 += 1 << 30) {
+    const int np = (int)std::min<int64_t>(nplan - p0, 1 << 30);
+    launch_k(nullptr, k_galerkin_blocks, np, 256, 0, s, (const GalPlan*)(d_plan + p0), (const long long*)d_z,
+             (const long long*)d_w, (const int*)d_k, (const long long*)d_c, (const long long*)d_rows,
+             (const long long*)d_grp, A0, (long long)nC);
+  }
+  if (cudaGetLastError() != cudaSuccess) return TLS_ERR_CUDA;
+  cudaFreeAsync(d_plan, s); cudaFreeAsync(d_z, s); cudaFreeAsync(d_w, s); cudaFreeAsync(d_c, s);
+  cudaFreeAsync(d_k, s); cudaFreeAsync(d_rows, s); cudaFreeAsync(d_grp, s);
+  return cudaStreamSynchronize(s) == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;  // host arrays
+}
+
+// K9b: banded LU with partial pivoting of a batch, in place, LAPACK format
+int32_t tls_band_lu(double* ap, int64_t ld, int32_t count, const int32_t* lreach, const int32_t* ureach, int32_t nbk,
+                    int32_t* piv, int32_t* info, void* stream) {
+  if (!ap || !lreach || !ureach || !piv || !info || count <= 0 || nbk <= 0 || ld != 64LL * nbk) return TLS_ERR_ARG;
+  for (int J = 0; J < nbk; ++J)
+    if (lreach[J] < 64 * (J + 1) || lreach[J] > ld || ureach[J] < 64 * (J + 1) || ureach[J] > ld ||
+        lreach[J] % 64 || ureach[J] % 64)
+      return TLS_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem = sizeof(double) * 3 * 64 * CP;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TLS_ERR_CUDA;
+  if (raise_smem(dev, (const void*)k_band_lu, smem) != cudaSuccess) return TLS_ERR_CUDA;
+  int* d_r = nullptr;
+  if (cudaMallocAsync((void**)&d_r, sizeof(int) * 2 * nbk, s) != cudaSuccess) return TLS_ERR_OOM;
+  if (cudaMemcpyAsync(d_r, lreach, sizeof(int) * nbk, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(d_r + nbk, ureach, sizeof(int) * nbk, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return TLS_ERR_CUDA;
+  launch_k(nullptr, k_band_lu, count, 256, smem, s, ap, (long long)ld, (const int*)d_r, (const int*)(d_r + nbk),
+           (int)nbk, piv, info);
+  if (cudaGetLastError() != cudaSuccess) return TLS_ERR_CUDA;
+  cudaFreeAsync(d_r, s);
+  return cudaStreamSynchronize(s) == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;  // host reach arrays
+}
+
 // K10: X <- (L L^T)^{-1} X for a batch of band Cholesky factors, many right-hand sides (DMMA)
 int32_t tls_band_solve_multi(const double* L, int64_t ld, int32_t count, const double* dinv, const int32_t* kc,
                              int32_t nb, double* X, int64_t nrhs, void* stream) {

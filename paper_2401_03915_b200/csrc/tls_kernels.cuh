@@ -2001,4 +2001,195 @@ __global__ void __launch_bounds__(256) k_pivoted_qr(double* __restrict__ Wall, c
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K9b  Banded LU with partial pivoting of a batch of general blocks (setup; the getrf of
+//      src/subdomain.py:83-89 on the block in its factor order), one CTA per block, in place in
+//      LAPACK's format (unit-lower L and U packed, piv 1-based, rows interchanged across the whole
+//      width).  Per 64-column panel J: an unblocked panel factorisation over rows [j0, lreach[J])
+//      (pivot = first largest |a|, as idamax), then U_J = L_JJ^{-1} A[J, right] and the trailing
+//      band update A[below, right] -= L_below U_J with the tile products on the FP64 tensor cores.
+//      lreach[J] / ureach[J] bound the rows / columns the band can touch (partial pivoting keeps
+//      L within the lower bandwidth and U within lower + upper).  info = first zero pivot (1-based).
+//      Dynamic smem: 3 padded 64 x 65 tiles.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1) k_band_lu(double* __restrict__ AP, long long ld,
+                                                    const int* __restrict__ lreach, const int* __restrict__ ureach,
+                                                    int nbk, int* __restrict__ pivots, int* __restrict__ info) {
+  PDL_ENTRY();
+  extern __shared__ __align__(16) double ls[];
+  double* Ls = ls;                 // L_JJ^{-1} (unit lower)
+  double* Ta = Ls + 64 * CP;
+  double* Tb = Ta + 64 * CP;
+  __shared__ double rv[8];
+  __shared__ int ri[8];
+  __shared__ int prow, bad;
+  double* A = AP + (long long)blockIdx.x * ld * ld;
+  int* piv = pivots + (long long)blockIdx.x * ld;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, gr = lane >> 2, gc = lane & 3;
+  if (tid == 0) bad = 0;
+  for (int J = 0; J < nbk; ++J) {
+    const long long j0 = 64LL * J;
+    const long long r1 = lreach[J], c1 = ureach[J];
+    // ---- unblocked panel factorisation with partial pivoting
+    for (int k = 0; k < 64; ++k) {
+      const long long jc = j0 + k;
+      double best = -1.0;
+      int bi = (int)jc;
+      for (long long i = jc + tid; i < r1; i += 256) {
+        const double v = fabs(A[i * ld + jc]);
+        if (v > best) { best = v; bi = (int)i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_down_sync(FULL, best, o);
+        const int oi = __shfl_down_sync(FULL, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) { rv[w] = best; ri[w] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        double b = rv[0];
+        int q = ri[0];
+        for (int ww = 1; ww < 8; ++ww)
+          if (rv[ww] > b || (rv[ww] == b && ri[ww] < q)) { b = rv[ww]; q = ri[ww]; }
+        prow = q;
+        piv[jc] = q + 1;
+        if (b == 0.0 && bad == 0) bad = (int)jc + 1;
+      }
+      __syncthreads();
+      const long long p = prow;
+      if (p != jc)
+        for (long long c = tid; c < c1; c += 256) {
+          const double t = A[jc * ld + c];
+          A[jc * ld + c] = A[p * ld + c];
+          A[p * ld + c] = t;
+        }
+      __syncthreads();
+      const double d = A[jc * ld + jc];
+      if (d != 0.0)
+        for (long long i = jc + 1 + tid; i < r1; i += 256) A[i * ld + jc] /= d;
+      __syncthreads();
+      const int nc = 63 - k;
+      const long long nr = r1 - jc - 1;
+      for (long long e = tid; e < nr * nc; e += 256) {
+        const long long i = jc + 1 + e / nc, c = jc + 1 + e % nc;
+        A[i * ld + c] -= A[i * ld + jc] * A[jc * ld + c];
+      }
+      __syncthreads();
+    }
+    if (c1 <= j0 + 64) continue;
+    // ---- L_JJ^{-1} (unit lower), one column per thread
+    if (tid < 64) {
+      const int j = tid;
+      for (int i = 0; i < 64; ++i) Ls[i * CP + j] = i == j ? 1.0 : 0.0;
+      for (int i = j + 1; i < 64; ++i) {
+        double acc = 0.0;
+        for (int q = j; q < i; ++q) acc += A[(j0 + i) * ld + j0 + q] * Ls[q * CP + j];
+        Ls[i * CP + j] = -acc;
+      }
+    }
+    __syncthreads();
+    // ---- U row block: U_J,t = L_JJ^{-1} A[J, t] for the column tiles right of the diagonal
+    const int nt = (int)((c1 - j0 - 64 + 63) / 64);
+    for (int t = 0; t < nt; ++t) {
+      double* G = A + j0 * ld + j0 + 64 + 64LL * t;
+      for (int e = tid; e < 64 * 64; e += 256) {   // Ta[n][k] = G[k][n]
+        const int kk = e >> 6, n = e & 63;
+        Ta[n * CP + kk] = G[(long long)kk * ld + n];
+      }
+      __syncthreads();
+      double acc[8][2];
+      tile_xyt(Ls, Ta, acc);
+      __syncthreads();
+#pragma unroll
+      for (int bj = 0; bj < 8; ++bj) {
+        G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc] = acc[bj][0];
+        G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc + 1] = acc[bj][1];
+      }
+      __syncthreads();
+    }
+    // ---- trailing band update: A[ti, tj] -= L[ti, J] U[J, tj]
+    const int mt = (int)((r1 - j0 - 64 + 63) / 64);
+    for (int ti = 0; ti < mt; ++ti) {
+      load_tile(Ta, A + (j0 + 64 + 64LL * ti) * ld + j0, ld);   // L tile (rows m, cols k)
+      for (int tj = 0; tj < nt; ++tj) {
+        const double* U = A + j0 * ld + j0 + 64 + 64LL * tj;
+        for (int e = tid; e < 64 * 64; e += 256) {               // Tb[n][k] = U[k][n]
+          const int kk = e >> 6, n = e & 63;
+          Tb[n * CP + kk] = U[(long long)kk * ld + n];
+        }
+        __syncthreads();
+        double acc[8][2];
+        tile_xyt(Ta, Tb, acc);
+        double* G = A + (j0 + 64 + 64LL * ti) * ld + j0 + 64 + 64LL * tj;
+#pragma unroll
+        for (int bj = 0; bj < 8; ++bj) {
+          G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc] -= acc[bj][0];
+          G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc + 1] -= acc[bj][1];
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) info[blockIdx.x] = bad;
+}
+
+// ---------------------------------------------------------------------------------------
+// K12b  Galerkin assembly A0 = Z^T (A Z) (setup; src/coarse.py:158-168 forms it as a sparse
+//       triple product).  Column block s of A Z is W_s = A_ii[:, :n_int] Z_s on the local rows of
+//       subdomain s; its rows owned by subdomain j contract with Z_j.  One CTA per (s, j) pair of
+//       the plan (rows[o0:o1] = interior positions in j, grp[o0:o1] = local rows of s), 32-row
+//       chunks staged in shared memory, thread (a, b) accumulates A0[cstart_j + a, cstart_s + b]
+//       in a fixed order (deterministic); every block of A0 has exactly one writer.
+// ---------------------------------------------------------------------------------------
+struct GalPlan { int s, j; long long o0, o1; };
+
+__global__ void __launch_bounds__(256) k_galerkin_blocks(const GalPlan* __restrict__ plan,
+                                                         const long long* __restrict__ zptr,
+                                                         const long long* __restrict__ wptr,
+                                                         const int* __restrict__ kcnt,
+                                                         const long long* __restrict__ cstart,
+                                                         const long long* __restrict__ rows,
+                                                         const long long* __restrict__ grp,
+                                                         double* __restrict__ A0, long long nC) {
+  PDL_ENTRY();
+  __shared__ double zs[32][64];
+  __shared__ double ws[32][64];
+  const GalPlan pl = plan[blockIdx.x];
+  const int kj = kcnt[pl.j], ks = kcnt[pl.s];
+  const double* Z = reinterpret_cast<const double*>(zptr[pl.j]);
+  const double* W = reinterpret_cast<const double*>(wptr[pl.s]);
+  const int tid = threadIdx.x;
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (long long r0 = pl.o0; r0 < pl.o1; r0 += 32) {
+    const int nr = (int)min(32LL, pl.o1 - r0);
+    for (int e = tid; e < 32 * 64; e += 256) {
+      const int r = e >> 6, c = e & 63;
+      zs[r][c] = (r < nr && c < kj) ? Z[rows[r0 + r] * kj + c] : 0.0;
+      ws[r][c] = (r < nr && c < ks) ? W[grp[r0 + r] * ks + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int o = tid + 256 * q;
+      const int a = o >> 6, b = o & 63;
+      if (a < kj && b < ks) {
+        double t = acc[q];
+        for (int r = 0; r < nr; ++r) t += zs[r][a] * ws[r][b];
+        acc[q] = t;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int o = tid + 256 * q;
+    const int a = o >> 6, b = o & 63;
+    if (a < kj && b < ks) A0[(cstart[pl.j] + a) * nC + cstart[pl.s] + b] = acc[q];
+  }
+}
+
 }  // namespace tls

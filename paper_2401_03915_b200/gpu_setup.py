@@ -862,6 +862,41 @@ def _lex_perm(torch, A, perms, n_list, ld):
     return AP, P, perms
 
 
+def _bandwidths(torch, AP):
+    """(lower, upper) bandwidth of a batch of dense blocks (max over the batch)."""
+    cnt, ld, _ = AP.shape
+    ar = torch.arange(ld, device=AP.device)
+    lo, up = 0, 0
+    for b0 in range(0, cnt, 16):  # bounded temporaries
+        nz = AP[b0:b0 + 16] != 0
+        has = nz.any(dim=2)
+        first = torch.argmax(nz.to(torch.int8), dim=2)
+        last = ld - 1 - torch.argmax(torch.flip(nz, dims=[2]).to(torch.int8), dim=2)
+        lo = max(lo, int(torch.where(has, ar[None, :] - first, 0).max()))
+        up = max(up, int(torch.where(has, last - ar[None, :], 0).max()))
+    return lo, up
+
+
+def band_lu_kernel(torch, AP):
+    """K9b (libtls_b200 ``tls_band_lu``): in-place banded LU with partial pivoting of the batch AP
+    (cnt, ld, ld); returns (LU, piv, info) in torch.linalg.lu_factor_ex's (LAPACK getrf) format."""
+    cnt, ld, _ = AP.shape
+    nbk = ld // 64
+    kl, ku = _bandwidths(torch, AP)
+    J = np.arange(nbk, dtype=np.int64)
+    up64 = lambda x: -(-x // 64) * 64  # noqa: E731
+    lreach = np.minimum(ld, up64(64 * (J + 1) + kl)).astype(np.int32)
+    ureach = np.minimum(ld, up64(64 * (J + 1) + kl + ku)).astype(np.int32)
+    piv = torch.empty((cnt, ld), dtype=torch.int32, device=AP.device)
+    info = torch.empty(cnt, dtype=torch.int32, device=AP.device)
+    AP = AP.contiguous()
+    rc = _lib.load().tls_band_lu(_lib.ptr(AP), ld, cnt, _lib.ptr(lreach), _lib.ptr(ureach), nbk, _lib.ptr(piv),
+                                 _lib.ptr(info), stream_ptr())
+    if rc != 0:
+        raise RuntimeError(f"tls_band_lu failed ({rc})")
+    return AP, piv, info
+
+
 def _band_lu_factor(torch, A, perm_list, n_list, ld):
     """Banded LU (partial pivoting) of a batch in lexicographic factor order.
 
@@ -873,7 +908,10 @@ def _band_lu_factor(torch, A, perm_list, n_list, ld):
     dev = A.device
     nbk = ld // 64
     AP, P, perms = _lex_perm(torch, A, perm_list, n_list, ld)
-    LU, piv, info = torch.linalg.lu_factor_ex(AP)
+    if AP.is_cuda and os.environ.get("TLS_BAND_LU_KERNEL", "1") != "0":
+        LU, piv, info = band_lu_kernel(torch, AP)
+    else:
+        LU, piv, info = torch.linalg.lu_factor_ex(AP)
     del AP
     LU = LU.contiguous()
     nzm = LU != 0
@@ -1045,6 +1083,29 @@ def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
             plan.append((s, j, off, off + grp.size))
             off += grp.size
     if not plan:
+        return A0
+    if device.type == "cuda" and max(counts) <= 64:
+        # K12b: one CTA per (s, j) block (tls_galerkin_assemble) instead of one small GEMM per pair
+        zs = {j: z_blocks[j].contiguous() for j in {p[1] for p in plan}}
+        ws = {s: w_blocks[s].contiguous() for s in {p[0] for p in plan}}
+        N = len(maps)
+        zptr = np.zeros(N, dtype=np.int64)
+        wptr = np.zeros(N, dtype=np.int64)
+        for j, t in zs.items():
+            zptr[j] = t.data_ptr()
+        for s, t in ws.items():
+            wptr[s] = t.data_ptr()
+        sj = np.array([(p[0], p[1]) for p in plan], dtype=np.int32).reshape(-1)
+        poff = np.array([p[2] for p in plan] + [plan[-1][3]], dtype=np.int64)
+        rows = np.concatenate(rows_cat).astype(np.int64)
+        grp = np.concatenate(grp_cat).astype(np.int64)
+        kc32 = np.asarray(counts, dtype=np.int32)
+        cs64 = cstart.astype(np.int64)
+        rc = _lib.load().tls_galerkin_assemble(_lib.ptr(sj), _lib.ptr(poff), len(plan), _lib.ptr(zptr),
+                                               _lib.ptr(wptr), _lib.ptr(kc32), _lib.ptr(cs64), N, _lib.ptr(rows),
+                                               _lib.ptr(grp), rows.size, _lib.ptr(A0), nC, stream_ptr())
+        if rc != 0:
+            raise RuntimeError(f"tls_galerkin_assemble failed ({rc})")
         return A0
     rows_d = torch.as_tensor(np.concatenate(rows_cat), device=device)
     grp_d = torch.as_tensor(np.concatenate(grp_cat), device=device)
