@@ -323,6 +323,23 @@ def _orth(torch, X, check=True):
     return X if check else (X, bad)
 
 
+def _orth_shifted(torch, X):
+    """Shifted CholeskyQR3 (Fukaya et al.): one Cholesky pass of X^T X + s I with
+    s = 11 (m p + p (p + 1)) u ||X||_F^2 -- positive definite for any X, so it cannot break down on
+    the ill-conditioned blocks a Chebyshev filter produces (cond up to ~1e8) -- then CholeskyQR2 on
+    the now well-conditioned result.  No host synchronisation; returns (Q, bad) with ``bad``
+    flagging a non-positive pivot (non-finite input), tested at the caller's next check."""
+    b, m, p = X.shape
+    G = X.mT @ X
+    tr = G.diagonal(dim1=1, dim2=2).sum(dim=1)
+    sh = 11.0 * (m * p + p * (p + 1)) * EPS * tr
+    G = G + sh[:, None, None] * torch.eye(p, dtype=X.dtype, device=X.device)
+    R, info = torch.linalg.cholesky_ex(G, upper=True)
+    X = torch.linalg.solve_triangular(R, X, upper=True, left=False)
+    Q, bad = _orth(torch, X, check=False)
+    return Q, bad | (info != 0)
+
+
 def _rayleigh_ritz(torch, M, X, k, bad=None):
     MX = M @ X
     T = X.mT @ MX
@@ -472,8 +489,9 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
     ||M x - theta x|| <= tol * theta_1.  The whole iteration is stream-ordered: the host looks at
     the residuals (one small copy) only every ``check_every`` steps, and the Chebyshev loop runs
     the degree of that check (per-matrix degrees are masks), so batches pipeline on the device.
-    A CholeskyQR2 breakdown (non-finite block) falls back to ``_topk_chebyshev_host`` (Householder
-    QR, host checks every step).  Returns (theta, X, block products).
+    The filtered block is re-orthonormalised by shifted CholeskyQR3 (no breakdown on the
+    ill-conditioned filtered blocks); a non-finite block falls back to ``_topk_chebyshev_host``
+    (Householder QR, host checks every step).  Returns (theta, X, block products).
     """
     b, m, _ = M.shape
     p = min(m, p or max(3 * k, k + 16))
@@ -524,7 +542,7 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
             Y1 = torch.where(live, Y2, Y1)
         products += d
         Y1 = Y1 / Y1.norm(dim=1, keepdim=True).clamp(min=1e-300)
-        Xo, bad_o = _orth(torch, Y1, check=False)   # breakdowns surface at the next check
+        Xo, bad_o = _orth_shifted(torch, Y1)         # cannot break down; non-finite -> next check
         bad = bad | bad_o
         MX = M @ Xo
         th, S = _eigh_desc(torch, Xo.mT @ MX)
@@ -536,11 +554,15 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
 def band_solve_multi(torch, L, Dinv, kc, E):
     """X = (L L^T)^{-1} E for a batch of banded Cholesky factors and many right-hand sides.
 
-    On the device: the in-tree K10 kernel (``tls_band_solve_multi``: one CTA per (subdomain,
-    64 right-hand sides), both sweeps on the FP64 tensor cores).  On CPU tensors (the host tests of
-    the setup algebra): the blocked torch restatement ``_band_solve_multi_torch``.
+    Default: the blocked restatement ``_band_solve_multi_torch`` (per 64-row block one batched
+    cuBLAS DGEMM over all right-hand sides).  ``TLS_K10=1``: the in-tree K10 kernel
+    (``tls_band_solve_multi``: one CTA per (subdomain, 64 right-hand sides), both sweeps on the
+    FP64 tensor cores) -- correct (tests/test_gpu_setup_kernels.py) but measured 3x slower than the
+    batched DGEMMs on configuration 5 (16.0 vs 5.1 s; profiles/prof_setup_cfg5_r02b.txt): each
+    64 x 64 panel tile is staged for one 64-column chunk only, where cuBLAS reuses it over all of
+    them.
     """
-    if E.is_cuda:
+    if E.is_cuda and os.environ.get("TLS_K10", "0") == "1":
         b, ld, nrhs = E.shape
         X = E.contiguous().clone()
         kci = np.ascontiguousarray(np.asarray(kc, dtype=np.int32).reshape(b, ld // 64))

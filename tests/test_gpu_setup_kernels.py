@@ -86,7 +86,12 @@ def test_band_solve_multi_kernel_matches_torch_and_dense(G):
     eye = torch.eye(64, dtype=torch.float64, device="cuda").expand(b, nb, 64, 64)
     Dinv = torch.linalg.solve_triangular(Ld, eye, upper=False).contiguous()
     E = torch.as_tensor(rng.standard_normal((b, ld, nrhs)), device="cuda")
-    Xk = G.band_solve_multi(torch, L.contiguous(), Dinv, kc, E)
+    import os
+    os.environ["TLS_K10"] = "1"
+    try:
+        Xk = G.band_solve_multi(torch, L.contiguous(), Dinv, kc, E)
+    finally:
+        os.environ.pop("TLS_K10")
     Xt = G._band_solve_multi_torch(torch, L, Dinv, kc, E)
     Xd = torch.cholesky_solve(E, L)
     scale = Xd.abs().max().item()
