@@ -489,9 +489,11 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
     ||M x - theta x|| <= tol * theta_1.  The whole iteration is stream-ordered: the host looks at
     the residuals (one small copy) only every ``check_every`` steps, and the Chebyshev loop runs
     the degree of that check (per-matrix degrees are masks), so batches pipeline on the device.
-    The filtered block is re-orthonormalised by shifted CholeskyQR3 (no breakdown on the
-    ill-conditioned filtered blocks); a non-finite block falls back to ``_topk_chebyshev_host``
-    (Householder QR, host checks every step).  Returns (theta, X, block products).
+    The filtered block (cond up to ~rmax) is re-orthonormalised by batched Householder QR, which
+    cannot break down (CholeskyQR2, shifted or not, broke down on ~30% of the configuration-5
+    batches and forced the host path; ``TLS_CHEB_ORTH=scqr3`` keeps the shifted variant); a
+    non-finite block still falls back to ``_topk_chebyshev_host``.  Returns (theta, X, block
+    products).
     """
     b, m, _ = M.shape
     p = min(m, p or max(3 * k, k + 16))
@@ -542,8 +544,11 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
             Y1 = torch.where(live, Y2, Y1)
         products += d
         Y1 = Y1 / Y1.norm(dim=1, keepdim=True).clamp(min=1e-300)
-        Xo, bad_o = _orth_shifted(torch, Y1)         # cannot break down; non-finite -> next check
-        bad = bad | bad_o
+        if os.environ.get("TLS_CHEB_ORTH", "qr") == "qr":
+            Xo = torch.linalg.qr(Y1).Q                # Householder: no breakdown, no host sync
+        else:
+            Xo, bad_o = _orth_shifted(torch, Y1)     # non-finite -> host path at the next check
+            bad = bad | bad_o
         MX = M @ Xo
         th, S = _eigh_desc(torch, Xo.mT @ MX)
         X, MX = Xo @ S, MX @ S
