@@ -306,6 +306,55 @@ def _subdomain_columns(torch, kind, A, Bring, n, ni, nin, tau, n_modes):
     return V.contiguous(), _cut_gap(sv, keep)
 
 
+def _svd_columns_lu_batch(torch, A, LU, piv, P, n_loc, n_int, n_bnd, first, cnt, ld, tau, n_modes):
+    """Top-k SVD coarse columns (src/spectral.py:135-154, fixed k) of a batch of LU-factored
+    subdomains, batched by shape: B[:, ring] by one batched lu_solve, E = F B22^{-1} (= ext[:n_int],
+    block-inverse identity) by one batched solve, then the top k+1 right singular vectors from the
+    Gram matrix E^T E (n_b x n_b) on the device (topk_chebyshev / dense eigh) and U = E V / sigma --
+    instead of one thin SVD per subdomain.  Returns {b: (Z (n_int x k), cut gap)}."""
+    dev = A.device
+    out = {}
+    groups = {}
+    for b in range(cnt):
+        s = first + b
+        groups.setdefault((int(n_loc[s]), int(n_int[s]), int(n_loc[s] - n_bnd[s])), []).append(b)
+    for (n, ni, nin), bs in groups.items():
+        nb = n - nin
+        if nb == 0:
+            for b in bs:
+                out[b] = (torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf"))
+            continue
+        g = len(bs)
+        bi = torch.as_tensor(bs, device=dev)
+        Pg = P.index_select(0, bi)
+        pinv = torch.empty_like(Pg)
+        pinv.scatter_(1, Pg, torch.arange(ld, device=dev).expand_as(Pg))
+        E = torch.zeros((g, ld, nb), dtype=torch.float64, device=dev)
+        E.view(g, -1)[torch.arange(g, device=dev)[:, None],
+                      pinv[:, nin:n] * nb + torch.arange(nb, device=dev)[None, :]] = 1.0
+        X = torch.linalg.lu_solve(LU.index_select(0, bi), piv.index_select(0, bi), E)
+        del E
+        Bring = torch.gather(X, 1, pinv[:, :n, None].expand(g, n, nb))
+        del X
+        Eint = torch.linalg.solve(Bring[:, nin:n], Bring[:, :ni], left=False)   # (g, ni, nb)
+        del Bring
+        kk = min(n_modes + 1, nb)
+        Gm = Eint.mT @ Eint
+        Gm = 0.5 * (Gm + Gm.mT)
+        th, V, _ = topk_chebyshev(torch, Gm, kk)
+        sig = torch.sqrt(torch.clamp(th, min=0.0))
+        U = (Eint @ V) / torch.where(sig > 0, sig, 1.0)[:, None, :]
+        sig_h = sig.cpu().numpy()
+        for j, b in enumerate(bs):
+            keep = _select(sig_h[j], tau, n_modes)
+            if keep.size == 0:
+                out[b] = (torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf"))
+                continue
+            Z = _fix_signs(torch, U[j][:, torch.as_tensor(keep, device=dev)])
+            out[b] = (Z.contiguous(), _cut_gap(sig_h[j], keep))
+    return out
+
+
 def _orth(torch, X, check=True):
     """Batched orthonormalisation: CholeskyQR2 (two GEMM + p x p Cholesky passes).
 
@@ -1294,7 +1343,20 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                                                          _lib.ptr(pout_c), _lib.ptr(lc_c), _lib.ptr(uc_c), s_ptr))
                 torch.cuda.current_stream().synchronize()
                 del Ldinv, Udinv
-                if want_coarse:
+                if want_coarse and coarse == "svd" and n_modes is not None and nu is None and \
+                        os.environ.get("TLS_SVD_GRAM", "1") != "0":
+                    for b, (Z, gap) in _svd_columns_lu_batch(torch, A, LU, piv, P, n_loc, n_int, n_bnd, first, cnt,
+                                                             ld, tau, n_modes).items():
+                        s = first + b
+                        n, ni = int(n_loc[s]), int(n_int[s])
+                        gaps[s] = gap
+                        if Z.shape[1]:
+                            nz = torch.any(Z != 0, dim=0)
+                            if not bool(nz.all()):
+                                Z = Z[:, nz].contiguous()
+                        z_dev[s] = Z
+                        w_dev[s] = A[b, :n, :ni] @ Z if Z.shape[1] else None
+                elif want_coarse:
                     for b in range(cnt):
                         s = first + b
                         n, ni = int(n_loc[s]), int(n_int[s])
