@@ -1397,24 +1397,54 @@ __global__ void __launch_bounds__(256, 1) k_band_chol(double* __restrict__ AP, l
     const long long j0 = 64LL * J;
     load_tile(Ds, A + j0 * ld + j0, ld);
     __syncthreads();
-    // 64 x 64 Cholesky in shared memory (right-looking, lower triangle only)
-    for (int k = 0; k < 64; ++k) {
-      if (tid == 0) {
-        double d = Ds[k * CP + k];
-        if (!(d > 0.0)) {
-          if (bad == 0) bad = (int)(j0 + k + 1);
-          d = 1.0;  // keep going without NaNs; the caller raises on info
+    // 64 x 64 Cholesky in shared memory, blocked by 8 columns (right-looking, lower triangle):
+    // the 8 x 8 diagonal block by warp 0 (lane = row, warp-synchronous), the 8-column panel below
+    // it by one thread per row, the trailing triangle by all threads -- 3 block barriers per 8
+    // columns instead of 3 per column
+    for (int c0 = 0; c0 < 64; c0 += 8) {
+      if (w == 0) {
+        for (int k = 0; k < 8; ++k) {
+          const int kk = c0 + k;
+          if (lane == 0) {
+            double d = Ds[kk * CP + kk];
+            if (!(d > 0.0)) {
+              if (bad == 0) bad = (int)(j0 + kk + 1);
+              d = 1.0;  // keep going without NaNs; the caller raises on info
+            }
+            Ds[kk * CP + kk] = sqrt(d);
+          }
+          __syncwarp();
+          const double piv = Ds[kk * CP + kk];
+          if (lane > k && lane < 8) Ds[(c0 + lane) * CP + kk] /= piv;
+          __syncwarp();
+          if (lane > k && lane < 8) {
+            const double lik = Ds[(c0 + lane) * CP + kk];
+            for (int j = k + 1; j <= lane; ++j) Ds[(c0 + lane) * CP + c0 + j] -= lik * Ds[(c0 + j) * CP + kk];
+          }
+          __syncwarp();
         }
-        Ds[k * CP + k] = sqrt(d);
       }
       __syncthreads();
-      const double piv = Ds[k * CP + k];
-      for (int i = k + 1 + tid; i < 64; i += blockDim.x) Ds[i * CP + k] /= piv;
+      // panel rows below the diagonal block: L[r, c0:c0+8] = A[r, c0:c0+8] L11^{-T}
+      for (int r = c0 + 8 + tid; r < 64; r += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          double v = Ds[r * CP + c0 + k];
+          for (int q = 0; q < k; ++q) v -= Ds[r * CP + c0 + q] * Ds[(c0 + k) * CP + c0 + q];
+          Ds[r * CP + c0 + k] = v / Ds[(c0 + k) * CP + c0 + k];
+        }
+      }
       __syncthreads();
-      const int m = 63 - k;
+      // trailing triangle: A[i][j] -= sum_q L[i][c0+q] L[j][c0+q], c0+8 <= j <= i < 64
+      const int m = 56 - c0;
       for (int e = tid; e < m * m; e += blockDim.x) {
-        const int i = k + 1 + e / m, j = k + 1 + e % m;
-        if (j <= i) Ds[i * CP + j] -= Ds[i * CP + k] * Ds[j * CP + k];
+        const int i = c0 + 8 + e / m, j = c0 + 8 + e % m;
+        if (j <= i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc += Ds[i * CP + c0 + q] * Ds[j * CP + c0 + q];
+          Ds[i * CP + j] -= acc;
+        }
       }
       __syncthreads();
     }
