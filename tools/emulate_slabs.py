@@ -66,16 +66,17 @@ def band_time(n, q):
     return ms.value, algo.value, hi - lo
 
 
-base = None
-for n in Ns:
-    ranks = [0] if n == 1 else sorted({0, n // 2, n - 1})
-    res = {q: band_time(n, q) for q in ranks}
-    tmax = max(v[0] for v in res.values())
-    if n == 1:
-        base = tmax
-    print(json.dumps({"config": cfg.name, "ranks": n, "slab_ranges": [list(r) for r in slab_ranges(n_loc ** 2, n)],
-                      "band_ms": {q: round(v[0], 4) for q, v in res.items()},
-                      "band_GBps": {q: round(v[1] / v[0] / 1e6, 1) for q, v in res.items()},
-                      "subdomains": {q: v[2] for q, v in res.items()},
-                      "band_ms_max": round(tmax, 4),
-                      "band_efficiency": round(base / (n * tmax), 4)}), flush=True)
+if __name__ == "__main__":
+    base = None
+    for n in Ns:
+        ranks = [0] if n == 1 else sorted({0, n // 2, n - 1})
+        res = {q: band_time(n, q) for q in ranks}
+        tmax = max(v[0] for v in res.values())
+        if n == 1:
+            base = tmax
+        print(json.dumps({"config": cfg.name, "ranks": n, "slab_ranges": [list(r) for r in slab_ranges(n_loc ** 2, n)],
+                          "band_ms": {q: round(v[0], 4) for q, v in res.items()},
+                          "band_GBps": {q: round(v[1] / v[0] / 1e6, 1) for q, v in res.items()},
+                          "subdomains": {q: v[2] for q, v in res.items()},
+                          "band_ms_max": round(tmax, 4),
+                          "band_efficiency": round(base / (n * tmax), 4)}), flush=True)
