@@ -580,7 +580,7 @@ def main():
     }
     log("cpu baseline")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(cfg, a, sym, owner, nsub, warmup=0, steps=1)
+        cb = cpu_reference(cfg, a, sym, owner, nsub, warmup=1, steps=2)
         cb.pop("times_s")
         line["cpu_baseline"] = cb
     if rank == 0:
