@@ -2390,15 +2390,44 @@ int32_t tls_band_cholesky(double* ap, int64_t ld, int32_t count, const int32_t* 
   cudaStream_t s = (cudaStream_t)stream;
   for (int J = 0; J < nbk; ++J)
     if (reach[J] < 64 * (J + 1) || reach[J] > ld || reach[J] % 64) return TLS_ERR_ARG;
-  const size_t smem = sizeof(double) * 5 * 64 * CP;
+  const size_t smem = sizeof(double) * 4 * 64 * CP;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return TLS_ERR_CUDA;
-  if (raise_smem(dev, (const void*)k_band_chol, smem) != cudaSuccess) return TLS_ERR_CUDA;
+  // cluster of CL CTAs per subdomain (TLS_K9_CLUSTER: 1, 2 or 4; default 4) -- the trailing-band
+  // tile products of a panel run on CL SMs instead of one
+  int cl = 4;
+  if (const char* e = getenv("TLS_K9_CLUSTER")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4) cl = v;
+  }
   int* d_reach = nullptr;
   if (cudaMallocAsync((void**)&d_reach, sizeof(int) * nbk, s) != cudaSuccess) return TLS_ERR_OOM;
   if (cudaMemcpyAsync(d_reach, reach, sizeof(int) * nbk, cudaMemcpyHostToDevice, s) != cudaSuccess) return TLS_ERR_CUDA;
-  launch_k(nullptr, k_band_chol, count, 256, smem, s, ap, ld, d_reach, nbk, dinv, info);
-  if (cudaGetLastError() != cudaSuccess) return TLS_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(count * cl));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (cl == 4) {
+    if (raise_smem(dev, (const void*)k_band_chol<4>, smem) != cudaSuccess) return TLS_ERR_CUDA;
+    e = cudaLaunchKernelEx(&cfg, k_band_chol<4>, ap, (long long)ld, (const int*)d_reach, (int)nbk, dinv, info);
+  } else if (cl == 2) {
+    if (raise_smem(dev, (const void*)k_band_chol<2>, smem) != cudaSuccess) return TLS_ERR_CUDA;
+    e = cudaLaunchKernelEx(&cfg, k_band_chol<2>, ap, (long long)ld, (const int*)d_reach, (int)nbk, dinv, info);
+  } else {
+    if (raise_smem(dev, (const void*)k_band_chol<1>, smem) != cudaSuccess) return TLS_ERR_CUDA;
+    cfg.numAttrs = 0;
+    e = cudaLaunchKernelEx(&cfg, k_band_chol<1>, ap, (long long)ld, (const int*)d_reach, (int)nbk, dinv, info);
+  }
+  if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) return TLS_ERR_CUDA;
   cudaFreeAsync(d_reach, s);
   // the host array must outlive the async copy
   return cudaStreamSynchronize(s) == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;

@@ -1380,6 +1380,22 @@ __device__ __forceinline__ void load_tile(double* T, const double* G, long long 
   for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) T[(e >> 6) * CP + (e & 63)] = G[(long long)(e >> 6) * ld + (e & 63)];
 }
 
+// CL > 1: a thread-block cluster of CL CTAs per subdomain (blockIdx.x / CL).  Rank 0 factors and
+// inverts the 64 x 64 diagonal block and publishes L_JJ / L_JJ^{-1} through global memory (L2);
+// the panel tiles and the trailing-band tile products -- the bulk of the work, ~mt^2/2 tile
+// products per panel -- are dealt round-robin to the CL CTAs; three cluster barriers per panel
+// (barrier.cluster arrive.release / wait.acquire order the global writes at cluster scope).
+// CL = 1 is the single-CTA kernel.
+template <int CL>
+__device__ __forceinline__ void k9_sync() {
+  if (CL > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+template <int CL>
 __global__ void __launch_bounds__(256, 1) k_band_chol(double* __restrict__ AP, long long ld, const int* __restrict__ reach,
                                                       int nbk, double* __restrict__ dinv, int* __restrict__ info) {
   PDL_ENTRY();
@@ -1388,86 +1404,94 @@ __global__ void __launch_bounds__(256, 1) k_band_chol(double* __restrict__ AP, l
   double* Ls = Ds + 64 * CP;       // L_JJ^{-1}
   double* Ta = Ls + 64 * CP;
   double* Tb = Ta + 64 * CP;
-  double* Tc = Tb + 64 * CP;
   __shared__ int bad;
-  double* A = AP + (long long)blockIdx.x * ld * ld;
+  const int sub = blockIdx.x / CL, crank = blockIdx.x % CL;
+  double* A = AP + (long long)sub * ld * ld;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, gr = lane >> 2, gc = lane & 3;
   if (tid == 0) bad = 0;
   for (int J = 0; J < nbk; ++J) {
     const long long j0 = 64LL * J;
-    load_tile(Ds, A + j0 * ld + j0, ld);
-    __syncthreads();
-    // 64 x 64 Cholesky in shared memory, blocked by 8 columns (right-looking, lower triangle):
-    // the 8 x 8 diagonal block by warp 0 (lane = row, warp-synchronous), the 8-column panel below
-    // it by one thread per row, the trailing triangle by all threads -- 3 block barriers per 8
-    // columns instead of 3 per column
-    for (int c0 = 0; c0 < 64; c0 += 8) {
-      if (w == 0) {
-        for (int k = 0; k < 8; ++k) {
-          const int kk = c0 + k;
-          if (lane == 0) {
-            double d = Ds[kk * CP + kk];
-            if (!(d > 0.0)) {
-              if (bad == 0) bad = (int)(j0 + kk + 1);
-              d = 1.0;  // keep going without NaNs; the caller raises on info
+    double* dv = dinv + ((long long)sub * nbk + J) * 4096;
+    if (crank == 0) {
+      load_tile(Ds, A + j0 * ld + j0, ld);
+      __syncthreads();
+      // 64 x 64 Cholesky in shared memory, blocked by 8 columns (right-looking, lower triangle):
+      // the 8 x 8 diagonal block by warp 0 (lane = row, warp-synchronous), the 8-column panel
+      // below it by one thread per row, the trailing triangle by all threads
+      for (int c0 = 0; c0 < 64; c0 += 8) {
+        if (w == 0) {
+          for (int k = 0; k < 8; ++k) {
+            const int kk = c0 + k;
+            if (lane == 0) {
+              double d = Ds[kk * CP + kk];
+              if (!(d > 0.0)) {
+                if (bad == 0) bad = (int)(j0 + kk + 1);
+                d = 1.0;  // keep going without NaNs; the caller raises on info
+              }
+              Ds[kk * CP + kk] = sqrt(d);
             }
-            Ds[kk * CP + kk] = sqrt(d);
+            __syncwarp();
+            const double piv = Ds[kk * CP + kk];
+            if (lane > k && lane < 8) Ds[(c0 + lane) * CP + kk] /= piv;
+            __syncwarp();
+            if (lane > k && lane < 8) {
+              const double lik = Ds[(c0 + lane) * CP + kk];
+              for (int j = k + 1; j <= lane; ++j) Ds[(c0 + lane) * CP + c0 + j] -= lik * Ds[(c0 + j) * CP + kk];
+            }
+            __syncwarp();
           }
-          __syncwarp();
-          const double piv = Ds[kk * CP + kk];
-          if (lane > k && lane < 8) Ds[(c0 + lane) * CP + kk] /= piv;
-          __syncwarp();
-          if (lane > k && lane < 8) {
-            const double lik = Ds[(c0 + lane) * CP + kk];
-            for (int j = k + 1; j <= lane; ++j) Ds[(c0 + lane) * CP + c0 + j] -= lik * Ds[(c0 + j) * CP + kk];
+        }
+        __syncthreads();
+        for (int r = c0 + 8 + tid; r < 64; r += blockDim.x) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            double v = Ds[r * CP + c0 + k];
+            for (int q = 0; q < k; ++q) v -= Ds[r * CP + c0 + q] * Ds[(c0 + k) * CP + c0 + q];
+            Ds[r * CP + c0 + k] = v / Ds[(c0 + k) * CP + c0 + k];
           }
+        }
+        __syncthreads();
+        const int m = 56 - c0;
+        for (int e = tid; e < m * m; e += blockDim.x) {
+          const int i = c0 + 8 + e / m, j = c0 + 8 + e % m;
+          if (j <= i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += Ds[i * CP + c0 + q] * Ds[j * CP + c0 + q];
+            Ds[i * CP + j] -= acc;
+          }
+        }
+        __syncthreads();
+      }
+      // L_JJ^{-1}: column j by the 4 lanes 4j..4j+3 (forward substitution, each row's dot product
+      // split 4 ways and completed by two xor-shuffles)
+      {
+        const int j = tid >> 2, sl = tid & 3;
+        for (int i = 0; i < 64; ++i) {
+          double part = 0.0;
+          if (i > j)
+            for (int q = j + sl; q < i; q += 4) part += Ds[i * CP + q] * Ls[q * CP + j];
+          part += __shfl_xor_sync(FULL, part, 1);
+          part += __shfl_xor_sync(FULL, part, 2);
+          if (sl == 0) Ls[i * CP + j] = i < j ? 0.0 : (i == j ? 1.0 / Ds[j * CP + j] : -part / Ds[i * CP + i]);
           __syncwarp();
         }
       }
       __syncthreads();
-      // panel rows below the diagonal block: L[r, c0:c0+8] = A[r, c0:c0+8] L11^{-T}
-      for (int r = c0 + 8 + tid; r < 64; r += blockDim.x) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          double v = Ds[r * CP + c0 + k];
-          for (int q = 0; q < k; ++q) v -= Ds[r * CP + c0 + q] * Ds[(c0 + k) * CP + c0 + q];
-          Ds[r * CP + c0 + k] = v / Ds[(c0 + k) * CP + c0 + k];
-        }
-      }
-      __syncthreads();
-      // trailing triangle: A[i][j] -= sum_q L[i][c0+q] L[j][c0+q], c0+8 <= j <= i < 64
-      const int m = 56 - c0;
-      for (int e = tid; e < m * m; e += blockDim.x) {
-        const int i = c0 + 8 + e / m, j = c0 + 8 + e % m;
-        if (j <= i) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) acc += Ds[i * CP + c0 + q] * Ds[j * CP + c0 + q];
-          Ds[i * CP + j] -= acc;
-        }
-      }
-      __syncthreads();
-    }
-    // inverse of the lower-triangular L_JJ, one column per thread (forward substitution)
-    if (tid < 64) {
-      const int j = tid;
-      for (int i = 0; i < j; ++i) Ls[i * CP + j] = 0.0;
-      Ls[j * CP + j] = 1.0 / Ds[j * CP + j];
-      for (int i = j + 1; i < 64; ++i) {
-        double acc = 0.0;
-        for (int q = j; q < i; ++q) acc += Ds[i * CP + q] * Ls[q * CP + j];
-        Ls[i * CP + j] = -acc / Ds[i * CP + i];
+      for (int e = tid; e < 64 * 64; e += blockDim.x) {
+        const int r = e >> 6, c = e & 63;
+        A[(j0 + r) * ld + j0 + c] = Ds[r * CP + c];
+        dv[e] = Ls[r * CP + c];
       }
     }
-    __syncthreads();
-    for (int e = tid; e < 64 * 64; e += blockDim.x) {
-      const int r = e >> 6, c = e & 63;
-      A[(j0 + r) * ld + j0 + c] = Ds[r * CP + c];
-      dinv[((long long)blockIdx.x * nbk + J) * 4096 + e] = Ls[r * CP + c];
+    k9_sync<CL>();  // L_JJ and L_JJ^{-1} published
+    if (crank != 0) {
+      for (int e = tid; e < 64 * 64; e += blockDim.x) Ls[(e >> 6) * CP + (e & 63)] = dv[e];
+      __syncthreads();
     }
     const int mt = (int)((reach[J] - j0 - 64) / 64);
-    // panel: P_t <- P_t L_JJ^{-T}
-    for (int t = 0; t < mt; ++t) {
+    // panel: P_t <- P_t L_JJ^{-T}, tiles dealt round-robin over the cluster
+    for (int t = crank; t < mt; t += CL) {
       double* G = A + (j0 + 64 + 64LL * t) * ld + j0;
       __syncthreads();
       load_tile(Ta, G, ld);
@@ -1480,11 +1504,17 @@ __global__ void __launch_bounds__(256, 1) k_band_chol(double* __restrict__ AP, l
         G[(long long)(8 * w + gr) * ld + 8 * bj + 2 * gc + 1] = acc[bj][1];
       }
     }
-    __syncthreads();
-    // trailing band square: T(ti, tj) -= P_ti P_tj^T, tj <= ti
+    k9_sync<CL>();  // the whole panel is final
+    // trailing band square: T(ti, tj) -= P_ti P_tj^T, tj <= ti, tile products round-robin
+    int q = 0, loaded = -1;
     for (int ti = 0; ti < mt; ++ti) {
-      load_tile(Ta, A + (j0 + 64 + 64LL * ti) * ld + j0, ld);
-      for (int tj = 0; tj <= ti; ++tj) {
+      for (int tj = 0; tj <= ti; ++tj, ++q) {
+        if (q % CL != crank) continue;
+        if (loaded != ti) {
+          __syncthreads();
+          load_tile(Ta, A + (j0 + 64 + 64LL * ti) * ld + j0, ld);
+          loaded = ti;
+        }
         double* G = A + (j0 + 64 + 64LL * ti) * ld + j0 + 64 + 64LL * tj;
         load_tile(Tb, A + (j0 + 64 + 64LL * tj) * ld + j0, ld);
         __syncthreads();
@@ -1498,9 +1528,9 @@ __global__ void __launch_bounds__(256, 1) k_band_chol(double* __restrict__ AP, l
         __syncthreads();
       }
     }
-    __syncthreads();
+    k9_sync<CL>();  // the trailing update is complete before the next diagonal block is read
   }
-  if (tid == 0) info[blockIdx.x] = bad;
+  if (tid == 0 && crank == 0) info[sub] = bad;
 }
 
 // ---------------------------------------------------------------------------------------
