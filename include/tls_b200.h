@@ -233,6 +233,14 @@ int32_t tls_rank_filter_pivots(double* W, const int64_t* woff, const int32_t* nr
  * projected problem. */
 int32_t tls_syevj_batched(const double* T, int64_t batch, int32_t p, double* w, double* V, void* stream);
 
+/* ---- setup helper: batched one-sided Jacobi SVD (one CTA per matrix) for the SVD coarse modes
+ * (src/spectral.py:135-154 calls LAPACK's thin SVD of the harmonic extension E; the setup takes
+ * E = Q R and passes the small R here).  X (batch x [m x n column-major, leading dimension m],
+ * device) is rotated in place to X V with mutually orthogonal columns: column j = sigma_j u_j
+ * (unsorted); sig (batch x n) receives the column norms, info (batch) the sweeps used or -1 when
+ * 40 sweeps did not converge.  Stream-ordered. */
+int32_t tls_svdj_batched(double* X, int64_t batch, int32_t m, int32_t n, double* sig, int32_t* info, void* stream);
+
 /* ---- SetupReport getters (src/precond.py:39-83) */
 int32_t tls_report(const tls_ctx* ctx, int64_t* n, int32_t* n_sub, int32_t* n_coarse,
                    int64_t* tile_bytes);
@@ -286,6 +294,13 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms,
  * tls_kernel_timing returns the mean duration of the launches that did work. */
 int32_t tls_set_kernel_timing(tls_ctx* ctx, int32_t on);
 int32_t tls_kernel_timing(const tls_ctx* ctx, double* avg_ms, int64_t* count);
+
+/* kernel trace (profiling aid): while on, every launch made outside graph capture -- the host-driven
+ * PCG / GMRES loops (selected by a callback) and the apply entry points -- is bracketed by CUDA
+ * events; tls_kernel_trace_dump synchronises, writes "kernel count total_ms" lines (descending
+ * total) into buf (NUL-terminated, truncated to cap) and returns the untruncated length. */
+int32_t tls_set_kernel_trace(tls_ctx* ctx, int32_t on);
+int64_t tls_kernel_trace_dump(tls_ctx* ctx, char* buf, int64_t cap);
 
 /* ---- setup: banded Cholesky of a batch of SPD blocks (factor order, dense ld x ld row-major,
  * ld = 64 nbk) in place on the device, one CTA per block, DMMA tile products; reach[J] (host,

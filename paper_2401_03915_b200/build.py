@@ -33,7 +33,7 @@ def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
     cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-I" + os.path.join(REPO, "include"), "-o", OUT + ".tmp", *SRC]
+           "-I" + os.path.join(REPO, "include"), "-o", OUT + ".tmp", *SRC, "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -6,6 +6,7 @@
 // with a device-side `done` flag turning the remaining kernels into no-ops after convergence,
 // so one host sync happens per 25 PCG iterations / per GMRES cycle instead of per kernel.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cub/device/device_segmented_sort.cuh>
 
@@ -38,6 +39,13 @@ constexpr size_t ring_bytes(int S) { return sizeof(double) * 8 * (size_t)S * 512
 constexpr size_t band_smem_bytes(int nb) { return sizeof(double) * ((size_t)nb * 64 + 8 * 64 + 64); }
 // largest subdomain (rows) whose local vector fits `optin` bytes of shared memory
 static int band_max_rows(size_t optin) { return (int)((optin / sizeof(double) - 8 * 64 - 64) / 64) * 64; }
+
+// NVTX range over a C entry point (visible to Nsight tools; a no-op without an injected tool)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define TLS_RANGE(name) NvtxRange nvtx_range_(name)
 
 template <class T>
 void dfree(T*& p) {
@@ -141,6 +149,10 @@ struct tls_ctx {
   int kt_n_graph[2][2] = {{0, 0}, {0, 0}};  // [pcg|gmres][prec]: pairs in that graph
   double kt_sum_ms = 0.0;
   long long kt_count = 0;
+  // ---- kernel trace (tls_set_kernel_trace): an event pair around EVERY launch of the host-driven
+  // loops (warm caches, the kernels' real inputs, no graph / PDL overlap): per-kernel durations
+  mutable bool ktrace = false;
+  mutable std::vector<std::pair<const void*, std::pair<cudaEvent_t, cudaEvent_t>>> kt_trace;
   // ---- banded Cholesky local operators (local_kind == 1)
   int local_kind = 0;                 // 0: packed inverse tiles, 1: band factors
   size_t restrict_smem = 0;
@@ -187,11 +199,22 @@ static void launch_k(const tls_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, di
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
-  if (ctx && ctx->pdl) {
+  const bool trace = ctx && ctx->ktrace && !ctx->capturing;
+  if (ctx && ctx->pdl && !trace) {
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+  }
+  if (trace) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+    cudaEventRecord(b, s);
+    ctx->kt_trace.push_back({(const void*)kernel, {a, b}});
+    return;
   }
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
@@ -713,6 +736,7 @@ int64_t tls_ctx_device_bytes(const tls_ctx* ctx) { return ctx ? ctx->dev_bytes :
 
 int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_t* indptr,
                           const int32_t* indices, const double* data, int32_t symmetric) {
+  TLS_RANGE("tls_matrix_upload");
   if (!ctx || nrows <= 0 || nrows > INT32_MAX || nnz < 0 || nnz >= INT32_MAX)
     return ctx ? fail(ctx, TLS_ERR_ARG, "matrix size out of the supported int32 range") : TLS_ERR_ARG;
   // host-side bounds check of the CSR structure: every device kernel indexes through indptr and
@@ -795,6 +819,7 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
 }
 
 int32_t tls_spmv(tls_ctx* ctx, const double* x, double* y, void* stream) {
+  TLS_RANGE("tls_spmv");
   if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "no matrix uploaded") : TLS_ERR_ARG;
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
@@ -807,6 +832,7 @@ int32_t tls_spmv(tls_ctx* ctx, const double* x, double* y, void* stream) {
 
 int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t* offsets_g,
                               const int64_t* indices_g, const int32_t* n_interior_g) {
+  TLS_RANGE("tls_subdomains_upload");
   if (!ctx || n_sub_global <= 0) return ctx ? fail(ctx, TLS_ERR_ARG, "n_sub must be positive") : TLS_ERR_ARG;
   if (!ctx->rowptr) return fail(ctx, TLS_ERR_STATE, "upload the matrix first");
   CK(cudaSetDevice(ctx->device));
@@ -942,6 +968,7 @@ int32_t tls_subdomain_max_size(const tls_ctx* ctx) { return ctx ? ctx->max_n : 0
 
 int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first_g, int32_t count, double* out, int64_t ld,
                            void* stream) {
+  TLS_RANGE("tls_extract_blocks");
   if (!ctx) return TLS_ERR_ARG;
   const int first = first_g - ctx->own_lo;
   if (first < 0 || count <= 0 || first + count > ctx->nsub)
@@ -980,6 +1007,7 @@ int32_t tls_extract_blocks(tls_ctx* ctx, int32_t first_g, int32_t count, double*
 
 int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first_g, int32_t count, const double* inv,
                                 int64_t ld, void* stream) {
+  TLS_RANGE("tls_store_local_inverse");
   if (!ctx) return TLS_ERR_ARG;
   const int first = first_g - ctx->own_lo;
   if (first < 0 || count <= 0 || first + count > ctx->nsub)
@@ -997,6 +1025,7 @@ int32_t tls_store_local_inverse(tls_ctx* ctx, int32_t first_g, int32_t count, co
 
 int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, const double* basis,
                           const double* a0inv, void* stream) {
+  TLS_RANGE("tls_coarse_upload");
   if (!ctx || !ctx->nsub) return ctx ? fail(ctx, TLS_ERR_STATE, "upload subdomains first") : TLS_ERR_ARG;
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
@@ -1083,6 +1112,7 @@ static void plan_block(int blk, int nt, int sym, int ur, int& slot, std::vector<
 }
 
 int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
+  TLS_RANGE("tls_precond_finalize");
   if (!ctx || !ctx->nsub) return ctx ? fail(ctx, TLS_ERR_STATE, "upload subdomains first") : TLS_ERR_ARG;
   if (one_level != TLS_ASM && one_level != TLS_RAS) return fail(ctx, TLS_ERR_ARG, "unknown one-level kind");
   if (combine < TLS_NONE || combine > TLS_DEFLATED) return fail(ctx, TLS_ERR_ARG, "unknown combination");
@@ -1329,6 +1359,7 @@ static int need_final(tls_ctx* ctx) {
 }
 
 int32_t tls_precond_apply(tls_ctx* ctx, const double* r, double* z, void* stream) {
+  TLS_RANGE("tls_precond_apply");
   TRY(need_final(ctx));
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
@@ -1340,6 +1371,7 @@ int32_t tls_precond_apply(tls_ctx* ctx, const double* r, double* z, void* stream
 }
 
 int32_t tls_apply_one_level(tls_ctx* ctx, const double* r, double* z, void* stream) {
+  TLS_RANGE("tls_apply_one_level");
   TRY(need_final(ctx));
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
@@ -1353,6 +1385,7 @@ int32_t tls_apply_one_level(tls_ctx* ctx, const double* r, double* z, void* stre
 }
 
 int32_t tls_coarse_apply(tls_ctx* ctx, const double* r, double* z, void* stream) {
+  TLS_RANGE("tls_coarse_apply");
   TRY(need_final(ctx));
   if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "no coarse space");
   CK(cudaSetDevice(ctx->device));
@@ -1468,6 +1501,7 @@ int32_t tls_galerkin_assemble(const int32_t* plan_sj, const int64_t* plan_off, i
                               const int64_t* wptr, const int32_t* kcnt, const int64_t* cstart, int32_t nsub,
                               const int64_t* rows, const int64_t* grp, int64_t nrows, double* A0, int64_t nC,
                               void* stream) {
+  TLS_RANGE("tls_galerkin_assemble");
   if (!plan_sj || !plan_off || nplan <= 0 || !zptr || !wptr || !kcnt || !cstart || !rows || !grp || !A0)
     return TLS_ERR_ARG;
   for (int s = 0; s < nsub; ++s)
@@ -1513,6 +1547,7 @@ int32_t tls_galerkin_assemble(const int32_t* plan_sj, const int64_t* plan_off, i
 // K9b: banded LU with partial pivoting of a batch, in place, LAPACK format
 int32_t tls_band_lu(double* ap, int64_t ld, int32_t count, const int32_t* lreach, const int32_t* ureach, int32_t nbk,
                     int32_t* piv, int32_t* info, void* stream) {
+  TLS_RANGE("tls_band_lu");
   if (!ap || !lreach || !ureach || !piv || !info || count <= 0 || nbk <= 0 || ld != 64LL * nbk) return TLS_ERR_ARG;
   for (int J = 0; J < nbk; ++J)
     if (lreach[J] < 64 * (J + 1) || lreach[J] > ld || ureach[J] < 64 * (J + 1) || ureach[J] > ld ||
@@ -1538,6 +1573,7 @@ int32_t tls_band_lu(double* ap, int64_t ld, int32_t count, const int32_t* lreach
 // K10: X <- (L L^T)^{-1} X for a batch of band Cholesky factors, many right-hand sides (DMMA)
 int32_t tls_band_solve_multi(const double* L, int64_t ld, int32_t count, const double* dinv, const int32_t* kc,
                              int32_t nb, double* X, int64_t nrhs, void* stream) {
+  TLS_RANGE("tls_band_solve_multi");
   if (!L || !dinv || !kc || !X || count <= 0 || nb <= 0 || ld != 64LL * nb || nrhs <= 0) return TLS_ERR_ARG;
   for (int64_t i = 0; i < (int64_t)count * nb; ++i)
     if (kc[i] < 0 || kc[i] > i % nb) return TLS_ERR_ARG;
@@ -1561,6 +1597,7 @@ int32_t tls_band_solve_multi(const double* L, int64_t ld, int32_t count, const d
 // K12a: pivoted-QR pivot magnitudes of every subdomain's coarse block (rank filter)
 int32_t tls_rank_filter_pivots(double* W, const int64_t* woff, const int32_t* nrows, const int32_t* ncols,
                                int32_t count, double* rdiag, int32_t* perm, void* stream) {
+  TLS_RANGE("tls_rank_filter_pivots");
   if (!W || !woff || !nrows || !ncols || !rdiag || !perm || count <= 0) return TLS_ERR_ARG;
   std::vector<long long> roff(count + 1, 0);
   for (int s = 0; s < count; ++s) {
@@ -1601,6 +1638,7 @@ int32_t tls_rank_filter_pivots(double* W, const int64_t* woff, const int32_t* nr
 
 // batched symmetric eigensolver (k_syevj_batched) for the setup's Rayleigh-Ritz matrices
 int32_t tls_syevj_batched(const double* T, int64_t batch, int32_t p, double* w, double* V, void* stream) {
+  TLS_RANGE("tls_syevj_batched");
   if (!T || !w || !V || batch <= 0 || p <= 0 || p > EJ_MAX) return TLS_ERR_ARG;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return TLS_ERR_CUDA;
@@ -1614,8 +1652,23 @@ int32_t tls_syevj_batched(const double* T, int64_t batch, int32_t p, double* w, 
   return cudaGetLastError() == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;
 }
 
+// batched one-sided Jacobi SVD (k_svdj_batched) for the SVD coarse modes (src/spectral.py:135-154)
+int32_t tls_svdj_batched(double* X, int64_t batch, int32_t m, int32_t n, double* sig, int32_t* info, void* stream) {
+  TLS_RANGE("tls_svdj_batched");
+  if (!X || !sig || !info || batch <= 0 || m <= 0 || n <= 0) return TLS_ERR_ARG;
+  // |cos(x_i, x_j)| <= tol ends a pair: above the rounding noise of an m-term dot product
+  const double tol = std::max(1.0e-14, 2.220446049250313e-16 * sqrt((double)m));
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int nb = (int)std::min<int64_t>(65535, batch - b0);
+    launch_k(nullptr, k_svdj_batched, nb, SVJ_THREADS, 0, (cudaStream_t)stream, X + b0 * m * n, (int)m, (int)n,
+             sig + b0 * n, info + b0, tol, 40);
+  }
+  return cudaGetLastError() == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;
+}
+
 // ---- decomposition on the device (tls_graph.cuh; src/sparsemat.py:180-195, src/partition.py:278-334)
 int32_t tls_graph_build(tls_ctx* ctx, int64_t* nedges) {
+  TLS_RANGE("tls_graph_build");
   if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "upload the matrix first") : TLS_ERR_ARG;
   if (!ctx->h_nofo.empty()) return fail(ctx, TLS_ERR_STATE, "tls_graph_build needs the caller's row numbering");
   CK(cudaSetDevice(ctx->device));
@@ -1644,6 +1697,7 @@ int32_t tls_graph_fetch(tls_ctx* ctx, int64_t* gptr, int32_t* gadj) {
 
 int32_t tls_overlap_build(tls_ctx* ctx, int32_t n_sub, const int64_t* owner, int32_t overlap, int64_t* total,
                           int32_t* k_c) {
+  TLS_RANGE("tls_overlap_build");
   if (!ctx || ctx->g_m < 0) return ctx ? fail(ctx, TLS_ERR_STATE, "build the graph first") : TLS_ERR_ARG;
   if (n_sub <= 0 || !owner) return fail(ctx, TLS_ERR_ARG, "bad subdomain count or owner vector");
   if (overlap < 1) return fail(ctx, TLS_ERR_ARG, "overlap must be at least 1");
@@ -1695,6 +1749,7 @@ int32_t tls_graph_release(tls_ctx* ctx) {
 
 // store A0 (row-major n_C x n_C, device) and turn on one refinement step of every coarse solve
 int32_t tls_coarse_refine(tls_ctx* ctx, const double* a0, void* stream) {
+  TLS_RANGE("tls_coarse_refine");
   if (!ctx || !ctx->nsub) return ctx ? fail(ctx, TLS_ERR_STATE, "upload subdomains first") : TLS_ERR_ARG;
   if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "upload the coarse space first");
   if (!ctx->h_nofo.empty()) return fail(ctx, TLS_ERR_STATE, "coarse refinement needs the whole A0^{-1} (one GPU)");
@@ -1774,6 +1829,7 @@ static int ensure_hist(tls_ctx* ctx, int maxit) {
 int32_t tls_pcg(tls_ctx* ctx, const double* b, double* x, double tol, int32_t maxit,
                 int32_t use_precond, double* history, double* coeffs, tls_status* st_out,
                 tls_iter_cb cb, void* user, void* stream) {
+  TLS_RANGE("tls_pcg");
   if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "no matrix uploaded") : TLS_ERR_ARG;
   if (use_precond) TRY(need_final(ctx));
   if (maxit < 0) return fail(ctx, TLS_ERR_ARG, "maxit must be non-negative");
@@ -2005,6 +2061,7 @@ static int ensure_gm(tls_ctx* ctx, int mcols) {
 int32_t tls_gmres(tls_ctx* ctx, const double* b, double* x, double tol, int32_t maxit,
                   int32_t restart, int32_t use_precond, double* history, tls_status* st_out,
                   tls_iter_cb cb, void* user, void* stream) {
+  TLS_RANGE("tls_gmres");
   if (!ctx || !ctx->rowptr) return ctx ? fail(ctx, TLS_ERR_STATE, "no matrix uploaded") : TLS_ERR_ARG;
   if (use_precond) TRY(need_final(ctx));
   const bool restarted = restart > 0 && restart < maxit;
@@ -2190,6 +2247,48 @@ int32_t tls_set_kernel_timing(tls_ctx* ctx, int32_t on) {
   return TLS_OK;
 }
 
+// Kernel trace: while on, every launch made OUTSIDE graph capture (the host-driven PCG / GMRES loops a
+// callback selects, and the apply entry points) is bracketed by an event pair.  tls_kernel_trace_dump
+// synchronises, writes "name count total_ms" lines (descending total) into buf and clears the trace.
+int32_t tls_set_kernel_trace(tls_ctx* ctx, int32_t on) {
+  if (!ctx) return TLS_ERR_ARG;
+  ctx->ktrace = on != 0;
+  return TLS_OK;
+}
+
+int64_t tls_kernel_trace_dump(tls_ctx* ctx, char* buf, int64_t cap) {
+  if (!ctx) return -1;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  std::map<std::string, std::pair<long long, double>> acc;
+  for (auto& e : ctx->kt_trace) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+    const char* nm = nullptr;
+    if (cudaFuncGetName(&nm, e.first) != cudaSuccess || !nm) nm = "?";
+    auto& a = acc[nm];
+    a.first++;
+    a.second += ms;
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  ctx->kt_trace.clear();
+  std::vector<std::pair<std::string, std::pair<long long, double>>> v(acc.begin(), acc.end());
+  std::sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return x.second.second > y.second.second; });
+  std::string out;
+  for (auto& e : v) {
+    char line[512];
+    snprintf(line, sizeof line, "%s %lld %.6f\n", e.first.c_str(), e.second.first, e.second.second);
+    out += line;
+  }
+  if (buf && cap > 0) {
+    const size_t k = std::min<size_t>(out.size(), (size_t)cap - 1);
+    memcpy(buf, out.data(), k);
+    buf[k] = 0;
+  }
+  return (int64_t)out.size();
+}
+
 int32_t tls_kernel_timing(const tls_ctx* ctx, double* avg_ms, int64_t* count) {
   if (!ctx) return TLS_ERR_ARG;
   if (avg_ms) *avg_ms = ctx->kt_count ? ctx->kt_sum_ms / (double)ctx->kt_count : 0.0;
@@ -2209,6 +2308,7 @@ int32_t tls_set_local_kind(tls_ctx* ctx, int32_t kind) {
 int32_t tls_store_local_band(tls_ctx* ctx, int32_t first_g, int32_t count, const double* L,
                              int64_t ld, const double* dinv, int32_t nbmax, const int32_t* perm,
                              const int32_t* kcnt, void* stream) {
+  TLS_RANGE("tls_store_local_band");
   if (!ctx) return TLS_ERR_ARG;
   if (ctx->local_kind != 1) return fail(ctx, TLS_ERR_STATE, "handle is not in band-Cholesky mode");
   if (!ctx->sym) return fail(ctx, TLS_ERR_ARG, "band factors need a symmetric matrix (Cholesky)");
@@ -2330,6 +2430,7 @@ int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first_g, int32_t count, co
                                 int64_t ld, const double* ldinv, const double* udinv, int32_t nbmax,
                                 const int32_t* perm_in, const int32_t* perm_out, const int32_t* lcode,
                                 const int32_t* ucode, void* stream) {
+  TLS_RANGE("tls_store_local_band_lu");
   if (!ctx) return TLS_ERR_ARG;
   if (ctx->local_kind != 2) return fail(ctx, TLS_ERR_STATE, "handle is not in band-LU mode");
   const int first = first_g - ctx->own_lo;
@@ -2386,6 +2487,7 @@ int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first_g, int32_t count, co
 // ---- setup: banded Cholesky of a batch (K9, DMMA) ----------------------------------------------
 int32_t tls_band_cholesky(double* ap, int64_t ld, int32_t count, const int32_t* reach, int32_t nbk,
                           double* dinv, int32_t* info, void* stream) {
+  TLS_RANGE("tls_band_cholesky");
   if (!ap || !dinv || !info || !reach || count <= 0 || nbk <= 0 || ld != 64LL * nbk) return TLS_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   for (int J = 0; J < nbk; ++J)

@@ -527,6 +527,89 @@ __global__ void __launch_bounds__(256) k_syevj_batched(const double* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K13: batched one-sided Jacobi SVD (Hestenes) for the SVD coarse modes (src/spectral.py:135-154
+// takes LAPACK's thin SVD of the harmonic extension; here E = Q R first, then this kernel on the
+// small R).  One CTA per matrix X (m x n, column-major, leading dimension m, in global memory --
+// L1/L2 resident: 268^2 doubles on configuration 3), rotated in place: X <- X V with mutually
+// orthogonal columns, so column j ends as sigma_j u_j and the left singular vectors need no
+// accumulation.  Round-robin pairing: n/2 disjoint column pairs per round, one warp per pair
+// (coalesced column reads, three dot products by warp shuffles, the rotation written back),
+// n-1 rounds per sweep, sweeps until no pair has |x_i . x_j| > tol |x_i| |x_j|.  The larger
+// column of each rotated pair is kept at the lower index (de Rijk), which speeds convergence.
+// sig[b*n + j] = |column j|; info[b] = sweeps used, or -1 if max_sweeps did not converge.
+// ---------------------------------------------------------------------------------------
+constexpr int SVJ_THREADS = 512;
+__global__ void __launch_bounds__(SVJ_THREADS) k_svdj_batched(double* __restrict__ Xall, int m, int n,
+                                                              double* __restrict__ sig,
+                                                              int* __restrict__ info, double tol,
+                                                              int max_sweeps) {
+  PDL_ENTRY();
+  double* X = Xall + (long long)blockIdx.x * m * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = SVJ_THREADS / 32;
+  const int P = (n + 1) & ~1, np_ = P / 2;
+  int sweeps = -1;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < P - 1; ++r) {
+      int mine = 0;
+      for (int q = warp; q < np_; q += NW) {
+        const int pa = q == 0 ? 0 : ((q - 1 + r) % (P - 1)) + 1;
+        const int pb = ((P - 2 - q + r) % (P - 1)) + 1;
+        const int i = min(pa, pb), j = max(pa, pb);
+        if (j >= n) continue;  // dummy partner (odd n)
+        double* xi = X + (long long)i * m;
+        double* xj = X + (long long)j * m;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int k = lane; k < m; k += 32) {
+          const double a = xi[k], b = xj[k];
+          al += a * a;
+          be += b * b;
+          ga += a * b;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(FULL, al, o);
+          be += __shfl_xor_sync(FULL, be, o);
+          ga += __shfl_xor_sync(FULL, ga, o);
+        }
+        const bool rot = fabs(ga) > tol * sqrt(al) * sqrt(be);  // false when a column is zero
+        if (!rot && al >= be) continue;
+        double c = 1.0, s = 0.0, t = 0.0;
+        if (rot) {
+          const double zeta = (be - al) / (2.0 * ga);
+          t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = c * t;
+          mine = 1;
+        }
+        const bool swap = (be + t * ga) > (al - t * ga);  // rotated norms^2: keep the larger first
+        for (int k = lane; k < m; k += 32) {
+          const double a = xi[k], b = xj[k];
+          const double u = c * a - s * b, v = s * a + c * b;
+          xi[k] = swap ? v : u;
+          xj[k] = swap ? u : v;
+        }
+      }
+      rotated += __syncthreads_count(mine);
+    }
+    if (rotated == 0) {
+      sweeps = sweep + 1;
+      break;
+    }
+  }
+  for (int j = warp; j < n; j += NW) {
+    const double* xj = X + (long long)j * m;
+    double al = 0.0;
+    for (int k = lane; k < m; k += 32) al += xj[k] * xj[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) al += __shfl_xor_sync(FULL, al, o);
+    if (lane == 0) sig[(long long)blockIdx.x * n + j] = sqrt(al);
+  }
+  if (threadIdx.x == 0) info[blockIdx.x] = sweeps;
+}
+
 // sharded dot products: part[0] = fixed-order sum of part[0..np), part[1..np) = 0 (one CTA)
 __global__ void __launch_bounds__(NTHR) k_fold_partials(double* __restrict__ part, int np) {
   PDL_ENTRY();

@@ -182,6 +182,25 @@ def _stage(name, t_prev):
     return t
 
 
+class _nvtx:
+    """NVTX range around a setup stage (torch.cuda.nvtx; a no-op without an attached tool)."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        try:
+            _torch().cuda.nvtx.range_push(self.name)
+            self.on = True
+        except Exception:
+            self.on = False
+
+    def __exit__(self, *exc):
+        if self.on:
+            _torch().cuda.nvtx.range_pop()
+        return False
+
+
 def _log(t0, msg):
     if VERBOSE:
         print(f"[tls setup {time.perf_counter() - t0:7.1f}s] {msg}", flush=True)
@@ -344,9 +363,8 @@ def _svd_columns_lu_batch(torch, A, LU, piv, P, n_loc, n_int, n_bnd, first, cnt,
         # correction on the saddle point: 1e-6 vs the reference, measured.)
         Q, R = torch.linalg.qr(Eint)
         del Eint
-        UR, sig, _ = torch.linalg.svd(R, full_matrices=False)
-        U = Q @ UR[:, :, :kk]
-        sig = sig[:, :kk]
+        UR, sig = _svd_left_topk(torch, R, kk)
+        U = Q @ UR
         del Q, R, UR
         sig_h = sig.cpu().numpy()
         for j, b in enumerate(bs):
@@ -357,6 +375,37 @@ def _svd_columns_lu_batch(torch, A, LU, piv, P, n_loc, n_int, n_bnd, first, cnt,
             Z = _fix_signs(torch, U[j][:, torch.as_tensor(keep, device=dev)])
             out[b] = (Z.contiguous(), _cut_gap(sig_h[j], keep))
     return out
+
+
+def _svd_left_topk(torch, R, kk):
+    """Leading kk left singular vectors (b, r, kk) and singular values (b, kk), descending, of a
+    batch of small matrices R (b, r, n).  Preconditioned one-sided Jacobi (Drmac-Veselic): a second
+    QR, R^T = Q2 R2, leaves R = L2 Q2^T with L2 = R2^T lower triangular and close to column-graded
+    form, so the left singular vectors of R are those of L2; the in-tree batched kernel
+    (tls_svdj_batched) rotates the columns of L2 until they are mutually orthogonal -- column j
+    ends as sigma_j u_j.  LAPACK-grade accuracy (also for graded spectra) without a cuSOLVER call
+    per matrix.  TLS_SVDJ=0 keeps torch.linalg.svd."""
+    b, r, n = R.shape
+    if not R.is_cuda or os.environ.get("TLS_SVDJ", "1") == "0":
+        UR, sig, _ = torch.linalg.svd(R, full_matrices=False)
+        return UR[:, :, :kk], sig[:, :kk]
+    X = torch.linalg.qr(R.mT, mode="r").R.contiguous()   # R2 row-major = L2 column-major (k x k)
+    k = X.shape[1]
+    sig = torch.empty((b, k), dtype=R.dtype, device=R.device)
+    info = torch.empty((b,), dtype=torch.int32, device=R.device)
+    rc = _lib.load().tls_svdj_batched(_lib.ptr(X), b, X.shape[2], k, _lib.ptr(sig), _lib.ptr(info), stream_ptr())
+    if rc != 0:
+        raise RuntimeError(f"tls_svdj_batched failed ({rc})")
+    kk = min(kk, k)
+    sv, idx = torch.topk(sig, kk, dim=1)                 # descending
+    W = torch.gather(X, 1, idx[:, :, None].expand(b, kk, X.shape[2]))
+    UR = (W / sv.clamp(min=1e-300)[:, :, None]).mT.contiguous()
+    if int(info.min()) < 0:                              # sweep limit reached: LAPACK for those
+        for j in torch.nonzero(info < 0).flatten().tolist():
+            Uj, sj, _ = torch.linalg.svd(R[j], full_matrices=False)
+            UR[j] = Uj[:, :kk]
+            sv[j] = sj[:kk]
+    return UR, sv
 
 
 def _orth(torch, X, check=True):
@@ -1327,11 +1376,13 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                 _log(t0, f"batch at {first}")
             tb0 = time.perf_counter() if VERBOSE else 0.0
             A = a_buf[:cnt]
-            handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
+            with _nvtx("tls.setup.extract_blocks"):
+                handle.check(lib.tls_extract_blocks(handle.ctx, first, cnt, _lib.ptr(A), ld, s_ptr))
             if band_lu:
                 n_list = [int(n_loc[first + b]) for b in range(cnt)]
-                LU, piv, Ldinv, Udinv, pin, pout, lcodes, ucodes, info, P = _band_lu_factor(
-                    torch, A, perm_list, n_list, ld)
+                with _nvtx("tls.setup.band_lu_factor"):
+                    LU, piv, Ldinv, Udinv, pin, pout, lcodes, ucodes, info, P = _band_lu_factor(
+                        torch, A, perm_list, n_list, ld)
                 for b in range(cnt):  # the reference's singularity rule (src/subdomain.py:86-88)
                     nb_ = n_list[b]
                     blk = LU[b, :nb_, :nb_]
@@ -1387,7 +1438,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                 tb = _stage("extract", tb0)
                 tb = _stage("orders (host, wait)", tb)
                 n_list = [int(n_loc[first + b]) for b in range(cnt)]
-                L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld)
+                with _nvtx("tls.setup.band_factor"):
+                    L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld)
                 tb = _stage("band factor", tb)
                 bad = torch.nonzero(info).flatten().cpu().numpy()
                 if bad.size:
@@ -1404,11 +1456,12 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                     kc_full = np.zeros((cnt, ld // 64), dtype=np.int64)
                     for b in range(cnt):
                         kc_full[b, : kcnts[b].size] = kcnts[b]
-                    cols = _coarse_band_batch(torch, coarse, A, L, P,
-                                              [int(n_loc[first + b]) for b in range(cnt)],
-                                              [int(n_int[first + b]) for b in range(cnt)],
-                                              [int(n_loc[first + b] - n_bnd[first + b]) for b in range(cnt)],
-                                              tau, n_modes, Dinv=Dinv, kc=kc_full)
+                    with _nvtx("tls.setup.coarse_modes"):
+                        cols = _coarse_band_batch(torch, coarse, A, L, P,
+                                                  [int(n_loc[first + b]) for b in range(cnt)],
+                                                  [int(n_int[first + b]) for b in range(cnt)],
+                                                  [int(n_loc[first + b] - n_bnd[first + b]) for b in range(cnt)],
+                                                  tau, n_modes, Dinv=Dinv, kc=kc_full)
                     for b in range(cnt):
                         s = first + b
                         n, ni = int(n_loc[s]), int(n_int[s])
@@ -1530,7 +1583,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     if VERBOSE:
         _log(t0, "stage times: " + ", ".join(f"{k} {v:.2f}s" for k, v in _STAGE.items()))
     _log(t0, f"local operators done; assembling A0 ({nC} x {nC})")
-    A0 = assemble_a0_columns(maps, owner, z_all, w_dev, counts, own, dev)
+    with _nvtx("tls.setup.galerkin_a0"):
+        A0 = assemble_a0_columns(maps, owner, z_all, w_dev, counts, own, dev)
     del w_dev
     if sharded:
         shard.coll.allreduce(A0, op="sum")

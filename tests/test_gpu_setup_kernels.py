@@ -148,3 +148,37 @@ def test_band_lu_kernel_matches_lapack(G):
     assert (LUk - LUr).abs().max().item() <= 1e-11 * LUr.abs().max().item()
     P, L, U = torch.lu_unpack(LUk, pivk)
     assert (P @ L @ U - At).abs().max().item() <= 1e-12 * At.abs().max().item()
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (5, 3), (3, 5), (40, 40), (131, 131), (268, 268), (100, 37)])
+def test_svdj_batched_matches_lapack(G, shape):
+    """K13 one-sided Jacobi SVD (tls_svdj_batched) against LAPACK on the same matrices: the thin
+    SVD of src/spectral.py:143.  Upper-triangular inputs (the R of E = QR), graded singular values
+    over 12 decades, a rank-deficient and a zero matrix."""
+    r, n = shape
+    rng = np.random.default_rng(r * 1000 + n)
+    b = 5
+    R = rng.standard_normal((b, r, n))
+    R[0] = np.triu(R[0])
+    k = min(r, n)
+    u, _ = np.linalg.qr(rng.standard_normal((r, r)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    R[1] = (u[:, :k] * np.logspace(0, -12, k)) @ v[:, :k].T           # graded
+    R[2] = (u[:, :max(k // 2, 1)] * 2.0) @ v[:, :max(k // 2, 1)].T     # rank-deficient, multiple sigma
+    R[3] = 0.0
+    kk = min(k, 21)
+    UR, sv = G._svd_left_topk(torch, torch.as_tensor(R, device="cuda"), kk)
+    UR, sv = UR.cpu().numpy(), sv.cpu().numpy()
+    for j in range(b):
+        U, S, Vt = np.linalg.svd(R[j], full_matrices=False)
+        s0 = max(S[0], 1e-300)
+        assert np.abs(sv[j] - S[:kk]).max() <= 2e-13 * s0, j
+        assert np.all(np.diff(sv[j]) <= 0)
+        live = np.nonzero(sv[j] > 1e-13 * s0)[0]
+        if live.size == 0:
+            continue
+        Uj = UR[j][:, live]
+        assert np.abs(Uj.T @ Uj - np.eye(live.size)).max() <= 1e-9, j
+        # singular-vector residual: |R^T u| = sigma, and R R^T u = sigma^2 u
+        res = R[j] @ (R[j].T @ Uj) - Uj * sv[j][live] ** 2
+        assert np.abs(res).max() <= 1e-12 * s0 * s0, j
