@@ -238,7 +238,7 @@ int32_t tls_syevj_batched(const double* T, int64_t batch, int32_t p, double* w, 
  * E = Q R and passes the small R here).  X (batch x [m x n column-major, leading dimension m],
  * device) is rotated in place to X V with mutually orthogonal columns: column j = sigma_j u_j
  * (unsorted); sig (batch x n) receives the column norms, info (batch) the sweeps used or -1 when
- * 40 sweeps did not converge.  Stream-ordered. */
+ * 60 sweeps did not converge.  Stream-ordered. */
 int32_t tls_svdj_batched(double* X, int64_t batch, int32_t m, int32_t n, double* sig, int32_t* info, void* stream);
 
 /* ---- SetupReport getters (src/precond.py:39-83) */

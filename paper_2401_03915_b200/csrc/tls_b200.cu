@@ -134,6 +134,7 @@ struct tls_ctx {
          *h1 = nullptr, *h2 = nullptr;
   int gm_cols = 0;
   bool gm_fused = true;               // CGS2 middle step as one kernel (TLS_GM_FUSED=0: two)
+  bool gm_givens_fused = true;        // Givens + v_{j+1} = w / hn in one launch (TLS_GM_GIVENS_FUSED=0: two)
   // ---- graphs
   cudaGraphExec_t pcg_exec[2] = {nullptr, nullptr};
   int pcg_exec_launches[2] = {0, 0};
@@ -1661,7 +1662,7 @@ int32_t tls_svdj_batched(double* X, int64_t batch, int32_t m, int32_t n, double*
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     const int nb = (int)std::min<int64_t>(65535, batch - b0);
     launch_k(nullptr, k_svdj_batched, nb, SVJ_THREADS, 0, (cudaStream_t)stream, X + b0 * m * n, (int)m, (int)n,
-             sig + b0 * n, info + b0, tol, 40);
+             sig + b0 * n, info + b0, tol, 60);
   }
   return cudaGetLastError() == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;
 }
@@ -1991,6 +1992,13 @@ static int enq_gm_step(tls_ctx* ctx, cudaStream_t s, int j, bool prec) {
   launch_k(ctx, k_gm_gemvn<1>, ctx->G, NTHR, 0, s, no, ctx->V + r0, ldv, nc, st, ctx->h2, w + r0, ctx->part, 1, stop);
   CKL();
   TRY(enq_allreduce_part(ctx, s, ctx->G));
+  if (ctx->gm_givens_fused) {
+    launch_k(ctx, k_gm_givens_scale, ctx->G, NTHR, 0, s, st, j, ctx->gm_cols + 1, ctx->H, ctx->h1, ctx->h2, ctx->part,
+             ctx->G, ctx->cs, ctx->sn, ctx->gv, ctx->hist, no, (const double*)(w + r0),
+             ctx->V + (long long)(j + 1) * ldv + r0);
+    CKL();
+    return TLS_OK;
+  }
   launch_k(ctx, k_gm_givens, 1, NTHR, 0, s, st, j, ctx->gm_cols + 1, ctx->H, ctx->h1, ctx->h2, ctx->part, ctx->G,
                                  ctx->cs, ctx->sn, ctx->gv, ctx->hist);
   CKL();
@@ -2046,6 +2054,7 @@ static int ensure_gm(tls_ctx* ctx, int mcols) {
   }
   ctx->gm_cols = mcols;
   if (const char* e = getenv("TLS_GM_FUSED")) ctx->gm_fused = atoi(e) != 0;
+  if (const char* e = getenv("TLS_GM_GIVENS_FUSED")) ctx->gm_givens_fused = atoi(e) != 0;
   if (ctx->gm_fused) {  // (nc + 1) x NTHR + nc doubles of shared memory for the widest fused step
 
     const int mc = std::min(mcols + 1, GM_FUSED_MAXCOLS);

@@ -175,18 +175,46 @@ __global__ void __launch_bounds__(1024) k_restrict(const long long* __restrict__
   const int* id = idx + sub_idxoff[s];
   for (int p = threadIdx.x; p < ni; p += blockDim.x) rs[p] = __ldg(r + __ldg(id + p));
   __syncthreads();
-  const double* zs = Z + zoff[s];
+  const long long zo = zoff[s];
+  const double* zs = Z + zo;
+  // even n_int and an even offset: every column starts 16-byte aligned -> 128-bit streaming loads,
+  // 8 in flight per lane (4 KB per warp); otherwise 64-bit loads, 4 in flight
+  const bool vec = ((ni | (int)(zo & 1)) & 1) == 0;
   for (int col = blockIdx.y * nw + warp; col < ks; col += nw * gridDim.y) {
     const double* zc = zs + (long long)col * ni;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int p = lane;
-    for (; p + 96 < ni; p += 128) {  // 4 independent coalesced loads in flight per lane
-      a0 += __ldg(zc + p) * rs[p];
-      a1 += __ldg(zc + p + 32) * rs[p + 32];
-      a2 += __ldg(zc + p + 64) * rs[p + 64];
-      a3 += __ldg(zc + p + 96) * rs[p + 96];
+    if (vec) {
+      const int n2 = ni >> 1;
+      const double2* rs2 = reinterpret_cast<const double2*>(rs);
+      int p = lane;
+      for (; p + 224 < n2; p += 256) {
+        double2 z[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) z[u] = ldg_stream2(zc + 2 * (p + 32 * u));
+#pragma unroll
+        for (int u = 0; u < 8; u += 4) {
+          const double2 r0 = rs2[p + 32 * u], r1 = rs2[p + 32 * (u + 1)];
+          const double2 r2 = rs2[p + 32 * (u + 2)], r3 = rs2[p + 32 * (u + 3)];
+          a0 += z[u].x * r0.x + z[u].y * r0.y;
+          a1 += z[u + 1].x * r1.x + z[u + 1].y * r1.y;
+          a2 += z[u + 2].x * r2.x + z[u + 2].y * r2.y;
+          a3 += z[u + 3].x * r3.x + z[u + 3].y * r3.y;
+        }
+      }
+      for (; p < n2; p += 32) {
+        const double2 z = ldg_stream2(zc + 2 * p), r0 = rs2[p];
+        a0 += z.x * r0.x + z.y * r0.y;
+      }
+    } else {
+      int p = lane;
+      for (; p + 96 < ni; p += 128) {  // 4 independent coalesced loads in flight per lane
+        a0 += __ldg(zc + p) * rs[p];
+        a1 += __ldg(zc + p + 32) * rs[p + 32];
+        a2 += __ldg(zc + p + 64) * rs[p + 64];
+        a3 += __ldg(zc + p + 96) * rs[p + 96];
+      }
+      for (; p < ni; p += 32) a0 += __ldg(zc + p) * rs[p];
     }
-    for (; p < ni; p += 32) a0 += __ldg(zc + p) * rs[p];
     double v = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -535,11 +563,13 @@ __global__ void __launch_bounds__(256) k_syevj_batched(const double* __restrict_
 // orthogonal columns, so column j ends as sigma_j u_j and the left singular vectors need no
 // accumulation.  Round-robin pairing: n/2 disjoint column pairs per round, one warp per pair
 // (coalesced column reads, three dot products by warp shuffles, the rotation written back),
-// n-1 rounds per sweep, sweeps until no pair has |x_i . x_j| > tol |x_i| |x_j|.  The larger
-// column of each rotated pair is kept at the lower index (de Rijk), which speeds convergence.
+// n-1 rounds per sweep, sweeps until no pair has |x_i . x_j| > tol |x_i| |x_j|.  (Keeping the larger
+// column of a rotated pair at the lower index -- de Rijk's device for the row-cyclic order -- was
+// measured to DOUBLE the sweep count under the round-robin order: 30 vs 18 on a harmonic
+// extension; the columns are ranked by norm after convergence instead.)
 // sig[b*n + j] = |column j|; info[b] = sweeps used, or -1 if max_sweeps did not converge.
 // ---------------------------------------------------------------------------------------
-constexpr int SVJ_THREADS = 512;
+constexpr int SVJ_THREADS = 1024;
 __global__ void __launch_bounds__(SVJ_THREADS) k_svdj_batched(double* __restrict__ Xall, int m, int n,
                                                               double* __restrict__ sig,
                                                               int* __restrict__ info, double tol,
@@ -574,22 +604,15 @@ __global__ void __launch_bounds__(SVJ_THREADS) k_svdj_batched(double* __restrict
           be += __shfl_xor_sync(FULL, be, o);
           ga += __shfl_xor_sync(FULL, ga, o);
         }
-        const bool rot = fabs(ga) > tol * sqrt(al) * sqrt(be);  // false when a column is zero
-        if (!rot && al >= be) continue;
-        double c = 1.0, s = 0.0, t = 0.0;
-        if (rot) {
-          const double zeta = (be - al) / (2.0 * ga);
-          t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          c = 1.0 / sqrt(1.0 + t * t);
-          s = c * t;
-          mine = 1;
-        }
-        const bool swap = (be + t * ga) > (al - t * ga);  // rotated norms^2: keep the larger first
+        if (!(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;  // also when a column is zero
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        mine = 1;
         for (int k = lane; k < m; k += 32) {
           const double a = xi[k], b = xj[k];
-          const double u = c * a - s * b, v = s * a + c * b;
-          xi[k] = swap ? v : u;
-          xj[k] = swap ? u : v;
+          xi[k] = c * a - s * b;
+          xj[k] = s * a + c * b;
         }
       }
       rotated += __syncthreads_count(mine);
@@ -960,6 +983,60 @@ __global__ void k_gm_givens(GmState* st, int j, int ldh, double* __restrict__ H,
   } else if (j + 1 >= st->m_cycle) {
     st->cycle_stop = 1;
   }
+}
+// Givens step + v_{j+1} = w / hn in ONE launch of G CTAs: every CTA sums the same norm partials in
+// the same fixed order (bit-identical hn everywhere), CTA 0 thread 0 updates the Hessenberg column,
+// the rotations and the stopping tests exactly as k_gm_givens, and all CTAs scale their rows.  When
+// this step ends the cycle the scaled column is simply never read (a CTA that already sees
+// cycle_stop = 1 from CTA 0 may skip its rows).
+__global__ void __launch_bounds__(NTHR) k_gm_givens_scale(GmState* st, int j, int ldh, double* __restrict__ H,
+                                                          const double* __restrict__ h1,
+                                                          const double* __restrict__ h2,
+                                                          const double* __restrict__ part, int np,
+                                                          double* __restrict__ cs, double* __restrict__ sn,
+                                                          double* __restrict__ g, double* __restrict__ hist,
+                                                          int n, const double* __restrict__ w,
+                                                          double* __restrict__ v) {
+  PDL_ENTRY();
+  if (*(volatile int*)&st->cycle_stop) return;
+  __shared__ double sh[32];
+  __shared__ double hn_s;
+  const double s = sum_partials(part, np, sh);
+  if (threadIdx.x == 0) hn_s = sqrt(s);
+  __syncthreads();
+  const double hn = hn_s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double* hc = H + (long long)j * ldh;
+    for (int i = 0; i <= j; ++i) hc[i] = h1[i] + h2[i];
+    st->hn = hn;
+    hc[j + 1] = hn;
+    for (int i = 0; i < j; ++i) {
+      const double t = cs[i] * hc[i] + sn[i] * hc[i + 1];
+      hc[i + 1] = -sn[i] * hc[i] + cs[i] * hc[i + 1];
+      hc[i] = t;
+    }
+    const double den = hypot(hc[j], hc[j + 1]);
+    cs[j] = den != 0.0 ? hc[j] / den : 1.0;
+    sn[j] = den != 0.0 ? hc[j + 1] / den : 0.0;
+    hc[j] = den;
+    hc[j + 1] = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    st->k = j + 1;
+    const double rel = fabs(g[j + 1]) / st->rn;
+    hist[st->total + j + 1] = st->restarted ? rel * st->scale : rel;
+    if (rel <= st->tolc) {
+      st->converged = 1;
+      st->cycle_stop = 1;
+    } else if (hn <= 1e-14 * st->rn) {
+      st->converged = 1;  // happy breakdown (src/krylov.py:187-189)
+      st->cycle_stop = 1;
+    } else if (j + 1 >= st->m_cycle) {
+      st->cycle_stop = 1;
+    }
+  }
+  if (hn == 0.0) return;
+  for (int i = blockIdx.x * NTHR + threadIdx.x; i < n; i += gridDim.x * NTHR) v[i] = w[i] / hn;
 }
 // v_{j+1} = w / hn
 __global__ void __launch_bounds__(NTHR) k_gm_scale(int n, const GmState* st, const double* __restrict__ w,

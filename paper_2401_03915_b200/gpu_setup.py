@@ -381,7 +381,8 @@ def _svd_left_topk(torch, R, kk):
     """Leading kk left singular vectors (b, r, kk) and singular values (b, kk), descending, of a
     batch of small matrices R (b, r, n).  Preconditioned one-sided Jacobi (Drmac-Veselic): a second
     QR, R^T = Q2 R2, leaves R = L2 Q2^T with L2 = R2^T lower triangular and close to column-graded
-    form, so the left singular vectors of R are those of L2; the in-tree batched kernel
+    form, so the left singular vectors of R are those of L2 (R's rows are sorted by norm before that
+    QR and the vectors permuted back); the in-tree batched kernel
     (tls_svdj_batched) rotates the columns of L2 until they are mutually orthogonal -- column j
     ends as sigma_j u_j.  LAPACK-grade accuracy (also for graded spectra) without a cuSOLVER call
     per matrix.  TLS_SVDJ=0 keeps torch.linalg.svd."""
@@ -389,7 +390,12 @@ def _svd_left_topk(torch, R, kk):
     if not R.is_cuda or os.environ.get("TLS_SVDJ", "1") == "0":
         UR, sig, _ = torch.linalg.svd(R, full_matrices=False)
         return UR[:, :, :kk], sig[:, :kk]
-    X = torch.linalg.qr(R.mT, mode="r").R.contiguous()   # R2 row-major = L2 column-major (k x k)
+    # rows of R by descending norm first (a cheap stand-in for column pivoting in the second QR:
+    # 13 instead of 18 Jacobi sweeps on a harmonic extension)
+    order = torch.argsort(R.norm(dim=2), dim=1, descending=True)
+    Rs = torch.gather(R, 1, order[:, :, None].expand(b, r, n))
+    X = torch.linalg.qr(Rs.mT, mode="r").R.contiguous()  # R2 row-major = L2 column-major (r x k)
+    del Rs
     k = X.shape[1]
     sig = torch.empty((b, k), dtype=R.dtype, device=R.device)
     info = torch.empty((b,), dtype=torch.int32, device=R.device)
@@ -399,7 +405,8 @@ def _svd_left_topk(torch, R, kk):
     kk = min(kk, k)
     sv, idx = torch.topk(sig, kk, dim=1)                 # descending
     W = torch.gather(X, 1, idx[:, :, None].expand(b, kk, X.shape[2]))
-    UR = (W / sv.clamp(min=1e-300)[:, :, None]).mT.contiguous()
+    UR = torch.empty((b, r, kk), dtype=R.dtype, device=R.device)
+    UR.scatter_(1, order[:, :, None].expand(b, r, kk), (W / sv.clamp(min=1e-300)[:, :, None]).mT)
     if int(info.min()) < 0:                              # sweep limit reached: LAPACK for those
         for j in torch.nonzero(info < 0).flatten().tolist():
             Uj, sj, _ = torch.linalg.svd(R[j], full_matrices=False)

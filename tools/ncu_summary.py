@@ -18,7 +18,15 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "launch__occupancy_limit_registers", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
            "lts__t_bytes.sum", "l1tex__t_bytes.sum", "smsp__inst_executed.sum",
            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
-           "smsp__average_warp_latency_issue_stalled_long_scoreboard", "sm__cycles_elapsed.avg.per_second"]
+           "smsp__average_warp_latency_issue_stalled_long_scoreboard", "sm__cycles_elapsed.avg.per_second",
+           "sm__inst_executed_pipe_tensor_op_dmma.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+           "smsp__cycles_active.avg", "launch__cluster_size", "launch__shared_mem_per_block_dynamic",
+           "sm__warps_active.avg.per_cycle_active", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
          "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1,
          "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
@@ -26,7 +34,10 @@ TIME_UNITS = ("nsecond", "usecond", "msecond", "second", "ns", "us", "ms", "s")
 
 
 def full(rep, out):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # the raw page exported on the GPU box (ncu -i ... --page raw --csv)
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     res = []
