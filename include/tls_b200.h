@@ -302,6 +302,13 @@ int32_t tls_kernel_timing(const tls_ctx* ctx, double* avg_ms, int64_t* count);
 int32_t tls_set_kernel_trace(tls_ctx* ctx, int32_t on);
 int64_t tls_kernel_trace_dump(tls_ctx* ctx, char* buf, int64_t cap);
 
+/* ---- setup: a batch of dense blocks a (count x ld x ld, row-major, device) in factor order, lower
+ * triangle only: ap[b, i, j] = a[b, perm[b,i], perm[b,j]] for j <= i, 0 above the diagonal, and the
+ * row profile first[b, i] = smallest j with a nonzero (count x ld int32) -- the input of
+ * tls_band_cholesky (src/subdomain.py:80-82 factors the block in its local order instead). */
+int32_t tls_perm_lower(const double* a, const int64_t* perm, double* ap, int32_t* first, int32_t count, int64_t ld,
+                       void* stream);
+
 /* ---- setup: banded Cholesky of a batch of SPD blocks (factor order, dense ld x ld row-major,
  * ld = 64 nbk) in place on the device, one CTA per block, DMMA tile products; reach[J] (host,
  * multiple of 64) = end row of the band below panel J; dinv receives the inverted 64 x 64

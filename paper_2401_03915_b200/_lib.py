@@ -103,6 +103,7 @@ SIGNATURES = {
     "tls_graph_release": (_I32, [_P]),
     "tls_syevj_batched": (_I32, [_P, _I64, _I32, _P, _P, _P]),
     "tls_svdj_batched": (_I32, [_P, _I64, _I32, _I32, _P, _P, _P]),
+    "tls_perm_lower": (_I32, [_P, _P, _P, _P, _I32, _I64, _P]),
     "tls_set_kernel_trace": (_I32, [_P, _I32]),
     "tls_kernel_trace_dump": (_I64, [_P, _P, _I64]),
     "tls_band_solve_multi": (_I32, [_P, _I64, _I32, _P, _P, _I32, _P, _I64, _P]),

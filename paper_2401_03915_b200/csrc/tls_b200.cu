@@ -2494,6 +2494,16 @@ int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first_g, int32_t count, co
 }
 
 // ---- setup: banded Cholesky of a batch (K9, DMMA) ----------------------------------------------
+// factor-order lower triangle + row profile of a batch of dense blocks (k_perm_lower)
+int32_t tls_perm_lower(const double* a, const int64_t* perm, double* ap, int32_t* first, int32_t count, int64_t ld,
+                       void* stream) {
+  TLS_RANGE("tls_perm_lower");
+  if (!a || !perm || !ap || !first || count <= 0 || ld <= 0 || ld > 65535 * 64) return TLS_ERR_ARG;
+  launch_k(nullptr, k_perm_lower, dim3((unsigned)ld, (unsigned)count), NTHR, 0, (cudaStream_t)stream, a,
+           (const long long*)perm, ap, (int*)first, (int)ld);
+  return cudaGetLastError() == cudaSuccess ? TLS_OK : TLS_ERR_CUDA;
+}
+
 int32_t tls_band_cholesky(double* ap, int64_t ld, int32_t count, const int32_t* reach, int32_t nbk,
                           double* dinv, int32_t* info, void* stream) {
   TLS_RANGE("tls_band_cholesky");

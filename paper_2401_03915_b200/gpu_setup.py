@@ -1145,7 +1145,7 @@ def _band_reach(kmax, nbk):
     return out
 
 
-def band_cholesky_kernel(torch, AP, kmax):
+def band_cholesky_kernel(torch, AP, kmax, clear_upper=True):
     """K9 (libtls_b200 ``tls_band_cholesky``): in-place banded Cholesky of the batch AP
     (cnt, ld, ld) in factor order; returns (L, Dinv, info) like the library path."""
     cnt, ld, _ = AP.shape
@@ -1157,11 +1157,12 @@ def band_cholesky_kernel(torch, AP, kmax):
                                        _lib.ptr(info), stream_ptr())
     if rc != 0:
         raise RuntimeError(f"tls_band_cholesky failed ({rc})")
-    AP.masked_fill_(torch.ones(ld, ld, dtype=torch.bool, device=AP.device).triu_(1), 0.0)
+    if clear_upper:  # (tls_perm_lower's output is zero above the diagonal and the kernel keeps it so)
+        AP.masked_fill_(torch.ones(ld, ld, dtype=torch.bool, device=AP.device).triu_(1), 0.0)
     return AP, Dinv, info
 
 
-def _band_factor(torch, A, perm_list, n_list, ld):
+def _band_factor(torch, A, perm_list, n_list, ld, out=None):
     """Lexicographic factor order, band profile, Cholesky and diagonal-tile inverses of a batch.
 
     Returns (L_P, Dinv, perms, kcnts, info, P, codes): L_P[b] is the Cholesky factor of A[b] with
@@ -1172,9 +1173,27 @@ def _band_factor(torch, A, perm_list, n_list, ld):
     cnt = A.shape[0]
     dev = A.device
     nbk = ld // 64
-    AP, P, perms = _lex_perm(torch, A, perm_list, n_list, ld)
+    use_kernel = A.is_cuda and BAND_CHOL != "torch"
+    if use_kernel and os.environ.get("TLS_PERM_KERNEL", "1") != "0":
+        # one pass (tls_perm_lower): factor-order lower triangle + row profile
+        Ph = np.tile(np.arange(ld, dtype=np.int64), (cnt, 1))
+        for b in range(cnt):
+            Ph[b, : n_list[b]] = perm_list[b]
+        P = torch.from_numpy(Ph).to(dev)
+        perms = perm_list
+        AP = out[:cnt] if out is not None else torch.empty_like(A)  # (the caller's reused buffer)
+        first = torch.empty((cnt, ld), dtype=torch.int32, device=dev)
+        rc = _lib.load().tls_perm_lower(_lib.ptr(A), _lib.ptr(P), _lib.ptr(AP), _lib.ptr(first), cnt, ld,
+                                        stream_ptr())
+        if rc != 0:
+            raise RuntimeError(f"tls_perm_lower failed ({rc})")
+        first = first.to(torch.int64)
+        lower_only = True
+    else:
+        AP, P, perms = _lex_perm(torch, A, perm_list, n_list, ld)
+        first = torch.argmax((AP != 0).to(torch.int8), dim=2)       # row profile f(i)
+        lower_only = False
     perms = [p.astype(np.int32) for p in perms]
-    first = torch.argmax((AP != 0).to(torch.int8), dim=2)           # row profile f(i)
     fmin = first.view(cnt, nbk, 64).min(dim=2).values
     bmin = fmin // 64
     kc = (torch.arange(nbk, device=dev)[None, :] - bmin).clamp(min=0).cpu().numpy().astype(np.int32)
@@ -1188,7 +1207,7 @@ def _band_factor(torch, A, perm_list, n_list, ld):
         eye = torch.eye(64, dtype=torch.float64, device=dev).expand(cnt, nbk, 64, 64)
         Dinv = torch.linalg.solve_triangular(Ld, eye, upper=False).contiguous()
     else:  # in-tree K9: one launch for the batch, DMMA tile products
-        L, Dinv, info = band_cholesky_kernel(torch, AP, kc.max(axis=0))
+        L, Dinv, info = band_cholesky_kernel(torch, AP, kc.max(axis=0), clear_upper=not lower_only)
     kcnts = [kc[b, : -(-n_list[b] // 64)] for b in range(cnt)]
     codes = [(kc[b] | (fz[b] << 16))[: -(-n_list[b] // 64)].astype(np.int32) for b in range(cnt)]
     return L, Dinv, perms, kcnts, info, P, codes
@@ -1364,6 +1383,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     t0 = time.perf_counter()
     _log(t0, f"subdomains [{lo},{hi}) of {N}, local={local}, ld={ld}, batch={batch}")
     a_buf = torch.empty((min(batch, hi - lo), ld, ld), dtype=torch.float64, device=dev)
+    # factor-order copy of the batch (band Cholesky path), allocated once like a_buf
+    ap_buf = torch.empty_like(a_buf) if band and not band_lu else None
     # the host factor orders of batch b+1 are computed on one worker thread while batch b's device
     # work runs (the main thread mostly waits in stream syncs); a single worker, so the shared
     # _LocalGraphs scratch is never used by two threads at once
@@ -1446,7 +1467,8 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                 tb = _stage("orders (host, wait)", tb)
                 n_list = [int(n_loc[first + b]) for b in range(cnt)]
                 with _nvtx("tls.setup.band_factor"):
-                    L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld)
+                    L, Dinv, perms, kcnts, info, P, codes = _band_factor(torch, A, perm_list, n_list, ld,
+                                                                         out=ap_buf)
                 tb = _stage("band factor", tb)
                 bad = torch.nonzero(info).flatten().cpu().numpy()
                 if bad.size:
@@ -1526,7 +1548,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         # an error in a batch must not leave the next batch's order computation running
         if order_pool is not None:
             order_pool.shutdown(cancel_futures=True)
-    del a_buf
+    del a_buf, ap_buf
     if not want_coarse:
         _release_cache(torch, dev)
         return None
@@ -1541,7 +1563,9 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         sh = tuple(z_dev[s].shape)
         z_host[s] = flat[off:off + sh[0] * sh[1]].reshape(sh)
         off += sh[0] * sh[1]
+    _log(t0, "basis copied to the host; rank filter")
     pivots = _rank_pivots(torch, z_dev, own, dev) if len(own) else []
+    _log(t0, "rank filter done")
     largest = max((p[0] for p in pivots), default=0.0)
     any_cols = float(len(pivots))
     if sharded:
@@ -1656,6 +1680,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         _make_room(torch, dev, 8 * nC * nC)
         handle.check(lib.tls_coarse_refine(handle.ctx, _lib.ptr(A0.contiguous()), s_ptr))
     torch.cuda.current_stream().synchronize()
+    _log(t0, "coarse operator uploaded")
     z_list = [z_host[s] if s in z_host else z_all[s].cpu().numpy() for s in range(N)]
     del A0inv, zcat, z_dev, z_all
     _release_cache(torch, dev)
@@ -1666,4 +1691,5 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     cd._a00_dev = A0
     cd._csr = csr
     cd._symmetric = symmetric
+    _log(t0, "build_device_operators done")
     return cd
