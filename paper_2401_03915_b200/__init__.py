@@ -7,15 +7,7 @@ numerics run in libtls_b200.so (hand-written sm_100a CUDA, C ABI in
 include/tls_b200.h).
 """
 
-import os as _os
-
-# The setup interleaves multi-GB batch workspaces with small long-lived blocks (coarse columns);
-# PyTorch's default caching allocator then pins partly-used segments and fragments the device:
-# configuration 5 (95 GB of factors + three 19 GB coarse buffers on a 178 GB device) needs its
-# expandable (virtual-memory) segments.  Read when the allocator is first used; a user setting wins.
-_os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
-
-from .errors import BreakdownError, SubdomainSetupError  # noqa: E402
+from .errors import BreakdownError, SubdomainSetupError
 from .partition import (
     Graph,
     Partition,

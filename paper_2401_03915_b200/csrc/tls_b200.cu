@@ -35,6 +35,7 @@ constexpr int MAX_GRID = 148 * 8;    // 148 SMs x 8 resident 256-thread CTAs
 constexpr int GM_FUSED_MAXCOLS = 96; // fused CGS2 step while (nc + 1) x 256 doubles fit in smem
 // shared memory of the per-warp rings of k_band_solve_ring<S> (8 warps x S tiles x 4 KB)
 constexpr size_t ring_bytes(int S) { return sizeof(double) * 8 * (size_t)S * 512; }
+constexpr size_t TMA_BAR_BYTES = 8 * 8 * 8;  // k_band_solve_tma: up to 8 mbarriers per warp
 // shared memory of k_band_solve for subdomains of up to nb 64-row blocks (local vector + scratch)
 constexpr size_t band_smem_bytes(int nb) { return sizeof(double) * ((size_t)nb * 64 + 8 * 64 + 64); }
 // largest subdomain (rows) whose local vector fits `optin` bytes of shared memory
@@ -169,6 +170,7 @@ struct tls_ctx {
   int band_pf = 2;                    // L2 prefetch distance of k_band_solve (items)
   int band_unr = 1;                   // tiles per load round (k_band_solve<UNR>)
   int band_ring = 0;                  // k_band_solve_ring (per-warp cp.async rings)
+  int band_tma = 0;                   // k_band_solve_tma<S> (rings fed by bulk TMA copies + mbarriers), S = 4 or 5
   // ---- sharding: this handle owns global subdomains [own_lo, own_hi) and the
   // rows [r0, r1) of the internal numbering (rows renumbered rank by rank: nofo[g] = internal id
   // of caller row g; identity and [0, n) on one GPU)
@@ -412,7 +414,13 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
       }
       CK(cudaEventRecordWithFlags(ctx->kt_a[ctx->kt_n], s, cudaEventRecordExternal));
     }
-    if (ctx->band_ring == 4)
+    if (ctx->band_tma == 5)
+      launch_k(ctx, k_band_solve_tma<5>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(5) + TMA_BAR_BYTES, s,
+               ctx->d_band, ctx->xloc, ctx->yloc, done, r_src ? ctx->d_gidx : nullptr, r_src);
+    else if (ctx->band_tma == 4)
+      launch_k(ctx, k_band_solve_tma<4>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4) + TMA_BAR_BYTES, s,
+               ctx->d_band, ctx->xloc, ctx->yloc, done, r_src ? ctx->d_gidx : nullptr, r_src);
+    else if (ctx->band_ring == 4)
       launch_k(ctx, k_band_solve_ring<4>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4), s, 
           ctx->d_band, ctx->xloc, ctx->yloc, done, r_src ? ctx->d_gidx : nullptr, r_src);
     else if (ctx->band_ring == 2)
@@ -934,6 +942,19 @@ int32_t tls_subdomains_upload(tls_ctx* ctx, int32_t n_sub_global, const int64_t*
     if (ctx->band_ring == 1) ctx->band_ring = 0;
     if (ctx->band_ring == 4)
       CK(raise_smem(ctx->device, (const void*)k_band_solve_ring<4>, ctx->band_smem + ring_bytes(4)));
+    // the same rings fed by the TMA engine (one 4 KB bulk copy + mbarrier per warp and tile instead
+    // of 256 16-byte cp.async): TLS_BAND_TMA=4|5 (ring depth) where the ring kernel would run
+    ctx->band_tma = 0;
+    if (const char* e = getenv("TLS_BAND_TMA")) {
+      const int v = atoi(e);
+      if ((v == 4 || v == 5) && ctx->band_ring == 4) ctx->band_tma = v;
+    }
+    if (ctx->band_tma == 5 && ctx->band_smem + ring_bytes(5) + TMA_BAR_BYTES > optin) ctx->band_tma = 4;
+    if (ctx->band_tma == 4 && ctx->band_smem + ring_bytes(4) + TMA_BAR_BYTES > optin) ctx->band_tma = 0;
+    if (ctx->band_tma == 5)
+      CK(raise_smem(ctx->device, (const void*)k_band_solve_tma<5>, ctx->band_smem + ring_bytes(5) + TMA_BAR_BYTES));
+    if (ctx->band_tma == 4)
+      CK(raise_smem(ctx->device, (const void*)k_band_solve_tma<4>, ctx->band_smem + ring_bytes(4) + TMA_BAR_BYTES));
     if (ctx->band_ring == 2)
       CK(raise_smem(ctx->device, (const void*)k_band_solve_ring<2>, ctx->band_smem + ring_bytes(2)));
     // one tile per load round: two (UNR = 2, 128 registers, 2 CTAs/SM) measured slower on
@@ -2215,7 +2236,13 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   for (int i = 0; i <= reps; ++i) {
     if (i == 1) CK(cudaEventRecord(e0, s));
     if (band)
-      if (ctx->band_ring == 4)
+      if (ctx->band_tma == 5)
+        launch_k(ctx, k_band_solve_tma<5>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(5) + TMA_BAR_BYTES, s,
+                 ctx->d_band, ctx->xloc, ctx->yloc, nullptr, nullptr, nullptr);
+      else if (ctx->band_tma == 4)
+        launch_k(ctx, k_band_solve_tma<4>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4) + TMA_BAR_BYTES, s,
+                 ctx->d_band, ctx->xloc, ctx->yloc, nullptr, nullptr, nullptr);
+      else if (ctx->band_ring == 4)
         launch_k(ctx, k_band_solve_ring<4>, ctx->nsub, NTHR, ctx->band_smem + ring_bytes(4), s, 
             ctx->d_band, ctx->xloc, ctx->yloc, nullptr, nullptr, nullptr);
       else if (ctx->band_ring == 2)
@@ -2514,9 +2541,13 @@ int32_t tls_band_cholesky(double* ap, int64_t ld, int32_t count, const int32_t* 
   const size_t smem = sizeof(double) * 4 * 64 * CP;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return TLS_ERR_CUDA;
-  // cluster of CL CTAs per subdomain (TLS_K9_CLUSTER: 1, 2 or 4; default 4) -- the trailing-band
-  // tile products of a panel run on CL SMs instead of one
-  int cl = 4;
+  // cluster of CL CTAs per subdomain (one CTA per SM: 133 KB of tiles) -- the trailing-band tile
+  // products of a panel run on CL SMs instead of one.  CL = the largest of 4, 2, 1 that keeps the
+  // whole batch in ONE wave (count * CL <= SMs): 59 subdomains x 4 CTAs ran as two waves of 9.9 ms,
+  // x 2 CTAs as one wave (TLS_K9_CLUSTER overrides).
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int cl = count * 4 <= sms ? 4 : (count * 2 <= sms ? 2 : 1);
   if (const char* e = getenv("TLS_K9_CLUSTER")) {
     const int v = atoi(e);
     if (v == 1 || v == 2 || v == 4) cl = v;

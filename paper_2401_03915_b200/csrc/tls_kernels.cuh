@@ -1977,6 +1977,300 @@ __global__ void __launch_bounds__(NTHR, S <= 2 ? 2 : 1) k_band_solve_ring(const 
   for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
 }
 
+// ---------------------------------------------------------------------------------------
+// K3e  k_band_solve_tma<S>: the per-warp rings of k_band_solve_ring fed by the TMA engine.  A
+//      warp's slice of a panel tile is 8 columns x 64 rows = 4 KB CONTIGUOUS in the packed factor,
+//      so one elected lane issues ONE bulk copy per tile (cp.async.bulk.shared.global with
+//      mbarrier::complete_tx, SASS UBLKCP) instead of 8 x 32 16-byte cp.async (LDGSTS); each ring
+//      slot has its own mbarrier (arrival count 1: the producer's expect_tx; tiles skipped as
+//      zero strips arrive without bytes), consumers spin on try_wait.parity.  The slot is refilled
+//      by the same warp after its lanes have consumed it (program order inside the warp), so no
+//      "empty" barrier is needed.  Same sweeps and arithmetic order as k_band_solve / _ring.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// producer cursor over one stream of panel tiles (modes as RingProducer); one bulk copy per tile
+struct TmaProducer {
+  int I, k, slot;
+  __device__ __forceinline__ void issue(const BandDesc& b, int mode, double* ring, unsigned long long* bars, int warp,
+                                        int lane, int S) {
+    const int c0 = warp * 8;
+    while (I >= 0 && I < b.nb) {
+      const int code = mode == 2 ? b.ucnt[I] : b.kcnt[I];
+      const int K = code & 0xffff;
+      if (k < K) break;
+      I += mode == 0 ? 1 : -1;
+      k = 0;
+    }
+    bool copy = false;
+    const double* tp = nullptr;
+    if (I >= 0 && I < b.nb) {
+      const int code = mode == 2 ? b.ucnt[I] : b.kcnt[I];
+      const int K = code & 0xffff, z = code >> 16;
+      const bool zero = mode == 2 ? (k * 8 + warp >= 8 * K - z) : (k * 8 + warp < z);
+      if (!zero) {
+        const double* base = mode == 2 ? b.udata + b.ustep_off[I] : b.data + b.step_off[I];
+        tp = base + (long long)k * TT * TT + c0 * TT;
+        copy = true;
+      }
+      ++k;
+    }
+    __syncwarp();  // every lane has consumed the slot's previous tile
+    if (lane == 0) {
+      if (copy) {
+        mbar_expect_tx(bars + slot, 4096u);
+        bulk_g2s(ring + (long long)slot * 512, tp, 4096u, bars + slot);
+      } else {
+        mbar_arrive(bars + slot);  // (skipped or past-the-end item: the phase completes without bytes)
+      }
+    }
+    slot = slot + 1 == S ? 0 : slot + 1;
+  }
+};
+
+template <int S>
+__global__ void __launch_bounds__(NTHR, 1) k_band_solve_tma(const BandDesc* __restrict__ bands,
+                                                             const double* __restrict__ x,
+                                                             double* __restrict__ y, const int* done,
+                                                             const int* __restrict__ gidx,
+                                                             const double* __restrict__ r) {
+  PDL_ENTRY();
+  if (done && *done) return;
+  extern __shared__ __align__(16) double sm[];
+  const BandDesc b = bands[blockIdx.x];
+  const int npad = b.nb * TT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c0 = warp * 8;
+  double* ringw = sm + (long long)warp * S * 512;  // this warp's ring (S x 512 doubles)
+  double* v = sm + 8 * S * 512;
+  double* red = v + npad;
+  double* t = red + 8 * TT;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(t + TT) + warp * S;  // this warp's S mbarriers
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < S; ++q) mbar_init(bars + q, 1);
+  }
+  mbar_fence_init();
+  __syncthreads();
+  unsigned cons = 0;  // tiles consumed so far (slot = cons % S, phase = (cons / S) & 1)
+  const int dlen = TT - 8 * warp;
+  const bool drow = lane >= 4 * warp;
+  const int doff = diag_strip_off(warp) + (2 * lane - 8 * warp);
+  TmaProducer prod{0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < S; ++q) prod.issue(b, 0, ringw, bars, warp, lane, S);
+  if (gidx) {
+    for (int i = threadIdx.x; i < npad; i += NTHR) {
+      const int g = __ldg(gidx + b.xoff + i);
+      v[i] = g >= 0 ? __ldg(r + g) : 0.0;
+    }
+  } else {
+    for (int i = threadIdx.x; i < npad; i += NTHR) v[i] = x[b.xoff + i];
+  }
+  __syncthreads();
+  int cs = 0;
+  // forward sweep
+  for (int I = 0; I < b.nb; ++I) {
+    const double* blk = b.data + b.step_off[I];
+    const int code = b.kcnt[I], K = code & 0xffff, fz = code >> 16;
+    double ra0 = 0.0, ra1 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      mbar_wait(bars + cs, (cons / S) & 1);
+      ++cons;
+      if (!(k * 8 + warp < fz)) {
+        const double* rs = ringw + (long long)cs * 512 + 2 * lane;
+        const double* uj = v + (I - K + k) * TT + c0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = *reinterpret_cast<const double2*>(rs + kk * 64);
+          ra0 += w.x * uj[kk];
+          ra1 += w.y * uj[kk];
+        }
+      }
+      cs = cs + 1 == S ? 0 : cs + 1;
+      prod.issue(b, 0, ringw, bars, warp, lane, S);
+    }
+    red[warp * TT + 2 * lane] = ra0;
+    red[warp * TT + 2 * lane + 1] = ra1;
+    __syncthreads();
+    if (threadIdx.x < TT) {
+      double sacc = v[I * TT + threadIdx.x];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc -= red[w * TT + threadIdx.x];
+      t[threadIdx.x] = sacc;
+    }
+    __syncthreads();
+    {
+      double d0 = 0.0, d1 = 0.0;
+      if (drow) {
+        const double* dp = blk + (long long)K * TT * TT + doff;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = ldg_stream2(dp + kk * dlen);
+          d0 += w.x * t[c0 + kk];
+          d1 += w.y * t[c0 + kk];
+        }
+      }
+      red[warp * TT + 2 * lane] = d0;
+      red[warp * TT + 2 * lane + 1] = d1;
+    }
+    __syncthreads();
+    if (threadIdx.x < TT) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc += red[w * TT + threadIdx.x];
+      v[I * TT + threadIdx.x] = sacc;
+    }
+    __syncthreads();
+  }
+  for (int q = 0; q < S; ++q) {  // the S (empty) items issued past the end of the sweep
+    mbar_wait(bars + cs, (cons / S) & 1);
+    ++cons;
+    cs = cs + 1 == S ? 0 : cs + 1;
+  }
+  __syncwarp();
+  if (b.udata) {
+    const int ulen = 8 * warp + 8;
+    const bool urow = lane <= 4 * warp + 3;
+    const int uoff = udiag_strip_off(warp) + 2 * lane;
+    TmaProducer up{b.nb - 1, 0, cs};
+#pragma unroll
+    for (int q = 0; q < S; ++q) up.issue(b, 2, ringw, bars, warp, lane, S);
+    for (int I = b.nb - 1; I >= 0; --I) {
+      const double* blk = b.udata + b.ustep_off[I];
+      const int code = b.ucnt[I], R = code & 0xffff, tz = code >> 16;
+      double ra0 = 0.0, ra1 = 0.0;
+      for (int k = 0; k < R; ++k) {
+        mbar_wait(bars + cs, (cons / S) & 1);
+      ++cons;
+        if (!(k * 8 + warp >= 8 * R - tz)) {
+          const double* rs = ringw + (long long)cs * 512 + 2 * lane;
+          const double* yj = v + (I + 1 + k) * TT + c0;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const double2 w = *reinterpret_cast<const double2*>(rs + kk * 64);
+            ra0 += w.x * yj[kk];
+            ra1 += w.y * yj[kk];
+          }
+        }
+        cs = cs + 1 == S ? 0 : cs + 1;
+        up.issue(b, 2, ringw, bars, warp, lane, S);
+      }
+      red[warp * TT + 2 * lane] = ra0;
+      red[warp * TT + 2 * lane + 1] = ra1;
+      __syncthreads();
+      if (threadIdx.x < TT) {
+        double sacc = v[I * TT + threadIdx.x];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sacc -= red[w * TT + threadIdx.x];
+        t[threadIdx.x] = sacc;
+      }
+      __syncthreads();
+      {
+        double d0 = 0.0, d1 = 0.0;
+        if (urow) {
+          const double* dp = blk + (long long)R * TT * TT + uoff;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const double2 w = ldg_stream2(dp + kk * ulen);
+            d0 += w.x * t[c0 + kk];
+            d1 += w.y * t[c0 + kk];
+          }
+        }
+        red[warp * TT + 2 * lane] = d0;
+        red[warp * TT + 2 * lane + 1] = d1;
+      }
+      __syncthreads();
+      if (threadIdx.x < TT) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sacc += red[w * TT + threadIdx.x];
+        v[I * TT + threadIdx.x] = sacc;
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
+    return;
+  }
+  // Cholesky backward: L^T y = u
+  const int colsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  TmaProducer bp{b.nb - 1, 0, cs};
+#pragma unroll
+  for (int q = 0; q < S; ++q) bp.issue(b, 1, ringw, bars, warp, lane, S);
+  for (int J = b.nb - 1; J >= 0; --J) {
+    const double* blk = b.data + b.step_off[J];
+    const int code = b.kcnt[J], K = code & 0xffff, fz = code >> 16;
+    {
+      const double u0 = v[J * TT + 2 * lane], u1 = v[J * TT + 2 * lane + 1];
+      double cp[8];
+      if (drow) {
+        const double* dp = blk + (long long)K * TT * TT + doff;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = ldg_stream2(dp + kk * dlen);
+          cp[kk] = w.x * u0 + w.y * u1;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) cp[kk] = 0.0;
+      }
+      const double yv = warp_reduce8(cp, lane);
+      __syncthreads();  // every warp has read v_J
+      if ((lane & 3) == 0) v[J * TT + c0 + colsel] = yv;
+      __syncthreads();
+    }
+    const double y0 = v[J * TT + 2 * lane], y1 = v[J * TT + 2 * lane + 1];
+    for (int k = 0; k < K; ++k) {
+      mbar_wait(bars + cs, (cons / S) & 1);
+      ++cons;
+      if (!(k * 8 + warp < fz)) {
+        const double* rs = ringw + (long long)cs * 512 + 2 * lane;
+        double cp[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 w = *reinterpret_cast<const double2*>(rs + kk * 64);
+          cp[kk] = w.x * y0 + w.y * y1;
+        }
+        const double val = warp_reduce8(cp, lane);
+        if ((lane & 3) == 0) v[(J - K + k) * TT + c0 + colsel] -= val;
+      }
+      cs = cs + 1 == S ? 0 : cs + 1;
+      bp.issue(b, 1, ringw, bars, warp, lane, S);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < npad; i += NTHR) y[b.xoff + i] = v[i];
+}
+
 // pack band steps of one subdomain batch: L (row-major ld x ld, factor order, identity
 // padding) and the inverted diagonal tiles dinv (nbmax x 64 x 64 row-major per subdomain)
 __global__ void k_pack_band(const BandDesc* __restrict__ bands, int first_band, const double* __restrict__ L,

@@ -29,30 +29,6 @@ def require_cuda(device=None):
     return torch.device(device).index if not isinstance(device, int) else device
 
 
-_ALLOC_SET = False
-
-
-def _expandable_segments():
-    """Expandable segments for torch's caching allocator (see the package __init__) when torch was
-    imported before the package set PYTORCH_CUDA_ALLOC_CONF; a user setting wins."""
-    global _ALLOC_SET
-    if _ALLOC_SET:
-        return
-    _ALLOC_SET = True
-    import os
-    if os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True") != "expandable_segments:True":
-        return
-    torch = _torch()
-    try:
-        setter = getattr(torch._C, "_accelerator_setAllocatorSettings", None)
-        if setter is not None:
-            setter("expandable_segments:True")
-        else:
-            torch.cuda.memory._set_allocator_settings("expandable_segments:True")
-    except Exception:
-        pass
-
-
 def stream_ptr():
     torch = _torch()
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -63,7 +39,6 @@ class Handle:
 
     def __init__(self, device=None):
         self.device = require_cuda(device)
-        _expandable_segments()
         self.lib = _lib.load()
         out = C.c_void_p()
         rc = self.lib.tls_ctx_create(self.device, C.byref(out))

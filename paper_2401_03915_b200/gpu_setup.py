@@ -1557,7 +1557,32 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     # one device->host copy of every owned block (the host keeps the basis for CoarseData), and
     # the column-pivoted QR of every block on the device (K12a, tls_rank_filter_pivots; the
     # reference runs LAPACK geqp3 per block)
-    flat = torch.cat([z_dev[s].reshape(-1) for s in own]).cpu().numpy() if len(own) else np.zeros(0)
+    # Defragment before the coarse stage: the per-group Z / W blocks were allocated between the
+    # multi-GB batch workspaces, so they pin partly-used allocator segments that empty_cache()
+    # cannot return.  Copy them into two flat tensors (views replace the blocks) and release the
+    # rest: the three n_C^2 coarse buffers (58 GB on configuration 5, next to 95 GB of factors)
+    # then get whole segments.  (PYTORCH_CUDA_ALLOC_CONF=expandable_segments:True also avoids the
+    # fragmentation but measured +3 s on the cold setups of configurations 2-4: every fresh block
+    # is mapped page by page.)
+    zflat = torch.cat([z_dev[s].reshape(-1) for s in own]) if len(own) else torch.zeros(0, dtype=torch.float64,
+                                                                                         device=dev)
+    off = 0
+    for s in own:
+        sh = tuple(z_dev[s].shape)
+        z_dev[s] = zflat[off:off + sh[0] * sh[1]].view(sh)
+        off += sh[0] * sh[1]
+    wl = [s for s in own if w_dev.get(s) is not None]
+    if wl:
+        wflat = torch.cat([w_dev[s].reshape(-1) for s in wl])
+        off = 0
+        for s in wl:
+            sh = tuple(w_dev[s].shape)
+            w_dev[s] = wflat[off:off + sh[0] * sh[1]].view(sh)
+            off += sh[0] * sh[1]
+        del wflat
+    _release_cache(torch, dev)
+    flat = zflat.cpu().numpy() if len(own) else np.zeros(0)
+    del zflat
     z_host, off = {}, 0
     for s in own:
         sh = tuple(z_dev[s].shape)
