@@ -205,3 +205,53 @@ def test_perm_lower_matches_torch_gathers(G):
     ref = np.stack([A[b][np.ix_(P[b], P[b])] for b in range(cnt)])
     assert np.array_equal(AP.cpu().numpy(), np.tril(ref))
     assert np.array_equal(first.cpu().numpy(), np.argmax(ref != 0, axis=2))
+
+
+@pytest.mark.parametrize("cl", [1, 2, 4])
+def test_band_cholesky_kernel_matches_lapack(G, cl, monkeypatch):
+    """K9 k_band_chol<CL> (banded Cholesky, a CL-CTA cluster per block) against LAPACK potrf on the
+    same banded SPD blocks: factor, inverted diagonal tiles, info of a non-SPD block."""
+    monkeypatch.setenv("TLS_K9_CLUSTER", str(cl))
+    rng = np.random.default_rng(cl)
+    cnt, ld, bw = 3, 320, 150
+    A = np.zeros((cnt, ld, ld))
+    for b in range(cnt):
+        M = rng.standard_normal((ld, ld))
+        M = np.tril(np.triu(M, -bw), bw)
+        A[b] = M @ M.T * 0.05 + np.diag(2.0 + rng.random(ld))
+        A[b] = np.tril(np.triu(A[b], -bw), bw)
+        A[b] += np.eye(ld) * (np.abs(A[b]).sum(axis=1).max())      # diagonally dominant -> SPD
+    A[2, 200, 200] = -1.0                                           # not positive definite
+    nbk = ld // 64
+    rows = np.arange(ld)
+    first = np.maximum(rows - bw, 0)
+    kmax = (np.arange(nbk) - first.reshape(nbk, 64).min(axis=1) // 64).clip(min=0)
+    AP = torch.as_tensor(np.tril(A), device="cuda").contiguous()
+    L, Dinv, info = G.band_cholesky_kernel(torch, AP, kmax, clear_upper=False)
+    L, Dinv, info = L.cpu().numpy(), Dinv.cpu().numpy(), info.cpu().numpy()
+    assert info[0] == 0 and info[1] == 0 and info[2] == 201
+    for b in range(2):
+        ref = np.linalg.cholesky(A[b])
+        assert np.abs(L[b] - ref).max() <= 1e-12 * np.abs(ref).max()
+        assert np.abs(np.triu(L[b], 1)).max() == 0.0
+        for J in range(nbk):
+            d = ref[64 * J:64 * J + 64, 64 * J:64 * J + 64]
+            assert np.abs(Dinv[b, J] @ d - np.eye(64)).max() <= 1e-11
+
+
+def test_tma_ring_kernel_is_bit_identical(G, monkeypatch):
+    """K3e k_band_solve_tma (rings fed by bulk TMA copies + mbarriers) against the default cp.async
+    ring kernel on the same band factors: identical sweeps, so identical bits (Cholesky and LU)."""
+    import paper_2401_03915_b200 as B
+    for cid, m, part in ((1, 48, 16), (3, 48, 16)):
+        cfg = B.problems.CONFIGS[cid].scaled(m, part)
+        a, sym, owner, nsub = cfg.build()
+        mat = B.SparseMat(a, symmetric=sym)
+        r = np.random.default_rng(7).standard_normal(a.shape[0])
+        outs = []
+        for tma in ("0", "4", "5"):
+            monkeypatch.setenv("TLS_BAND_TMA", tma)
+            pre = B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=4, local="band")
+            assert pre.local_kind.startswith("band")
+            outs.append(pre.apply_one_level(r))
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
