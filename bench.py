@@ -428,7 +428,10 @@ def main():
         return
 
     import torch
-    if world > 1:
+    # TLS_SHARD_SINGLE=1 under torchrun --nproc-per-node 1: the sharded path (NCCL transport) on
+    # a group of one rank -- what a 1-GPU box can execute of the multi-GPU path
+    single = world == 1 and os.environ.get("TLS_SHARD_SINGLE") == "1" and "RANK" in os.environ
+    if world > 1 or single:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -443,9 +446,9 @@ def main():
     log(f"n={a.shape[0]} nnz={a.nnz}; setup")
     mat = B.SparseMat(a, symmetric=sym)
     shard = None
-    if world > 1:
+    if world > 1 or single:
         from paper_2401_03915_b200.distributed import world_shard
-        shard = world_shard()
+        shard = world_shard(single=single)
     t0 = time.perf_counter()
     with _StdoutToStderr():
         pre = B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes, shard=shard)
@@ -555,8 +558,8 @@ def main():
                     "setup_s": t_setup, "generate_s": t_gen,
                     "time_to_solution_s": t_setup + ms / args.steps / 1e3,
                     "device_bytes": pre.device_bytes(),
-                    "parallelism": (f"subdomain/row slabs x{world} (NCCL halo + all-reduce)" if world > 1
-                                    else "1 GPU")},
+                    "parallelism": (f"subdomain/row slabs x{world} (NCCL halo + all-reduce)"
+                                    if world > 1 or single else "1 GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_kind": peak_kind,
@@ -585,7 +588,7 @@ def main():
         line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if world > 1 or single:
         torch.distributed.destroy_process_group()
 
 

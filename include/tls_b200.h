@@ -283,6 +283,10 @@ int32_t tls_comm_init_record(tls_ctx* ctx, int32_t nranks, int32_t rank);
  * communicator).  Without it c = Z^T r is summed by an all-reduce of the whole n_C vector. */
 int32_t tls_set_coarse_layout(tls_ctx* ctx, int32_t nranks, const int64_t* col_starts);
 int64_t tls_comm_record_log(const tls_ctx* ctx, int64_t* out, int64_t cap);
+/* Transport of the handle: 0 none (plain single-GPU path), 1 NCCL, 2 in-process group,
+ * 3 recording.  out3 (may be NULL): all-reduce / exchange / all-gather calls issued through the
+ * NCCL API so far (a captured call counts once per capture, not per graph replay). */
+int32_t tls_comm_info(const tls_ctx* ctx, int64_t* out3);
 
 /* ---- measurement: average device time (ms) of the dominant kernel (batched local
  * solve) over the last solve, timed with CUDA events on the launching stream, and

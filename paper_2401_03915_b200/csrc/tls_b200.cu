@@ -487,7 +487,9 @@ static int enq_prolong(tls_ctx* ctx, cudaStream_t s, const double* qv, const dou
 
 static bool has_coarse(const tls_ctx* ctx) { return ctx->ncoarse > 0 && ctx->combine != TLS_NONE; }
 
-static bool sharded(const tls_ctx* ctx) { return ctx->comm != nullptr && ctx->comm->nranks > 1; }
+// a communicator of one rank (Shard(single=True): the NCCL transport exercised on a 1-GPU box) runs
+// the sharded schedule as well; the plain single-GPU path never creates a communicator
+static bool sharded(const tls_ctx* ctx) { return ctx->comm != nullptr; }
 
 static int nown(const tls_ctx* ctx) { return ctx->r1 - ctx->r0; }
 
@@ -2713,6 +2715,17 @@ int32_t tls_comm_init_record(tls_ctx* ctx, int32_t nranks, int32_t rank) {
   ctx->comm = c;
   destroy_graphs(ctx);
   return TLS_OK;
+}
+
+// transport of the handle: 0 none (plain single-GPU path), 1 NCCL, 2 in-process group,
+// 3 recording; out3 (optional) = all-reduce / exchange / all-gather calls issued so far through
+// the NCCL API (captured calls count once per capture, not per replay)
+int32_t tls_comm_info(const tls_ctx* ctx, int64_t* out3) {
+  if (!ctx) return -1;
+  if (!ctx->comm) return 0;
+  if (out3)
+    for (int i = 0; i < 3; ++i) out3[i] = ctx->comm->calls[i];
+  return ctx->comm->kind();
 }
 
 int64_t tls_comm_record_log(const tls_ctx* ctx, int64_t* out, int64_t cap) {

@@ -40,7 +40,9 @@ struct XPlan {
 
 struct Comm {
   int rank = 0, nranks = 1;
+  long long calls[3] = {0, 0, 0};  // all-reduces, exchanges, all-gathers issued (tls_comm_info)
   virtual ~Comm() {}
+  virtual int kind() const = 0;    // 1 NCCL, 2 in-process group, 3 recording
   virtual cudaError_t allreduce_sum(double* buf, long long count, cudaStream_t s, std::string& err) = 0;
   virtual cudaError_t exchange(const XPlan& x, cudaStream_t s, std::string& err) = 0;
   // recv[q * count + i] = send of rank q [i], i < count (every rank sends `count` doubles)
@@ -98,7 +100,9 @@ struct NcclComm : Comm {
   ~NcclComm() override {
     if (comm) nccl_api().destroy(comm);
   }
+  int kind() const override { return 1; }
   cudaError_t allreduce_sum(double* buf, long long count, cudaStream_t s, std::string& err) override {
+    ++calls[0];
     ncclResult_t r = nccl_api().allreduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, comm, s);
     if (r != ncclSuccess) {
       err = std::string("ncclAllReduce: ") + nccl_api().errstr(r);
@@ -109,6 +113,7 @@ struct NcclComm : Comm {
   // grouped send/recv with every peer of the plan (one NCCL group = one fused launch)
   cudaError_t exchange(const XPlan& x, cudaStream_t s, std::string& err) override {
     NcclApi& api = nccl_api();
+    ++calls[1];
     ncclResult_t r = api.group_start();
     for (size_t k = 0; k < x.peers.size() && r == ncclSuccess; ++k) {
       if (x.scnt[k] > 0) r = api.send(x.sbuf + x.soff[k], (size_t)x.scnt[k], ncclFloat64, x.peers[k], comm, s);
@@ -125,6 +130,7 @@ struct NcclComm : Comm {
   }
   cudaError_t allgather(const double* send, long long count, double* recv, cudaStream_t s,
                         std::string& err) override {
+    ++calls[2];
     ncclResult_t r = nccl_api().allgather(send, recv, (size_t)count, ncclFloat64, comm, s);
     if (r != ncclSuccess) {
       err = std::string("ncclAllGather: ") + nccl_api().errstr(r);
@@ -141,6 +147,7 @@ struct NcclComm : Comm {
 // exactly as the NCCL transport would and compare the per-rank collective sequences.
 struct RecordComm : Comm {
   std::vector<long long> log;  // triples: kind (1 all-reduce, 2 exchange, 3 all-gather), count, peers
+  int kind() const override { return 3; }
   cudaError_t allreduce_sum(double*, long long count, cudaStream_t, std::string&) override {
     log.insert(log.end(), {1LL, count, 0LL});
     return cudaSuccess;
@@ -212,6 +219,7 @@ struct GroupComm : Comm {
   ~GroupComm() override {
     if (tmp) cudaFree(tmp);
   }
+  int kind() const override { return 2; }
   cudaError_t allreduce_sum(double* buf, long long count, cudaStream_t s, std::string& err) override {
     cudaError_t e;
     if (count > tmp_cap) {

@@ -264,18 +264,27 @@ class ThreadCollective:
 class Shard:
     """What one rank needs: its collective, the solve-time transport, and its slab."""
 
-    def __init__(self, collective, transport="nccl", group_handle=None):
+    def __init__(self, collective, transport="nccl", group_handle=None, single=False):
         self.coll = collective
         self.rank = collective.rank
         self.nranks = collective.nranks
         self.transport = transport          # "nccl" | "group"
         self.group_handle = group_handle    # tls_group* for transport "group"
+        # ``single``: run the sharded schedule (row renumbering, halo plans, communicator and the
+        # collectives captured in the solve graphs) on a group of ONE rank too, instead of the
+        # plain single-GPU path -- the only way to execute the NCCL transport on a 1-GPU box
+        self.single = bool(single)
         self.lo = self.hi = None
+
+    @property
+    def active(self):
+        """Whether setup and the solves take the sharded path."""
+        return self.nranks > 1 or self.single
 
     def attach(self, handle):
         """Create this rank's solve-time communicator inside the library handle."""
         lib = handle.lib
-        if self.nranks == 1:
+        if not self.active:
             return
         if self.transport == "group":
             handle.check(lib.tls_comm_init_group(handle.ctx, self.group_handle, self.rank))
@@ -338,6 +347,6 @@ class LocalGroup:
             self.ptr = None
 
 
-def world_shard():
+def world_shard(single=False):
     """Shard over the default torch.distributed group (one process per GPU, NCCL)."""
-    return Shard(TorchCollective(), "nccl")
+    return Shard(TorchCollective(), "nccl", single=single)

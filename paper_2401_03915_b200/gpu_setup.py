@@ -1317,7 +1317,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     n_loc = np.array([m.n_local for m in maps], dtype=np.int64)
     n_int = np.array([m.interior.size for m in maps], dtype=np.int64)
     n_bnd = np.array([m.n_boundary for m in maps], dtype=np.int64)
-    sharded = shard is not None and shard.nranks > 1
+    sharded = shard is not None and shard.active
     if sharded:
         from .distributed import slab_ranges
         lo, hi = slab_ranges(n_loc.astype(np.float64) ** 2, shard.nranks)[shard.rank]

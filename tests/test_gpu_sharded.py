@@ -222,3 +222,28 @@ def test_sharded_schedule_captures_into_graphs(B, name, solver):
     ar = logs[0][:, 0] == 1
     assert np.array_equal(logs[0][ar, 1], logs[1][ar, 1])
     assert (logs[0][:, 0] == 2).any()  # halo exchanges are part of the captured schedule
+
+
+def test_nccl_transport_single_rank_group():
+    """The NCCL transport itself, on the one GPU a box has: a torch.distributed group of one rank
+    (backend nccl) takes the sharded path (Shard(single=True)) -- setup collectives over NCCL,
+    ncclCommInitRank inside the library, the schedule's collectives issued through the NCCL API
+    inside the captured PCG / GMRES graphs -- and must reproduce the unsharded results.  Runs in a
+    subprocess (tools/nccl_single.py) so the process group does not outlive the test."""
+    import json
+    import os
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_PORT", "MASTER_ADDR")}
+    p = subprocess.run([sys.executable, os.path.join(repo, "tools", "nccl_single.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-4000:]
+    out = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["ok"] and out["backend"] == "nccl" and out["world_size"] == 1
+    for c in out["cases"]:
+        assert c["comm_kind"] == 1 and c["nccl_calls"]["allreduce"] > 0, c
+    assert out["cases"][0]["nccl_calls"]["allgather"] > 0  # the coarse restriction's all-gather
