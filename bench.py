@@ -449,6 +449,13 @@ def main():
     if world > 1 or single:
         from paper_2401_03915_b200.distributed import world_shard
         shard = world_shard(single=single)
+    # one-time process initialisation (CUDA context, cuBLAS / cuSOLVER handles and their lazily
+    # loaded kernels), timed on its own: setup_s is the preconditioner setup proper, and
+    # time_to_solution_s = library_init_s + setup_s + one solve
+    t0 = time.perf_counter()
+    from paper_2401_03915_b200.gpu_setup import warm_linalg
+    warm_linalg()
+    t_init = time.perf_counter() - t0
     t0 = time.perf_counter()
     with _StdoutToStderr():
         pre = B.setup(mat, nsub, overlap=cfg.overlap, owner=owner, n_modes=cfg.n_modes, shard=shard)
@@ -555,8 +562,8 @@ def main():
                     "coarse_refined": bool(getattr(cs, "refined", False)) if cs is not None else False,
                     "final_rel_residual": float(rep.residuals[-1]), "true_rel_residual": true_res,
                     "converged": bool(rep.converged),
-                    "setup_s": t_setup, "generate_s": t_gen,
-                    "time_to_solution_s": t_setup + ms / args.steps / 1e3,
+                    "setup_s": t_setup, "library_init_s": t_init, "generate_s": t_gen,
+                    "time_to_solution_s": t_init + t_setup + ms / args.steps / 1e3,
                     "device_bytes": pre.device_bytes(),
                     "parallelism": (f"subdomain/row slabs x{world} (NCCL halo + all-reduce)"
                                     if world > 1 or single else "1 GPU")},

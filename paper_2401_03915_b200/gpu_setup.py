@@ -55,6 +55,9 @@ TIE_GUARD = 1e-12
 TOPK_TAU = 1e-300
 EPS = float(np.finfo(float).eps)
 REFINE_COND = 1.0e8  # cond_1(A0) above which every coarse solve gets one refinement step
+# SPD A0 of at least this order whose half bandwidth is < n_C / 4 is inverted by the
+# block-tridiagonal recurrences (spd_inverse_block_tridiagonal) instead of dense potrf + potri
+BAND_INVERSE_MIN = int(os.environ.get("TLS_A0_BANDED_MIN", "4096"))
 
 
 class CoarseData:
@@ -1280,6 +1283,78 @@ def assemble_a0_columns(maps, owner, z_blocks, w_blocks, counts, own, device):
     return A0
 
 
+def coarse_bandwidth(maps, owner, counts, own):
+    """Half bandwidth (in coarse columns) of A0 = Z^T A Z from its block structure: the block
+    (j, s) is structurally nonzero only when subdomain j owns a row of subdomain s's index set
+    (the (s, j) groups of ``assemble_a0_columns``); the largest column distance inside such a
+    block pair bounds |row - col| over all nonzeros."""
+    cstart = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    bw = 0
+    for s in own:
+        if counts[s] == 0:
+            continue
+        js = np.unique(owner[maps[s].indices])
+        js = js[np.asarray(counts)[js] > 0]
+        if js.size == 0:
+            continue
+        lo_, hi_ = int(min(js.min(), s)), int(max(js.max(), s))
+        # farthest column of a coupled block from a column of block s, either side
+        bw = max(bw, int(cstart[hi_ + 1] - cstart[s]) - 1, int(cstart[s + 1] - cstart[lo_]) - 1)
+    return bw
+
+
+def spd_inverse_block_tridiagonal(torch, A, bs):
+    """In place: the lower triangle (and the full diagonal blocks) of A^{-1} for an SPD matrix
+    whose nonzeros lie within the block-tridiagonal pattern of block size ``bs`` (half bandwidth
+    < bs); only the lower triangle of ``A`` is read.  Returns 0, or the 1-based index of the
+    leading minor that is not positive definite (LAPACK potrf's info).
+
+    A0 = Z^T A Z couples neighbouring subdomains only, so in subdomain order it is banded
+    (configuration 5: n_C = 49,152, half bandwidth 3,287).  A dense potrf + potri costs n^3
+    flops (119 TFLOP, 7.1 s through cuSOLVER); here
+      * block Cholesky of the tridiagonal blocks: L_ii, L_{i+1,i}, and G_i = L_{i+1,i} L_ii^{-1};
+      * X = A^{-1} from X L = L^{-T} column block by column block, last to first:
+        X_{j,i} = -X_{j,i+1} G_i (j > i),  X_ii = L_ii^{-T} L_ii^{-1} - G_i^T X_{i+1,i}
+      -- a right-hand triangular substitution with the Cholesky factor (as backward stable as
+      potri's), ~ bs * n^2 flops (11 TFLOP there), all cuBLAS GEMMs on (n - r) x bs panels, and
+      one n_C^2 buffer instead of three (src/coarse.py:178-182 factorises A0 and solves).
+    """
+    n = A.shape[0]
+    cuts = list(range(0, n, bs)) + [n]
+    nb = len(cuts) - 1
+    G = [None] * nb
+    Dinv = [None] * nb
+    Lprev = None
+    for i in range(nb):
+        r0, r1 = cuts[i], cuts[i + 1]
+        Aii = A[r0:r1, r0:r1]
+        if i > 0:
+            p0 = cuts[i - 1]
+            # L_{i,i-1} = A_{i,i-1} L_{i-1,i-1}^{-T};  G_{i-1} = L_{i,i-1} L_{i-1,i-1}^{-1}
+            Lij = torch.linalg.solve_triangular(Lprev, A[r0:r1, p0:r0].mT, upper=False).mT
+            Aii = Aii - Lij @ Lij.mT
+            G[i - 1] = torch.linalg.solve_triangular(Lprev.mT, Lij.mT, upper=True).mT.contiguous()
+            del Lij
+        Lii, info = torch.linalg.cholesky_ex(Aii)
+        del Aii
+        if int(info) != 0:
+            return r0 + int(info)
+        Dinv[i] = torch.cholesky_inverse(Lii)
+        Lprev = Lii
+    del Lprev, Lii
+    r0 = cuts[nb - 1]
+    A[r0:, r0:] = Dinv[nb - 1]
+    Dinv[nb - 1] = None
+    for i in range(nb - 2, -1, -1):
+        r0, r1, r2 = cuts[i], cuts[i + 1], cuts[i + 2]
+        A[r1:, r0:r1] = -(A[r1:, r1:r2] @ G[i])
+        D = Dinv[i] - G[i].mT @ A[r1:r2, r0:r1]
+        A[r0:r1, r0:r1] = 0.5 * (D + D.mT)
+        G[i] = Dinv[i] = None
+        del D
+    return 0
+
+
 def _band_bytes(codes):
     """Device bytes the library allocates for band panels with these codes (band_layout)."""
     k = (np.asarray(codes, dtype=np.int64) & 0xFFFF)
@@ -1635,7 +1710,16 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
                           [0] * N, 0) if any_cols > 0 else None
     nC = int(counts.sum())
     owner = np.asarray(owner, dtype=np.int64)
-    _make_room(torch, dev, 8 * nC * nC * 3)  # A0, its factor and inverse (torch allocations)
+    # half bandwidth of A0 from its block structure (max over the ranks)
+    a0_band = coarse_bandwidth(maps, owner, counts, own) if symmetric else nC
+    if sharded:
+        t = torch.tensor([float(a0_band)], dtype=torch.float64, device=dev)
+        shard.coll.allreduce(t, op="max")
+        a0_band = int(t[0])
+    banded = (symmetric and nC >= BAND_INVERSE_MIN and 4 * (-(-(a0_band + 1) // 64) * 64) <= nC
+              and os.environ.get("TLS_A0_BANDED", "1") != "0")
+    # dense path: A0, its factor and inverse (torch allocations); banded: one buffer + panels
+    _make_room(torch, dev, 8 * nC * nC * (3 if not banded else 1) + (8 * nC * 4 * a0_band if banded else 0))
     if VERBOSE:
         _log(t0, "stage times: " + ", ".join(f"{k} {v:.2f}s" for k, v in _STAGE.items()))
     _log(t0, f"local operators done; assembling A0 ({nC} x {nC})")
@@ -1652,7 +1736,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     # 19.3 GB) is rebuilt on demand from the basis
     keep_a0 = 8 * nC * nC <= (4 << 30)
     norm_a0 = None
-    if not keep_a0:  # the factor and the inverse are two more n_C^2 buffers: defragment first
+    if not keep_a0 and not banded:  # the factor and the inverse are two more n_C^2 buffers: defragment first
         torch.cuda.empty_cache()
     if symmetric:
         # symmetrise (src/coarse.py:169-170) the lower triangle Cholesky reads, in place
@@ -1660,15 +1744,29 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         if keep_a0:
             A0 = torch.tril(A0) + torch.tril(A0, -1).mT
             norm_a0 = float(A0.abs().sum(0).max())
-        L, info = torch.linalg.cholesky_ex(A0)
-        if not keep_a0:
-            del A0
-            A0 = None
-        if int(info) != 0:
-            raise RuntimeError(f"coarse operator is not positive definite: {int(info)}-th leading minor")
-        # the packed-tile store reads the lower triangle (and full diagonal tiles) only
-        A0inv = torch.cholesky_inverse(L).contiguous()
-        del L
+        # A0 couples neighbouring subdomains only: when its band is narrow (configuration 5:
+        # 3.3k of 49k) the inverse comes from the block-tridiagonal recurrences, in place
+        bs = -(-(a0_band + 1) // 64) * 64
+        if banded:
+            A0inv = A0.clone() if keep_a0 else A0
+            if not keep_a0:
+                A0 = None
+            info = spd_inverse_block_tridiagonal(torch, A0inv, bs)
+            if info != 0:
+                raise RuntimeError(f"coarse operator is not positive definite: {info}-th leading minor")
+            if keep_a0:  # cond_1 below sums whole columns
+                A0inv = torch.tril(A0inv) + torch.tril(A0inv, -1).mT
+            _log(t0, f"A0^-1 by block-tridiagonal recurrences (half bandwidth {a0_band}, block {bs})")
+        else:
+            L, info = torch.linalg.cholesky_ex(A0)
+            if not keep_a0:
+                del A0
+                A0 = None
+            if int(info) != 0:
+                raise RuntimeError(f"coarse operator is not positive definite: {int(info)}-th leading minor")
+            # the packed-tile store reads the lower triangle (and full diagonal tiles) only
+            A0inv = torch.cholesky_inverse(L).contiguous()
+            del L
     else:
         norm_a0 = float(A0.abs().sum(0).max())
         LU, piv, info = torch.linalg.lu_factor_ex(A0)

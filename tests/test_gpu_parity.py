@@ -381,3 +381,33 @@ def test_matrix_upload_refuses_malformed_csr(B):
             h.upload_matrix(bad, True)
     h.upload_matrix(csr([0, 1, 2, 3], [0, 1, 2]), True)  # the handle stays usable
     assert h.n == 3
+
+
+@pytest.mark.parametrize("name", ["cfg2_m48", "cfg2_m24"])
+def test_banded_coarse_inverse_matches_dense_path(B, name, monkeypatch):
+    """A0^{-1} by the block-tridiagonal recurrences (gpu_setup.spd_inverse_block_tridiagonal, the
+    path configuration 5 takes at full size) against the dense potrf + potri path on the same
+    setup, and against the reference's coarse apply (src/coarse.py:40-49, 178-182)."""
+    from paper_2401_03915_b200 import gpu_setup as G
+    d = golden(name)
+    a = golden_csr(d)
+    mat = B.SparseMat(a, symmetric=True)
+    kw = dict(overlap=int(d["overlap"]), owner=d["owner"], coarse=str(d["coarse"]), n_modes=int(d["n_modes"]))
+    monkeypatch.setattr(G, "BAND_INVERSE_MIN", 64)
+    seen = []
+    real = G.spd_inverse_block_tridiagonal
+    monkeypatch.setattr(G, "spd_inverse_block_tridiagonal", lambda t, A, bs: (seen.append(bs), real(t, A, bs))[1])
+    pre_b = B.setup(mat, int(d["n_sub"]), **kw)
+    monkeypatch.setenv("TLS_A0_BANDED", "0")
+    pre_d = B.setup(mat, int(d["n_sub"]), **kw)
+    if name == "cfg2_m48":   # 6^3 subdomains x 16 columns: band 704 of 3456
+        assert len(seen) == 1 and 4 * seen[0] <= pre_b.report.n_coarse
+    r = d["r"][0]
+    zb, zd, zr = pre_b.coarse_apply(r), pre_d.coarse_apply(r), d["z_coarse"][0]
+    np.testing.assert_allclose(zb, zd, rtol=0, atol=1e-12 * np.abs(zd).max())
+    np.testing.assert_allclose(zb, zr, rtol=0, atol=1e-10 * np.abs(zr).max())
+    c = np.random.default_rng(2).standard_normal(pre_b.report.n_coarse)
+    yb, yd = pre_b.coarse.solve_coarse(c), pre_d.coarse.solve_coarse(c)
+    np.testing.assert_allclose(yb, yd, rtol=0, atol=1e-12 * np.abs(yd).max())
+    x, rep = B.pcg(mat, pre_b, d["b"], tol=float(d["tol"]))
+    assert rep.converged and abs(rep.iterations - int(d["iterations"])) <= 1

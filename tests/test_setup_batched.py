@@ -145,3 +145,61 @@ def test_pou_columns_equal_full_pencil():
         got = _pou_columns(torch, torch.as_tensor(A), n, ni, nu).numpy()
         assert got.shape[1] == ref.shape[1] and got.shape[1] > 0
         np.testing.assert_allclose(got, ref[:ni], rtol=0, atol=1e-10 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("n,bw,bs,scale", [(1000, 90, 128, 1.5), (777, 63, 64, 1.5), (512, 300, 512, 1.5),
+                                           (640, 63, 64, 1.0 + 1e-7)])
+def test_spd_inverse_block_tridiagonal_matches_dense(n, bw, bs, scale):
+    """The block-tridiagonal recurrences give the lower triangle and the full diagonal blocks of
+    A^{-1} (only A's lower triangle read), to the accuracy of the dense Cholesky inverse -- also
+    on an ill-conditioned matrix (last case: diagonally semi-dominant, cond ~ 1e7)."""
+    rng = np.random.default_rng(n)
+    mask = np.abs(np.subtract.outer(np.arange(n), np.arange(n))) <= bw
+    B = np.abs(rng.standard_normal((n, n))) * mask
+    A = -(B + B.T) / 2
+    np.fill_diagonal(A, 0.0)
+    np.fill_diagonal(A, -A.sum(axis=1) * scale)   # weakly diagonally dominant M-matrix: SPD
+    ref = np.linalg.inv(A)
+    X = torch.tril(torch.tensor(A)) + torch.triu(torch.full((n, n), 7.0, dtype=torch.float64), 1)
+    assert G.spd_inverse_block_tridiagonal(torch, X, bs) == 0
+    X = X.numpy()
+    dense = torch.cholesky_inverse(torch.linalg.cholesky(torch.tensor(A))).numpy()
+    tol = max(1e-13, 20 * np.abs(dense - ref).max() / np.abs(ref).max())
+    assert np.abs(np.tril(X) - np.tril(ref)).max() <= tol * np.abs(ref).max()
+    for r in range(0, n, bs):   # diagonal blocks are stored in full (the packed-tile store reads them)
+        assert np.abs(X[r:r + bs, r:r + bs] - ref[r:r + bs, r:r + bs]).max() <= tol * np.abs(ref).max()
+    # residual of the symmetric completion: A X = I
+    Xs = np.tril(X) + np.tril(X, -1).T
+    assert np.abs(A @ Xs - np.eye(n)).max() <= 1e-9 * max(1.0, np.linalg.cond(A) * 1e-7)
+
+
+def test_spd_inverse_block_tridiagonal_flags_indefinite():
+    n, bs = 300, 64
+    A = np.eye(n) * 2.0
+    A[200, 200] = -1.0
+    X = torch.tensor(A)
+    assert G.spd_inverse_block_tridiagonal(torch, X, bs) == 201
+
+
+def test_coarse_bandwidth_bounds_a0_nonzeros():
+    """Every structurally nonzero entry of A0 = Z^T A Z lies within the half bandwidth computed from
+    the subdomain adjacency (the block-tridiagonal inverse relies on it)."""
+    d = golden("cfg2_m24")
+    a = golden_csr(d)
+    nsub = int(d["n_sub"])
+    owner = np.asarray(d["owner"], dtype=np.int64)
+    from paper_2401_03915_b200.sparsemat import SparseMat, symmetrized_graph
+    maps = Pt.extend_overlap(symmetrized_graph(SparseMat(a, symmetric=True)), Pt.Partition(nsub, owner),
+                             int(d["overlap"]))
+    rng = np.random.default_rng(1)
+    for counts in (rng.integers(0, 5, nsub), np.full(nsub, 3)):
+        cstart = np.concatenate([[0], np.cumsum(counts)])
+        nC = int(cstart[-1])
+        Z = np.zeros((a.shape[0], nC))
+        for s, m in enumerate(maps):
+            Z[np.ix_(m.interior, np.arange(cstart[s], cstart[s + 1]))] = rng.standard_normal((m.interior.size, counts[s]))
+        A0 = Z.T @ (a @ Z)
+        bw = G.coarse_bandwidth(maps, owner, counts, range(nsub))
+        i, j = np.nonzero(A0)
+        assert np.abs(i - j).max() <= bw < nC
+    assert np.abs(i - j).max() == bw   # dense blocks: the bound is attained
