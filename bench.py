@@ -205,6 +205,8 @@ def iteration_bytes(cfg, a, pre, local_bytes):
     if nC and pre.coarse is not None:
         zk = float(sum(m.interior.size * k for m, k in zip(pre.maps, pre.coarse.column_counts())))
         a0 = 8.0 * nC * (nC + 1) / 2 if pre.report.symmetric else 8.0 * nC * nC
+        if getattr(pre.coarse, "solve_kind", "") == "block-tridiagonal":
+            a0 = pre.coarse.solve_bytes  # inverted Schur blocks (twice) + sparse off-diagonal blocks
         coarse = 16.0 * zk + 24.0 * n + a0
     if cfg.solver == "pcg":
         total = spmv + local + coarse + 80.0 * n + (spmv + 24.0 * n) / 25.0
@@ -559,6 +561,8 @@ def main():
                     "min_cut_gap": (min(cs.cut_gaps.values()) if cs is not None
                                     and getattr(cs, "cut_gaps", None) else None),
                     "coarse_cond1": getattr(cs, "cond1", None) if cs is not None else None,
+                    "coarse_solve": getattr(cs, "solve_kind", None) if cs is not None else None,
+                    "coarse_solve_bytes": getattr(cs, "solve_bytes", None) if cs is not None else None,
                     "coarse_refined": bool(getattr(cs, "refined", False)) if cs is not None else False,
                     "final_rel_residual": float(rep.residuals[-1]), "true_rel_residual": true_res,
                     "converged": bool(rep.converged),

@@ -133,9 +133,26 @@ int32_t tls_store_local_band_lu(tls_ctx* ctx, int32_t first, int32_t count, cons
  * n_interior[s] x k[s] stored column by column (k[s] x n_interior[s] row-major, device,
  * concatenated in subdomain order), columns
  * [col_start[s], col_start[s]+k[s]) of the global basis; a0inv = (Z^T A Z)^{-1}
- * (row-major n_coarse^2, device).  k == NULL or n_coarse == 0 disables the coarse level. */
+ * (row-major n_coarse^2, device; NULL when tls_coarse_chain supplies the operator).  k == NULL or
+ * n_coarse == 0 disables the coarse level. */
 int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, const double* basis,
                           const double* a0inv, void* stream);
+/* Block-tridiagonal coarse solve instead of a stored dense inverse (call tls_coarse_upload with
+ * a0inv == NULL first).  A0 = Z^T A Z (src/coarse.py:158-170) couples neighbouring subdomains
+ * only, so in subdomain order it is block tridiagonal for blocks of block_size >= half bandwidth
+ * + 1 columns (a multiple of 64; n_blocks = ceil(n_coarse / block_size) >= 2).  sinv[i] (host
+ * array of n_blocks DEVICE addresses): the inverse of the Schur block S_i (S_0 = A_00,
+ * S_i = A_ii - A_{i,i-1} S_{i-1}^{-1} A_{i-1,i}), row-major n_i x n_i, symmetric.  lo_* / up_*:
+ * the strictly block-lower part of A0 and its transpose as CSR over all n_coarse rows with
+ * global column indices (device, int32 / fp64, nnz entries each).  The coarse solve of
+ * src/coarse.py:178-182 (a Cholesky solve with A0) then runs as a block forward / backward
+ * substitution: 2 n_blocks - 1 products with the S_i^{-1} tiles and 2 (n_blocks - 1) sparse block
+ * rows -- ~2 n_C * block_size doubles per solve instead of n_C^2 / 2.  Symmetric operators only;
+ * excludes tls_coarse_refine.  Call before tls_precond_finalize. */
+int32_t tls_coarse_chain(tls_ctx* ctx, int32_t n_blocks, int32_t block_size, const uint64_t* sinv,
+                         const int32_t* lo_indptr, const int32_t* lo_indices, const double* lo_values,
+                         const int32_t* up_indptr, const int32_t* up_indices, const double* up_values,
+                         int64_t nnz, void* stream);
 /* One step of iterative refinement on every coarse solve: y = X c; y += X (c - A0 y), X the
  * stored A0^{-1}.  a0 = Z^T A Z (row-major n_coarse^2, device).  The reference solves with an LU /
  * Cholesky factor of A0 (src/coarse.py:172-182, backward stable); the explicit inverse alone
@@ -287,6 +304,11 @@ int64_t tls_comm_record_log(const tls_ctx* ctx, int64_t* out, int64_t cap);
  * 3 recording.  out3 (may be NULL): all-reduce / exchange / all-gather calls issued through the
  * NCCL API so far (a captured call counts once per capture, not per graph replay). */
 int32_t tls_comm_info(const tls_ctx* ctx, int64_t* out3);
+/* How the coarse solve of src/coarse.py:178-182 runs (after tls_precond_finalize): 0 no coarse
+ * level, 1 stored dense A0^{-1} tiles, 2 block-tridiagonal substitution (tls_coarse_chain).
+ * out4 (may be NULL): {n_coarse, blocks, block size, algorithmic bytes one coarse solve streams
+ * on this rank}. */
+int32_t tls_coarse_info(const tls_ctx* ctx, double* out4);
 
 /* ---- measurement: average device time (ms) of the dominant kernel (batched local
  * solve) over the last solve, timed with CUDA events on the launching stream, and

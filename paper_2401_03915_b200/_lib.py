@@ -63,6 +63,7 @@ SIGNATURES = {
     "tls_apply_one_level": (_I32, [_P, _P, _P, _P]),
     "tls_coarse_apply": (_I32, [_P, _P, _P, _P]),
     "tls_coarse_refine": (_I32, [_P, _P, _P]),
+    "tls_coarse_chain": (_I32, [_P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I64, _P]),
     "tls_local_solve": (_I32, [_P, _P, _I32, _P, _P, _P]),
     "tls_coarse_restrict": (_I32, [_P, _P, _P, _P]),
     "tls_coarse_solve": (_I32, [_P, _P, _P, _P]),
@@ -96,6 +97,7 @@ SIGNATURES = {
     "tls_comm_init_record": (_I32, [_P, _I32, _I32]),
     "tls_comm_record_log": (_I64, [_P, _P, _I64]),
     "tls_comm_info": (_I32, [_P, _P]),
+    "tls_coarse_info": (_I32, [_P, _P]),
     "tls_set_coarse_layout": (_I32, [_P, _I32, _P]),
     "tls_graph_build": (_I32, [_P, C.POINTER(_I64)]),
     "tls_graph_fetch": (_I32, [_P, _P, _P]),

@@ -94,6 +94,16 @@ struct tls_ctx {
   double* a0tiles = nullptr;
   long long cpad = 0;                 // padded coarse length (nt * TT)
   int nu_ref1 = 0, no_ref1 = 0, nu_ref2 = 0, no_ref2 = 0;
+  // block-tridiagonal coarse solve (tls_coarse_chain): A0 is banded in subdomain order, so the
+  // coarse solve runs as a block forward / backward substitution with the inverted Schur blocks
+  // S_i^{-1} (tile blocks nsub+3 .. nsub+3+nb-1) and the sparse off-diagonal blocks of A0 (two
+  // CSR matrices: strictly block-lower part and its transpose) instead of a dense n_C^2 inverse
+  int chain_nb = 0, chain_bs = 0;
+  double* chain_tiles = nullptr;
+  int *d_lo_ptr = nullptr, *d_lo_idx = nullptr, *d_up_ptr = nullptr, *d_up_idx = nullptr;
+  double *d_lo_val = nullptr, *d_up_val = nullptr;
+  long long chain_nnz = 0;
+  std::vector<int> chain_u0, chain_nu, chain_o0, chain_no;
   // sharded coarse restriction: every rank's columns [ccol[q], ccol[q+1]) travel by one
   // all-gather of cmax doubles per rank (instead of an all-reduce of the whole n_C vector)
   std::vector<long long> ccol;
@@ -400,6 +410,44 @@ static int enq_coarse_refine(tls_ctx* ctx, cudaStream_t s, const int* done) {
 }
 
 // r_src (band local operators only): gather R_i r inside the band kernel instead of from xloc
+// Coarse solve A0 yc = c by block forward / backward substitution on the block-tridiagonal A0
+// (blocks of chain_bs columns; S_0 = A_00, S_i = A_ii - A_{i,i-1} S_{i-1}^{-1} A_{i-1,i}):
+//   forward   z_i = c_i - A_{i,i-1} y_{i-1},  y_i = S_i^{-1} z_i
+//   backward  x_i = S_i^{-1} (z_i - A_{i,i+1} x_{i+1})          (x_{nb-1} = y_{nb-1})
+// in place on the coarse segments: z overwrites c in xloc, y and then x live in yloc.  The
+// products with S_i^{-1} are tile blocks of k_symv_tiles, the off-diagonal ones sparse row sweeps.
+// Replaces the solve_coarse closure of src/coarse.py:178-182 (a Cholesky solve with A0).
+static int enq_coarse_chain(tls_ctx* ctx, cudaStream_t s, const int* done) {
+  const int nb = ctx->chain_nb, bs = ctx->chain_bs, nc = ctx->ncoarse;
+  double* z = ctx->xloc + ctx->coarse_xoff;
+  double* y = ctx->yloc + ctx->coarse_xoff;
+  auto block = [&](int i) -> int {
+    launch_k(ctx, k_symv_tiles, ctx->chain_nu[i], NTHR, 0, s, ctx->d_blk, ctx->d_units + ctx->chain_u0[i],
+             ctx->xloc, ctx->slots, done);
+    CKL();
+    launch_k(ctx, k_reduce_tiles, (ctx->chain_no[i] + 7) / 8, NTHR, 0, s, ctx->d_blk,
+             ctx->d_outs + ctx->chain_o0[i], ctx->chain_no[i], ctx->d_red, ctx->slots, ctx->yloc, done);
+    CKL();
+    return TLS_OK;
+  };
+  auto offdiag = [&](int i, const int* ptr, const int* idx, const double* val) -> int {
+    const int r0 = i * bs, r1 = std::min(nc, r0 + bs);
+    launch_k(ctx, k_chain_spmv, grid_for((long long)(r1 - r0) * 32, NTHR), NTHR, 0, s, r0, r1, ptr, idx, val,
+             (const double*)y, z, done);
+    CKL();
+    return TLS_OK;
+  };
+  for (int i = 0; i < nb; ++i) {
+    if (i > 0) TRY(offdiag(i, ctx->d_lo_ptr, ctx->d_lo_idx, ctx->d_lo_val));
+    TRY(block(i));
+  }
+  for (int i = nb - 2; i >= 0; --i) {
+    TRY(offdiag(i, ctx->d_up_ptr, ctx->d_up_idx, ctx->d_up_val));
+    TRY(block(i));
+  }
+  return TLS_OK;
+}
+
 static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
                      const double* r_src = nullptr) {
   if (ctx->local_kind >= 1 && which != L_COARSE) {
@@ -436,6 +484,10 @@ static int enq_solve(tls_ctx* ctx, cudaStream_t s, int which, const int* done,
     if (timed) CK(cudaEventRecordWithFlags(ctx->kt_b[ctx->kt_n++], s, cudaEventRecordExternal));
     if (which == L_LOCAL) return TLS_OK;
     which = L_COARSE;
+  }
+  if (ctx->chain_nb > 0 && which != L_LOCAL) {
+    if (which == L_ALL) TRY(enq_solve(ctx, s, L_LOCAL, done));
+    return enq_coarse_chain(ctx, s, done);
   }
   int u0 = 0, nu = 0, o0 = 0, no = 0;
   if (which == L_LOCAL) { nu = ctx->nu_local; no = ctx->no_local; }
@@ -712,6 +764,8 @@ void tls_ctx_destroy(tls_ctx* ctx) {
   dfree(ctx->rowptr); dfree(ctx->col); dfree(ctx->val);
   dfree(ctx->d_sub_idxoff); dfree(ctx->d_sub_n); dfree(ctx->d_idx); dfree(ctx->d_nint);
   dfree(ctx->d_blk); dfree(ctx->tiles); dfree(ctx->d_Z); dfree(ctx->ctiles); dfree(ctx->a0tiles); dfree(ctx->d_zoff);
+  dfree(ctx->chain_tiles); dfree(ctx->d_lo_ptr); dfree(ctx->d_lo_idx); dfree(ctx->d_lo_val);
+  dfree(ctx->d_up_ptr); dfree(ctx->d_up_idx); dfree(ctx->d_up_val);
   dfree(ctx->d_kcnt); dfree(ctx->d_cstart); dfree(ctx->d_units); dfree(ctx->d_outs); dfree(ctx->d_red);
   dfree(ctx->d_gidx); dfree(ctx->d_pull_ptr); dfree(ctx->d_pull_pos); dfree(ctx->d_zrow);
   dfree(ctx->d_zk); dfree(ctx->d_zc); dfree(ctx->d_zst); dfree(ctx->xloc); dfree(ctx->yloc); dfree(ctx->slots);
@@ -1056,6 +1110,8 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
   ctx->finalized = false;
   destroy_graphs(ctx);
   ctx->cref = false;
+  ctx->chain_nb = 0;
+  dfree(ctx->chain_tiles);
   if (n_coarse <= 0 || !k) {
     ctx->ncoarse = 0;
     return TLS_OK;
@@ -1090,14 +1146,108 @@ int32_t tls_coarse_upload(tls_ctx* ctx, int32_t n_coarse, const int32_t* k, cons
   cb.sym = ctx->sym;
   cb.xoff = ctx->Xloc;
   const int64_t ntiles = cb.sym ? (int64_t)cb.nt * (cb.nt + 1) / 2 : (int64_t)cb.nt * cb.nt;
+  ctx->cpad = (long long)cb.nt * TT;
+  ctx->h_blk.resize(ctx->nsub + 3);
+  if (!a0inv) {  // no dense inverse: the operator follows as a block-tridiagonal chain
+    dfree(ctx->ctiles);
+    cb.tiles = nullptr;
+    ctx->h_blk[ctx->nsub] = cb;
+    return TLS_OK;
+  }
   TRY(dalloc(ctx, ctx->ctiles, ntiles * TT * TT));
   cb.tiles = ctx->ctiles;
   ctx->h_blk[ctx->nsub] = cb;
-  ctx->cpad = (long long)cb.nt * TT;
-  CK(cudaMemcpy(ctx->d_blk, ctx->h_blk.data(), sizeof(BlkDesc) * (ctx->nsub + 3), cudaMemcpyHostToDevice));
+  TRY(upload(ctx, ctx->d_blk, ctx->h_blk.data(), ctx->nsub + 3));
   dim3 g((unsigned)std::min<int64_t>(ntiles, 8192), 1);
   launch_k(ctx, k_pack_tiles, g, NTHR, 0, s, ctx->d_blk, ctx->nsub, a0inv, n_coarse, 0);
   CKL();
+  return TLS_OK;
+}
+
+int32_t tls_coarse_chain(tls_ctx* ctx, int32_t n_blocks, int32_t block_size, const uint64_t* sinv,
+                         const int32_t* lo_indptr, const int32_t* lo_indices, const double* lo_values,
+                         const int32_t* up_indptr, const int32_t* up_indices, const double* up_values,
+                         int64_t nnz, void* stream) {
+  TLS_RANGE("tls_coarse_chain");
+  if (!ctx || ctx->ncoarse <= 0) return ctx ? fail(ctx, TLS_ERR_STATE, "upload the coarse basis first") : TLS_ERR_ARG;
+  if (!ctx->sym) return fail(ctx, TLS_ERR_ARG, "the block-tridiagonal coarse solve needs a symmetric operator");
+  if (ctx->cref) return fail(ctx, TLS_ERR_STATE, "coarse refinement and the block-tridiagonal solve exclude each other");
+  const int nc = ctx->ncoarse;
+  if (n_blocks < 2 || block_size <= 0 || block_size % TT != 0 ||
+      (long long)(n_blocks - 1) * block_size >= nc || (long long)n_blocks * block_size < nc)
+    return fail(ctx, TLS_ERR_ARG, "block size must be a multiple of 64 and n_blocks = ceil(n_coarse / block_size) >= 2");
+  if (!sinv || !lo_indptr || !up_indptr || nnz < 0 || (nnz > 0 && (!lo_indices || !lo_values || !up_indices || !up_values)))
+    return fail(ctx, TLS_ERR_ARG, "null chain array");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->finalized = false;
+  destroy_graphs(ctx);
+  dfree(ctx->ctiles);
+  ctx->h_blk.resize(ctx->nsub + 3);
+  ctx->h_blk[ctx->nsub].tiles = nullptr;
+  int64_t tiles = 0;
+  std::vector<int64_t> tb(n_blocks);
+  for (int i = 0; i < n_blocks; ++i) {
+    const int ni = std::min(block_size, nc - i * block_size), nt = (ni + TT - 1) / TT;
+    tb[i] = tiles;
+    tiles += (int64_t)nt * (nt + 1) / 2;
+  }
+  TRY(dalloc(ctx, ctx->chain_tiles, tiles * TT * TT));
+  for (int i = 0; i < n_blocks; ++i) {
+    BlkDesc b{};
+    b.n = std::min(block_size, nc - i * block_size);
+    b.nt = (b.n + TT - 1) / TT;
+    b.sym = 1;
+    b.xoff = ctx->Xloc + (long long)i * block_size;
+    b.tiles = ctx->chain_tiles + tb[i] * TT * TT;
+    ctx->h_blk.push_back(b);
+  }
+  TRY(upload(ctx, ctx->d_blk, ctx->h_blk.data(), (int64_t)ctx->h_blk.size()));
+  for (int i = 0; i < n_blocks; ++i) {
+    const BlkDesc& b = ctx->h_blk[ctx->nsub + 3 + i];
+    if (!sinv[i]) return fail(ctx, TLS_ERR_ARG, "null S_i^{-1} block");
+    const int64_t nt = (int64_t)b.nt * (b.nt + 1) / 2;
+    dim3 g((unsigned)std::min<int64_t>(nt, 8192), 1);
+    launch_k(ctx, k_pack_tiles, g, NTHR, 0, s, ctx->d_blk, ctx->nsub + 3 + i,
+             reinterpret_cast<const double*>(sinv[i]), (long long)b.n, 0LL);
+    CKL();
+  }
+  TRY(dalloc(ctx, ctx->d_lo_ptr, (int64_t)nc + 1));
+  TRY(dalloc(ctx, ctx->d_up_ptr, (int64_t)nc + 1));
+  TRY(dalloc(ctx, ctx->d_lo_idx, nnz));
+  TRY(dalloc(ctx, ctx->d_up_idx, nnz));
+  TRY(dalloc(ctx, ctx->d_lo_val, nnz));
+  TRY(dalloc(ctx, ctx->d_up_val, nnz));
+  CK(cudaMemcpyAsync(ctx->d_lo_ptr, lo_indptr, sizeof(int) * ((size_t)nc + 1), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(ctx->d_up_ptr, up_indptr, sizeof(int) * ((size_t)nc + 1), cudaMemcpyDeviceToDevice, s));
+  if (nnz > 0) {
+    CK(cudaMemcpyAsync(ctx->d_lo_idx, lo_indices, sizeof(int) * (size_t)nnz, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_up_idx, up_indices, sizeof(int) * (size_t)nnz, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_lo_val, lo_values, sizeof(double) * (size_t)nnz, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_up_val, up_values, sizeof(double) * (size_t)nnz, cudaMemcpyDeviceToDevice, s));
+  }
+  // the structure the substitution relies on: row r of the lower part only reads columns of the
+  // block before r's, row r of the upper part only columns of the block after it
+  std::vector<int> hp((size_t)nc + 1), hi((size_t)std::max<int64_t>(nnz, 1));
+  for (int pass = 0; pass < 2; ++pass) {
+    CK(cudaMemcpyAsync(hp.data(), pass ? ctx->d_up_ptr : ctx->d_lo_ptr, sizeof(int) * ((size_t)nc + 1), cudaMemcpyDeviceToHost, s));
+    if (nnz > 0)
+      CK(cudaMemcpyAsync(hi.data(), pass ? ctx->d_up_idx : ctx->d_lo_idx, sizeof(int) * (size_t)nnz, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hp[0] != 0 || hp[nc] != nnz) return fail(ctx, TLS_ERR_ARG, "chain CSR: indptr[0] != 0 or indptr[n] != nnz");
+    for (int r = 0; r < nc; ++r) {
+      if (hp[r + 1] < hp[r]) return fail(ctx, TLS_ERR_ARG, "chain CSR: indptr decreases at row " + std::to_string(r));
+      const int b = r / block_size + (pass ? 1 : -1);
+      const long long c0 = (long long)b * block_size, c1 = std::min<long long>(c0 + block_size, nc);
+      for (int e = hp[r]; e < hp[r + 1]; ++e)
+        if (b < 0 || b >= n_blocks || hi[e] < c0 || hi[e] >= c1)
+          return fail(ctx, TLS_ERR_ARG, "chain CSR: entry (" + std::to_string(r) + ", " + std::to_string(hi[e]) +
+                                            ") outside the neighbouring block");
+    }
+  }
+  ctx->chain_nb = n_blocks;
+  ctx->chain_bs = block_size;
+  ctx->chain_nnz = nnz;
   return TLS_OK;
 }
 
@@ -1195,7 +1345,28 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
   ctx->no_local = (int)outs.size();
   ctx->nu_coarse = ctx->no_coarse = 0;
   ctx->algo_coarse = 0.0;
-  if (ctx->ncoarse > 0) {
+  ctx->chain_u0.clear(); ctx->chain_nu.clear(); ctx->chain_o0.clear(); ctx->chain_no.clear();
+  if (ctx->ncoarse > 0 && ctx->chain_nb == 0 && !ctx->h_blk[nsub].tiles)
+    return fail(ctx, TLS_ERR_STATE, "coarse basis uploaded without a coarse operator (tls_coarse_chain missing)");
+  if (ctx->ncoarse > 0 && ctx->chain_nb > 0) {
+    // block-tridiagonal coarse solve: one tile plan per inverted Schur block, launched one after
+    // the other (every rank runs the whole substitution: it does not partition by rows)
+    double bytes = 0.0;
+    for (int i = 0; i < ctx->chain_nb; ++i) {
+      const BlkDesc& b = ctx->h_blk[nsub + 3 + i];
+      ctx->chain_u0.push_back((int)units.size());
+      ctx->chain_o0.push_back((int)outs.size());
+      plan_block(nsub + 3 + i, b.nt, 1, 2, slot, units, outs, red);
+      ctx->chain_nu.push_back((int)units.size() - ctx->chain_u0.back());
+      ctx->chain_no.push_back((int)outs.size() - ctx->chain_o0.back());
+      const double ni = b.n;
+      bytes += (i + 1 < ctx->chain_nb ? 2.0 : 1.0) * (8.0 * ni * (ni + 1) / 2 + 16.0 * ni);
+    }
+    ctx->algo_coarse = bytes + 2.0 * (12.0 * (double)ctx->chain_nnz + 4.0 * ctx->ncoarse);
+    ctx->nu_coarse = (int)units.size() - ctx->nu_local;
+    ctx->no_coarse = (int)outs.size() - ctx->no_local;
+    ctx->nu_ref1 = ctx->no_ref1 = ctx->nu_ref2 = ctx->no_ref2 = 0;
+  } else if (ctx->ncoarse > 0) {
     // the coarse operator is ONE block: thinner units (2 tile-rows) to fill the machine
     plan_block(nsub, ctx->h_blk[nsub].nt, ctx->sym, 2, slot, units, outs, red);
     const double nc = ctx->ncoarse;
@@ -1778,6 +1949,8 @@ int32_t tls_coarse_refine(tls_ctx* ctx, const double* a0, void* stream) {
   if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "upload the coarse space first");
   if (!ctx->h_nofo.empty()) return fail(ctx, TLS_ERR_STATE, "coarse refinement needs the whole A0^{-1} (one GPU)");
   if (!a0) return fail(ctx, TLS_ERR_ARG, "null A0");
+  if (ctx->chain_nb > 0 || !ctx->h_blk[ctx->nsub].tiles)
+    return fail(ctx, TLS_ERR_STATE, "coarse refinement needs the stored A0^{-1} (not the block-tridiagonal solve)");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int nsub = ctx->nsub;
@@ -2230,7 +2403,7 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   cudaStream_t s = (cudaStream_t)stream;
   const int which = ctx->combine == TLS_ADDITIVE ? L_ALL : L_LOCAL;
   const int u0 = 0;
-  const int nu = which == L_ALL ? ctx->nu_local + ctx->nu_coarse : ctx->nu_local;
+  const int nu = which == L_ALL && ctx->chain_nb == 0 ? ctx->nu_local + ctx->nu_coarse : ctx->nu_local;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -2268,7 +2441,7 @@ int32_t tls_profile_local_solve(tls_ctx* ctx, int32_t reps, double* avg_ms, doub
   cudaEventDestroy(e1);
   if (avg_ms) *avg_ms = ms / reps;
   if (algorithmic_bytes)
-    *algorithmic_bytes = ctx->algo_local + (which == L_ALL && !band ? ctx->algo_coarse : 0.0);
+    *algorithmic_bytes = ctx->algo_local + (which == L_ALL && !band && ctx->chain_nb == 0 ? ctx->algo_coarse : 0.0);
   return TLS_OK;
 }
 
@@ -2726,6 +2899,20 @@ int32_t tls_comm_info(const tls_ctx* ctx, int64_t* out3) {
   if (out3)
     for (int i = 0; i < 3; ++i) out3[i] = ctx->comm->calls[i];
   return ctx->comm->kind();
+}
+
+// how the coarse solve runs (after tls_precond_finalize): returns 0 = no coarse level, 1 = stored
+// dense inverse tiles, 2 = block-tridiagonal substitution; out4 (optional) = {n_coarse, blocks,
+// block size, algorithmic bytes one coarse solve on this rank streams}
+int32_t tls_coarse_info(const tls_ctx* ctx, double* out4) {
+  if (!ctx) return -1;
+  if (out4) {
+    out4[0] = ctx->ncoarse;
+    out4[1] = ctx->chain_nb;
+    out4[2] = ctx->chain_bs;
+    out4[3] = ctx->algo_coarse;
+  }
+  return ctx->ncoarse <= 0 ? 0 : ctx->chain_nb > 0 ? 2 : 1;
 }
 
 int64_t tls_comm_record_log(const tls_ctx* ctx, int64_t* out, int64_t cap) {

@@ -147,6 +147,34 @@ __global__ void __launch_bounds__(NTHR) k_gather(long long m, const int* __restr
   }
 }
 
+// Block-tridiagonal coarse solve (tls_coarse_chain): z[r] -= sum_e val[e] * y[idx[e]] for the rows
+// r in [r0, r1) of one sparse off-diagonal block row of A0 = Z^T A Z (src/coarse.py:158-183).
+// One warp per row, lanes stride the row's entries, fixed xor-butterfly -> deterministic.
+__global__ void __launch_bounds__(NTHR) k_chain_spmv(int r0, int r1, const int* __restrict__ ptr,
+                                                     const int* __restrict__ idx,
+                                                     const double* __restrict__ val,
+                                                     const double* __restrict__ y, double* z,
+                                                     const int* done) {
+  PDL_ENTRY();
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int row = r0 + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  if (row >= r1) return;
+  const int e0 = __ldg(ptr + row), e1 = __ldg(ptr + row + 1);
+  double a0 = 0.0, a1 = 0.0;
+  int e = e0 + lane;
+  for (; e + 32 < e1; e += 64) {
+    a0 += __ldg(val + e) * y[__ldg(idx + e)];
+    a1 += __ldg(val + e + 32) * y[__ldg(idx + e + 32)];
+  }
+  if (e < e1) a0 += __ldg(val + e) * y[__ldg(idx + e)];
+  double v = a0 + a1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  if (lane == 0 && e1 > e0) z[row] -= v;
+}
+
+
 // ---------------------------------------------------------------------------------------
 // K5  coarse restriction c = Z^T r (CoarseSpace.restrict, src/coarse.py:40-41).  Z is
 //     block-diagonal by subdomain with interior support (src/coarse.py:1-7): one CTA per

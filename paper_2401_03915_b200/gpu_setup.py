@@ -58,6 +58,11 @@ REFINE_COND = 1.0e8  # cond_1(A0) above which every coarse solve gets one refine
 # SPD A0 of at least this order whose half bandwidth is < n_C / 4 is inverted by the
 # block-tridiagonal recurrences (spd_inverse_block_tridiagonal) instead of dense potrf + potri
 BAND_INVERSE_MIN = int(os.environ.get("TLS_A0_BANDED_MIN", "4096"))
+# ... and from this order on no inverse is formed at all: the coarse solve runs as a block
+# forward / backward substitution with the inverted Schur blocks (tls_coarse_chain): ~2 n_C * bs
+# doubles per solve instead of n_C^2 / 2 (configuration 5: 1.5 GB instead of 9.7 GB per iteration)
+def _chain_min():
+    return int(os.environ.get("TLS_A0_CHAIN_MIN", "16384"))
 
 
 class CoarseData:
@@ -83,6 +88,9 @@ class CoarseData:
         self._symmetric = False
         self.cond1 = None
         self.refined = False
+        self.solve_kind = "none"      # "dense-inverse" | "block-tridiagonal" (tls_coarse_info)
+        self.solve_blocks = self.solve_block_size = 0
+        self.solve_bytes = 0.0
 
     @staticmethod
     def _ranges(counts):
@@ -1355,6 +1363,70 @@ def spd_inverse_block_tridiagonal(torch, A, bs):
     return 0
 
 
+def spd_block_tridiagonal_chain(torch, A, bs):
+    """Block-tridiagonal factorisation of an SPD matrix whose nonzeros lie within the
+    block-tridiagonal pattern of block size ``bs`` (only the lower triangle of ``A`` is read), for
+    the coarse solve by block substitution (``tls_coarse_chain``):
+
+      S_0 = A_00,  S_i = A_ii - A_{i,i-1} S_{i-1}^{-1} A_{i-1,i}   (formed as A_ii - L_{i,i-1} L_{i,i-1}^T
+      from the block Cholesky factor, as in ``spd_inverse_block_tridiagonal``).
+
+    Returns ``(info, sinv, lo, up)``: ``info`` = 0 or the 1-based index of the leading minor that
+    is not positive definite (LAPACK potrf's info); ``sinv[i]`` = S_i^{-1} (dense, symmetric);
+    ``lo`` / ``up`` = (indptr, indices, values) CSR triples (int32 / fp64, device) of the strictly
+    block-lower part of A and of its transpose, over all rows, global column indices.
+    src/coarse.py:178-182 factorises A0 once and solves with the factor; this is the same
+    Cholesky factorisation organised by blocks, n * bs^2 flops instead of n^3 / 3.
+    """
+    n = A.shape[0]
+    dev = A.device
+    cuts = list(range(0, n, bs)) + [n]
+    nb = len(cuts) - 1
+    sinv = []
+    lo_r, lo_c, lo_v, up_r, up_c, up_v = [], [], [], [], [], []
+    Lprev = None
+    for i in range(nb):
+        r0, r1 = cuts[i], cuts[i + 1]
+        Aii = A[r0:r1, r0:r1]
+        if i > 0:
+            p0 = cuts[i - 1]
+            B = A[r0:r1, p0:r0]
+            Lij = torch.linalg.solve_triangular(Lprev, B.mT, upper=False).mT
+            Aii = Aii - Lij @ Lij.mT
+            del Lij
+            nz = B.nonzero()
+            lo_r.append(nz[:, 0] + r0)
+            lo_c.append(nz[:, 1] + p0)
+            lo_v.append(B[nz[:, 0], nz[:, 1]])
+            Bt = B.mT.contiguous()
+            nz = Bt.nonzero()
+            up_r.append(nz[:, 0] + p0)
+            up_c.append(nz[:, 1] + r0)
+            up_v.append(Bt[nz[:, 0], nz[:, 1]])
+            del B, Bt, nz
+        Lii, info = torch.linalg.cholesky_ex(Aii)
+        del Aii
+        if int(info) != 0:
+            return r0 + int(info), None, None, None
+        D = torch.cholesky_inverse(Lii)
+        sinv.append((0.5 * (D + D.mT)).contiguous())
+        del D
+        Lprev = Lii
+    del Lprev, Lii
+
+    def csr(rows, cols, vals):
+        if rows:
+            r, c, v = torch.cat(rows), torch.cat(cols), torch.cat(vals)
+        else:
+            r = c = torch.zeros(0, dtype=torch.int64, device=dev)
+            v = torch.zeros(0, dtype=torch.float64, device=dev)
+        ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        ptr[1:] = torch.cumsum(torch.bincount(r, minlength=n), 0)
+        return ptr.to(torch.int32).contiguous(), c.to(torch.int32).contiguous(), v.contiguous()
+
+    return 0, sinv, csr(lo_r, lo_c, lo_v), csr(up_r, up_c, up_v)
+
+
 def _band_bytes(codes):
     """Device bytes the library allocates for band panels with these codes (band_layout)."""
     k = (np.asarray(codes, dtype=np.int64) & 0xFFFF)
@@ -1747,7 +1819,17 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         # A0 couples neighbouring subdomains only: when its band is narrow (configuration 5:
         # 3.3k of 49k) the inverse comes from the block-tridiagonal recurrences, in place
         bs = -(-(a0_band + 1) // 64) * 64
-        if banded:
+        chain = banded and nC >= _chain_min()
+        if chain:
+            info, sinv, lo_csr, up_csr = spd_block_tridiagonal_chain(torch, A0, bs)
+            if info != 0:
+                raise RuntimeError(f"coarse operator is not positive definite: {info}-th leading minor")
+            if not keep_a0:
+                A0 = None
+            A0inv = None
+            _log(t0, f"A0 factorised by blocks for the block-tridiagonal coarse solve (half bandwidth "
+                     f"{a0_band}, block {bs}, {len(sinv)} blocks, {int(lo_csr[2].numel())} off-diagonal entries)")
+        elif banded:
             A0inv = A0.clone() if keep_a0 else A0
             if not keep_a0:
                 A0 = None
@@ -1780,7 +1862,7 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     # 1-norm condition number ||A0||_1 ||A0^{-1}||_1 (both explicit here): above 1e8 the explicit
     # inverse alone leaves a coarse residual ~cond * eps, so every coarse solve gets one
     # refinement step (tls_coarse_refine) -- the reference's LU/Cholesky solve is backward stable
-    cond1 = norm_a0 * float(A0inv.abs().sum(0).max()) if norm_a0 is not None else None
+    cond1 = norm_a0 * float(A0inv.abs().sum(0).max()) if norm_a0 is not None and A0inv is not None else None
     refine = (A0 is not None and cond1 is not None and cond1 > REFINE_COND and not sharded
               and os.environ.get("TLS_COARSE_REFINE", "1") != "0")
     _log(t0, "coarse operator inverted; uploading")
@@ -1790,9 +1872,20 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
     k32 = np.asarray(counts, dtype=np.int32)
     # the library cudaMalloc's the packed coarse operator (~4 nC^2 bytes, 8 nC^2 if general):
     # torch's cached blocks go back to the driver only when that would not fit
-    _make_room(torch, dev, 8 * nC * nC if not symmetric else 4 * nC * nC + 8 * nC * 64)
-    handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
-                                       _lib.ptr(A0inv), s_ptr))
+    if A0inv is None:  # block-tridiagonal coarse solve: the inverted Schur blocks + sparse off-diagonals
+        _make_room(torch, dev, sum(4 * t.numel() + 8 * 64 * t.shape[0] for t in sinv) + 24 * int(lo_csr[2].numel()))
+        handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat), None, s_ptr))
+        ptrs = np.array([t.data_ptr() for t in sinv], dtype=np.uint64)
+        handle.check(lib.tls_coarse_chain(handle.ctx, len(sinv), bs, _lib.ptr(ptrs),
+                                          _lib.ptr(lo_csr[0]), _lib.ptr(lo_csr[1]), _lib.ptr(lo_csr[2]),
+                                          _lib.ptr(up_csr[0]), _lib.ptr(up_csr[1]), _lib.ptr(up_csr[2]),
+                                          int(lo_csr[2].numel()), s_ptr))
+        torch.cuda.current_stream().synchronize()
+        del sinv, lo_csr, up_csr
+    else:
+        _make_room(torch, dev, 8 * nC * nC if not symmetric else 4 * nC * nC + 8 * nC * 64)
+        handle.check(lib.tls_coarse_upload(handle.ctx, nC, _lib.ptr(k32), _lib.ptr(zcat),
+                                           _lib.ptr(A0inv), s_ptr))
     if sharded:  # the restriction's all-gather layout: rank q's columns are contiguous
         from .distributed import slab_ranges
         csum = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)

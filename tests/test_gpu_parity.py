@@ -411,3 +411,44 @@ def test_banded_coarse_inverse_matches_dense_path(B, name, monkeypatch):
     np.testing.assert_allclose(yb, yd, rtol=0, atol=1e-12 * np.abs(yd).max())
     x, rep = B.pcg(mat, pre_b, d["b"], tol=float(d["tol"]))
     assert rep.converged and abs(rep.iterations - int(d["iterations"])) <= 1
+
+
+@pytest.mark.parametrize("name", ["cfg2_m48", "cfg2_m24"])
+def test_block_tridiagonal_coarse_solve_matches_dense_path(B, name, monkeypatch):
+    """The coarse solve by block forward / backward substitution (tls_coarse_chain, the path
+    configuration 5 takes at full size: no n_C^2 inverse is formed or streamed) against the dense
+    potrf + potri path on the same setup and against the reference's coarse apply
+    (src/coarse.py:40-49, 178-182); the additive apply, a PCG solve and bit-reproducibility."""
+    from paper_2401_03915_b200 import gpu_setup as G
+    d = golden(name)
+    a = golden_csr(d)
+    mat = B.SparseMat(a, symmetric=True)
+    kw = dict(overlap=int(d["overlap"]), owner=d["owner"], coarse=str(d["coarse"]), n_modes=int(d["n_modes"]))
+    monkeypatch.setattr(G, "BAND_INVERSE_MIN", 64)
+    monkeypatch.setenv("TLS_A0_CHAIN_MIN", "64")
+    seen = []
+    real = G.spd_block_tridiagonal_chain
+    monkeypatch.setattr(G, "spd_block_tridiagonal_chain", lambda t, A, bs: (seen.append(bs), real(t, A, bs))[1])
+    pre_c = B.setup(mat, int(d["n_sub"]), **kw)
+    monkeypatch.setenv("TLS_A0_BANDED", "0")
+    pre_d = B.setup(mat, int(d["n_sub"]), **kw)
+    if name == "cfg2_m48":   # 6^3 subdomains x 16 columns: band 704 of 3456 -> 5 blocks
+        assert len(seen) == 1 and 4 * seen[0] <= pre_c.report.n_coarse
+        assert pre_c.coarse.cond1 is None and pre_d.coarse.cond1 is not None
+    else:
+        assert len(seen) <= 1
+    r = d["r"][0]
+    zc, zd, zr = pre_c.coarse_apply(r), pre_d.coarse_apply(r), d["z_coarse"][0]
+    np.testing.assert_allclose(zc, zd, rtol=0, atol=1e-12 * np.abs(zd).max())
+    np.testing.assert_allclose(zc, zr, rtol=0, atol=1e-10 * np.abs(zr).max())
+    np.testing.assert_array_equal(zc, pre_c.coarse_apply(r))
+    c = np.random.default_rng(2).standard_normal(pre_c.report.n_coarse)
+    yc, yd = pre_c.coarse.solve_coarse(c), pre_d.coarse.solve_coarse(c)
+    np.testing.assert_allclose(yc, yd, rtol=0, atol=1e-12 * np.abs(yd).max())
+    za, zda = pre_c.apply(r), pre_d.apply(r)
+    np.testing.assert_allclose(za, zda, rtol=0, atol=1e-12 * np.abs(zda).max())
+    np.testing.assert_allclose(za, d["z"][0], rtol=0, atol=1e-10 * np.abs(d["z"][0]).max())
+    x, rep = B.pcg(mat, pre_c, d["b"], tol=float(d["tol"]))
+    assert rep.converged and abs(rep.iterations - int(d["iterations"])) <= 1
+    x2, rep2 = B.pcg(mat, pre_c, d["b"], tol=float(d["tol"]))
+    np.testing.assert_array_equal(x, x2)

@@ -78,6 +78,23 @@ def test_sharded_additive_pcg_matches_single(B, nranks):
         assert other[4].iterations == res[0][4].iterations
 
 
+def test_sharded_block_tridiagonal_coarse_solve(B, monkeypatch):
+    """Every rank runs the whole block substitution of tls_coarse_chain (it does not partition by
+    rows) on the all-gathered coarse coefficients: same applies and solves as one handle."""
+    from paper_2401_03915_b200 import gpu_setup as G
+    monkeypatch.setattr(G, "BAND_INVERSE_MIN", 64)
+    monkeypatch.setenv("TLS_A0_CHAIN_MIN", "64")
+    seen = []
+    real = G.spd_block_tridiagonal_chain
+    monkeypatch.setattr(G, "spd_block_tridiagonal_chain", lambda t, A, bs: (seen.append(bs), real(t, A, bs))[1])
+    d, a, res = _sharded_run(B, "cfg2_m48", 2, _pcg)
+    assert len(seen) == 3  # both ranks and the single handle
+    for report, _, z, x, rep, _z1 in res:
+        np.testing.assert_allclose(z, d["z"][0], rtol=0, atol=1e-10 * np.abs(d["z"][0]).max())
+        assert abs(rep.iterations - int(d["iterations"])) <= 1 and rep.converged
+    assert np.array_equal(res[1][2], res[0][2]) and np.array_equal(res[1][3], res[0][3])
+
+
 def test_sharded_deflated_gmres_matches_single(B):
     d, a, res = _sharded_run(B, "cfg3_m64", 2, _gmres)
     for report, _, z, x, rep, _z1 in res:

@@ -173,6 +173,65 @@ def test_spd_inverse_block_tridiagonal_matches_dense(n, bw, bs, scale):
     assert np.abs(A @ Xs - np.eye(n)).max() <= 1e-9 * max(1.0, np.linalg.cond(A) * 1e-7)
 
 
+def _chain_solve(sinv, lo, up, bs, c):
+    """Host restatement of the library's block substitution (enq_coarse_chain in csrc/tls_b200.cu)."""
+    import scipy.sparse as sp
+    n = c.size
+    Lo = sp.csr_matrix((lo[2].numpy(), lo[1].numpy(), lo[0].numpy()), shape=(n, n))
+    Up = sp.csr_matrix((up[2].numpy(), up[1].numpy(), up[0].numpy()), shape=(n, n))
+    z, y = c.copy(), np.zeros(n)
+    nb = len(sinv)
+    for i in range(nb):
+        r = slice(i * bs, min(n, (i + 1) * bs))
+        if i > 0:
+            z[r] -= (Lo @ y)[r]
+        y[r] = sinv[i].numpy() @ z[r]
+    for i in range(nb - 2, -1, -1):
+        r = slice(i * bs, min(n, (i + 1) * bs))
+        z[r] -= (Up @ y)[r]
+        y[r] = sinv[i].numpy() @ z[r]
+    return y
+
+
+@pytest.mark.parametrize("n,bw,bs,scale", [(1000, 90, 128, 1.5), (777, 63, 64, 1.5), (640, 63, 64, 1.0 + 1e-7)])
+def test_spd_block_tridiagonal_chain_solves(n, bw, bs, scale):
+    """The block factorisation behind tls_coarse_chain: the substitution with the inverted Schur
+    blocks and the sparse off-diagonal blocks solves A x = c like a dense Cholesky solve
+    (src/coarse.py:178-182); the two CSR parts are each other's transposes and only hold entries
+    of the neighbouring block; only A's lower triangle is read."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(n)
+    mask = np.abs(np.subtract.outer(np.arange(n), np.arange(n))) <= bw
+    Bm = np.abs(rng.standard_normal((n, n))) * mask
+    A = -(Bm + Bm.T) / 2
+    np.fill_diagonal(A, 0.0)
+    np.fill_diagonal(A, -A.sum(axis=1) * scale)
+    X = torch.tril(torch.tensor(A)) + torch.triu(torch.full((n, n), 7.0, dtype=torch.float64), 1)
+    info, sinv, lo, up = G.spd_block_tridiagonal_chain(torch, X, bs)
+    assert info == 0 and len(sinv) == -(-n // bs)
+    Lo = sp.csr_matrix((lo[2].numpy(), lo[1].numpy(), lo[0].numpy()), shape=(n, n))
+    Up = sp.csr_matrix((up[2].numpy(), up[1].numpy(), up[0].numpy()), shape=(n, n))
+    assert abs(Lo - Up.T).max() == 0.0
+    r, cidx = Lo.nonzero()
+    assert np.all(cidx // bs == r // bs - 1)
+    full = np.zeros((n, n))
+    for i in range(len(sinv)):
+        full[i * bs:(i + 1) * bs, i * bs:(i + 1) * bs] = A[i * bs:(i + 1) * bs, i * bs:(i + 1) * bs]
+    assert np.abs(full + Lo.toarray() + Up.toarray() - A).max() == 0.0
+    c = rng.standard_normal(n)
+    y = _chain_solve(sinv, lo, up, bs, c)
+    ref = np.linalg.solve(A, c)
+    dense = torch.cholesky_solve(torch.tensor(c)[:, None], torch.linalg.cholesky(torch.tensor(A)))[:, 0].numpy()
+    tol = max(1e-13, 20 * np.abs(dense - ref).max() / np.abs(ref).max())
+    assert np.abs(y - ref).max() <= tol * np.abs(ref).max()
+
+
+def test_spd_block_tridiagonal_chain_flags_indefinite():
+    A = np.eye(300) * 2.0
+    A[200, 200] = -1.0
+    assert G.spd_block_tridiagonal_chain(torch, torch.tensor(A), 64)[0] == 201
+
+
 def test_spd_inverse_block_tridiagonal_flags_indefinite():
     n, bs = 300, 64
     A = np.eye(n) * 2.0
