@@ -304,6 +304,10 @@ int64_t tls_comm_record_log(const tls_ctx* ctx, int64_t* out, int64_t cap);
  * 3 recording.  out3 (may be NULL): all-reduce / exchange / all-gather calls issued through the
  * NCCL API so far (a captured call counts once per capture, not per graph replay). */
 int32_t tls_comm_info(const tls_ctx* ctx, int64_t* out3);
+/* The uploaded basis blocks (per owned subdomain k[s] x n_interior[s] row-major, subdomain order,
+ * count = sum n_interior[s] * k[s] doubles) copied to HOST memory: the data behind
+ * CoarseSpace.basis (src/coarse.py:23-38), read on demand instead of during setup. */
+int32_t tls_coarse_basis_fetch(tls_ctx* ctx, double* out, int64_t count);
 /* How the coarse solve of src/coarse.py:178-182 runs (after tls_precond_finalize): 0 no coarse
  * level, 1 stored dense A0^{-1} tiles, 2 block-tridiagonal substitution (tls_coarse_chain).
  * out4 (may be NULL): {n_coarse, blocks, block size, algorithmic bytes one coarse solve streams

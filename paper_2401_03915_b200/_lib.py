@@ -98,6 +98,7 @@ SIGNATURES = {
     "tls_comm_record_log": (_I64, [_P, _P, _I64]),
     "tls_comm_info": (_I32, [_P, _P]),
     "tls_coarse_info": (_I32, [_P, _P]),
+    "tls_coarse_basis_fetch": (_I32, [_P, _P, _I64]),
     "tls_set_coarse_layout": (_I32, [_P, _I32, _P]),
     "tls_graph_build": (_I32, [_P, C.POINTER(_I64)]),
     "tls_graph_fetch": (_I32, [_P, _P, _P]),

@@ -1655,6 +1655,20 @@ int32_t tls_coarse_solve(tls_ctx* ctx, const double* c, double* y, void* stream)
   return TLS_OK;
 }
 
+// the basis blocks as uploaded (per owned subdomain k_s x n_interior[s] row-major, subdomain
+// order) copied to HOST memory: behind CoarseSpace.basis (src/coarse.py:23-38), read on demand
+int32_t tls_coarse_basis_fetch(tls_ctx* ctx, double* out, int64_t count) {
+  if (!ctx || !out) return ctx ? fail(ctx, TLS_ERR_ARG, "null output") : TLS_ERR_ARG;
+  if (ctx->ncoarse == 0 || !ctx->d_Z) return fail(ctx, TLS_ERR_STATE, "no coarse space");
+  long long total = 0;
+  for (int i = 0; i < ctx->nsub; ++i) total += (long long)ctx->h_nint[i] * ctx->h_k[i];
+  if (count != total) return fail(ctx, TLS_ERR_ARG, "basis size mismatch: the handle holds " + std::to_string(total) + " doubles");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  if (total) CK(cudaMemcpy(out, ctx->d_Z, sizeof(double) * (size_t)total, cudaMemcpyDeviceToHost));
+  return TLS_OK;
+}
+
 int32_t tls_coarse_prolong(tls_ctx* ctx, const double* y, double* z, void* stream) {
   TRY(need_final(ctx));
   if (ctx->ncoarse == 0) return fail(ctx, TLS_ERR_STATE, "no coarse space");

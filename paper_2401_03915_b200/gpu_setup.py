@@ -65,6 +65,37 @@ def _chain_min():
     return int(os.environ.get("TLS_A0_CHAIN_MIN", "16384"))
 
 
+class _LazyBasisBlocks:
+    """The per-subdomain basis blocks Z_s (n_int x k_s host arrays) of one handle, fetched from the
+    library's device copy (tls_coarse_basis_fetch) the first time one is read."""
+
+    def __init__(self, handle, n_int, counts):
+        self._handle, self._n_int, self._counts = handle, n_int, counts
+        self._blocks = None
+
+    def _load(self):
+        if self._blocks is None:
+            total = int(sum(ni * k for ni, k in zip(self._n_int, self._counts)))
+            flat = np.empty(max(total, 1), dtype=np.float64)
+            h = self._handle
+            h.check(h.lib.tls_coarse_basis_fetch(h.ctx, _lib.ptr(flat), total))
+            blocks, off = [], 0
+            for ni, k in zip(self._n_int, self._counts):   # stored k x n_int (column by column)
+                blocks.append(flat[off:off + ni * k].reshape(k, ni).T)
+                off += ni * k
+            self._blocks = blocks
+        return self._blocks
+
+    def __len__(self):
+        return len(self._counts)
+
+    def __getitem__(self, i):
+        return self._load()[i]
+
+    def __iter__(self):
+        return iter(self._load())
+
+
 class CoarseData:
     """Device coarse space + the host bookkeeping of CoarseSpace (src/coarse.py:23-49).
 
@@ -685,8 +716,12 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
     raise RuntimeError(f"Chebyshev subspace iteration did not converge: residual {res:.2e} after {maxit} steps")
 
 
-def band_solve_multi(torch, L, Dinv, kc, E):
+def band_solve_multi(torch, L, Dinv, kc, E, lead=None):
     """X = (L L^T)^{-1} E for a batch of banded Cholesky factors and many right-hand sides.
+
+    ``lead`` (host, ascending, one entry per right-hand side): no right-hand side j has a nonzero
+    above row ``lead[j]`` in any matrix of the batch, so the forward sweep skips the columns that
+    are still identically zero at each block row (unit right-hand sides: half the forward work).
 
     Default: the blocked restatement ``_band_solve_multi_torch`` (per 64-row block one batched
     cuBLAS DGEMM over all right-hand sides).  ``TLS_K10=1``: the in-tree K10 kernel
@@ -705,10 +740,10 @@ def band_solve_multi(torch, L, Dinv, kc, E):
         if rc != 0:
             raise RuntimeError(f"tls_band_solve_multi failed ({rc})")
         return X
-    return _band_solve_multi_torch(torch, L, Dinv, kc, E)
+    return _band_solve_multi_torch(torch, L, Dinv, kc, E, lead)
 
 
-def _band_solve_multi_torch(torch, L, Dinv, kc, E):
+def _band_solve_multi_torch(torch, L, Dinv, kc, E, lead=None):
     """X = (L L^T)^{-1} E for a batch of banded Cholesky factors and many right-hand sides.
 
     Blocked banded forward/backward substitution over 64-row blocks with batched GEMMs: block
@@ -720,13 +755,25 @@ def _band_solve_multi_torch(torch, L, Dinv, kc, E):
     nb = ld // 64
     kmax = kc.max(axis=0) if kc.size else np.zeros(nb, dtype=np.int64)
     X = E.clone()
+    # columns [0, live[I]) can be nonzero in block rows <= I (the others start further down)
+    live = (np.searchsorted(np.asarray(lead), np.arange(1, nb + 1) * 64, side="left")
+            if lead is not None else np.full(nb, nrhs))
     for I in range(nb):  # forward: X_I = D_I^{-1} (E_I - L[I, J0:I] X[J0:I])
         r0, r1 = I * 64, (I + 1) * 64
         K = int(kmax[I])
+        nc = int(live[I])
+        if nc == 0:
+            continue
+        if nc == nrhs:
+            if K:
+                c0 = r0 - K * 64
+                X[:, r0:r1] -= L[:, r0:r1, c0:r0] @ X[:, c0:r0]
+            X[:, r0:r1] = Dinv[:, I] @ X[:, r0:r1]
+            continue
         if K:
             c0 = r0 - K * 64
-            X[:, r0:r1] -= L[:, r0:r1, c0:r0] @ X[:, c0:r0]
-        X[:, r0:r1] = Dinv[:, I] @ X[:, r0:r1]
+            X[:, r0:r1, :nc] -= L[:, r0:r1, c0:r0] @ X[:, c0:r0, :nc]
+        X[:, r0:r1, :nc] = Dinv[:, I] @ X[:, r0:r1, :nc]
     for I in range(nb - 1, -1, -1):  # backward: X_I = D_I^{-T} X_I; X[J0:I] -= L[I, J0:I]^T X_I
         r0, r1 = I * 64, (I + 1) * 64
         X[:, r0:r1] = Dinv[:, I].mT @ X[:, r0:r1]
@@ -793,15 +840,25 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
         pinv.scatter_(1, Pg, torch.arange(ld, device=dev).expand_as(Pg))
         E = torch.zeros((len(bs), ld, nbr), dtype=torch.float64, device=dev)
         rows = pinv[:, nin:n]                                       # (g, nbr) factor positions of the ring
+        # unit right-hand sides sorted by the factor position of their 1: the forward sweep skips
+        # the columns that are still zero (column j of E is zero above row rows[b, j])
+        order = lead = None
+        if Dinv is not None and os.environ.get("TLS_RING_SKIP", "1") != "0":
+            rows, order = rows.sort(dim=1)
+            lead = rows.amin(dim=0).cpu().numpy()
         E.view(len(bs), -1)[torch.arange(len(bs), device=dev)[:, None],
                             rows * nbr + torch.arange(nbr, device=dev)[None, :]] = 1.0
         ts = _stage("coarse: ring rhs", time.perf_counter() if VERBOSE else 0.0)
         if Dinv is not None:   # banded blocked solve (batched GEMMs on the band only)
             X = band_solve_multi(torch, L.index_select(0, bi), Dinv.index_select(0, bi),
-                                 kc[bs], E)
+                                 kc[bs], E, lead)
         else:
             X = torch.cholesky_solve(E, L.index_select(0, bi))      # A_P^{-1} E  (factor order)
         del E
+        if order is not None:  # back to the ring order of the local numbering
+            inv = torch.empty_like(order)
+            inv.scatter_(1, order, torch.arange(nbr, device=dev).expand_as(order))
+            X = torch.gather(X, 2, inv[:, None, :].expand(len(bs), ld, nbr))
         Bring = torch.gather(X, 1, pinv[:, :n, None].expand(len(bs), n, nbr))  # local order
         del X
         ts = _stage("coarse: ring solve", ts)
@@ -1728,14 +1785,20 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             off += sh[0] * sh[1]
         del wflat
     _release_cache(torch, dev)
-    flat = zflat.cpu().numpy() if len(own) else np.zeros(0)
+    # one GPU: the host copy of the basis (CoarseData._z, behind the ``basis`` attribute of
+    # src/coarse.py:23-38) is fetched from the library on first use, not during setup
+    # (configuration 5: 1.6 GB through pageable memory, 1.2 s); sharded: copied now (the blocks of
+    # the other ranks are gathered below)
+    z_host = {}
+    if sharded:
+        flat = zflat.cpu().numpy() if len(own) else np.zeros(0)
+        off = 0
+        for s in own:
+            sh = tuple(z_dev[s].shape)
+            z_host[s] = flat[off:off + sh[0] * sh[1]].reshape(sh)
+            off += sh[0] * sh[1]
     del zflat
-    z_host, off = {}, 0
-    for s in own:
-        sh = tuple(z_dev[s].shape)
-        z_host[s] = flat[off:off + sh[0] * sh[1]].reshape(sh)
-        off += sh[0] * sh[1]
-    _log(t0, "basis copied to the host; rank filter")
+    _log(t0, "basis defragmented; rank filter")
     pivots = _rank_pivots(torch, z_dev, own, dev) if len(own) else []
     _log(t0, "rank filter done")
     largest = max((p[0] for p in pivots), default=0.0)
@@ -1750,12 +1813,13 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
             keep_cols[s].append(j)
     for s in own:
         kc = sorted(keep_cols[s])
-        if len(kc) != z_host[s].shape[1]:
+        if len(kc) != z_dev[s].shape[1]:
             idx = torch.as_tensor(kc, dtype=torch.long, device=dev)
             z_dev[s] = z_dev[s][:, idx].contiguous()
             w_dev[s] = w_dev[s][:, idx].contiguous() if len(kc) else None
-            z_host[s] = z_host[s][:, kc]
-    counts_own = np.array([z_host[s].shape[1] for s in own], dtype=np.int64)
+            if s in z_host:
+                z_host[s] = z_host[s][:, kc]
+    counts_own = np.array([z_dev[s].shape[1] for s in own], dtype=np.int64)
     if sharded:
         parts = shard.coll.allgather_list(torch.as_tensor(counts_own, device=dev))
         counts = np.concatenate([p.cpu().numpy() for p in parts]).astype(np.int64)
@@ -1897,7 +1961,10 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         handle.check(lib.tls_coarse_refine(handle.ctx, _lib.ptr(A0.contiguous()), s_ptr))
     torch.cuda.current_stream().synchronize()
     _log(t0, "coarse operator uploaded")
-    z_list = [z_host[s] if s in z_host else z_all[s].cpu().numpy() for s in range(N)]
+    if sharded:
+        z_list = [z_host[s] if s in z_host else z_all[s].cpu().numpy() for s in range(N)]
+    else:
+        z_list = _LazyBasisBlocks(handle, [int(n_int[s]) for s in range(N)], [int(c) for c in counts])
     del A0inv, zcat, z_dev, z_all
     _release_cache(torch, dev)
     cd = CoarseData(csr.shape[0], maps, z_list, [int(c) for c in counts], nnz)
