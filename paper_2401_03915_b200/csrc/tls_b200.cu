@@ -18,6 +18,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -285,6 +286,82 @@ template <class T>
 static int upload(tls_ctx* ctx, T*& d, const T* h, int64_t count) {
   TRY(dalloc(ctx, d, count));
   if (count > 0) CK(cudaMemcpy(d, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+  return TLS_OK;
+}
+
+// Host worker threads for the large host-side passes (CSR validation, staging copies)
+static int host_threads() {
+  const unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(8u, hc ? hc : 1u));
+}
+
+template <class F>
+static void parallel_chunks(int64_t count, int nthreads, F f) {  // f(thread, begin, end)
+  if (nthreads <= 1 || count < (1 << 20)) {
+    f(0, (int64_t)0, count);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t per = (count + nthreads - 1) / nthreads;
+  for (int t = 0; t < nthreads; ++t) {
+    const int64_t b = std::min<int64_t>(count, t * per), e = std::min<int64_t>(count, b + per);
+    th.emplace_back([=] { f(t, b, e); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// Large host arrays (the CSR of configuration 5: 5.4 GB) go to the device through a ring of
+// pinned staging buffers filled by several host threads while the previous chunk is in flight
+// (pageable cudaMemcpy ran at ~5 GB/s: 1.0 s of that setup); small ones by a plain copy.
+template <class T>
+static int upload_staged(tls_ctx* ctx, T*& d, const T* h, int64_t count) {
+  const size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(count, 0);
+  size_t CH = (size_t)32 << 20, min_bytes = (size_t)256 << 20;
+  if (const char* e = getenv("TLS_STAGED_CHUNK_BYTES")) CH = std::max<size_t>(4096, (size_t)atoll(e));  // tests
+  if (const char* e = getenv("TLS_STAGED_MIN_BYTES")) min_bytes = (size_t)atoll(e);
+  constexpr int NBUF = 3;
+  if (bytes < min_bytes || bytes == 0) return upload(ctx, d, h, count);
+  TRY(dalloc(ctx, d, count));
+  void* pin[NBUF] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[NBUF];
+  cudaStream_t st = nullptr;
+  bool ok = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess;
+  int nev = 0;
+  for (int i = 0; ok && i < NBUF; ++i) {
+    ok = cudaHostAlloc(&pin[i], CH, cudaHostAllocDefault) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) == cudaSuccess;
+    if (ok) ++nev;
+  }
+  cudaError_t err = cudaSuccess;
+  if (ok) {
+    const int nt = host_threads();
+    const char* src = reinterpret_cast<const char*>(h);
+    char* dst = reinterpret_cast<char*>(d);
+    int c = 0;
+    for (size_t off = 0; off < bytes && err == cudaSuccess; off += CH, ++c) {
+      const int b = c % NBUF;
+      const size_t nb = std::min(CH, bytes - off);
+      if (c >= NBUF) err = cudaEventSynchronize(ev[b]);
+      if (err != cudaSuccess) break;
+      char* p = static_cast<char*>(pin[b]);
+      parallel_chunks((int64_t)nb, nt, [&](int, int64_t b0, int64_t e0) { memcpy(p + b0, src + off + b0, (size_t)(e0 - b0)); });
+      err = cudaMemcpyAsync(dst + off, p, nb, cudaMemcpyHostToDevice, st);
+      if (err == cudaSuccess) err = cudaEventRecord(ev[b], st);
+    }
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  } else {
+    cudaGetLastError();
+  }
+  for (int i = 0; i < NBUF; ++i) {
+    if (i < nev) cudaEventDestroy(ev[i]);
+    if (pin[i]) cudaFreeHost(pin[i]);
+  }
+  if (st) cudaStreamDestroy(st);
+  if (!ok) {  // no pinned memory: plain copy
+    CK(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+    return TLS_OK;
+  }
+  CK(err);
   return TLS_OK;
 }
 
@@ -813,9 +890,20 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
   for (int64_t i = 0; i < nrows; ++i)
     if (indptr[i + 1] < indptr[i])
       return fail(ctx, TLS_ERR_DIM, "indptr decreases at row " + std::to_string(i));
-  for (int64_t k = 0; k < nnz; ++k)
-    if ((uint32_t)indices[k] >= (uint32_t)nrows)
-      return fail(ctx, TLS_ERR_DIM, "column index out of range at entry " + std::to_string(k));
+  {  // the first out-of-range column, found by all host threads
+    const int nt = host_threads();
+    std::vector<int64_t> bad(nt, -1);
+    parallel_chunks(nnz, nt, [&](int t, int64_t b, int64_t e) {
+      for (int64_t k = b; k < e; ++k)
+        if ((uint32_t)indices[k] >= (uint32_t)nrows) {
+          bad[t] = k;
+          return;
+        }
+    });
+    for (int t = 0; t < nt; ++t)
+      if (bad[t] >= 0)
+        return fail(ctx, TLS_ERR_DIM, "column index out of range at entry " + std::to_string(bad[t]));
+  }
   CK(cudaSetDevice(ctx->device));
   const bool renum = !ctx->h_nofo.empty();
   if (renum && (int64_t)ctx->h_nofo.size() != nrows)
@@ -827,8 +915,8 @@ int32_t tls_matrix_upload(tls_ctx* ctx, int64_t nrows, int64_t nnz, const int64_
   if (!renum) {
     for (int64_t i = 0; i <= nrows; ++i) rp[i] = (int)indptr[i];
     TRY(upload(ctx, ctx->rowptr, rp.data(), nrows + 1));
-    TRY(upload(ctx, ctx->col, indices, nnz));
-    TRY(upload(ctx, ctx->val, data, nnz));
+    TRY(upload_staged(ctx, ctx->col, indices, nnz));
+    TRY(upload_staged(ctx, ctx->val, data, nnz));
     ctx->r0 = 0;
     ctx->r1 = (int)nrows;
   } else {

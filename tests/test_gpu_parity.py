@@ -452,3 +452,43 @@ def test_block_tridiagonal_coarse_solve_matches_dense_path(B, name, monkeypatch)
     assert rep.converged and abs(rep.iterations - int(d["iterations"])) <= 1
     x2, rep2 = B.pcg(mat, pre_c, d["b"], tol=float(d["tol"]))
     np.testing.assert_array_equal(x, x2)
+    if name == "cfg2_m48":
+        assert pre_c.coarse.solve_kind == "block-tridiagonal" and pre_d.coarse.solve_kind == "dense-inverse"
+        assert 0 < pre_c.coarse.solve_bytes < 0.6 * pre_d.coarse.solve_bytes
+        # backward stability of the substitution: ||A0 y - c|| at the level of a Cholesky solve
+        a00 = pre_c.coarse.a00
+        res = np.abs(a00 @ yc - c).max() / (np.abs(a00).sum(1).max() * np.abs(yc).max())
+        assert res <= 1e-14, res
+        # the basis blocks come back from the library on demand, bit for bit
+        for s in (0, 17, 215):
+            np.testing.assert_array_equal(pre_c.coarse._z[s], pre_d.coarse._z[s])
+        # malformed chains are refused before anything changes (the handle keeps working)
+        h = pre_c.handle
+        import ctypes as C
+        ptrs = (C.c_uint64 * 3)(1, 1, 1)
+        for nb_, bs_ in ((3, 100), (1, 3456), (2, 64)):
+            rc = h.lib.tls_coarse_chain(h.ctx, nb_, bs_, ptrs, None, None, None, None, None, None, 0, None)
+            assert rc != 0
+        np.testing.assert_array_equal(zc, pre_c.coarse_apply(r))
+
+
+def test_staged_matrix_upload_is_exact(B, monkeypatch):
+    """Large CSR arrays travel through a ring of pinned staging buffers filled by host threads
+    (tls_matrix_upload; configuration 5's 5.4 GB).  Forced on a small matrix with 16 KB chunks:
+    the SpMV (src/sparsemat.py:125-129) is bit-identical to the plain upload's, and the first
+    out-of-range column is still reported."""
+    d = golden("cfg2_m48")
+    a = golden_csr(d)
+    v = np.random.default_rng(0).standard_normal(a.shape[0])
+    from paper_2401_03915_b200.device import Handle
+    y0 = B.SparseMat(a, symmetric=True).matvec(v)
+    monkeypatch.setenv("TLS_STAGED_MIN_BYTES", "1")
+    monkeypatch.setenv("TLS_STAGED_CHUNK_BYTES", "16384")
+    np.testing.assert_array_equal(B.SparseMat(a, symmetric=True).matvec(v), y0)
+    np.testing.assert_allclose(y0, a @ v, rtol=0, atol=1e-13 * np.abs(a @ v).max())
+    h1 = Handle()
+    bad = a.copy()
+    bad.indices = bad.indices.copy()
+    bad.indices[123457] = a.shape[0]
+    with pytest.raises(ValueError, match="entry 123457"):
+        h1.upload_matrix(bad, True)
