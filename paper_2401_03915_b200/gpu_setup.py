@@ -866,13 +866,28 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
             F = Bring[:, :ni]
             B22 = Bring[:, nin:n]
             Ag = A.index_select(0, bi)
-            H = _harmonic_h(torch, Ag, Bring, n, ni)
-            H = 0.5 * (H + H.mT)
-            ts = _stage("coarse: H = F^T A_II F", ts)
-            C, info = torch.linalg.cholesky_ex(0.5 * (B22 + B22.mT))
-            Xs = torch.linalg.solve_triangular(C, H, upper=False)
-            M = torch.linalg.solve_triangular(C, Xs.mT, upper=False)
-            M = 0.5 * (M + M.mT)
+            if ni == nin and os.environ.get("TLS_PENCIL_DIRECT", "1") != "0":
+                # overlap 1 (F = all non-ring rows of Bring): the rows of A Bring = E_ring give
+                # A_II F = -A_IG B22 and A_GI F = I - A_GG B22 (G = ring), hence
+                #   H = F^T A_II F = B22 A_GG B22 - B22   and, with B22 = C C^T,
+                #   M = C^{-1} H C^{-T} = C^T A_GG C - I
+                # -- two GEMMs with the Cholesky factor instead of the sparse-row gathers + GEMM
+                # for H and two triangular solves.  The top eigenvalues wanted are O(1) or larger
+                # relative to the subtracted identity's rounding (eps * ||C^T A_GG C||).
+                ts = _stage("coarse: H = F^T A_II F", ts)
+                C, info = torch.linalg.cholesky_ex(0.5 * (B22 + B22.mT))
+                M = C.mT @ (Ag[:, nin:n, nin:n] @ C)
+                M.diagonal(dim1=1, dim2=2).sub_(1.0)
+                M = 0.5 * (M + M.mT)
+                H = Xs = None
+            else:
+                H = _harmonic_h(torch, Ag, Bring, n, ni)
+                H = 0.5 * (H + H.mT)
+                ts = _stage("coarse: H = F^T A_II F", ts)
+                C, info = torch.linalg.cholesky_ex(0.5 * (B22 + B22.mT))
+                Xs = torch.linalg.solve_triangular(C, H, upper=False)
+                M = torch.linalg.solve_triangular(C, Xs.mT, upper=False)
+                M = 0.5 * (M + M.mT)
             kk = min(n_modes + 1, nbr)
             ts = _stage("coarse: pencil reduction", ts)
             th, Q, _ = topk_chebyshev(torch, M, kk)

@@ -55,8 +55,12 @@ def test_topk_chebyshev_matches_dense_eigh(decay):
         assert float(sv.min()) > 1 - 1e-12
 
 
+@pytest.mark.parametrize("direct", ["1", "0"])
 @pytest.mark.parametrize("name,sel", [("cfg2_m24", [0, 4, 13, 26]), ("cfg5_m16", [0, 3, 7])])
-def test_batched_band_coarse_columns_match_dense_path(name, sel):
+def test_batched_band_coarse_columns_match_dense_path(name, sel, direct, monkeypatch):
+    # direct = "1": the reduced pencil formed as M = C^T A_GG C - I (overlap 1), "0": from
+    # H = F^T A_II F by two triangular solves; both against the dense eigensolve of the pencil
+    monkeypatch.setenv("TLS_PENCIL_DIRECT", direct)
     d, ms, A, ld = _batch(name, sel)
     k = int(d["n_modes"])
     L, Dinv, perms, kcnts, info, P, codes = G._band_factor(torch, A, [np.argsort(m.indices, kind="stable") for m in ms],
