@@ -627,6 +627,12 @@ def _eigh_desc(torch, T):
     return w, S
 
 
+def _block_width(k):
+    """Columns of the subspace-iteration block for k wanted pairs (TLS_CHEB_P overrides)."""
+    e = int(os.environ.get("TLS_CHEB_P", "0"))
+    return e if e > 0 else max(3 * k, k + 16)
+
+
 def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rmax=1e8, dmax=16,
                    trace=None, check_every=2):
     """Top-k eigenpairs (descending) of a batch of symmetric PSD matrices M (b, m, m).
@@ -651,7 +657,7 @@ def topk_chebyshev(torch, M, k, tol=1e-14, p=None, maxit=400, seed=20240103, rma
     (theta, X, block products).
     """
     b, m, _ = M.shape
-    p = min(m, p or max(3 * k, k + 16))
+    p = min(m, p or _block_width(k))
     if m <= max(96, 2 * p) or p > 64:
         return _topk_chebyshev_host(torch, M, k, tol=tol, p=p, maxit=maxit, seed=seed, rmax=rmax,
                                     dmax=dmax, trace=trace)
@@ -835,38 +841,43 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
             for b in bs:
                 out[b] = (torch.zeros((ni, 0), dtype=torch.float64, device=dev), float("inf"), None)
             continue
-        Pg = P.index_select(0, bi)
+        # a group that is the whole batch (the common case) reads the batch tensors in place
+        sel = (lambda t: t) if len(bs) == cnt else (lambda t: t.index_select(0, bi))
+        Pg = sel(P)
         pinv = torch.empty_like(Pg)
         pinv.scatter_(1, Pg, torch.arange(ld, device=dev).expand_as(Pg))
         E = torch.zeros((len(bs), ld, nbr), dtype=torch.float64, device=dev)
         rows = pinv[:, nin:n]                                       # (g, nbr) factor positions of the ring
+        direct = (kind == "gevp" and n_modes is not None and ni == nin
+                  and os.environ.get("TLS_PENCIL_DIRECT", "1") != "0")
         # unit right-hand sides sorted by the factor position of their 1: the forward sweep skips
-        # the columns that are still zero (column j of E is zero above row rows[b, j])
-        order = lead = None
-        if Dinv is not None and os.environ.get("TLS_RING_SKIP", "1") != "0":
+        # the columns that are still zero (column j of E is zero above row rows[b, j]).  Bring then
+        # has its columns in that order; only the direct pencil below reads it that way (B22's
+        # columns and the rows of U are permuted instead of the n x n_b block)
+        order = lead = inv = None
+        if Dinv is not None and direct and os.environ.get("TLS_RING_SKIP", "1") != "0":
             rows, order = rows.sort(dim=1)
             lead = rows.amin(dim=0).cpu().numpy()
+            inv = torch.empty_like(order)
+            inv.scatter_(1, order, torch.arange(nbr, device=dev).expand_as(order))
         E.view(len(bs), -1)[torch.arange(len(bs), device=dev)[:, None],
                             rows * nbr + torch.arange(nbr, device=dev)[None, :]] = 1.0
         ts = _stage("coarse: ring rhs", time.perf_counter() if VERBOSE else 0.0)
         if Dinv is not None:   # banded blocked solve (batched GEMMs on the band only)
-            X = band_solve_multi(torch, L.index_select(0, bi), Dinv.index_select(0, bi),
-                                 kc[bs], E, lead)
+            X = band_solve_multi(torch, sel(L), sel(Dinv), kc[bs], E, lead)
         else:
-            X = torch.cholesky_solve(E, L.index_select(0, bi))      # A_P^{-1} E  (factor order)
+            X = torch.cholesky_solve(E, sel(L))                     # A_P^{-1} E  (factor order)
         del E
-        if order is not None:  # back to the ring order of the local numbering
-            inv = torch.empty_like(order)
-            inv.scatter_(1, order, torch.arange(nbr, device=dev).expand_as(order))
-            X = torch.gather(X, 2, inv[:, None, :].expand(len(bs), ld, nbr))
         Bring = torch.gather(X, 1, pinv[:, :n, None].expand(len(bs), n, nbr))  # local order
         del X
         ts = _stage("coarse: ring solve", ts)
         if kind == "gevp" and n_modes is not None:
             F = Bring[:, :ni]
             B22 = Bring[:, nin:n]
-            Ag = A.index_select(0, bi)
-            if ni == nin and os.environ.get("TLS_PENCIL_DIRECT", "1") != "0":
+            if inv is not None:  # columns back to the ring order (n_b x n_b only)
+                B22 = torch.gather(B22, 2, inv[:, None, :].expand(len(bs), nbr, nbr))
+            Ag = sel(A)
+            if direct:
                 # overlap 1 (F = all non-ring rows of Bring): the rows of A Bring = E_ring give
                 # A_II F = -A_IG B22 and A_GI F = I - A_GG B22 (G = ring), hence
                 #   H = F^T A_II F = B22 A_GG B22 - B22   and, with B22 = C C^T,
@@ -894,6 +905,8 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
             ts = _stage("coarse: subspace iteration", ts)
             sig = torch.sqrt(torch.clamp(th, min=0.0)).cpu().numpy()
             U = torch.linalg.solve_triangular(C.mT, Q, upper=True)
+            if order is not None:  # Bring's columns are in sorted order: permute U's rows to match
+                U = torch.gather(U, 1, order[:, :, None].expand(len(bs), nbr, U.shape[2]))
             V = Bring @ U
             idx = torch.argmax(V.abs(), dim=1)
             sgn = torch.where(torch.gather(V, 1, idx[:, None, :])[:, 0, :] < 0, -1.0, 1.0)
@@ -1508,8 +1521,12 @@ def _band_bytes(codes):
 def _release_cache(torch, dev, frac=0.25):
     """End of setup: hand torch's cached setup workspace back to the driver only when it is a
     large share of the device (every cudaFree synchronises and costs ms; SURVEY.md §8d TTS)."""
-    _, total = torch.cuda.mem_get_info(dev)
-    if torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev) > frac * total:
+    free, total = torch.cuda.mem_get_info(dev)
+    cached = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+    # ... and only when the device is nearly full: the flush itself cost 5.6 s at the end of a
+    # configuration-5 setup (thousands of cudaFree calls), the cached blocks are reused by the
+    # solves' work vectors, and torch flushes on its own when an allocation does not fit
+    if cached > frac * total and free < 0.1 * total:
         torch.cuda.empty_cache()
 
 
