@@ -821,6 +821,36 @@ def _harmonic_h(torch, Ag, Bring, n, ni):
     return -(Fr.mT @ Y)
 
 
+def _ctac(torch, C, S):
+    """C^T S C (symmetric, both triangles filled) for batched lower-triangular C and symmetric S,
+    skipping the zero blocks of C in a 2 x 2 splitting and computing the off-diagonal block once:
+    1.25 m^3 multiply-adds instead of the 2 m^3 of two full GEMMs.
+
+      C = [C11 0; C21 C22]   W = S C = [S[:, :h] C11 + S[:, h:] C21,  S[:, h:] C22]
+      M11 = C[:, :h]^T W[:, :h],  M21 = C22^T W[h:, :h],  M22 = C22^T W[h:, h:]
+    """
+    m = C.shape[1]
+    h = (m // 2 + 63) // 64 * 64
+    if m < 256 or h >= m:
+        M = C.mT @ (S @ C)
+        return 0.5 * (M + M.mT)
+    S = S.contiguous()                         # one copy of the strided ring-ring slice
+    W1 = S @ C[:, :, :h]                       # (g, m, h)   columns of C11 / C21
+    W2 = S[:, :, h:] @ C[:, h:, h:]            # (g, m, m-h) columns of C22 (rows below h only)
+    C22t = C[:, h:, h:].mT
+    M = torch.empty_like(C)
+    M11 = C[:, :, :h].mT @ W1
+    M[:, :h, :h] = 0.5 * (M11 + M11.mT)
+    del M11
+    M21 = C22t @ W1[:, h:]                     # (g, m-h, h)
+    M[:, h:, :h] = M21
+    M[:, :h, h:] = M21.mT
+    del M21, W1
+    M22 = C22t @ W2[:, h:]
+    M[:, h:, h:] = 0.5 * (M22 + M22.mT)
+    return M
+
+
 def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=None, kc=None):
     """Coarse columns of a batch of band-factored subdomains, batched by shape.
 
@@ -887,9 +917,8 @@ def _coarse_band_batch(torch, kind, A, L, P, ns, nis, nins, tau, n_modes, Dinv=N
                 # relative to the subtracted identity's rounding (eps * ||C^T A_GG C||).
                 ts = _stage("coarse: H = F^T A_II F", ts)
                 C, info = torch.linalg.cholesky_ex(0.5 * (B22 + B22.mT))
-                M = C.mT @ (Ag[:, nin:n, nin:n] @ C)
+                M = _ctac(torch, C, Ag[:, nin:n, nin:n])
                 M.diagonal(dim1=1, dim2=2).sub_(1.0)
-                M = 0.5 * (M + M.mT)
                 H = Xs = None
             else:
                 H = _harmonic_h(torch, Ag, Bring, n, ni)
