@@ -11,7 +11,7 @@ for c in range(1, 6):
     if not os.path.exists(f):
         continue
     d = json.loads([l for l in open(f) if l.startswith("{")][-1])
-    cfg, rf, lr, cb = d["config"], d["roofline"], d.get("loop_roofline", {}), d.get("cpu_baseline", {})
+    cfg, rf, lr, cb = d.get("results", d["config"]), d["roofline"], d.get("loop_roofline", {}), d.get("cpu_baseline", {})
     cpu = cb.get("value")
     rows.append(
         f"| {c} | {d['value']:,.1f} ({d['e2e']['value']:,.1f}) | {cfg['iterations_per_solve']} | "
