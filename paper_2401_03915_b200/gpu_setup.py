@@ -831,7 +831,7 @@ def _ctac(torch, C, S):
     """
     m = C.shape[1]
     h = (m // 2 + 63) // 64 * 64
-    if m < 256 or h >= m:
+    if m < 256 or h >= m or os.environ.get("TLS_PENCIL_CTAC", "1") == "0":
         M = C.mT @ (S @ C)
         return 0.5 * (M + M.mT)
     S = S.contiguous()                         # one copy of the strided ring-ring slice
