@@ -63,14 +63,6 @@ struct tls_ctx {
   int64_t dev_bytes = 0;
   cudaStream_t cap = nullptr;
   cudaStream_t aux = nullptr;                          // side branch (coarse chain overlap)
-  // The side branch runs next to the band solve, whose grid (one CTA per subdomain: 7 waves on
-  // configuration 5) keeps every SM slot busy; the block scheduler hands freed slots to the oldest
-  // grid first, so side-branch kernels of equal priority only started in the band solve's last
-  // wave and the coarse chain ran AFTER it (k_restrict: 18.7 ms from launch to end in the kernel
-  // trace).  The side stream and its kernel nodes therefore carry the greatest stream priority:
-  // their CTAs take the slots the band solve's retiring CTAs free.  TLS_AUX_PRIORITY=0 disables.
-  int aux_prio = 0;
-  bool aux_prio_on = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // ---- matrix (CSR, int32 indices)
   int n = 0;
@@ -220,22 +212,13 @@ static void launch_k(const tls_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, di
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[1];
   const bool trace = ctx && ctx->ktrace && !ctx->capturing;
-  unsigned na = 0;
   if (ctx && ctx->pdl && !trace) {
-    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  if (ctx && ctx->aux_prio_on && s == ctx->aux) {  // explicit, so captured kernel nodes carry it too
-    at[na].id = cudaLaunchAttributePriority;
-    at[na].val.priority = ctx->aux_prio;
-    ++na;
-  }
-  if (na) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = na;
+    cfg.numAttrs = 1;
   }
   if (trace) {
     cudaEvent_t a, b;
@@ -832,18 +815,7 @@ int32_t tls_ctx_create(int32_t device, tls_ctx** out) {
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking);
-  if (e == cudaSuccess) {
-    int least = 0, greatest = 0;
-    const char* env = getenv("TLS_AUX_PRIORITY");
-    if (!(env && atoi(env) == 0) && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess &&
-        greatest < least) {
-      ctx->aux_prio = greatest;
-      ctx->aux_prio_on = true;
-      e = cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, greatest);
-    } else {
-      e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
-    }
-  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&ctx->h_flag, sizeof(int) * 4);
