@@ -1440,11 +1440,13 @@ int32_t tls_precond_finalize(tls_ctx* ctx, int32_t one_level, int32_t combine) {
     // block-tridiagonal coarse solve: one tile plan per inverted Schur block, launched one after
     // the other (every rank runs the whole substitution: it does not partition by rows)
     double bytes = 0.0;
+    int chain_ur = 2;  // tile-rows per work unit (TLS_CHAIN_UR: tuning override, 1..8)
+    if (const char* e = getenv("TLS_CHAIN_UR")) chain_ur = std::max(1, std::min(UR, atoi(e)));
     for (int i = 0; i < ctx->chain_nb; ++i) {
       const BlkDesc& b = ctx->h_blk[nsub + 3 + i];
       ctx->chain_u0.push_back((int)units.size());
       ctx->chain_o0.push_back((int)outs.size());
-      plan_block(nsub + 3 + i, b.nt, 1, 2, slot, units, outs, red);
+      plan_block(nsub + 3 + i, b.nt, 1, chain_ur, slot, units, outs, red);
       ctx->chain_nu.push_back((int)units.size() - ctx->chain_u0.back());
       ctx->chain_no.push_back((int)outs.size() - ctx->chain_o0.back());
       const double ni = b.n;

@@ -1946,6 +1946,11 @@ def build_device_operators(handle, csr, symmetric, maps, owner, coarse, tau, n_m
         bs = -(-(a0_band + 1) // 64) * 64
         chain = banded and nC >= _chain_min()
         if chain:
+            # TLS_A0_CHAIN_MUL: blocks of mul * (smallest admissible size) -- fewer, larger steps
+            mul = max(1, int(os.environ.get("TLS_A0_CHAIN_MUL", "1")))
+            while mul > 1 and -(-nC // (bs * mul)) < 2:
+                mul -= 1
+            bs *= mul
             info, sinv, lo_csr, up_csr = spd_block_tridiagonal_chain(torch, A0, bs)
             if info != 0:
                 raise RuntimeError(f"coarse operator is not positive definite: {info}-th leading minor")
